@@ -1,0 +1,444 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 FCS hot path (driver contract: one JSON line on rank 0).
+
+Headline workload: BASELINE config 4 — dense FCS of a 1024^3 float32 tensor
+(4 GiB, iid N(0,1), seeded device fill), J_n = 16384 (J~ = 49150), D = 4
+families. A step is one K1 pass (st_fcs_dense) over the rank's slab of the
+tensor (elements sharded by the last mode), plus — for N > 1 — the single NCCL
+all-reduce of the D x J~ fp64 partials. value = tensor elements / s for the
+whole job (strong scaling: the 1024^3 tensor is split across ranks).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Also reported: roofline of K1 against the measured HBM copy bandwidth
+(MEASURED_PEAKS.json), e2e through the host-buffer C-ABI call
+(st_fcs_dense_host, pinned host tensor, H2D + compute + D2H inside the timed
+region), the reference CPU path on a bounded sample (cpu_baseline), clocks
+sampled during the timed region, and secondary lines for configs 2, 3, 5.
+The input (4 GiB) is larger than L2 (126 MB), so no L2 flush is needed.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+C4_DIMS = (1024, 1024, 1024)
+C4_J, C4_D, C4_SEED = 16384, 4, 4
+METRIC = "fcs_dense_tensor_elements_per_sec"
+UNIT = "elements/s"
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+           0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+           0x100: "display_clock_setting"}
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def jt_of(dims, J):
+    return len(dims) * J - len(dims) + 1
+
+
+def algorithmic_bytes(elems, dims, D, J, esz=4):
+    """tensor read once + D x sum(I) x 5 B tables + D x J~ x esz out."""
+    return elems * esz + D * sum(dims) * 5 + D * jt_of(dims, J) * esz
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms (B200_PROFILING.md)."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 3:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        busy = [s for s in self.samples if not (s[2] & 0x1)] or self.samples
+        reasons = set()
+        for s in busy:
+            for bit, name in REASONS.items():
+                if s[2] & bit:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(s[0] for s in busy),
+                "sm_max_mhz": max(s[1] for s in busy), "reasons": sorted(reasons),
+                "samples": len(busy)}
+
+
+# --------------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2106_13062_b200 as st
+    from paper_2106_13062_b200 import _lib as L
+    from paper_2106_13062_b200.dist import shard_range
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = L.lib()
+    stream = torch.cuda.current_stream()
+    sp = C.c_void_p(stream.cuda_stream)
+    dims = list(C4_DIMS)
+    lo, hi = shard_range(dims[-1], rank, world)
+    per_slab = dims[0] * dims[1]
+    elems_local = per_slab * (hi - lo)
+    jt = jt_of(dims, C4_J)
+
+    # synthetic slab (device fill; see paper_2106_13062_b200/configs.py) and tables
+    x = torch.empty(elems_local, dtype=torch.float32, device="cuda")
+    L.check(lib.st_device_gaussian(L.ST_F32, C4_SEED ^ (rank << 32), elems_local,
+                                   C.c_void_p(x.data_ptr()), sp))
+    seeds = [st.family_seed(C4_SEED, d) for d in range(C4_D)]
+    packed = torch.empty(C4_D * sum(dims), dtype=torch.int32, device="cuda")
+    dims_a, lens_a = L.size_array(dims), L.size_array([C4_J] * 3)
+    L.check(lib.st_family_tables(3, dims_a, lens_a, C4_D, L.u64_array(seeds),
+                                 C.c_void_p(packed.data_ptr()), sp))
+    out = torch.empty((C4_D, jt), dtype=torch.float64, device="cuda")
+    ws_bytes = lib.st_fcs_dense_workspace(L.ST_F32, 3, dims_a, hi - lo, C4_D, lens_a)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device="cuda")
+
+    def sketch():
+        L.check(lib.st_fcs_dense(L.ST_F32, C.c_void_p(x.data_ptr()), 3, dims_a, lo, hi - lo, C4_D,
+                                 C.c_void_p(packed.data_ptr()), lens_a, C.c_void_p(out.data_ptr()),
+                                 0, C.c_void_p(ws.data_ptr()), ws_bytes, sp))
+
+    def step():
+        sketch()
+        if world > 1:
+            dist.all_reduce(out, op=dist.ReduceOp.SUM)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    # timed region: K steps, CUDA events on the launching stream
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for i in range(args.steps):
+            k_ev[i][0].record(stream)
+            sketch()
+            k_ev[i][1].record(stream)
+            if world > 1:
+                dist.all_reduce(out, op=dist.ReduceOp.SUM)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_ms = ev0.elapsed_time(ev1)
+    k_ms = statistics.mean(a.elapsed_time(b) for a, b in k_ev)
+    if world > 1:
+        tt = torch.tensor([t_ms, k_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms, k_ms = float(tt[0]), float(tt[1])
+    ms_per_step = t_ms / args.steps
+    total_elems = int(np.prod(dims))
+    value = total_elems / (ms_per_step * 1e-3)
+
+    peak, peak_kind = hbm_peak()
+    alg = algorithmic_bytes(elems_local, dims, C4_D, C4_J)
+    achieved = alg / (k_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("c4_fcs_dense_smem_kernel_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # e2e: host-buffer C-ABI call (pinned host tensor; H2D + tables + K1 + D2H)
+    e2e = None
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    host = torch.empty(elems_local, dtype=torch.float32, pin_memory=True)
+    host.copy_(x)
+    hout = np.empty((C4_D, jt), np.float64)
+    slab_dims = L.size_array([dims[0], dims[1], hi - lo])
+    seeds_a = L.u64_array(seeds)
+    for _ in range(1):
+        L.check(lib.st_fcs_dense_host(L.ST_F32, C.c_void_p(host.data_ptr()), 3, slab_dims, C4_D,
+                                      seeds_a, lens_a, hout.ctypes.data_as(C.c_void_p)))
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        L.check(lib.st_fcs_dense_host(L.ST_F32, C.c_void_p(host.data_ptr()), 3, slab_dims, C4_D,
+                                      seeds_a, lens_a, hout.ctypes.data_as(C.c_void_p)))
+        if world > 1:
+            tmp = torch.from_numpy(hout).cuda()
+            dist.all_reduce(tmp)
+            hout[:] = tmp.cpu().numpy()
+    t_e2e = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        tt = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt[0])
+    e2e = {"value": total_elems / t_e2e, "unit": UNIT, "h2d_bytes_per_step": elems_local * 4,
+           "d2h_bytes_per_step": C4_D * jt * 8, "ms_per_step": t_e2e * 1e3,
+           "api": "st_fcs_dense_host (fcs_sketch(DenseTensor, HashFamily) x D)"}
+    del host
+
+    line = None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic: seeded SplitMix64/Box-Muller N(0,1) device fill",
+            "config": {"workload": "c4: dense FCS 1024x1024x1024 float32, J_n=16384 (J~=49150), "
+                                   "D=4", "dims": dims, "hash_len": C4_J, "sketch_count": C4_D,
+                       "composed_len": jt, "parallelism": f"element-shard x{world} + nccl "
+                                                         "allreduce" if world > 1 else "single",
+                       "l2": "input 4 GiB > L2 126 MB: no flush needed"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_kind": peak_kind, "kernel_ms": k_ms,
+                         "algorithmic_bytes_per_launch": alg,
+                         "kernel": "fcs_dense_smem_kernel<float,float> + reduce_partials"},
+            "e2e": e2e,
+            "gpu_launches": 2 * args.steps,
+            "clocks": clk.summary(),
+        }
+    if world == 1 and not args.no_secondary:
+        try:
+            line["secondary"] = secondary()
+        except Exception as e:  # never lose the headline
+            line["secondary"] = {"error": repr(e)}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            line["cpu_baseline"] = cpu_baseline(threads=1, target_s=args.cpu_seconds)
+        except Exception as e:
+            line["cpu_baseline"] = {"error": repr(e)}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def secondary():
+    """Configs 2, 3, 5 (and c1) on one GPU: device-resident inputs, CUDA events."""
+    import torch
+
+    import paper_2106_13062_b200 as st
+    from paper_2106_13062_b200 import configs
+
+    def timeit(fn, reps):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    res = {}
+    c = configs.C1
+    x = st.DenseTensor.from_array(configs.c1_tensor(c))
+    fams = st.families_for(list(c.dims), st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
+    packed = st.packed_families(fams)
+    ms = timeit(lambda: st.fcs_dense_batched(x, fams, packed=packed), 50)
+    res["c1_dense_fcs"] = {"ms": ms, "elements_per_sec": 1e6 / (ms * 1e-3)}
+    c = configs.C2
+    w, fs = configs.c2_cp(c)
+    cp = st.CpTensor(w, fs)
+    fams = st.families_for(list(c.dims), st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
+    packed = st.packed_families(fams)
+    ms = timeit(lambda: st.fcs_cp_batched(cp, fams, packed=packed), 10)
+    res["c2_cp_fcs"] = {"ms": ms, "sketches_per_sec": c.sketch_count / (ms * 1e-3),
+                        "metric": "CP-FCS sketches/s (D=10 sketches of a rank-50 400^3 CP tensor)"}
+    c = configs.C3
+    t, lam, V = configs.c3_tensor(c)
+    dt = st.DenseTensor.from_array(t)
+    eng = st.FcsEngine(dt, st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
+    U = torch.randn(configs.C3_INITS, 200, dtype=torch.float64, device="cuda")
+    ms_iuv = timeit(lambda: eng.iuv_batch(U, U, 0), 20)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    cpd = st.rtpm(dt, st.RtpmConfig(c.rank, configs.C3_INITS, configs.C3_ITERS,
+                                    estimator=st.EstimatorConfig(c.hash_len, c.sketch_count,
+                                                                 c.seed)))
+    t_rtpm = time.perf_counter() - t0
+    err = float(np.abs(np.sort(cpd.weights.cpu().numpy())[::-1] - np.sort(lam)[::-1]).max())
+    res["c3_rtpm"] = {"iuv_step_ms": ms_iuv, "estimates_per_sec": configs.C3_INITS / (ms_iuv * 1e-3),
+                      "rtpm_total_s": t_rtpm, "max_weight_error": err}
+    c = configs.C5
+    A, B = configs.c5_matrices(c)
+    fams = st.families_for(list(c.dims), st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
+    ms = timeit(lambda: st.fcs_kron(A, B, fams), 10)
+    res["c5_kron"] = {"ms_incl_h2d": ms}
+    return res
+
+
+# ------------------------------------------------------------ reference (CPU)
+def cpu_baseline(threads: int, target_s: float = 10.0, slabs: int = None):
+    """The reference's own fcs_sketch(DenseTensor) (oracle/_ref, unmodified
+    sources) on a bounded sample of the config-4 workload: the first `slabs`
+    i_3-slabs (1024 x 1024 x slabs) widened to fp64 (the reference is fp64-only),
+    all D = 4 families. Work is split over (slab chunk, family) tasks when
+    threads > 1 (harness-level)."""
+    import concurrent.futures as cf
+
+    from oracle import ref
+    from paper_2106_13062_b200 import configs
+
+    lib = ref.lib()
+    seeds = [ref.family_seed(C4_SEED, d) for d in range(C4_D)]
+    per = C4_DIMS[0] * C4_DIMS[1]
+
+    def run(nslab, nthreads):
+        x = configs.host_gaussian(C4_SEED, per * nslab)  # fp64 sample
+        chunks = []
+        step = max(1, nslab // max(1, nthreads // C4_D if nthreads > C4_D else 1))
+        for s0 in range(0, nslab, step):
+            chunks.append((s0, min(nslab, s0 + step)))
+        tasks = [(c, d) for c in chunks for d in range(C4_D)]
+        jt = jt_of(C4_DIMS, C4_J)
+
+        def one(task):
+            (s0, s1), d = task
+            # slab shard of the full 1024^3 family: the tables are the full ones,
+            # the reference needs a tensor whose shape matches the family, so a
+            # slab is sketched with the family over (1024, 1024, s1 - s0) whose
+            # last-mode table is the slice [s0, s1) — via explicit tables.
+            b, s, _ = ref.hash_family(C4_DIMS, C4_J, seeds[d])
+            bs = [b[0], b[1], b[2][s0:s1]]
+            ss = [s[0], s[1], s[2][s0:s1]]
+            t = x[s0 * per:s1 * per].reshape((1024, 1024, s1 - s0), order="F")
+            return ref.fcs_dense_tables(t, bs, ss, [C4_J] * 3)
+
+        t0 = time.perf_counter()
+        if nthreads == 1:
+            outs = [one(tk) for tk in tasks]
+        else:
+            with cf.ThreadPoolExecutor(nthreads) as ex:
+                outs = list(ex.map(one, tasks))
+        dt = time.perf_counter() - t0
+        assert all(o.shape == (jt,) for o in outs)
+        return dt
+
+    if slabs is None:
+        dt1 = run(2, threads)
+        slabs = int(min(256, max(2, target_s / max(dt1, 1e-3) * 2)))
+    dt = run(slabs, threads)
+    elems = per * slabs
+    return {"value": elems / dt, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"1024x1024x{slabs} slab of config 4 (fp64-widened, {elems} elements), "
+                      f"D=4 families, reference fcs_sketch(DenseTensor) via oracle/_ref",
+            "seconds": dt}
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    nthreads = os.cpu_count() or 1
+    slabs = args.ref_slabs
+    times = []
+    base = None
+    for i in range(max(args.warmup, 0) + args.steps):
+        b = cpu_baseline(threads=nthreads, slabs=slabs)
+        if i >= args.warmup:
+            times.append(b["seconds"])
+            base = b
+    per = C4_DIMS[0] * C4_DIMS[1] * slabs
+    ms = statistics.mean(times) * 1e3
+    value = per / (ms * 1e-3)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded SplitMix64/Box-Muller N(0,1) host stream",
+            "config": {"workload": "c4: dense FCS 1024x1024x1024, J_n=16384, D=4 (bounded "
+                                   f"sample: {slabs} slabs of 1024x1024 per step)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "reference",
+                             "sample": base["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-slabs", type=int, default=16)
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

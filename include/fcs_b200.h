@@ -1,0 +1,219 @@
+/*
+ * fcs_b200.h — C-ABI of the B200-native fast count sketch (FCS) library.
+ *
+ * This is the drop-in boundary for the FCS hot path of the reference
+ * (`/root/reference/proj`, namespace `sketchtensor`). Every entry point takes
+ * plain pointers and sizes (no torch, Eigen or C++ types) and names the
+ * reference interface it replaces as file:line. Unless marked HOST, tensor /
+ * table / output pointers are DEVICE pointers on the current CUDA device and
+ * work is stream-ordered on `stream` (a cudaStream_t, NULL = legacy default).
+ *
+ * Errors: every int-returning call returns one of the ST_* codes below.
+ * ST_EINVAL mirrors the reference's std::invalid_argument (validation is on
+ * the host, before any launch); ST_ENUMERIC mirrors std::runtime_error
+ * (idft_real's imaginary-residue check, fft.cpp:69-71). st_last_error()
+ * returns the thread's last message (same text as the reference where one
+ * exists). There is no CPU fallback: with no usable GPU every compute entry
+ * fails with ST_ECUDA.
+ *
+ * Table layout ("packed family tables"): for D families over N modes with
+ * dims I_0..I_{N-1}, entry (d, n, i) lives at
+ *     packed[d * sum(I) + (I_0 + ... + I_{n-1}) + i]
+ * as  bucket | (sign < 0 ? 1u << 31 : 0)   (bucket < 2^31).
+ * Dense tensors are column-major, first index fastest (tensor.hpp:10-13).
+ * Sketch outputs are fp64, D rows of J~ = sum(J_n) - N + 1, row-major.
+ */
+#ifndef FCS_B200_H
+#define FCS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  ST_OK = 0,
+  ST_EINVAL = 1,   /* std::invalid_argument in the reference */
+  ST_ENUMERIC = 2, /* std::runtime_error (idft_real residue) */
+  ST_ECUDA = 3,
+  ST_ENCCL = 4,
+  ST_ENOMEM = 5
+};
+
+enum { ST_F32 = 0, ST_F64 = 1 };
+
+#define ST_MAX_ORDER 8
+
+/* Thread-local text of the last failure. */
+const char* st_last_error(void);
+/* ABI version of this header (bumped on any signature change). */
+int st_abi_version(void);
+/* Device facts used for grid sizing: SM count, opt-in smem per block, L2. */
+int st_device_query(int* sm_count, size_t* smem_optin, size_t* l2_bytes);
+
+/* ------------------------------------------------------------------ hashing */
+
+/* HOST. family_seed(base, d) = SplitMix64::mix(base + d).
+ * Replaces sketchtensor::family_seed, hashing.cpp:123-125. */
+uint64_t st_family_seed(uint64_t base_seed, size_t d);
+
+/* K0. Tabulates HashPair(input_dim, hash_len, seed) on the device: bucket[i]
+ * from draw 2i+1 (Lemire mulhi), sign[i] from the top bit of draw 2i+2,
+ * bit-exact with the serial host stream.
+ * Replaces HashPair::HashPair(size_t, size_t, uint64_t), hashing.cpp:10-22. */
+int st_hash_tabulate(uint64_t seed, size_t input_dim, size_t hash_len, uint32_t* bucket,
+                     int8_t* sign, void* stream);
+
+/* K0 over a whole estimator configuration: D families (master seed
+ * master_seeds[d], pair n seeded master ^ n), written as packed tables.
+ * Replaces HashFamily(dims, hash_lens, master), hashing.cpp:42-54, and
+ * families_for, estimators.cpp:104-115 (callers pass family_seed(seed, d)). */
+int st_family_tables(size_t order, const size_t* dims, const size_t* hash_lens,
+                     size_t sketch_count, const uint64_t* master_seeds /* HOST */,
+                     uint32_t* packed, void* stream);
+
+/* Packs explicit (hand-built) device tables bucket[total], sign[total] into
+ * packed form; validates bucket < hash_len per mode on the host side caller.
+ * Serves HashPair(bucket_map, sign_map, hash_len), hashing.cpp:24-40. */
+int st_pack_tables(size_t total, const uint32_t* bucket, const int8_t* sign, uint32_t* packed,
+                   void* stream);
+
+/* ------------------------------------------------------------- dense FCS */
+
+/* Workspace bytes st_fcs_dense needs for this problem (0 if none). */
+size_t st_fcs_dense_workspace(int dtype, size_t order, const size_t* dims, size_t last_count,
+                              size_t sketch_count, const size_t* hash_lens);
+
+/* K1. Dense FCS of a column-major order-N tensor for D families at once:
+ *   out[d][sum_n h_{d,n}(i_n)] (+)= prod_n s_{d,n}(i_n) * T[i]
+ * over every element; exact zeros contribute nothing (sketch.cpp:48-61).
+ * `tensor` holds the slab i_{N-1} in [last_begin, last_begin + last_count)
+ * of the full tensor `dims` (contiguous because the last mode is slowest) —
+ * the shard a rank owns under element sharding; pass 0 / dims[N-1] for the
+ * whole tensor. dtype ST_F32 accumulates per-block partials in fp32 and
+ * reduces them in fp64; ST_F64 is fp64 throughout. accumulate != 0 adds to
+ * out instead of overwriting it.
+ * Replaces fcs_sketch(const DenseTensor&, const HashFamily&), sketch.cpp:187-201
+ * (D calls, one per family). */
+int st_fcs_dense(int dtype, const void* tensor, size_t order, const size_t* dims,
+                 size_t last_begin, size_t last_count, size_t sketch_count,
+                 const uint32_t* packed, const size_t* hash_lens, double* out, int accumulate,
+                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* HOST-buffer convenience: H2D of the tensor (pinned or pageable), K0 on the
+ * device from the seeds, K1, D2H of the D x J~ result, synchronised. The
+ * end-to-end call a reference caller makes.
+ * Replaces D x fcs_sketch(DenseTensor(dims, data), HashFamily(dims, J, seeds[d])). */
+int st_fcs_dense_host(int dtype, const void* host_tensor, size_t order, const size_t* dims,
+                      size_t sketch_count, const uint64_t* master_seeds, const size_t* hash_lens,
+                      double* host_out);
+
+/* Count sketch of R columns (cs_sketch_columns, sketch.cpp:118-133; R = 1 is
+ * cs_sketch, sketch.cpp:105-116): u is I x R column-major (device), table is
+ * one packed pair, out is hash_len x R column-major fp64 (overwritten). */
+int st_cs_columns(const double* u, size_t input_dim, size_t cols, const uint32_t* packed_pair,
+                  size_t hash_len, double* out, void* stream);
+
+/* --------------------------------------------------------------- CP-form FCS */
+
+/* Workspace bytes for st_fcs_cp. */
+size_t st_fcs_cp_workspace(size_t order, const size_t* dims, size_t rank, size_t sketch_count,
+                           const size_t* hash_lens);
+
+/* K2-K5. FCS of a CP tensor sum_r w_r u_r^(1) o ... o u_r^(N) for D families:
+ * per (d, r) the mode sketches CS_n(U^(n)[:, r]) are transformed, multiplied
+ * pointwise, weighted and summed over r in the frequency domain, then one
+ * inverse transform per d gives the length-J~ linear convolution. Only ranks
+ * [r_begin, r_begin + r_count) are included (rank sharding); zero weights
+ * are skipped like the reference. factors[n] is a device I_n x R column-major
+ * fp64 matrix; weights is a device R-vector. accumulate != 0 adds into out.
+ * Replaces fcs_sketch(const CpTensor&, const HashFamily&), sketch.cpp:203-207
+ * (convolved_cp_sketch :65-86, fft_convolve fft.cpp:75-84). */
+int st_fcs_cp(const double* weights, size_t rank, size_t order, const size_t* dims,
+              const double* const* factors /* HOST array of device ptrs */, size_t r_begin,
+              size_t r_count, size_t sketch_count, const uint32_t* packed,
+              const size_t* hash_lens, double* out, int accumulate, void* workspace,
+              size_t workspace_bytes, void* stream);
+
+/* Linear convolution of two batched real sequences (D rows each):
+ * out[d] = a[d] (*) b[d], length la + lb - 1. Serves the Kronecker path
+ * (FCS(A (x) B) = FCS(A) (*) FCS(B)) and fft_convolve with
+ * two inputs, fft.cpp:75-84. */
+int st_convolve_pairs(const double* a, size_t la, const double* b, size_t lb, size_t batch,
+                      double* out, void* stream);
+
+/* Kronecker-product compression (BASELINE config 5): for D 4-mode families
+ * (pairs p0..p3 over dims ra, ca, rb, cb) returns FCS of the outer-product
+ * tensor A o B = conv(FCS_{p0,p1}(vec A), FCS_{p2,p3}(vec B)), D x J~.
+ * Composition of fcs_sketch(tensor_from_matrix(.)) (sketch.cpp:187-201,
+ * tensor.cpp:272-276) and fft_convolve (fft.cpp:75-84). */
+int st_fcs_kron(const double* a, size_t ra, size_t ca, const double* b, size_t rb, size_t cb,
+                size_t sketch_count, const uint32_t* packed, const size_t* hash_lens,
+                double* out, void* stream);
+
+/* --------------------------------------------- sketched contraction engine */
+
+typedef struct st_engine st_engine;
+
+/* Builds D FCS sketches of an order-3 device tensor and caches their
+ * spectra on the device (FcsEngine ctor, cpd.cpp:63-67 -> families_for +
+ * precompute_fcs, estimators.cpp:104-115,140-149). The tensor is consumed
+ * once and not retained. */
+int st_engine_create(st_engine** engine, int dtype, const void* tensor, const size_t* dims,
+                     size_t hash_len, size_t sketch_count, uint64_t seed, void* stream);
+int st_engine_destroy(st_engine* engine);
+/* J~ and the current D x J~ sketch values (device out). */
+size_t st_engine_composed_len(const st_engine* engine);
+int st_engine_sketches(st_engine* engine, double* out, void* stream);
+
+/* Batched T(I, a, b) with the identity at free_mode: for each of `batch`
+ * vector pairs (rows of a: batch x I_c1, rows of b: batch x I_c2, device
+ * fp64) the median over D of s_f(i) * z_d[h_f(i)], z_d = IFFT(S_d conj(F cs_a)
+ * conj(F cs_b)); out is batch x I_free. median != 0 applies median_reduce;
+ * median == 0 writes all D estimates (batch x D x I_free) instead.
+ * Replaces ContractionEngine::iuv / FcsEngine::iuv, cpd.cpp:74-77 ->
+ * estimate_iuv, estimators.cpp:180-186 (iuv_spectral :66-90, median :125-138). */
+int st_engine_iuv(st_engine* engine, size_t batch, const double* a, const double* b,
+                  size_t free_mode, double* out, int median, void* stream);
+
+/* Batched T(u, v, w): out[k] = median over D of (1/n) sum Re(S conj(G)).
+ * Replaces FcsEngine::uvw, cpd.cpp:69-72 -> estimate_uvw, estimators.cpp:169-174
+ * (uvw_spectral :48-64, spectral_dot :38-45). */
+int st_engine_uvw(st_engine* engine, size_t batch, const double* u, const double* v,
+                  const double* w, double* out, int median, void* stream);
+
+/* T <- T - weight * u o v o w in sketch space (device vectors).
+ * Replaces FcsEngine::deflate, cpd.cpp:79-87. */
+int st_engine_deflate(st_engine* engine, double weight, const double* u, const double* v,
+                      const double* w, void* stream);
+
+/* HOST. Sketched robust tensor power method on a cubical device tensor:
+ * FCS engine, num_inits restarts advanced in lockstep as one batch, strict-`>`
+ * argmax, refinement, weight, deflation — cpd.cpp:234-277 with the same
+ * initial-vector stream (SplitMix64(mix(seed ^ 0x7274706d)), random_unit
+ * cpd.cpp:199-204). Outputs host weights[rank] and factor dim x rank
+ * (column-major). Replaces rtpm(const DenseTensor&, const RtpmConfig&)
+ * with backend FCS. */
+int st_rtpm(int dtype, const void* tensor, size_t dim, size_t rank, size_t num_inits,
+            size_t num_iters, size_t hash_len, size_t sketch_count, uint64_t seed,
+            double* weights, double* factor, void* stream);
+
+/* ---------------------------------------------------------- synthetic data */
+
+/* HOST. n draws of SplitMix64(seed).next_gaussian() (rng.cpp:8-21), host libm,
+ * multi-threaded through the counter identity; bit-identical to the serial
+ * reference stream. */
+int st_host_gaussian(uint64_t seed, size_t n, double* out, int threads);
+
+/* Device fill of n iid N(0,1) values (SplitMix64 counter + Box-Muller, CUDA
+ * libm: same distribution as the host stream, not bit-identical). For the
+ * large benchmark tensor only. dtype ST_F32 / ST_F64. */
+int st_device_gaussian(int dtype, uint64_t seed, size_t n, void* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FCS_B200_H */

@@ -1,0 +1,16 @@
+"""B200-native fast count sketch (FCS) — arXiv 2106.13062 hot path.
+
+sm_100a CUDA kernels behind the C-ABI in ``include/fcs_b200.h``
+(``_lib/libfcs_b200.so``), with a host mirror of the reference's
+``sketchtensor`` API. Importing the package does not touch the GPU; the first
+compute call loads the library and fails loudly if it or the GPU is missing.
+"""
+from .sketchtensor import (CpTensor, DenseTensor, EstimatorConfig, HashFamily, HashPair,  # noqa
+                           SketchKind, SketchVec, convolve_pairs, cs_sketch, cs_sketch_columns,
+                           families_for, family_seed, fcs_cp_batched, fcs_dense_batched,
+                           fcs_kron, fcs_sketch, hcs_sketch, median_reduce, packed_families,
+                           ts_sketch)
+from .engine import (ContractionEngine, FcsEngine, RtpmConfig, SketchBackend,  # noqa
+                     backend_from_name, backend_name, make_contraction_engine, rtpm)
+
+__all__ = [n for n in dir() if not n.startswith("_")]

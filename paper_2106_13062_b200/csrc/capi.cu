@@ -1,0 +1,217 @@
+// C-ABI layer (include/fcs_b200.h): host-side validation, workspace and
+// dispatch to the sm_100a kernels. No CPU compute path exists: every compute
+// entry launches device kernels or fails.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <numbers>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+
+namespace fcs {
+
+thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(int status, const std::string& msg) {
+  g_last_error = msg;
+  return status;
+}
+
+int device_info(DeviceInfo* out) {
+  static std::mutex mu;
+  static DeviceInfo cache[64];
+  int dev = 0;
+  FCS_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(ST_ECUDA, "device index out of range");
+  std::lock_guard<std::mutex> lock(mu);
+  if (cache[dev].device != dev) {
+    cudaDeviceProp p;
+    FCS_CUDA_TRY(cudaGetDeviceProperties(&p, dev));
+    if (p.major < 10) return fail(ST_ECUDA, "fcs_b200 requires an sm_100 (Blackwell) device");
+    cache[dev].device = dev;
+    cache[dev].sm_count = p.multiProcessorCount;
+    cache[dev].smem_optin = p.sharedMemPerBlockOptin;
+    cache[dev].l2_bytes = p.l2CacheSize;
+  }
+  *out = cache[dev];
+  return ST_OK;
+}
+
+// kernels (hash.cu, fcs_dense.cu)
+int launch_hash_tabulate(uint64_t, size_t, size_t, uint32_t*, int8_t*, cudaStream_t);
+int launch_family_tables(size_t, const size_t*, const size_t*, size_t, const uint64_t*,
+                         uint32_t*, cudaStream_t);
+int launch_pack_tables(size_t, const uint32_t*, const int8_t*, uint32_t*, cudaStream_t);
+int launch_device_gaussian(int, uint64_t, size_t, void*, cudaStream_t);
+size_t dense_workspace(int, size_t, const size_t*, size_t, size_t, const size_t*);
+int launch_fcs_dense(int, const void*, size_t, const size_t*, size_t, size_t, size_t,
+                     const uint32_t*, const size_t*, double*, int, void*, size_t, cudaStream_t,
+                     size_t fam_stride = 0);
+
+// RAII device buffer for the host-buffer conveniences.
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  int alloc(size_t bytes) {
+    if (bytes == 0) bytes = 1;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) return fail(ST_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    return ST_OK;
+  }
+};
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+}  // namespace fcs
+
+using namespace fcs;
+
+extern "C" {
+
+const char* st_last_error(void) { return g_last_error.c_str(); }
+
+int st_abi_version(void) { return 1; }
+
+int st_device_query(int* sm_count, size_t* smem_optin, size_t* l2_bytes) {
+  DeviceInfo di;
+  if (int rc = device_info(&di)) return rc;
+  if (sm_count) *sm_count = di.sm_count;
+  if (smem_optin) *smem_optin = di.smem_optin;
+  if (l2_bytes) *l2_bytes = di.l2_bytes;
+  return ST_OK;
+}
+
+uint64_t st_family_seed(uint64_t base_seed, size_t d) {
+  return splitmix_draw(base_seed + static_cast<uint64_t>(d), 1);
+}
+
+int st_hash_tabulate(uint64_t seed, size_t input_dim, size_t hash_len, uint32_t* bucket,
+                     int8_t* sign, void* stream) {
+  FCS_CHECK_ARG(input_dim > 0 && hash_len > 0, "HashPair: dimensions must be positive");
+  FCS_CHECK_ARG(input_dim < (1ull << 32), "HashPair: input_dim too large");
+  return launch_hash_tabulate(seed, input_dim, hash_len, bucket, sign, as_stream(stream));
+}
+
+int st_family_tables(size_t order, const size_t* dims, const size_t* hash_lens,
+                     size_t sketch_count, const uint64_t* master_seeds, uint32_t* packed,
+                     void* stream) {
+  FCS_CHECK_ARG(order >= 1 && order <= ST_MAX_ORDER, "HashFamily: need one hash length per mode");
+  FCS_CHECK_ARG(sketch_count >= 1,
+                "EstimatorConfig: hash_len and sketch_count must be >= 1");
+  uint64_t total = 0;
+  for (size_t n = 0; n < order; ++n) {
+    FCS_CHECK_ARG(dims[n] > 0 && hash_lens[n] > 0, "HashPair: dimensions must be positive");
+    FCS_CHECK_ARG(hash_lens[n] < (1ull << 30), "HashPair: hash_len too large");
+    total += dims[n];
+  }
+  FCS_CHECK_ARG(total < (1ull << 32), "HashFamily: tables too large");
+  return launch_family_tables(order, dims, hash_lens, sketch_count, master_seeds, packed,
+                              as_stream(stream));
+}
+
+int st_pack_tables(size_t total, const uint32_t* bucket, const int8_t* sign, uint32_t* packed,
+                   void* stream) {
+  return launch_pack_tables(total, bucket, sign, packed, as_stream(stream));
+}
+
+size_t st_fcs_dense_workspace(int dtype, size_t order, const size_t* dims, size_t last_count,
+                              size_t sketch_count, const size_t* hash_lens) {
+  return dense_workspace(dtype, order, dims, last_count, sketch_count, hash_lens);
+}
+
+int st_fcs_dense(int dtype, const void* tensor, size_t order, const size_t* dims,
+                 size_t last_begin, size_t last_count, size_t sketch_count,
+                 const uint32_t* packed, const size_t* hash_lens, double* out, int accumulate,
+                 void* workspace, size_t workspace_bytes, void* stream) {
+  return launch_fcs_dense(dtype, tensor, order, dims, last_begin, last_count, sketch_count,
+                          packed, hash_lens, out, accumulate, workspace, workspace_bytes,
+                          as_stream(stream));
+}
+
+int st_fcs_dense_host(int dtype, const void* host_tensor, size_t order, const size_t* dims,
+                      size_t sketch_count, const uint64_t* master_seeds, const size_t* hash_lens,
+                      double* host_out) {
+  FCS_CHECK_ARG(dtype == ST_F32 || dtype == ST_F64, "st_fcs_dense_host: unknown dtype");
+  FCS_CHECK_ARG(order >= 1 && order <= ST_MAX_ORDER, "fcs_sketch: unsupported tensor order");
+  size_t total = 1, sum_dims = 0, sum_j = 0;
+  for (size_t n = 0; n < order; ++n) {
+    FCS_CHECK_ARG(dims[n] > 0 && hash_lens[n] > 0, "HashPair: dimensions must be positive");
+    total *= dims[n];
+    sum_dims += dims[n];
+    sum_j += hash_lens[n];
+  }
+  const size_t jt = sum_j - order + 1;
+  const size_t esz = dtype == ST_F32 ? 4 : 8;
+  cudaStream_t st;
+  FCS_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamDestroy(s); }
+  } guard{st};
+  DevBuf dt, dtab, dout, dws;
+  if (int rc = dt.alloc(total * esz)) return rc;
+  if (int rc = dtab.alloc(sketch_count * sum_dims * sizeof(uint32_t))) return rc;
+  if (int rc = dout.alloc(sketch_count * jt * sizeof(double))) return rc;
+  const size_t ws =
+      st_fcs_dense_workspace(dtype, order, dims, dims[order - 1], sketch_count, hash_lens);
+  if (int rc = dws.alloc(ws)) return rc;
+  FCS_CUDA_TRY(cudaMemcpyAsync(dt.p, host_tensor, total * esz, cudaMemcpyHostToDevice, st));
+  if (int rc = st_family_tables(order, dims, hash_lens, sketch_count, master_seeds,
+                                static_cast<uint32_t*>(dtab.p), st))
+    return rc;
+  if (int rc = st_fcs_dense(dtype, dt.p, order, dims, 0, dims[order - 1], sketch_count,
+                            static_cast<uint32_t*>(dtab.p), hash_lens,
+                            static_cast<double*>(dout.p), 0, dws.p, ws, st))
+    return rc;
+  FCS_CUDA_TRY(cudaMemcpyAsync(host_out, dout.p, sketch_count * jt * sizeof(double),
+                               cudaMemcpyDeviceToHost, st));
+  FCS_CUDA_TRY(cudaStreamSynchronize(st));
+  return ST_OK;
+}
+
+int st_host_gaussian(uint64_t seed, size_t n, double* out, int threads) {
+  // Pair p consumes draws 2p+1 (u1) and 2p+2 (u2) and yields (r cos, r sin):
+  // exactly the serial next_gaussian sequence (rng.cpp:8-21), host libm.
+  const size_t pairs = (n + 1) / 2;
+  auto work = [&](size_t p0, size_t p1) {
+    for (size_t p = p0; p < p1; ++p) {
+      const uint64_t d1 = splitmix_draw(seed, 2 * p + 1);
+      const uint64_t d2 = splitmix_draw(seed, 2 * p + 2);
+      const double u1 = static_cast<double>((d1 >> 11) + 1) * 0x1.0p-53;
+      const double u2 = static_cast<double>(d2 >> 11) * 0x1.0p-53;
+      const double radius = std::sqrt(-2.0 * std::log(u1));
+      const double angle = 2.0 * std::numbers::pi * u2;
+      out[2 * p] = radius * std::cos(angle);
+      if (2 * p + 1 < n) out[2 * p + 1] = radius * std::sin(angle);
+    }
+  };
+  if (threads <= 0) threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  if (pairs < (1u << 16) || threads == 1) {
+    work(0, pairs);
+    return ST_OK;
+  }
+  std::vector<std::thread> pool;
+  const size_t per = (pairs + threads - 1) / threads;
+  for (int t = 0; t < threads; ++t) {
+    const size_t p0 = std::min(pairs, t * per), p1 = std::min(pairs, p0 + per);
+    pool.emplace_back(work, p0, p1);
+  }
+  for (auto& th : pool) th.join();
+  return ST_OK;
+}
+
+int st_device_gaussian(int dtype, uint64_t seed, size_t n, void* out, void* stream) {
+  FCS_CHECK_ARG(dtype == ST_F32 || dtype == ST_F64, "st_device_gaussian: unknown dtype");
+  return launch_device_gaussian(dtype, seed, n, out, as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,314 @@
+// Shared-memory fp64 FFT for the spectral FCS paths (sm_100a).
+//
+// Real sequences of length M (zero-padded sketches) are transformed as
+// complex sequences of P = M/2 points (z[j] = x[2j] + i x[2j+1]) with an
+// in-place mixed-radix decimation-in-frequency Cooley-Tukey over radices
+// {3, 16, 8, 4, 2}: each butterfly reads R slots and writes its results back
+// to the same slots, so passes need one barrier and no second buffer, and
+// the spectrum comes out in digit-reversed slot order. Every spectrum in the
+// library (cached tensor spectra, factor spectra, products) lives in that
+// same slot order, so pointwise products never permute; the inverse
+// (decimation-in-time, the exact reverse of the forward passes) returns
+// natural order. r2c_post / c2r_pre convert between the packed P-point
+// transform and the Hermitian half spectrum X[0..P] of the length-M real
+// transform; slot pos(0) holds the two real bins (X[0], X[P]).
+//
+// Reference semantics (fft.cpp:42-84): dft zero-pads to n = J~ and the
+// inverse is normalised by 1/n. Padding to any M >= J~ leaves every value the
+// reference reads unchanged (linear convolution support [0, J~-1]; the
+// correlation read z[h] only touches lags < J~; Parseval dot over [0, J~-1]).
+#pragma once
+
+#include "common.cuh"
+
+namespace fcs {
+
+constexpr int kFftMaxPasses = 10;
+constexpr int kTwLoBits = 6;  // two-level twiddle table: w_M^e = lo[e & 63] * hi[e >> 6]
+constexpr int kFftThreads = 256;
+constexpr int kMaxFftM = 12288;  // largest supported padded length (P = 6144)
+
+struct FftPlan {
+  int M;                       // real transform length (even)
+  int P;                       // complex points = M / 2
+  int npass;
+  int radix[kFftMaxPasses];    // DIF order
+  int len[kFftMaxPasses];      // sub-transform length L entering each pass
+  int hi_count;                // entries of the hi table (= M >> kTwLoBits, rounded up)
+  const double2* tw;           // device: lo[64] then hi[hi_count]
+  const int* f2p;              // device: slot position of frequency k, k in [0, P)
+};
+
+__device__ __forceinline__ uint32_t swz(uint32_t s) { return s ^ ((s >> 4) & 7u); }
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+// multiply by sign * i
+__device__ __forceinline__ double2 cmul_si(double2 a, double sign) { return make_double2(-sign * a.y, sign * a.x); }
+
+// w_M^e = exp(-2 pi i e / M) for 0 <= e < M (forward convention).
+__device__ __forceinline__ double2 twiddle(const double2* tw, int hi_off, uint32_t e) {
+  return cmul(tw[e & ((1u << kTwLoBits) - 1)], tw[hi_off + (e >> kTwLoBits)]);
+}
+
+// ------------------------------------------------------ in-register DFTs
+// cos(2 pi k / 16); sin(2 pi k / 16) = cos16(k - 4). Folds to constants once
+// the butterfly loops are unrolled.
+__host__ __device__ constexpr double cos16(int k) {
+  constexpr double t[16] = {1.0,
+                            0.92387953251128675613,
+                            0.70710678118654752440,
+                            0.38268343236508977173,
+                            0.0,
+                            -0.38268343236508977173,
+                            -0.70710678118654752440,
+                            -0.92387953251128675613,
+                            -1.0,
+                            -0.92387953251128675613,
+                            -0.70710678118654752440,
+                            -0.38268343236508977173,
+                            0.0,
+                            0.38268343236508977173,
+                            0.70710678118654752440,
+                            0.92387953251128675613};
+  return t[k & 15];
+}
+
+// y[k] = sum_r x[r] exp(sign * 2 pi i r k / R), sign = -1 forward.
+template <int R>
+struct RegDft {
+  static __device__ __forceinline__ void run(double2* x, double sign) {
+    constexpr int H = R / 2;
+    double2 e[H], o[H];
+#pragma unroll
+    for (int r = 0; r < H; ++r) {
+      e[r] = x[2 * r];
+      o[r] = x[2 * r + 1];
+    }
+    RegDft<H>::run(e, sign);
+    RegDft<H>::run(o, sign);
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+      // w_R^k = exp(sign * 2 pi i k / R) from the 16th-root table
+      const int q = k * (16 / R);
+      const double2 w = make_double2(cos16(q), sign * cos16(q - 4));
+      const double2 t = (k == 0) ? o[k] : cmul(w, o[k]);
+      x[k] = cadd(e[k], t);
+      x[k + H] = csub(e[k], t);
+    }
+  }
+};
+
+template <>
+struct RegDft<1> {
+  static __device__ __forceinline__ void run(double2*, double) {}
+};
+
+template <>
+struct RegDft<2> {
+  static __device__ __forceinline__ void run(double2* x, double) {
+    const double2 a = x[0], b = x[1];
+    x[0] = cadd(a, b);
+    x[1] = csub(a, b);
+  }
+};
+
+template <>
+struct RegDft<4> {
+  static __device__ __forceinline__ void run(double2* x, double sign) {
+    const double2 s02 = cadd(x[0], x[2]), d02 = csub(x[0], x[2]);
+    const double2 s13 = cadd(x[1], x[3]), d13 = cmul_si(csub(x[1], x[3]), sign);
+    x[0] = cadd(s02, s13);
+    x[2] = csub(s02, s13);
+    x[1] = cadd(d02, d13);
+    x[3] = csub(d02, d13);
+  }
+};
+
+template <>
+struct RegDft<3> {
+  static __device__ __forceinline__ void run(double2* x, double sign) {
+    constexpr double kS = 0.86602540378443864676372317075294;  // sqrt(3)/2
+    const double2 t = cadd(x[1], x[2]);
+    const double2 u = cmul_si(csub(x[1], x[2]), sign * kS);
+    const double2 m = make_double2(x[0].x - 0.5 * t.x, x[0].y - 0.5 * t.y);
+    x[0] = cadd(x[0], t);
+    x[1] = cadd(m, u);
+    x[2] = csub(m, u);
+  }
+};
+
+// ----------------------------------------------------- block-wide passes
+// One radix-R pass over all butterflies of sub-transforms of length L.
+// Forward (DIF): DFT then twiddle w_L^{j r'}; inverse (DIT): conj twiddle then DFT.
+template <int R, bool kForward>
+__device__ __forceinline__ void fft_pass(double2* buf, const double2* tw, int hi_off, int M, int P,
+                                         int L) {
+  const int stride = L / R;
+  const int nbfly = P / R;
+  const uint32_t tw_scale = static_cast<uint32_t>(M / L);  // w_L = w_M^{M/L}
+  for (int b = threadIdx.x; b < nbfly; b += blockDim.x) {
+    const int blk = b / stride;
+    const int j = b - blk * stride;
+    const int base = blk * L + j;
+    double2 x[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r] = buf[swz(base + r * stride)];
+    if (kForward) {
+      RegDft<R>::run(x, -1.0);
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        const uint32_t e = static_cast<uint32_t>(j * r) * tw_scale;
+        if (e) x[r] = cmul(x[r], twiddle(tw, hi_off, e));
+      }
+    } else {
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        const uint32_t e = static_cast<uint32_t>(j * r) * tw_scale;
+        if (e) x[r] = cmul(x[r], cconj(twiddle(tw, hi_off, e)));
+      }
+      RegDft<R>::run(x, +1.0);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) buf[swz(base + r * stride)] = x[r];
+  }
+}
+
+template <bool kForward>
+__device__ __forceinline__ void fft_dispatch(double2* buf, const double2* tw, int hi_off, int M,
+                                             int P, int radix, int L) {
+  switch (radix) {
+    case 16: fft_pass<16, kForward>(buf, tw, hi_off, M, P, L); break;
+    case 8: fft_pass<8, kForward>(buf, tw, hi_off, M, P, L); break;
+    case 4: fft_pass<4, kForward>(buf, tw, hi_off, M, P, L); break;
+    case 3: fft_pass<3, kForward>(buf, tw, hi_off, M, P, L); break;
+    default: fft_pass<2, kForward>(buf, tw, hi_off, M, P, L); break;
+  }
+}
+
+// Natural-order packed input -> digit-reversed spectrum (unnormalised, e^{-i}).
+__device__ __forceinline__ void fft_forward(double2* buf, const FftPlan& pl, const double2* tw) {
+  for (int p = 0; p < pl.npass; ++p) {
+    fft_dispatch<true>(buf, tw, 1 << kTwLoBits, pl.M, pl.P, pl.radix[p], pl.len[p]);
+    __syncthreads();
+  }
+}
+
+// Digit-reversed spectrum -> natural order (unnormalised, e^{+i}).
+__device__ __forceinline__ void fft_inverse(double2* buf, const FftPlan& pl, const double2* tw) {
+  for (int p = pl.npass - 1; p >= 0; --p) {
+    fft_dispatch<false>(buf, tw, 1 << kTwLoBits, pl.M, pl.P, pl.radix[p], pl.len[p]);
+    __syncthreads();
+  }
+}
+
+// Packed P-point spectrum Z -> Hermitian half spectrum X of the M-point real
+// transform (in place, pairs (k, P-k) per thread; slot pos(0) = (X0, XP)).
+__device__ __forceinline__ void r2c_post(double2* buf, const FftPlan& pl, const double2* tw) {
+  const int hi_off = 1 << kTwLoBits;
+  const int half = pl.P / 2;
+  for (int k = threadIdx.x; k <= half; k += blockDim.x) {
+    if (k == 0) {
+      const uint32_t s0 = swz(__ldg(pl.f2p));
+      const double2 z = buf[s0];
+      buf[s0] = make_double2(z.x + z.y, z.x - z.y);
+      continue;
+    }
+    const int kn = pl.P - k;
+    const uint32_t sa = swz(__ldg(pl.f2p + k)), sb = swz(__ldg(pl.f2p + kn));
+    const double2 za = buf[sa], zb = buf[sb];
+    // E = (Z[k] + conj Z[P-k]) / 2, O = (Z[k] - conj Z[P-k]) / (2i)
+    const double2 e = make_double2(0.5 * (za.x + zb.x), 0.5 * (za.y - zb.y));
+    const double2 o = make_double2(0.5 * (za.y + zb.y), -0.5 * (za.x - zb.x));
+    const double2 wo = cmul(twiddle(tw, hi_off, static_cast<uint32_t>(k)), o);
+    const double2 xa = cadd(e, wo);              // X[k]
+    const double2 xb = cconj(csub(e, wo));       // X[P-k]
+    buf[sa] = xa;
+    if (kn != k) buf[sb] = xb;
+  }
+}
+
+// Inverse of r2c_post: Hermitian half spectrum X -> packed Z with
+// Z = DFT_P(x_even + i x_odd); after fft_inverse, slot j holds P*(x[2j] + i x[2j+1]).
+__device__ __forceinline__ void c2r_pre(double2* buf, const FftPlan& pl, const double2* tw) {
+  const int hi_off = 1 << kTwLoBits;
+  const int half = pl.P / 2;
+  for (int k = threadIdx.x; k <= half; k += blockDim.x) {
+    if (k == 0) {
+      const uint32_t s0 = swz(__ldg(pl.f2p));
+      const double2 x = buf[s0];  // (X0, XP), both real
+      const double e = 0.5 * (x.x + x.y), o = 0.5 * (x.x - x.y);
+      buf[s0] = make_double2(e, o);
+      continue;
+    }
+    const int kn = pl.P - k;
+    const uint32_t sa = swz(__ldg(pl.f2p + k)), sb = swz(__ldg(pl.f2p + kn));
+    const double2 xa = buf[sa], xb = buf[sb];
+    const double2 e = make_double2(0.5 * (xa.x + xb.x), 0.5 * (xa.y - xb.y));  // (X[k] + conj X[P-k]) / 2
+    const double2 dif = make_double2(0.5 * (xa.x - xb.x), 0.5 * (xa.y + xb.y)); // (X[k] - conj X[P-k]) / 2
+    const double2 o = cmul(dif, cconj(twiddle(tw, hi_off, static_cast<uint32_t>(k))));
+    // Z[k] = E + i O ; Z[P-k] = conj(E) + i conj(O)
+    buf[sa] = make_double2(e.x - o.y, e.y + o.x);
+    if (kn != k) buf[sb] = make_double2(e.x + o.y, -e.y + o.x);
+  }
+}
+
+// Zero the P packed slots.
+__device__ __forceinline__ void zero_slots(double2* buf, int P) {
+  for (int s = threadIdx.x; s < P; s += blockDim.x) buf[s] = make_double2(0.0, 0.0);
+}
+
+// Real value x[t] of a natural-order packed buffer.
+__device__ __forceinline__ double& packed_real(double2* buf, uint32_t t) {
+  double2& s = buf[swz(t >> 1)];
+  return (t & 1u) ? s.y : s.x;
+}
+
+// Loads the twiddle table into shared memory (lo then hi).
+__device__ __forceinline__ void load_twiddles(double2* sm_tw, const FftPlan& pl) {
+  const int n = (1 << kTwLoBits) + pl.hi_count;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sm_tw[i] = pl.tw[i];
+}
+
+// Pointwise helpers on the half-spectrum slot layout (slot 0 holds two reals).
+__device__ __forceinline__ double2 hmul(double2 a, double2 b, bool slot0) {
+  return slot0 ? make_double2(a.x * b.x, a.y * b.y) : cmul(a, b);
+}
+__device__ __forceinline__ double2 hconj(double2 a, bool slot0) { return slot0 ? a : cconj(a); }
+
+// Shared-memory bytes a spectral kernel with this plan needs (buffer + twiddles).
+inline size_t fft_smem_bytes(const FftPlan& pl) {
+  return static_cast<size_t>(pl.P) * sizeof(double2) +
+         static_cast<size_t>((1 << kTwLoBits) + pl.hi_count) * sizeof(double2);
+}
+
+// Host: plan for the smallest supported M >= min_len (cached per device).
+int get_fft_plan(size_t min_len, FftPlan* out);
+
+// Kernel argument blocks shared by spectral.cu (kernels) and engine.cu (host).
+struct CpArgs {
+  int order;
+  int dims[ST_MAX_ORDER];
+  int tab_off[ST_MAX_ORDER];
+  int fam_stride;
+  const double* factors[ST_MAX_ORDER];  // I_n x R column-major
+  const double* weights;
+  int r_begin;
+  int r_count;
+};
+
+struct EngArgs {
+  int dims[3];
+  int tab_off[3];
+  int fam_stride;
+  int D;
+  const uint32_t* packed;  // D families x 3 modes, packed tables
+  const double2* spec;     // D x P cached spectra S_d (slot order)
+};
+
+}  // namespace fcs

@@ -1,0 +1,99 @@
+// Host-side FFT plans: padded length choice, radix schedule, twiddle table
+// and frequency -> slot map, cached per (device, M).
+#include <cmath>
+#include <map>
+#include <mutex>
+#include <utility>
+#include <vector>
+
+#include "fft.cuh"
+
+namespace fcs {
+
+namespace {
+
+// Smallest M >= n (M even, M = 2^a 3^b with b <= 2) not above kMaxFftM.
+int choose_m(size_t n) {
+  int best = 0;
+  for (int b3 = 1; b3 <= 9; b3 *= 3) {
+    for (long m = 2L * b3; m <= kMaxFftM; m *= 2) {
+      if (m >= static_cast<long>(n) && m >= 32 && (best == 0 || m < best)) best = static_cast<int>(m);
+    }
+  }
+  return best;
+}
+
+// Slot position -> frequency for the DIF schedule (radices in pass order):
+// freq(p) = r' + R * freq_sub(p mod (L/R)) with r' = p / (L/R).
+int freq_of(int p, const std::vector<int>& radix, size_t level, int L) {
+  if (level == radix.size() || L == 1) return 0;
+  const int R = radix[level];
+  const int sub = L / R;
+  return p / sub + R * freq_of(p % sub, radix, level + 1, sub);
+}
+
+}  // namespace
+
+int get_fft_plan(size_t min_len, FftPlan* out) {
+  const int M = choose_m(min_len);
+  if (M == 0)
+    return fail(ST_EINVAL, "fft: composed length " + std::to_string(min_len) +
+                               " exceeds the shared-memory FFT limit " + std::to_string(kMaxFftM));
+  int dev = 0;
+  FCS_CUDA_TRY(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, FftPlan> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find({dev, M});
+  if (it != cache.end()) {
+    *out = it->second;
+    return ST_OK;
+  }
+  FftPlan pl{};
+  pl.M = M;
+  pl.P = M / 2;
+  // radix schedule: 3s first, then 16s, then the remainder
+  std::vector<int> radix;
+  int rem = pl.P;
+  while (rem % 3 == 0) {
+    radix.push_back(3);
+    rem /= 3;
+  }
+  while (rem % 16 == 0) {
+    radix.push_back(16);
+    rem /= 16;
+  }
+  if (rem > 1) radix.push_back(rem);  // 8, 4 or 2
+  pl.npass = static_cast<int>(radix.size());
+  int L = pl.P;
+  for (int p = 0; p < pl.npass; ++p) {
+    pl.radix[p] = radix[p];
+    pl.len[p] = L;
+    L /= radix[p];
+  }
+  pl.hi_count = (M + (1 << kTwLoBits) - 1) >> kTwLoBits;
+  std::vector<double2> tw((1 << kTwLoBits) + pl.hi_count);
+  auto root = [M](long e) {
+    // exp(-2 pi i e / M), angle reduced exactly in integers first
+    const long r = e % M;
+    const long double ang = -2.0L * 3.141592653589793238462643383279502884L * r / M;
+    return make_double2(static_cast<double>(std::cos(ang)), static_cast<double>(std::sin(ang)));
+  };
+  for (int e = 0; e < (1 << kTwLoBits); ++e) tw[e] = root(e);
+  for (int e = 0; e < pl.hi_count; ++e) tw[(1 << kTwLoBits) + e] = root(static_cast<long>(e) << kTwLoBits);
+  std::vector<int> f2p(pl.P);
+  for (int p = 0; p < pl.P; ++p) f2p[freq_of(p, radix, 0, pl.P)] = p;
+  double2* dtw = nullptr;
+  int* df2p = nullptr;
+  FCS_CUDA_TRY(cudaMalloc(&dtw, tw.size() * sizeof(double2)));
+  FCS_CUDA_TRY(cudaMalloc(&df2p, f2p.size() * sizeof(int)));
+  FCS_CUDA_TRY(cudaMemcpy(dtw, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  FCS_CUDA_TRY(cudaMemcpy(df2p, f2p.data(), f2p.size() * sizeof(int), cudaMemcpyHostToDevice));
+  pl.tw = dtw;
+  pl.f2p = df2p;
+  cache[{dev, M}] = pl;
+  *out = pl;
+  return ST_OK;
+}
+
+}  // namespace fcs

@@ -1,0 +1,486 @@
+// Spectral FCS kernels (K2-K9): CP-form FCS, batched linear convolution,
+// and the sketched-contraction estimators T(I,a,b) / T(u,v,w) with the D
+// families batched per launch, all built on the shared-memory FFT of fft.cuh.
+//
+// One CTA owns one (item, family) transform; every real sequence is count-
+// sketched straight into the CTA's shared FFT buffer (K2 fused into the FFT
+// prologue), and products / sums over rank happen in the frequency domain
+// (K4) so each output needs a single inverse transform (K5).
+#include <algorithm>
+
+#include "fft.cuh"
+
+namespace fcs {
+
+namespace {
+
+__device__ __forceinline__ int tid() { return threadIdx.x; }
+
+// Shared memory carve-up: twiddles, then the P-slot FFT buffer, then a
+// 32-double reduction scratch.
+struct Smem {
+  double2* tw;
+  double2* buf;
+  double* red;
+};
+
+__device__ __forceinline__ Smem carve(const FftPlan& pl) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem s;
+  s.tw = reinterpret_cast<double2*>(smem_raw);
+  s.buf = s.tw + (1 << kTwLoBits) + pl.hi_count;
+  s.red = reinterpret_cast<double*>(s.buf + pl.P);
+  return s;
+}
+
+// Count sketch of vec[0..I) under a packed pair, scattered into the packed
+// real buffer (cs_sketch, sketch.cpp:105-116: zeros skipped), then the
+// length-M real transform -> half spectrum in slot order.
+__device__ void rfft_of_cs(const Smem& sm, const FftPlan& pl, const double* __restrict__ vec,
+                           int I, const uint32_t* __restrict__ tab) {
+  zero_slots(sm.buf, pl.P);
+  __syncthreads();
+  for (int i = tid(); i < I; i += blockDim.x) {
+    const double v = vec[i];
+    if (v != 0.0) {
+      const uint32_t e = __ldg(tab + i);
+      atomicAdd(&packed_real(sm.buf, e & 0x7fffffffu), (e >> 31) ? -v : v);
+    }
+  }
+  __syncthreads();
+  fft_forward(sm.buf, pl, sm.tw);
+  r2c_post(sm.buf, pl, sm.tw);
+  __syncthreads();
+}
+
+// Zero-padded real x[0..len) -> half spectrum (dft, fft.cpp:42-51).
+__device__ void rfft_of_real(const Smem& sm, const FftPlan& pl, const double* __restrict__ x,
+                             int len) {
+  for (int s = tid(); s < pl.P; s += blockDim.x) {
+    const int t = 2 * s;
+    sm.buf[swz(s)] = make_double2(t < len ? x[t] : 0.0, t + 1 < len ? x[t + 1] : 0.0);
+  }
+  __syncthreads();
+  fft_forward(sm.buf, pl, sm.tw);
+  r2c_post(sm.buf, pl, sm.tw);
+  __syncthreads();
+}
+
+// Half spectrum already in sm.buf -> natural-order real sequence scaled by P
+// (caller divides by P; idft_real's 1/n, fft.cpp:61-66).
+__device__ void irfft_in_place(const Smem& sm, const FftPlan& pl) {
+  __syncthreads();
+  c2r_pre(sm.buf, pl, sm.tw);
+  __syncthreads();
+  fft_inverse(sm.buf, pl, sm.tw);
+}
+
+__device__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (warp == 0) {
+    t = lane < static_cast<int>(blockDim.x >> 5) ? red[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  }
+  return t;  // valid in thread 0
+}
+
+}  // namespace
+
+// --------------------------------------------------------------- kernels
+__global__ void __launch_bounds__(kFftThreads) spec_from_real_kernel(FftPlan pl, const double* x,
+                                                                     size_t ldx, int len,
+                                                                     double2* spec) {
+  const Smem sm = carve(pl);
+  load_twiddles(sm.tw, pl);
+  __syncthreads();
+  rfft_of_real(sm, pl, x + blockIdx.x * ldx, len);
+  double2* o = spec + static_cast<size_t>(blockIdx.x) * pl.P;
+  for (int s = tid(); s < pl.P; s += blockDim.x) o[s] = sm.buf[swz(s)];
+}
+
+__global__ void __launch_bounds__(kFftThreads) real_from_spec_kernel(FftPlan pl,
+                                                                     const double2* spec,
+                                                                     double* out, size_t ldo,
+                                                                     int out_len, int accumulate) {
+  const Smem sm = carve(pl);
+  load_twiddles(sm.tw, pl);
+  const double2* in = spec + static_cast<size_t>(blockIdx.x) * pl.P;
+  for (int s = tid(); s < pl.P; s += blockDim.x) sm.buf[swz(s)] = in[s];
+  irfft_in_place(sm, pl);
+  const double inv = 1.0 / pl.P;
+  double* o = out + blockIdx.x * ldo;
+  for (int t = tid(); t < out_len; t += blockDim.x) {
+    const double v = packed_real(sm.buf, t) * inv;
+    o[t] = accumulate ? o[t] + v : v;
+  }
+}
+
+// K2-K4: per (rank r, family d) the product of the mode spectra times w_r.
+__global__ void __launch_bounds__(kFftThreads) cp_rank_kernel(FftPlan pl, CpArgs a,
+                                                              const uint32_t* __restrict__ packed,
+                                                              double2* __restrict__ Q) {
+  const Smem sm = carve(pl);
+  load_twiddles(sm.tw, pl);
+  const int rl = blockIdx.x, d = blockIdx.y;
+  const int r = a.r_begin + rl;
+  const double w = a.weights[r];
+  double2* q = Q + (static_cast<size_t>(d) * a.r_count + rl) * pl.P;
+  const uint32_t* tab = packed + static_cast<size_t>(d) * a.fam_stride;
+  if (w == 0.0) return;  // convolved_cp_sketch skips zero weights (sketch.cpp:75)
+  for (int n = 0; n < a.order; ++n) {
+    __syncthreads();
+    rfft_of_cs(sm, pl, a.factors[n] + static_cast<size_t>(r) * a.dims[n], a.dims[n],
+               tab + a.tab_off[n]);
+    for (int s = tid(); s < pl.P; s += blockDim.x) {
+      const double2 v = sm.buf[swz(s)];
+      double2 acc = n == 0 ? v : hmul(q[s], v, s == 0);
+      if (n == a.order - 1) acc = cscale(acc, w);
+      q[s] = acc;
+    }
+  }
+}
+
+// K4-K5: fixed-order sum over ranks per family, one inverse transform, first J~ values.
+__global__ void __launch_bounds__(kFftThreads) cp_sum_kernel(FftPlan pl,
+                                                             const double2* __restrict__ Q,
+                                                             const double* weights, int r_begin,
+                                                             int r_count, double* out, int jt,
+                                                             int accumulate) {
+  const Smem sm = carve(pl);
+  load_twiddles(sm.tw, pl);
+  const int d = blockIdx.x;
+  for (int s = tid(); s < pl.P; s += blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int rl = 0; rl < r_count; ++rl) {
+      if (weights[r_begin + rl] == 0.0) continue;
+      acc = cadd(acc, Q[(static_cast<size_t>(d) * r_count + rl) * pl.P + s]);
+    }
+    sm.buf[swz(s)] = acc;
+  }
+  irfft_in_place(sm, pl);
+  const double inv = 1.0 / pl.P;
+  double* o = out + static_cast<size_t>(d) * jt;
+  for (int t = tid(); t < jt; t += blockDim.x) {
+    const double v = packed_real(sm.buf, t) * inv;
+    o[t] = accumulate ? o[t] + v : v;
+  }
+}
+
+// Linear convolution of row pairs: out[b] = a[b] (*) b[b] (fft_convolve, fft.cpp:75-84).
+__global__ void __launch_bounds__(kFftThreads) conv_kernel(FftPlan pl, const double* a, int la,
+                                                           size_t lda, const double* b, int lb,
+                                                           size_t ldb, double2* scratch,
+                                                           double* out, size_t ldo) {
+  const Smem sm = carve(pl);
+  load_twiddles(sm.tw, pl);
+  __syncthreads();
+  const int item = blockIdx.x;
+  double2* scr = scratch + static_cast<size_t>(item) * pl.P;
+  rfft_of_real(sm, pl, a + item * lda, la);
+  for (int s = tid(); s < pl.P; s += blockDim.x) scr[s] = sm.buf[swz(s)];
+  __syncthreads();
+  rfft_of_real(sm, pl, b + item * ldb, lb);
+  for (int s = tid(); s < pl.P; s += blockDim.x) sm.buf[swz(s)] = hmul(scr[s], sm.buf[swz(s)], s == 0);
+  irfft_in_place(sm, pl);
+  const double inv = 1.0 / pl.P;
+  const int lo = la + lb - 1;
+  double* o = out + item * ldo;
+  for (int t = tid(); t < lo; t += blockDim.x) o[t] = packed_real(sm.buf, t) * inv;
+}
+
+// K6: z = IFFT(S_d conj(F cs_a) conj(F cs_b)); est = s_f(i) z[h_f(i)]
+// (iuv_spectral, estimators.cpp:66-90). Grid (batch, D).
+__global__ void __launch_bounds__(kFftThreads) iuv_kernel(FftPlan pl, EngArgs e, const double* A,
+                                                          const double* B, int c1, int c2, int f,
+                                                          double2* scratch, double* est) {
+  const Smem sm = carve(pl);
+  load_twiddles(sm.tw, pl);
+  __syncthreads();
+  const int b = blockIdx.x, d = blockIdx.y;
+  const size_t item = static_cast<size_t>(b) * e.D + d;
+  double2* scr = scratch + item * pl.P;
+  const uint32_t* tab = e.packed + static_cast<size_t>(d) * e.fam_stride;
+  const double2* S = e.spec + static_cast<size_t>(d) * pl.P;
+  rfft_of_cs(sm, pl, A + static_cast<size_t>(b) * e.dims[c1], e.dims[c1], tab + e.tab_off[c1]);
+  for (int s = tid(); s < pl.P; s += blockDim.x) scr[s] = sm.buf[swz(s)];
+  __syncthreads();
+  rfft_of_cs(sm, pl, B + static_cast<size_t>(b) * e.dims[c2], e.dims[c2], tab + e.tab_off[c2]);
+  for (int s = tid(); s < pl.P; s += blockDim.x) {
+    const bool s0 = s == 0;
+    const double2 ab = hmul(scr[s], sm.buf[swz(s)], s0);
+    sm.buf[swz(s)] = hmul(S[s], hconj(ab, s0), s0);
+  }
+  irfft_in_place(sm, pl);
+  const double inv = 1.0 / pl.P;
+  const int nf = e.dims[f];
+  const uint32_t* tf = tab + e.tab_off[f];
+  double* o = est + item * nf;
+  for (int i = tid(); i < nf; i += blockDim.x) {
+    const uint32_t t = __ldg(tf + i);
+    const double z = packed_real(sm.buf, t & 0x7fffffffu) * inv;
+    o[i] = (t >> 31) ? -z : z;
+  }
+}
+
+// K7: (1/M) sum_k Re(S_d conj(F cs_u F cs_v F cs_w)) (uvw_spectral + spectral_dot,
+// estimators.cpp:38-64). Grid (batch, D); est[b][d].
+__global__ void __launch_bounds__(kFftThreads) uvw_kernel(FftPlan pl, EngArgs e, const double* U,
+                                                          const double* V, const double* W,
+                                                          double2* scratch, double* est) {
+  const Smem sm = carve(pl);
+  load_twiddles(sm.tw, pl);
+  __syncthreads();
+  const int b = blockIdx.x, d = blockIdx.y;
+  const size_t item = static_cast<size_t>(b) * e.D + d;
+  double2* scr = scratch + item * pl.P;
+  const uint32_t* tab = e.packed + static_cast<size_t>(d) * e.fam_stride;
+  const double2* S = e.spec + static_cast<size_t>(d) * pl.P;
+  const double* vecs[3] = {U + static_cast<size_t>(b) * e.dims[0],
+                           V + static_cast<size_t>(b) * e.dims[1],
+                           W + static_cast<size_t>(b) * e.dims[2]};
+  double acc = 0.0;
+  for (int n = 0; n < 3; ++n) {
+    __syncthreads();
+    rfft_of_cs(sm, pl, vecs[n], e.dims[n], tab + e.tab_off[n]);
+    for (int s = tid(); s < pl.P; s += blockDim.x) {
+      const double2 v = sm.buf[swz(s)];
+      if (n == 0) {
+        scr[s] = v;
+      } else if (n == 1) {
+        scr[s] = hmul(scr[s], v, s == 0);
+      } else {
+        const double2 g = hmul(scr[s], v, s == 0);
+        const double2 sd = S[s];
+        const double re = sd.x * g.x + sd.y * g.y;  // Re(S conj(G)) / (X0*G0 + XP*GP at slot 0)
+        acc += s == 0 ? re : 2.0 * re;
+      }
+    }
+  }
+  const double tot = block_sum(acc, sm.red);
+  if (threadIdx.x == 0) est[item] = tot / pl.M;
+}
+
+// K9: S_d -= weight * F cs_u F cs_v F cs_w (FcsEngine::deflate, cpd.cpp:79-87, by linearity).
+__global__ void __launch_bounds__(kFftThreads) deflate_kernel(FftPlan pl, EngArgs e, double weight,
+                                                              const double* U, const double* V,
+                                                              const double* W, double2* scratch,
+                                                              double2* spec) {
+  const Smem sm = carve(pl);
+  load_twiddles(sm.tw, pl);
+  __syncthreads();
+  const int d = blockIdx.x;
+  double2* scr = scratch + static_cast<size_t>(d) * pl.P;
+  const uint32_t* tab = e.packed + static_cast<size_t>(d) * e.fam_stride;
+  double2* S = spec + static_cast<size_t>(d) * pl.P;
+  const double* vecs[3] = {U, V, W};
+  for (int n = 0; n < 3; ++n) {
+    __syncthreads();
+    rfft_of_cs(sm, pl, vecs[n], e.dims[n], tab + e.tab_off[n]);
+    for (int s = tid(); s < pl.P; s += blockDim.x) {
+      const double2 v = sm.buf[swz(s)];
+      if (n == 0) {
+        scr[s] = v;
+      } else if (n == 1) {
+        scr[s] = hmul(scr[s], v, s == 0);
+      } else {
+        const double2 g = hmul(scr[s], v, s == 0);
+        S[s] = csub(S[s], cscale(g, weight));
+      }
+    }
+  }
+}
+
+// K8: elementwise median over D (median_reduce, estimators.cpp:117-138):
+// est[b][d][i] -> out[b][i]; even D averages the two middle order statistics.
+__global__ void median_kernel(const double* __restrict__ est, int batch, int D, int len,
+                              double* __restrict__ out) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= batch * len) return;
+  const int b = idx / len, i = idx - b * len;
+  double v[64];
+  for (int d = 0; d < D; ++d) {
+    const double x = est[(static_cast<size_t>(b) * D + d) * len + i];
+    int k = d;
+    while (k > 0 && v[k - 1] > x) {
+      v[k] = v[k - 1];
+      --k;
+    }
+    v[k] = x;
+  }
+  out[idx] = (D & 1) ? v[D / 2] : 0.5 * (v[D / 2 - 1] + v[D / 2]);
+}
+
+// Per-column count sketch into global memory (cs_sketch_columns, sketch.cpp:118-133).
+__global__ void cs_columns_kernel(const double* __restrict__ u, int I, int cols,
+                                  const uint32_t* __restrict__ tab, int J, double* __restrict__ out) {
+  const size_t n = static_cast<size_t>(I) * cols;
+  for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(k % I);
+    const size_t r = k / I;
+    const double v = u[k];
+    if (v == 0.0) continue;
+    const uint32_t e = __ldg(tab + i);
+    atomicAdd(out + r * J + (e & 0x7fffffffu), (e >> 31) ? -v : v);
+  }
+}
+
+// Row normalisation for the batched power iteration: u <- u/||u|| or 0 when
+// ||u|| < 1e-150 (normalize_or_zero, cpd.cpp:208-216). One block per row.
+__global__ void normalize_rows_kernel(double* __restrict__ U, int dim) {
+  __shared__ double red[32];
+  double* u = U + static_cast<size_t>(blockIdx.x) * dim;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < dim; i += blockDim.x) acc += u[i] * u[i];
+  double tot = block_sum(acc, red);
+  __shared__ double norm;
+  if (threadIdx.x == 0) norm = sqrt(tot);
+  __syncthreads();
+  const double nv = norm;
+  for (int i = threadIdx.x; i < dim; i += blockDim.x) u[i] = nv < 1e-150 ? 0.0 : u[i] / nv;
+}
+
+// Refinement step of rtpm (cpd.cpp:266-270): best <- next/||next|| unless the
+// norm underflows, which stops the refinement for good (sticky flag).
+__global__ void refine_update_kernel(double* __restrict__ best, const double* __restrict__ next,
+                                     int dim, int* __restrict__ stopped) {
+  __shared__ double red[32];
+  __shared__ double norm;
+  if (*stopped) return;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < dim; i += blockDim.x) acc += next[i] * next[i];
+  const double tot = block_sum(acc, red);
+  if (threadIdx.x == 0) norm = sqrt(tot);
+  __syncthreads();
+  const double nv = norm;
+  if (nv < 1e-150) {
+    if (threadIdx.x == 0) *stopped = 1;
+    return;
+  }
+  for (int i = threadIdx.x; i < dim; i += blockDim.x) best[i] = next[i] / nv;
+}
+
+// ------------------------------------------------------------ launchers
+namespace {
+
+template <typename K>
+int prep(K kernel, const FftPlan& pl, size_t* smem) {
+  *smem = fft_smem_bytes(pl) + 32 * sizeof(double);
+  FCS_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(*smem)));
+  return ST_OK;
+}
+
+}  // namespace
+
+int launch_spec_from_real(const FftPlan& pl, const double* x, size_t ldx, int len, int items,
+                          double2* spec, cudaStream_t st) {
+  size_t sm;
+  if (int rc = prep(spec_from_real_kernel, pl, &sm)) return rc;
+  spec_from_real_kernel<<<items, kFftThreads, sm, st>>>(pl, x, ldx, len, spec);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+int launch_real_from_spec(const FftPlan& pl, const double2* spec, int items, double* out,
+                          size_t ldo, int out_len, int accumulate, cudaStream_t st) {
+  size_t sm;
+  if (int rc = prep(real_from_spec_kernel, pl, &sm)) return rc;
+  real_from_spec_kernel<<<items, kFftThreads, sm, st>>>(pl, spec, out, ldo, out_len, accumulate);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+int launch_cp(const FftPlan& pl, const CpArgs& a, int D, const uint32_t* packed, double2* Q,
+              double* out, int jt, int accumulate, cudaStream_t st) {
+  size_t sm;
+  if (int rc = prep(cp_rank_kernel, pl, &sm)) return rc;
+  if (a.r_count > 0) {
+    cp_rank_kernel<<<dim3(a.r_count, D), kFftThreads, sm, st>>>(pl, a, packed, Q);
+    FCS_CUDA_TRY(cudaGetLastError());
+  }
+  if (int rc = prep(cp_sum_kernel, pl, &sm)) return rc;
+  cp_sum_kernel<<<D, kFftThreads, sm, st>>>(pl, Q, a.weights, a.r_begin, a.r_count, out, jt,
+                                            accumulate);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+int launch_conv(const FftPlan& pl, const double* a, int la, size_t lda, const double* b, int lb,
+                size_t ldb, int items, double2* scratch, double* out, size_t ldo, cudaStream_t st) {
+  size_t sm;
+  if (int rc = prep(conv_kernel, pl, &sm)) return rc;
+  conv_kernel<<<items, kFftThreads, sm, st>>>(pl, a, la, lda, b, lb, ldb, scratch, out, ldo);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+int launch_iuv(const FftPlan& pl, const EngArgs& e, int batch, const double* A, const double* B,
+               int c1, int c2, int f, double2* scratch, double* est, cudaStream_t st) {
+  size_t sm;
+  if (int rc = prep(iuv_kernel, pl, &sm)) return rc;
+  iuv_kernel<<<dim3(batch, e.D), kFftThreads, sm, st>>>(pl, e, A, B, c1, c2, f, scratch, est);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+int launch_uvw(const FftPlan& pl, const EngArgs& e, int batch, const double* U, const double* V,
+               const double* W, double2* scratch, double* est, cudaStream_t st) {
+  size_t sm;
+  if (int rc = prep(uvw_kernel, pl, &sm)) return rc;
+  uvw_kernel<<<dim3(batch, e.D), kFftThreads, sm, st>>>(pl, e, U, V, W, scratch, est);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+int launch_deflate(const FftPlan& pl, const EngArgs& e, double weight, const double* U,
+                   const double* V, const double* W, double2* scratch, double2* spec,
+                   cudaStream_t st) {
+  size_t sm;
+  if (int rc = prep(deflate_kernel, pl, &sm)) return rc;
+  deflate_kernel<<<e.D, kFftThreads, sm, st>>>(pl, e, weight, U, V, W, scratch, spec);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+int launch_median(const double* est, int batch, int D, int len, double* out, cudaStream_t st) {
+  if (D > 64) return fail(ST_EINVAL, "median_reduce: at most 64 sketches supported");
+  const int n = batch * len;
+  if (n == 0) return ST_OK;
+  median_kernel<<<ceil_div(n, 128), 128, 0, st>>>(est, batch, D, len, out);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+int launch_cs_columns(const double* u, int I, int cols, const uint32_t* tab, int J, double* out,
+                      cudaStream_t st) {
+  FCS_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double) * static_cast<size_t>(J) * cols, st));
+  const size_t n = static_cast<size_t>(I) * cols;
+  if (n == 0) return ST_OK;
+  cs_columns_kernel<<<std::min<unsigned>(ceil_div(n, 256), 4096), 256, 0, st>>>(u, I, cols, tab, J,
+                                                                                 out);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+int launch_normalize_rows(double* U, int rows, int dim, cudaStream_t st) {
+  if (rows == 0) return ST_OK;
+  normalize_rows_kernel<<<rows, 256, 0, st>>>(U, dim);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+int launch_refine_update(double* best, const double* next, int dim, int* stopped,
+                         cudaStream_t st) {
+  refine_update_kernel<<<1, 256, 0, st>>>(best, next, dim, stopped);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+}  // namespace fcs

@@ -1,0 +1,210 @@
+"""ContractionEngine plug-in and the sketched RTPM driver over the B200 C-ABI.
+
+Mirrors ``cpd.hpp:12-84``: ``SketchBackend``, ``ContractionEngine``
+(uvw / iuv / deflate / uuu / iuu / shape), ``make_contraction_engine`` and
+``rtpm``. Only the FCS backend exists on the B200 path (the north star's
+scope); Plain/CS/TS/HCS raise ValueError naming the missing backend, which is
+the reference's own error class for an unusable backend (cpd.cpp:27).
+
+The engine keeps the D sketches' spectra resident on the device
+(``st_engine_*``); batched entry points (``iuv_batch`` / ``uvw_batch``) are
+the GPU-native extension that lets ``rtpm`` run all restarts in lockstep.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import List
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .sketchtensor import (CpTensor, DenseTensor, EstimatorConfig, _check, _dev, _ptr,
+                           _stream)
+
+
+class SketchBackend(enum.Enum):
+    """SketchBackend (cpd.hpp:12), names per cpd.cpp:10-28."""
+    Plain = 0
+    CS = 1
+    TS = 2
+    HCS = 3
+    FCS = 4
+
+
+def backend_name(b: SketchBackend) -> str:
+    return {SketchBackend.Plain: "plain", SketchBackend.CS: "cs", SketchBackend.TS: "ts",
+            SketchBackend.HCS: "hcs", SketchBackend.FCS: "fcs"}[b]
+
+
+def backend_from_name(name: str) -> SketchBackend:
+    for b in SketchBackend:
+        if backend_name(b) == name:
+            return b
+    raise ValueError("unknown backend: " + name)
+
+
+def _vec(x, n: int, op: str) -> torch.Tensor:
+    t = torch.as_tensor(np.asarray(x, np.float64) if not torch.is_tensor(x) else x,
+                        dtype=torch.float64)
+    if t.shape[-1] != n:
+        raise ValueError(f"{op}: vector length mismatch")
+    return t.to(_dev()).contiguous()
+
+
+class ContractionEngine:
+    """ContractionEngine (cpd.hpp:21-41)."""
+
+    def uvw(self, u, v, w) -> float:
+        raise NotImplementedError
+
+    def iuv(self, a, b, free_mode: int):
+        raise NotImplementedError
+
+    def deflate(self, weight: float, u, v, w) -> None:
+        raise NotImplementedError
+
+    def uuu(self, u) -> float:
+        return self.uvw(u, u, u)
+
+    def iuu(self, u):
+        return self.iuv(u, u, 0)
+
+    def shape(self) -> List[int]:
+        raise NotImplementedError
+
+
+class FcsEngine(ContractionEngine):
+    """FcsEngine (cpd.cpp:61-94) on the device: D = cfg.sketch_count families
+    from families_for (estimators.cpp:104-115), sketches built once by K1 and
+    their spectra cached (precompute_fcs, estimators.cpp:140-149)."""
+
+    def __init__(self, t: DenseTensor, cfg: EstimatorConfig):
+        if not isinstance(t, DenseTensor):
+            t = DenseTensor.from_array(t)
+        if t.order() != 3:
+            raise ValueError("make_contraction_engine: order-3 tensor required")
+        if cfg.hash_len == 0 or cfg.sketch_count == 0:
+            raise ValueError("EstimatorConfig: hash_len and sketch_count must be >= 1")
+        self._shape = t.shape()
+        self.cfg = cfg
+        h = C.c_void_p()
+        _check(L.lib().st_engine_create(C.byref(h), t.st_dtype, _ptr(t.flat),
+                                        L.size_array(self._shape), cfg.hash_len,
+                                        cfg.sketch_count, C.c_uint64(cfg.seed & ((1 << 64) - 1)),
+                                        _stream()))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            L.lib().st_engine_destroy(h)
+            self._h = None
+
+    def shape(self) -> List[int]:
+        return list(self._shape)
+
+    def composed_len(self) -> int:
+        return int(L.lib().st_engine_composed_len(self._h))
+
+    def sketches(self) -> torch.Tensor:
+        """Current D x J~ sketch values (after any deflations)."""
+        out = torch.empty((self.cfg.sketch_count, self.composed_len()), dtype=torch.float64,
+                          device=_dev())
+        _check(L.lib().st_engine_sketches(self._h, _ptr(out), _stream()))
+        return out
+
+    # ---- batched (GPU-native) forms
+    def iuv_batch(self, a, b, free_mode: int, median: bool = True) -> torch.Tensor:
+        if free_mode > 2:
+            raise ValueError("estimate_iuv: mode out of range")
+        c1 = 1 if free_mode == 0 else 0
+        c2 = 1 if free_mode == 2 else 2
+        A = _vec(a, self._shape[c1], "estimate_iuv")
+        B = _vec(b, self._shape[c2], "estimate_iuv")
+        A2, B2 = A.reshape(-1, self._shape[c1]), B.reshape(-1, self._shape[c2])
+        if A2.shape[0] != B2.shape[0]:
+            raise ValueError("estimate_iuv: batch mismatch")
+        n = A2.shape[0]
+        shape = (n, self._shape[free_mode]) if median else (n, self.cfg.sketch_count,
+                                                            self._shape[free_mode])
+        out = torch.empty(shape, dtype=torch.float64, device=_dev())
+        _check(L.lib().st_engine_iuv(self._h, n, _ptr(A2), _ptr(B2), free_mode, _ptr(out),
+                                     1 if median else 0, _stream()))
+        return out
+
+    def uvw_batch(self, u, v, w, median: bool = True) -> torch.Tensor:
+        U = _vec(u, self._shape[0], "estimate_uvw").reshape(-1, self._shape[0])
+        V = _vec(v, self._shape[1], "estimate_uvw").reshape(-1, self._shape[1])
+        W = _vec(w, self._shape[2], "estimate_uvw").reshape(-1, self._shape[2])
+        n = U.shape[0]
+        out = torch.empty((n,) if median else (n, self.cfg.sketch_count), dtype=torch.float64,
+                          device=_dev())
+        _check(L.lib().st_engine_uvw(self._h, n, _ptr(U), _ptr(V), _ptr(W), _ptr(out),
+                                     1 if median else 0, _stream()))
+        return out
+
+    # ---- reference interface
+    def uvw(self, u, v, w) -> float:
+        return float(self.uvw_batch(u, v, w)[0].item())
+
+    def iuv(self, a, b, free_mode: int) -> np.ndarray:
+        return self.iuv_batch(a, b, free_mode)[0].cpu().numpy()
+
+    def deflate(self, weight: float, u, v, w) -> None:
+        U = _vec(u, self._shape[0], "deflate")
+        V = _vec(v, self._shape[1], "deflate")
+        W = _vec(w, self._shape[2], "deflate")
+        _check(L.lib().st_engine_deflate(self._h, C.c_double(weight), _ptr(U), _ptr(V), _ptr(W),
+                                         _stream()))
+
+
+def make_contraction_engine(t, backend: SketchBackend, cfg: EstimatorConfig) -> ContractionEngine:
+    """make_contraction_engine (cpd.cpp:220-232)."""
+    if not isinstance(t, DenseTensor):
+        t = DenseTensor.from_array(t)
+    if t.order() != 3:
+        raise ValueError("make_contraction_engine: order-3 tensor required")
+    if backend == SketchBackend.FCS:
+        return FcsEngine(t, cfg)
+    raise ValueError(f"make_contraction_engine: backend '{backend_name(backend)}' is not "
+                     "provided by the B200 FCS library")
+
+
+@dataclass
+class RtpmConfig:
+    """RtpmConfig (cpd.hpp:49-55)."""
+    target_rank: int = 1
+    num_inits: int = 15
+    num_power_iters: int = 20
+    backend: SketchBackend = SketchBackend.FCS
+    estimator: EstimatorConfig = field(default_factory=EstimatorConfig)
+
+
+def rtpm(t, cfg: RtpmConfig) -> CpTensor:
+    """rtpm (cpd.cpp:234-277) with the FCS backend: restarts batched on the
+    device (st_rtpm); same initial-vector stream, argmax rule and deflation."""
+    if not isinstance(t, DenseTensor):
+        t = DenseTensor.from_array(t)
+    if t.order() != 3:
+        raise ValueError("rtpm: order-3 tensor required")
+    dims = t.shape()
+    if dims[0] != dims[1] or dims[1] != dims[2]:
+        raise ValueError("rtpm: cubical tensor required")
+    if cfg.backend != SketchBackend.FCS:
+        raise ValueError(f"make_contraction_engine: backend '{backend_name(cfg.backend)}' is not "
+                         "provided by the B200 FCS library")
+    if cfg.target_rank == 0 or cfg.num_inits == 0 or cfg.num_power_iters == 0:
+        raise ValueError("rtpm: rank, inits, and iterations must be >= 1")
+    dim, R = dims[0], cfg.target_rank
+    w = np.empty(R, np.float64)
+    f = np.empty(dim * R, np.float64)
+    e = cfg.estimator
+    _check(L.lib().st_rtpm(t.st_dtype, _ptr(t.flat), dim, R, cfg.num_inits, cfg.num_power_iters,
+                           e.hash_len, e.sketch_count, C.c_uint64(e.seed & ((1 << 64) - 1)),
+                           w.ctypes.data_as(C.c_void_p), f.ctypes.data_as(C.c_void_p),
+                           _stream()))
+    factor = f.reshape((R, dim)).T
+    return CpTensor(w, [factor, factor, factor])

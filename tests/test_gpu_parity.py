@@ -1,0 +1,313 @@
+"""GPU parity tests: the sm_100a path (through the C-ABI) against the CPU
+oracle (oracle/fcs_oracle.py, pinned to the unmodified reference by
+tests/test_oracle.py) and the golden vectors.
+
+Tolerances: hash tables, bucket indices and integer-valued
+sketches bit-exact; fp64 values |g - c| <= 1e-10 (|c| + ||c||_inf) per entry;
+fp32 inputs 1e-4 on the same rule.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import fcs_oracle as O
+import paper_2106_13062_b200 as st
+from paper_2106_13062_b200 import configs
+
+pytestmark = pytest.mark.gpu
+GOLD = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden.npz"))
+RTOL64, RTOL32 = 1e-10, 1e-4
+
+
+def rel_close(got, want, rtol):
+    got = got.detach().cpu().numpy() if torch.is_tensor(got) else np.asarray(got)
+    want = np.asarray(want)
+    tol = rtol * (np.abs(want) + np.abs(want).max(initial=0.0))
+    err = np.abs(got - want)
+    assert got.shape == want.shape, (got.shape, want.shape)
+    assert np.all(err <= tol), f"max err {err.max()} vs tol {tol.min()}"
+    return True
+
+
+def oracle_family(fam: st.HashFamily):
+    return ([fam.pair(n).bucket_map() for n in range(fam.modes())],
+            [fam.pair(n).sign_map() for n in range(fam.modes())], fam.hash_lens())
+
+
+# ------------------------------------------------------------------ K0
+@pytest.mark.parametrize("I,J,seed", [(100, 1000, 1), (1024, 16384, 0xDEADBEEF), (1, 1, 0),
+                                      (512, 2048, 7), (4097, 3, 2 ** 63 + 5)])
+def test_hash_pair_bitexact(cuda, I, J, seed):
+    p = st.HashPair(I, J, seed)
+    b, s = O.hash_pair(I, J, seed)
+    assert (p.bucket_map() == b).all() and (p.sign_map() == s).all()
+
+
+def test_family_tables_bitexact(cuda):
+    cfg = st.EstimatorConfig(hash_len=3000, sketch_count=10, seed=3)
+    fams = st.families_for([200, 200, 200], cfg)
+    packed = st.packed_families(fams).cpu().numpy().view(np.uint32)
+    want = []
+    for fb, fs, _ in O.families_for([200, 200, 200], 3000, 10, 3):
+        for b, s in zip(fb, fs):
+            want.append(b.astype(np.uint64) | np.where(s < 0, 1 << 31, 0).astype(np.uint64))
+    assert (packed == np.concatenate(want).astype(np.uint32)).all()
+    # Appendix A: first entries of HashFamily({100,100,100},1000,family_seed(0,0))
+    f = st.HashFamily([100, 100, 100], 1000, st.family_seed(0, 0))
+    assert f.pair(0).bucket_map()[:6].tolist() == [652, 387, 787, 778, 375, 401]
+    assert f.composed_len() == 2998
+
+
+def test_hash_errors(cuda):
+    with pytest.raises(ValueError):
+        st.HashPair(0, 5, 1)
+    with pytest.raises(ValueError):
+        st.HashPair(bucket_map=[0, 5], sign_map=[1, 1], hash_len=5)
+    with pytest.raises(ValueError):
+        st.HashPair(bucket_map=[0, 1], sign_map=[1, 0], hash_len=5)
+
+
+# ------------------------------------------------------------------ K1
+def test_dense_kat_2x2(cuda):
+    fam = st.HashFamily(pairs=[st.HashPair(bucket_map=[0, 1], sign_map=[1, 1], hash_len=2),
+                               st.HashPair(bucket_map=[0, 0], sign_map=[1, 1], hash_len=2)])
+    out = st.fcs_sketch(st.DenseTensor.from_array(np.outer([1.0, 2.0], [1.0, 1.0])), fam)
+    assert out.values.cpu().tolist() == [2.0, 4.0, 0.0]
+
+
+def test_dense_golden(cuda):
+    x = GOLD["dense_small_x"]
+    fam = st.HashFamily(x.shape, 7, st.family_seed(3, 0))
+    rel_close(st.fcs_sketch(x, fam).values, GOLD["dense_small_sketch"], 1e-13)
+    x4 = GOLD["dense_o4_x"]
+    fam4 = st.HashFamily(x4.shape, 5, st.family_seed(9, 1))
+    rel_close(st.fcs_sketch(x4, fam4).values, GOLD["dense_o4_sketch"], 1e-13)
+
+
+@pytest.mark.parametrize("shape,J,D,dtype", [((37, 11, 23), 29, 3, np.float64),
+                                             ((64, 48, 40), 500, 4, np.float32),
+                                             ((5, 4, 3, 2, 3), 7, 2, np.float64),
+                                             ((1000,), 77, 2, np.float64)])
+def test_dense_integer_bitexact(cuda, shape, J, D, dtype):
+    """Small-integer data: every partial sum is exact, so any bucket or sign
+    error shows up as an exact mismatch (bucket indices bit-exact)."""
+    rng = np.random.default_rng(11)
+    x = rng.integers(-8, 9, size=shape).astype(dtype)
+    fams = st.families_for(list(shape), st.EstimatorConfig(J, D, 99))
+    got = st.fcs_dense_batched(st.DenseTensor.from_array(x), fams).cpu().numpy()
+    for d, f in enumerate(fams):
+        b, s, j = oracle_family(f)
+        assert (got[d] == O.fcs_dense(x.astype(np.float64), b, s, j)).all()
+
+
+def test_dense_c1_full(cuda):
+    """BASELINE config 1: 100^3 fp64, J=1000, D=1 -> 2998 buckets."""
+    c = configs.C1
+    x = configs.c1_tensor(c)
+    fams = st.families_for(list(c.dims), st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
+    got = st.fcs_dense_batched(st.DenseTensor.from_array(x), fams)
+    assert got.shape == (1, 2998)
+    b, s, j = oracle_family(fams[0])
+    rel_close(got[0], O.fcs_dense(x, b, s, j), RTOL64)
+
+
+def test_dense_f32_wide_sketch(cuda):
+    """c4 geometry on a slab: fp32, J=16384 per mode -> J~=49150 (one family per SM)."""
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((1024, 32, 16)).astype(np.float32)
+    fams = st.families_for([1024, 32, 16], st.EstimatorConfig(16384, 4, 4))
+    got = st.fcs_dense_batched(st.DenseTensor.from_array(x), fams)
+    assert got.shape == (4, 49150)
+    for d, f in enumerate(fams):
+        b, s, j = oracle_family(f)
+        rel_close(got[d], O.fcs_dense(x.astype(np.float64), b, s, j), RTOL32)
+
+
+def test_dense_global_fallback(cuda):
+    """fp64 sketch larger than shared memory (J~ = 29998 -> 240 KB): global path."""
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((30, 20, 10))
+    fams = st.families_for([30, 20, 10], st.EstimatorConfig(10000, 2, 8))
+    got = st.fcs_dense_batched(st.DenseTensor.from_array(x), fams)
+    for d, f in enumerate(fams):
+        b, s, j = oracle_family(f)
+        rel_close(got[d], O.fcs_dense(x, b, s, j), RTOL64)
+
+
+def test_dense_slabs_sum_to_full(cuda):
+    """Element sharding by the last mode (the multi-GPU partition): partial
+    sketches of the slabs add up to the full sketch (linearity)."""
+    from paper_2106_13062_b200 import dist
+    rng = np.random.default_rng(6)
+    x = rng.integers(-4, 5, size=(40, 30, 24)).astype(np.float64)
+    t = st.DenseTensor.from_array(x)
+    fams = st.families_for([40, 30, 24], st.EstimatorConfig(50, 3, 1))
+    full = st.fcs_dense_batched(t, fams)
+    acc = torch.zeros_like(full)
+    for rank in range(5):
+        acc += dist.shard_sketch(t, fams, rank, 5)
+    assert torch.equal(acc, full)
+
+
+def test_dense_zero_and_empty_effects(cuda):
+    x = np.zeros((8, 9, 10))
+    fams = st.families_for([8, 9, 10], st.EstimatorConfig(5, 2, 1))
+    assert (st.fcs_dense_batched(st.DenseTensor.from_array(x), fams) == 0).all()
+
+
+def test_dense_errors(cuda):
+    fam = st.HashFamily([4, 5], 3, 1)
+    with pytest.raises(ValueError):
+        st.fcs_sketch(np.ones((5, 4)), fam)
+    with pytest.raises(ValueError):
+        st.fcs_sketch(np.ones((4, 5, 1)), fam)
+    with pytest.raises(ValueError):
+        st.DenseTensor([3, 0])
+
+
+# ------------------------------------------------------------- CS / CP
+def test_cs_kat_and_columns(cuda):
+    pair = st.HashPair(bucket_map=[0, 1, 0], sign_map=[1, -1, 1], hash_len=2)
+    assert st.cs_sketch([1.0, 2.0, 3.0], pair).values.cpu().tolist() == [4.0, -2.0]
+    p = st.HashPair(400, 4000, 12)
+    u = np.random.default_rng(1).standard_normal((400, 7))
+    got = st.cs_sketch_columns(u, p).cpu().numpy()
+    want = O.cs_sketch_columns(u, p.bucket_map(), p.sign_map(), 4000)
+    np.testing.assert_allclose(got, want, rtol=0, atol=1e-14)
+
+
+def test_cp_golden(cuda):
+    fs = [GOLD[f"cp_f{i}"] for i in range(3)]
+    fam = st.HashFamily([10, 12, 14], 9, st.family_seed(4, 2))
+    got = st.fcs_sketch(st.CpTensor(GOLD["cp_w"], fs), fam).values
+    rel_close(got, GOLD["cp_sketch"], RTOL64)
+    rel_close(got, GOLD["cp_dense_sketch"], 1e-9)  # path identity
+
+
+def test_cp_c2_full(cuda):
+    """BASELINE config 2: CP 400^3, R=50, J=4000 (J~=11998), D=10."""
+    c = configs.C2
+    w, fs = configs.c2_cp(c)
+    fams = st.families_for(list(c.dims), st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
+    got = st.fcs_cp_batched(st.CpTensor(w, fs), fams)
+    assert got.shape == (10, 11998)
+    for d in (0, 7):
+        b, s, j = oracle_family(fams[d])
+        rel_close(got[d], O.fcs_cp(w, fs, b, s, j), RTOL64)
+
+
+def test_cp_vs_dense_path(cuda):
+    """fcs_cp == fcs_dense(densify) on a random rank-5 10x12x14."""
+    rng = np.random.default_rng(3)
+    fs = [rng.standard_normal((d, 5)) for d in (10, 12, 14)]
+    w = rng.standard_normal(5)
+    fams = st.families_for([10, 12, 14], st.EstimatorConfig(33, 3, 8))
+    cp = st.fcs_cp_batched(st.CpTensor(w, fs), fams)
+    dense = st.fcs_dense_batched(st.DenseTensor.from_array(configs.densify(w, fs)), fams)
+    rel_close(cp, dense.cpu().numpy(), 1e-9)
+
+
+def test_convolve_pairs(cuda):
+    rng = np.random.default_rng(2)
+    a, b = rng.standard_normal((3, 4095)), rng.standard_normal((3, 4095))
+    got = st.convolve_pairs(torch.from_numpy(a), torch.from_numpy(b)).cpu().numpy()
+    for i in range(3):
+        rel_close(got[i], np.convolve(a[i], b[i]), 1e-11)
+    k = st.convolve_pairs(torch.tensor([[1.0, 2.0]]), torch.tensor([[2.0, 0.0]]))
+    np.testing.assert_allclose(k.cpu().numpy()[0], [2, 4, 0], atol=1e-14)
+
+
+# ------------------------------------------------------------ Kronecker
+def test_kron_c5_and_slice(cuda):
+    """BASELINE config 5: FCS(A (x) B) = conv(FCS(A), FCS(B)), J=2048, D=8; checked
+    against the oracle composition and, on 64x64 slices, against the direct dense
+    FCS of the explicit Kronecker product (shape (I3,I1,I4,I2), family (p2,p0,p3,p1))."""
+    c = configs.C5
+    A, B = configs.c5_matrices(c)
+    fams = st.families_for(list(c.dims), st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
+    got = st.fcs_kron(A, B, fams)
+    assert got.shape == (8, 8189)
+    for d in (0, 5):
+        b, s, j = oracle_family(fams[d])
+        fa = O.fcs_dense(A, b[:2], s[:2], j[:2])
+        fb = O.fcs_dense(B, b[2:], s[2:], j[2:])
+        rel_close(got[d], np.convolve(fa, fb), RTOL64)
+    # slice check (prefix property: families over dims 64 are prefixes of the 512 ones)
+    As, Bs = A[:64, :64], B[:64, :64]
+    fams64 = st.families_for([64] * 4, st.EstimatorConfig(c.hash_len, 2, c.seed))
+    got64 = st.fcs_kron(As, Bs, fams64)
+    K = np.kron(As, Bs).reshape((64, 64, 64, 64), order="F")  # (i3, i1, i4, i2)
+    for d in range(2):
+        b, s, j = oracle_family(fams64[d])
+        perm = [2, 0, 3, 1]
+        direct = O.fcs_dense(K, [b[p] for p in perm], [s[p] for p in perm], [j[p] for p in perm])
+        rel_close(got64[d], direct, 1e-9)
+
+
+# ------------------------------------------------------------ estimators
+def test_engine_golden(cuda):
+    eng = st.FcsEngine(st.DenseTensor.from_array(GOLD["eng_t"]), st.EstimatorConfig(6, 3, 5))
+    u, v, w = GOLD["eng_u"], GOLD["eng_v"], GOLD["eng_w"]
+    rel_close(eng.iuu(u), GOLD["eng_iuu"], RTOL64)
+    rel_close(eng.iuv(u, v, 1), GOLD["eng_iuv1"], RTOL64)
+    rel_close(eng.iuv(u, v, 2), GOLD["eng_iuv2"], RTOL64)
+    rel_close(eng.uvw(u, v, w), GOLD["eng_uvw"][0], RTOL64)
+    eng.deflate(0.7, u, v, w)
+    rel_close(eng.iuu(u), GOLD["eng_defl_iuu"], RTOL64)
+    rel_close(eng.uvw(u, v, w), GOLD["eng_defl_uvw"][0], RTOL64)
+    with pytest.raises(ValueError):
+        eng.iuv(u, v, 3)
+    with pytest.raises(ValueError):
+        eng.iuv(u[:5], v, 0)
+
+
+def test_engine_medium_batched(cuda):
+    """Batched T(I,u,u) and T(u,u,u) for 15 vectors at once vs the oracle engine
+    (60^3, J=300, D=10 — the c3 estimator with a smaller tensor)."""
+    rng = np.random.default_rng(8)
+    t = rng.standard_normal((60, 60, 60))
+    cfg = st.EstimatorConfig(300, 10, 3)
+    eng = st.FcsEngine(st.DenseTensor.from_array(t), cfg)
+    oeng = O.FcsEngine(t, 300, 10, 3)
+    U = rng.standard_normal((15, 60))
+    got = eng.iuv_batch(U, U, 0).cpu().numpy()
+    vals = eng.uvw_batch(U, U, U).cpu().numpy()
+    for l in (0, 9, 14):
+        rel_close(got[l], oeng.iuu(U[l]), RTOL64)
+        rel_close(vals[l], oeng.uuu(U[l]), RTOL64)
+    # sketches survive the round trip through the cached spectra
+    rel_close(eng.sketches()[2], oeng.pres[2].values, 1e-12)
+
+
+def test_engine_c3_size(cuda):
+    """BASELINE config 3 estimator geometry: 200^3, J=3000 (J~=8998), D=10."""
+    c = configs.C3
+    t, lam, V = configs.c3_tensor(c)
+    eng = st.FcsEngine(st.DenseTensor.from_array(t), st.EstimatorConfig(c.hash_len, 10, c.seed))
+    oeng = O.FcsEngine(t, c.hash_len, 10, c.seed)
+    u = V[:, 0] + 0.1 * V[:, 1]
+    rel_close(eng.iuu(u), oeng.iuu(u), RTOL64)
+    rel_close(eng.uuu(u), oeng.uuu(u), RTOL64)
+
+
+def test_rtpm_golden(cuda):
+    cfg = st.RtpmConfig(target_rank=2, num_inits=3, num_power_iters=5,
+                        estimator=st.EstimatorConfig(12, 3, 21))
+    cp = st.rtpm(st.DenseTensor.from_array(GOLD["rtpm_t"]), cfg)
+    rel_close(cp.weights, GOLD["rtpm_weights"], 1e-8)
+    f = cp._factors_cm[0].t()
+    rel_close(f, GOLD["rtpm_factor"], 1e-8)
+
+
+def test_device_gaussian_distribution(cuda):
+    import ctypes as C
+    from paper_2106_13062_b200 import _lib
+    x = torch.empty(1 << 22, dtype=torch.float32, device="cuda")
+    _lib.check(_lib.lib().st_device_gaussian(_lib.ST_F32, 4, x.numel(), C.c_void_p(x.data_ptr()),
+                                             None))
+    torch.cuda.synchronize()
+    assert abs(float(x.mean())) < 3e-3 and abs(float(x.std()) - 1) < 3e-3
+    h = configs.host_gaussian(4, 1000)
+    np.testing.assert_allclose(x[:1000].cpu().numpy(), h.astype(np.float32), rtol=1e-6, atol=1e-6)

@@ -1,0 +1,161 @@
+"""CPU tests: pin the numpy restatement (oracle/fcs_oracle.py) against the
+spec's known-answer tests and the golden vectors produced by the unmodified
+reference (tests/golden/make_golden.py), and — where oracle/_ref is built —
+against the reference library directly."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import fcs_oracle as O
+from oracle import ref
+
+GOLD = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden.npz"))
+
+
+def rel_close(got, want, rtol):
+    """|g - c| <= rtol * (|c| + ||c||_inf) per entry (SURVEY.md §8(d) parity rule)."""
+    got, want = np.asarray(got), np.asarray(want)
+    tol = rtol * (np.abs(want) + np.abs(want).max(initial=0.0))
+    return bool(np.all(np.abs(got - want) <= tol))
+
+
+# ------------------------------------------------------------- spec KATs
+def test_kat_count_sketch():
+    assert O.cs_sketch([1, 2, 3], [0, 1, 0], [1, -1, 1], 2).tolist() == [4.0, -2.0]
+
+
+def test_kat_fcs_2x2():  # u=[1,2], v=[1,1], h1=[0,1], h2=[0,0]
+    t = np.outer([1, 2], [1, 1])
+    out = O.fcs_dense(t, [[0, 1], [0, 0]], [[1, 1], [1, 1]], [2, 2])
+    assert out.tolist() == [2.0, 4.0, 0.0]
+
+
+def test_kat_fcs_cp_fft():  # conv([1,2],[2,0]) -> [2,4,0]
+    np.testing.assert_allclose(O.fft_convolve([[1, 2], [2, 0]], 3), [2, 4, 0], atol=1e-12)
+    np.testing.assert_allclose(GOLD["conv_12_20"], [2, 4, 0], atol=1e-12)
+
+
+def test_kat_compose():  # maps [0,1],[0,0], index (1,0) -> (1,+1)
+    b, s = O.composed_tables([[0, 1], [0, 0]], [[1, 1], [1, 1]])
+    assert (int(b[1]), int(s[1])) == (1, 1)
+
+
+def test_kat_median():
+    assert O.median_reduce([1, 2, 100]) == 2
+    assert O.median_reduce([1, 2, 3, 10]) == 2.5
+    with pytest.raises(ValueError):
+        O.median_reduce([])
+
+
+# ------------------------------------------------------------ golden pins
+def test_golden_rng():
+    assert [int(x) for x in O.splitmix_draw(0, np.arange(1, 4))] == [int(x) for x in
+                                                                    GOLD["draws_seed0"]]
+    assert (O.splitmix_draw(42, np.arange(1, 1001)) == GOLD["draws_seed42"]).all()
+    assert [O.family_seed(0, d) for d in range(3)] == [int(x) for x in GOLD["family_seed0"]]
+    assert hex(O.family_seed(0, 0)) == "0xe220a8397b1dcdaf"
+    assert (O.gaussian_stream(1, 9) == GOLD["gauss_seed1"]).all()
+    rng = O.SplitMix64(1)
+    assert [rng.next_gaussian() for _ in range(9)] == GOLD["gauss_seed1"].tolist()
+
+
+def test_golden_hash_family():
+    b, s, j = O.hash_family([100, 100, 100], 1000, O.family_seed(0, 0))
+    assert (np.stack(b) == GOLD["fam100_buckets"]).all()
+    assert (np.stack(s) == GOLD["fam100_signs"]).all()
+    assert O.composed_len(j) == int(GOLD["fam100_composed_len"][0]) == 2998
+    assert b[0][:6].tolist() == [652, 387, 787, 778, 375, 401]  # Appendix A
+    assert s[2][:6].tolist() == [-1, 1, -1, -1, 1, 1]
+
+
+def test_golden_prefix_property():
+    b, s = O.hash_pair(512, 2048, 7)
+    assert (b == GOLD["pair512_b"]).all() and (s == GOLD["pair512_s"]).all()
+    assert (GOLD["pair512_b"][:64] == GOLD["pair64_b"]).all()
+    assert (GOLD["pair512_s"][:64] == GOLD["pair64_s"]).all()
+
+
+def test_golden_dense_bitexact():
+    x = GOLD["dense_small_x"]
+    b, s, j = O.hash_family(x.shape, 7, O.family_seed(3, 0))
+    assert (O.fcs_dense(x, b, s, j) == GOLD["dense_small_sketch"]).all()
+    x4 = GOLD["dense_o4_x"]
+    b, s, j = O.hash_family(x4.shape, 5, O.family_seed(9, 1))
+    assert (O.fcs_dense(x4, b, s, j) == GOLD["dense_o4_sketch"]).all()
+
+
+def test_golden_materialize():
+    tb, ts = GOLD["mat_tables_b"], GOLD["mat_tables_s"]
+    b = [tb[0:3], tb[3:7], tb[7:12]]
+    s = [ts[0:3], ts[3:7], ts[7:12]]
+    cb, cs = O.composed_tables(b, s)
+    assert (cb == GOLD["mat_b"]).all() and (cs == GOLD["mat_s"]).all()
+
+
+def test_golden_cp():
+    fs = [GOLD[f"cp_f{i}"] for i in range(3)]
+    b, s, j = O.hash_family([10, 12, 14], 9, O.family_seed(4, 2))
+    got = O.fcs_cp(GOLD["cp_w"], fs, b, s, j)
+    assert rel_close(got, GOLD["cp_sketch"], 1e-12)
+    # path identity fcs_cp == fcs_dense(densify)
+    assert rel_close(GOLD["cp_sketch"], GOLD["cp_dense_sketch"], 1e-9)
+
+
+def test_golden_engine():
+    t = GOLD["eng_t"]
+    eng = O.FcsEngine(t, 6, 3, 5)
+    u, v, w = GOLD["eng_u"], GOLD["eng_v"], GOLD["eng_w"]
+    assert rel_close(eng.iuu(u), GOLD["eng_iuu"], 1e-10)
+    assert rel_close(eng.iuv(u, v, 1), GOLD["eng_iuv1"], 1e-10)
+    assert rel_close(eng.iuv(u, v, 2), GOLD["eng_iuv2"], 1e-10)
+    assert rel_close(eng.uvw(u, v, w), GOLD["eng_uvw"][0], 1e-10)
+    eng.deflate(0.7, u, v, w)
+    assert rel_close(eng.iuu(u), GOLD["eng_defl_iuu"], 1e-10)
+    assert rel_close(eng.uvw(u, v, w), GOLD["eng_defl_uvw"][0], 1e-10)
+
+
+def test_golden_rtpm():
+    t = GOLD["rtpm_t"]
+    eng = O.FcsEngine(t, 12, 3, 21)
+    w, f = O.rtpm(eng, 10, 2, 3, 5, 21)
+    assert rel_close(w, GOLD["rtpm_weights"], 1e-8)
+    assert rel_close(f, GOLD["rtpm_factor"], 1e-8)
+
+
+# ------------------------------------------------------------- error paths
+def test_errors_match_reference():
+    with pytest.raises(ValueError):
+        O.hash_pair(0, 5, 1)
+    with pytest.raises(ValueError):
+        O.hash_family([3, 4], [5], 1)
+    b, s, j = O.hash_family([3, 4], 5, 1)
+    with pytest.raises(ValueError):
+        O.fcs_dense(np.zeros((4, 3)), b, s, j)
+    with pytest.raises(ValueError):
+        O.dft([1.0], 0)
+    with pytest.raises(RuntimeError):
+        O.idft_real(np.array([0, 1j, 0, -2j]) * 1e3 + np.array([1, 0, 0, 0]))
+
+
+# ---------------------------------------------- direct reference cross-check
+needs_ref = pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+
+
+@needs_ref
+def test_restatement_vs_reference_random():
+    rng = np.random.default_rng(7)
+    for shape, J, seed in (((7, 3, 5), 11, 3), ((16, 9), 40, 9), ((5, 4, 3, 2), 6, 2)):
+        x = rng.standard_normal(shape)
+        x[rng.random(shape) < 0.1] = 0.0
+        master = O.family_seed(seed, 1)
+        b, s, j = O.hash_family(shape, J, master)
+        assert (O.fcs_dense(x, b, s, j) == ref.fcs_dense(x, J, master)).all()
+
+
+@needs_ref
+def test_restatement_vs_reference_errors():
+    with pytest.raises(ValueError):
+        ref.hash_pair(1, 0, 4)
+    with pytest.raises(ValueError):
+        ref.median([])
