@@ -3,61 +3,40 @@
 //
 // Reference: fcs_sketch(const DenseTensor&, const HashFamily&),
 // sketch.cpp:187-201, over the odometer walk for_each_nonzero,
-// sketch.cpp:48-61 (zeros skipped). The reference sums serially in fp64;
-// here each block privatises one family's sketch in shared memory, streams a
-// contiguous range of mode-0 fibers (coalesced loads of the fastest mode),
-// and the per-block partials are reduced in a fixed order in fp64
-// (deterministic).
+// sketch.cpp:48-61 (zeros skipped; adding +/-0 is equivalent). The reference
+// sums serially in fp64; here each CTA privatises ONE family's full sketch in
+// shared memory and streams a contiguous chunk of mode-0 fibers (a "fiber" is
+// the I_0 contiguous elements T[:, i_1, ..., i_{N-1}], whose offset
+// c = sum_{n>=1} h_n(i_n) and sign are warp-uniform). Grid index d is the
+// fastest-varying, so the D CTAs that read the same chunk run together and
+// share it through L2. Per-CTA partials are reduced in a fixed order in fp64.
 //
-// Work decomposition: a "fiber" is one mode-0 column T[:, i_1, ..., i_{N-1}]
-// (I_0 contiguous elements). Its offset c = sum_{n>=1} h_n(i_n) and sign
-// sigma = prod_{n>=1} s_n(i_n) are warp-uniform, so the per-element work is
-// one packed mode-0 table load, one add and one shared-memory accumulate.
+// float32 fast path (fcs_dense_fx_kernel): shared-memory float atomics are
+// compare-and-swap loops on sm_100a, integer atomics are native
+// (ATOMS.ADD). The fp32 path therefore accumulates in int32 fixed point with
+// a scale 2^S chosen from a sampled bound on the partial sums; every
+// accumulate returns the old word, so overflow (and non-finite input) is
+// detected exactly, and a CTA that overflowed redoes its chunk with float
+// atomics. Rounding error per element <= 2^-(S+1) (K1).
 #include <algorithm>
+#include <cmath>
 
-#include "common.cuh"
+#include "dense_common.cuh"
 
 namespace fcs {
 
-struct DenseArgs {
-  int order;
-  int D;
-  uint32_t dims[ST_MAX_ORDER];
-  uint32_t tab_off[ST_MAX_ORDER];  // start of mode n inside one family's tables
-  uint32_t fam_stride;             // sum(dims): distance between families
-  uint32_t jt;                     // composed length J~
-  uint32_t last_begin;             // first i_{N-1} of this slab
-  uint32_t i0_shift;               // mode-0 table shift (order-1 slabs only)
-  uint64_t fibers;                 // mode-0 fibers in this slab
-  uint64_t fibers_per_chunk;
+// Sampled statistics of the input and the fixed-point exponent derived from them.
+struct FxStats {
+  unsigned maxbits;  // max |x| over the sample, float bits (non-negative floats order as ints)
+  int S;             // fixed-point fractional bits
+  double sum;
+  double sumsq;
+  double count;
 };
 
-// Offset and sign bit of fiber f (slab-local) for the family at `tab`.
-__device__ __forceinline__ void fiber_offset(const DenseArgs& a, const uint32_t* __restrict__ tab,
-                                             uint64_t f, uint32_t& c, uint32_t& sbit) {
-  c = 0;
-  sbit = 0;
-  for (int n = 1; n < a.order; ++n) {
-    uint64_t i;
-    if (n < a.order - 1) {
-      i = f % a.dims[n];
-      f /= a.dims[n];
-    } else {
-      i = f + a.last_begin;
-    }
-    const uint32_t e = __ldg(tab + a.tab_off[n] + i);
-    c += e & 0x7fffffffu;
-    sbit ^= e & 0x80000000u;
-  }
-}
-
-template <typename Tacc>
-__device__ __forceinline__ Tacc signed_val(Tacc v, uint32_t sbit) {
-  return sbit ? -v : v;
-}
-
-// Block-private shared-memory sketch of family d = blockIdx.x % D over the
-// fiber chunk blockIdx.x / D; partial written to part[chunk][d][:].
+// ------------------------------------------------------------------ kernels
+// Generic block-private kernel (any shape, fp32 or fp64): one family per CTA,
+// fibers strided over warps, shared-memory atomicAdd.
 template <typename Tin, typename Tacc>
 __global__ void __launch_bounds__(1024) fcs_dense_smem_kernel(DenseArgs a,
                                                               const Tin* __restrict__ t,
@@ -69,24 +48,18 @@ __global__ void __launch_bounds__(1024) fcs_dense_smem_kernel(DenseArgs a,
   const uint64_t chunk = blockIdx.x / a.D;
   const uint32_t* tab = packed + static_cast<uint64_t>(d) * a.fam_stride;
   const uint32_t* tab0 = tab + a.i0_shift;
-
   for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) sk[b] = Tacc(0);
   __syncthreads();
-
   const uint64_t f_begin = chunk * a.fibers_per_chunk;
   const uint64_t f_end = min(a.fibers, f_begin + a.fibers_per_chunk);
   const uint32_t i0n = a.dims[0];
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int nwarps = blockDim.x >> 5;
-
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (uint64_t f = f_begin + warp; f < f_end; f += nwarps) {
     uint32_t c, sbit;
     fiber_offset(a, tab, f, c, sbit);
     const Tin* fib = t + f * i0n;
     uint32_t i = lane;
-    // 4 independent loads in flight per lane before the accumulates.
-    for (; i + 96 < i0n; i += 128) {
+    for (; i + 96 < i0n; i += 128) {  // 4 independent loads in flight per lane
       Tacc v[4];
       uint32_t e[4];
 #pragma unroll
@@ -95,21 +68,171 @@ __global__ void __launch_bounds__(1024) fcs_dense_smem_kernel(DenseArgs a,
         e[k] = __ldg(tab0 + i + 32 * k);
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < 4; ++k)
         if (v[k] != Tacc(0))
           atomicAdd(&sk[(e[k] & 0x7fffffffu) + c], signed_val(v[k], (e[k] ^ sbit) & 0x80000000u));
-      }
     }
     for (; i < i0n; i += 32) {
       const Tacc v = static_cast<Tacc>(__ldcs(fib + i));
       const uint32_t e = __ldg(tab0 + i);
-      if (v != Tacc(0))
-        atomicAdd(&sk[(e & 0x7fffffffu) + c], signed_val(v, (e ^ sbit) & 0x80000000u));
+      if (v != Tacc(0)) atomicAdd(&sk[(e & 0x7fffffffu) + c], signed_val(v, (e ^ sbit) & 0x80000000u));
     }
   }
   __syncthreads();
   Tacc* dst = part + (chunk * a.D + d) * static_cast<uint64_t>(a.jt);
   for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) dst[b] = sk[b];
+}
+
+// Sampled max|x|, sum and sum of squares over up to `nsample` evenly spaced fibers.
+__global__ void fx_sample_kernel(DenseArgs a, const float* __restrict__ t, uint64_t nsample,
+                                 FxStats* __restrict__ st) {
+  const uint32_t i0n = a.dims[0];
+  float mx = 0.f;
+  double s = 0.0, s2 = 0.0, cnt = 0.0;
+  for (uint64_t k = blockIdx.x; k < nsample; k += gridDim.x) {
+    const uint64_t f = (k * a.fibers) / nsample;
+    for (uint32_t i = threadIdx.x; i < i0n; i += blockDim.x) {
+      const float x = t[f * i0n + i];
+      mx = fmaxf(mx, fabsf(x));  // NaN is ignored here and caught by the main kernel
+      s += x;
+      s2 += static_cast<double>(x) * x;
+      cnt += 1.0;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&st->maxbits, __float_as_uint(mx));
+    atomicAdd(&st->sum, s);
+    atomicAdd(&st->sumsq, s2);
+    atomicAdd(&st->count, cnt);
+  }
+}
+
+// Fixed-point exponent: the largest S with a comfortable margin between the
+// expected largest per-CTA bucket partial and 2^31 (bias * N + 8 sigma sqrt(N)
+// + max, N = the expected count of elements a CTA adds to its busiest bucket).
+__global__ void fx_scale_kernel(FxStats* st, double n_center) {
+  const double n = fmax(st->count, 1.0);
+  const double mean = st->sum / n;
+  const double rms = sqrt(fmax(st->sumsq / n, 0.0));
+  const double mx = static_cast<double>(__uint_as_float(st->maxbits));
+  const double bound = fabs(mean) * n_center + 8.0 * rms * sqrt(n_center) + 2.0 * mx;
+  int S = 30;
+  if (bound > 0.0) S = static_cast<int>(floor(log2(1073741824.0 / bound)));
+  // single elements must stay below 2^21 (the kernel's exact-rounding range is 2^22)
+  if (mx > 0.0) S = min(S, static_cast<int>(floor(log2(2097152.0 / mx))));
+  st->S = max(-60, min(30, S));
+}
+
+__device__ __forceinline__ void fiber_offset_fast(const DenseArgs& a, const uint32_t* tab,
+                                                  uint64_t f, uint32_t& c, uint32_t& sbit) {
+  if (a.order == 3 && a.fibers < 0xffffffffull) {
+    const uint32_t ff = static_cast<uint32_t>(f);
+    const uint32_t i1 = ff % a.dims[1], i2 = ff / a.dims[1] + a.last_begin;
+    const uint32_t e1 = __ldg(tab + a.tab_off[1] + i1), e2 = __ldg(tab + a.tab_off[2] + i2);
+    c = (e1 & 0x7fffffffu) + (e2 & 0x7fffffffu);
+    sbit = (e1 ^ e2) & 0x80000000u;
+  } else {
+    fiber_offset(a, tab, f, c, sbit);
+  }
+}
+
+// float32 fast path (I_0 % 4 == 0, 16-byte aligned fibers, I_0 <= 128 * NV):
+// warp per fiber, lane-owned mode-0 indices with their table entries in
+// registers, NV 128-bit loads per lane with the next fiber prefetched,
+// int32 fixed-point shared-memory accumulation with exact overflow detection.
+template <int NV>
+__global__ void __launch_bounds__(512, 1) fcs_dense_fx_kernel(DenseArgs a,
+                                                              const float* __restrict__ t,
+                                                              const uint32_t* __restrict__ packed,
+                                                              const FxStats* __restrict__ st,
+                                                              int32_t* __restrict__ part,
+                                                              int* __restrict__ flags) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int32_t* sk = reinterpret_cast<int32_t*>(smem_raw);
+  const int d = blockIdx.x % a.D;
+  const uint64_t chunk = blockIdx.x / a.D;
+  const uint32_t* tab = packed + static_cast<uint64_t>(d) * a.fam_stride;
+  const float scale = ldexpf(1.0f, st->S);
+  for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) sk[b] = 0;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint32_t i0n = a.dims[0];
+  const uint32_t nvec = i0n / 4;
+  uint32_t e0[NV][4];  // packed mode-0 entries (bucket | sign << 31)
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const uint32_t v = lane + 32 * j;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) e0[j][k] = v < nvec ? __ldg(tab + a.i0_shift + v * 4 + k) : 0u;
+  }
+  __syncthreads();
+
+  const uint64_t f_begin = chunk * a.fibers_per_chunk;
+  const uint64_t f_end = min(a.fibers, f_begin + a.fibers_per_chunk);
+  int ovf = 0;
+  float4 cur[NV], nxt[NV];
+  auto load = [&](uint64_t fib, float4* dst) {
+    const float4* src = reinterpret_cast<const float4*>(t + fib * i0n);
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      if (lane + 32 * j < nvec) dst[j] = __ldcs(src + lane + 32 * j);
+  };
+  uint64_t f = f_begin + warp;
+  if (f < f_end) load(f, cur);
+  for (; f < f_end; f += nwarps) {
+    if (f + nwarps < f_end) load(f + nwarps, nxt);
+    uint32_t c, sbit;
+    fiber_offset_fast(a, tab, f, c, sbit);
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      if (lane + 32 * j < nvec) {
+        const float* x = reinterpret_cast<const float*>(&cur[j]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t e = e0[j][k];
+          const float y =
+              __uint_as_float(__float_as_uint(x[k]) ^ ((e ^ sbit) & 0x80000000u)) * scale;
+          ovf |= !(fabsf(y) < 4194304.0f);  // |y| < 2^22 (also catches NaN / Inf)
+          // round-to-nearest int via the 1.5 * 2^23 magic number (exact for |y| < 2^22)
+          const int32_t q = __float_as_int(y + 12582912.0f) - 0x4B400000;
+          const int32_t old = atomicAdd(&sk[(e & 0x7fffffffu) + c], q);
+          const int32_t now = old + q;
+          ovf |= ((old ^ now) & (q ^ now)) < 0;  // signed overflow of the partial
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NV; ++j) cur[j] = nxt[j];
+  }
+
+  const bool overflowed = __syncthreads_or(ovf);
+  if (overflowed) {
+    // Exact fallback for this CTA: float atomics over the same chunk.
+    float* skf = reinterpret_cast<float*>(smem_raw);
+    for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) skf[b] = 0.f;
+    __syncthreads();
+    for (uint64_t g = f_begin + warp; g < f_end; g += nwarps) {
+      uint32_t c, sbit;
+      fiber_offset(a, tab, g, c, sbit);
+      for (uint32_t i = lane; i < i0n; i += 32) {
+        const float x = __ldcs(t + g * i0n + i);
+        const uint32_t e = __ldg(tab + a.i0_shift + i);
+        atomicAdd(&skf[(e & 0x7fffffffu) + c],
+                  __uint_as_float(__float_as_uint(x) ^ ((e ^ sbit) & 0x80000000u)));
+      }
+    }
+    __syncthreads();
+  }
+  int32_t* dst = part + (chunk * a.D + d) * static_cast<uint64_t>(a.jt);
+  for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) dst[b] = sk[b];
+  if (threadIdx.x == 0) flags[chunk * a.D + d] = overflowed ? 1 : 0;
 }
 
 // Fixed-order fp64 reduction of the chunk partials: out[d][b] (+)= sum_c part[c][d][b].
@@ -121,6 +244,24 @@ __global__ void reduce_partials_kernel(const Tacc* __restrict__ part, uint64_t n
   if (i >= per_chunk) return;
   double acc = accumulate ? out[i] : 0.0;
   for (uint64_t c = 0; c < nchunk; ++c) acc += static_cast<double>(part[c * per_chunk + i]);
+  out[i] = acc;
+}
+
+// Same for fixed-point partials (flag 0: int32 * 2^-S, flag 1: float bits).
+__global__ void reduce_fx_kernel(const int32_t* __restrict__ part, const int* __restrict__ flags,
+                                 uint64_t nchunk, int D, uint32_t jt,
+                                 const FxStats* __restrict__ st, double* __restrict__ out,
+                                 int accumulate) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t per = static_cast<uint64_t>(D) * jt;
+  if (i >= per) return;
+  const int d = static_cast<int>(i / jt);
+  const double inv = ldexp(1.0, -st->S);
+  double acc = accumulate ? out[i] : 0.0;
+  for (uint64_t c = 0; c < nchunk; ++c) {
+    const int32_t w = part[c * per + i];
+    acc += flags[c * D + d] ? static_cast<double>(__int_as_float(w)) : static_cast<double>(w) * inv;
+  }
   out[i] = acc;
 }
 
@@ -149,44 +290,81 @@ __global__ void fcs_dense_global_kernel(DenseArgs a, const Tin* __restrict__ t,
   }
 }
 
+// -------------------------------------------------------------- planning
 namespace {
 
+enum class Path { Global, Smem, Fx };
+
 struct Plan {
-  bool smem = false;
+  Path path = Path::Global;
   size_t smem_bytes = 0;
   int threads = 0;
+  int nv = 0;
   uint64_t nchunk = 0;
+  size_t part_bytes = 0;
   size_t ws = 0;
 };
 
+// Vectors per lane for the fx kernel (0: not applicable to this shape).
+int fx_nv(const DenseArgs& a) {
+  if (a.dims[0] % 4 != 0) return 0;
+  const uint32_t per_lane = (a.dims[0] / 4 + 31) / 32;
+  if (per_lane == 0 || per_lane > 8) return 0;
+  return per_lane <= 1 ? 1 : per_lane <= 2 ? 2 : per_lane <= 4 ? 4 : 8;
+}
+
+using FxKernel = void (*)(DenseArgs, const float*, const uint32_t*, const FxStats*, int32_t*, int*);
+FxKernel fx_kernel(int nv) {
+  switch (nv) {
+    case 1: return fcs_dense_fx_kernel<1>;
+    case 2: return fcs_dense_fx_kernel<2>;
+    case 4: return fcs_dense_fx_kernel<4>;
+    default: return fcs_dense_fx_kernel<8>;
+  }
+}
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+// The workspace depends only on the shape (never on the pointer), so
+// st_fcs_dense_workspace never under-reports; an unaligned fp32 tensor simply
+// takes the generic kernel with the same partition.
 template <typename Tin, typename Tacc>
 int make_plan(const DenseArgs& a, Plan* p) {
   DeviceInfo di;
   if (int rc = device_info(&di)) return rc;
   p->smem_bytes = static_cast<size_t>(a.jt) * sizeof(Tacc);
   if (p->smem_bytes > di.smem_optin) {
-    p->smem = false;
+    p->path = Path::Global;
     p->ws = 0;
     return ST_OK;
   }
-  p->smem = true;
-  auto kern = fcs_dense_smem_kernel<Tin, Tacc>;
-  FCS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(p->smem_bytes)));
-  // One 1024-thread block per SM when the sketch fills shared memory,
-  // otherwise 512-thread blocks packed by occupancy.
-  p->threads = p->smem_bytes > di.smem_optin / 2 ? 1024 : 512;
   int per_sm = 0;
-  FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, p->threads,
-                                                             p->smem_bytes));
+  p->nv = sizeof(Tin) == 4 ? fx_nv(a) : 0;
+  if (p->nv) {
+    p->path = Path::Fx;
+    p->threads = 512;
+    auto k = fx_kernel(p->nv);
+    FCS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(p->smem_bytes)));
+    FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
+                                                               p->smem_bytes));
+  } else {
+    p->path = Path::Smem;
+    auto k = fcs_dense_smem_kernel<Tin, Tacc>;
+    FCS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(p->smem_bytes)));
+    p->threads = p->smem_bytes > di.smem_optin / 2 ? 1024 : 512;
+    FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
+                                                               p->smem_bytes));
+  }
   per_sm = std::max(per_sm, 1);
   const uint64_t resident = static_cast<uint64_t>(per_sm) * di.sm_count;
   uint64_t nchunk = std::max<uint64_t>(1, resident / static_cast<uint64_t>(a.D));
-  // Keep at least a few fibers per warp so table setup amortises.
-  const uint64_t min_fibers = std::max<uint64_t>(1, static_cast<uint64_t>(p->threads / 32));
-  nchunk = std::min<uint64_t>(nchunk, std::max<uint64_t>(1, a.fibers / min_fibers));
+  nchunk = std::min<uint64_t>(nchunk, std::max<uint64_t>(1, a.fibers / 16));
   p->nchunk = nchunk;
-  p->ws = nchunk * a.D * static_cast<size_t>(a.jt) * sizeof(Tacc);
+  p->part_bytes = nchunk * a.D * static_cast<size_t>(a.jt) * sizeof(Tacc);
+  p->ws = align_up(p->part_bytes) + align_up(nchunk * a.D * sizeof(int)) + align_up(sizeof(FxStats));
   return ST_OK;
 }
 
@@ -235,7 +413,7 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
   }
   Plan p;
   if (int rc = make_plan<Tin, Tacc>(a, &p)) return rc;
-  if (!p.smem) {
+  if (p.path == Path::Global) {
     if (!accumulate) FCS_CUDA_TRY(cudaMemsetAsync(out, 0, out_elems * sizeof(double), st));
     DeviceInfo di;
     if (int rc = device_info(&di)) return rc;
@@ -246,9 +424,39 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
   FCS_CHECK_ARG(ws != nullptr && ws_bytes >= p.ws, "st_fcs_dense: workspace too small");
   a.fibers_per_chunk = (a.fibers + p.nchunk - 1) / p.nchunk;
   const uint64_t nchunk = (a.fibers + a.fibers_per_chunk - 1) / a.fibers_per_chunk;
+  const bool aligned = (reinterpret_cast<uintptr_t>(t) & 15u) == 0;
+  if (p.path == Path::Fx && aligned) {
+    char* base = static_cast<char*>(ws);
+    auto* part = reinterpret_cast<int32_t*>(base);
+    auto* flags = reinterpret_cast<int*>(base + align_up(p.part_bytes));
+    auto* stats = reinterpret_cast<FxStats*>(base + align_up(p.part_bytes) +
+                                             align_up(p.nchunk * a.D * sizeof(int)));
+    FCS_CUDA_TRY(cudaMemsetAsync(stats, 0, sizeof(FxStats), st));
+    const uint64_t nsample = std::min<uint64_t>(a.fibers, 2048);
+    fx_sample_kernel<<<static_cast<unsigned>(std::min<uint64_t>(nsample, 296)), 256, 0, st>>>(
+        a, reinterpret_cast<const float*>(t), nsample, stats);
+    FCS_CUDA_TRY(cudaGetLastError());
+    const double per_cta = static_cast<double>(a.fibers_per_chunk) * a.dims[0];
+    fx_scale_kernel<<<1, 1, 0, st>>>(stats, 3.0 * per_cta / a.jt + 16.0);
+    FCS_CUDA_TRY(cudaGetLastError());
+    fx_kernel(p.nv)<<<static_cast<unsigned>(nchunk * a.D), p.threads, p.smem_bytes, st>>>(
+        a, reinterpret_cast<const float*>(t), packed, stats, part, flags);
+    FCS_CUDA_TRY(cudaGetLastError());
+    reduce_fx_kernel<<<ceil_div(out_elems, 256), 256, 0, st>>>(part, flags, nchunk, a.D, a.jt,
+                                                               stats, out, accumulate);
+    FCS_CUDA_TRY(cudaGetLastError());
+    return ST_OK;
+  }
+  int threads = p.threads;
+  if (p.path == Path::Fx) {  // unaligned fp32 tensor: generic kernel, same partition
+    auto k = fcs_dense_smem_kernel<Tin, Tacc>;
+    FCS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(p.smem_bytes)));
+    threads = 1024;
+  }
   Tacc* part = static_cast<Tacc*>(ws);
   fcs_dense_smem_kernel<Tin, Tacc>
-      <<<static_cast<unsigned>(nchunk * a.D), p.threads, p.smem_bytes, st>>>(a, t, packed, part);
+      <<<static_cast<unsigned>(nchunk * a.D), threads, p.smem_bytes, st>>>(a, t, packed, part);
   FCS_CUDA_TRY(cudaGetLastError());
   reduce_partials_kernel<Tacc><<<ceil_div(out_elems, 256), 256, 0, st>>>(part, nchunk, out_elems,
                                                                          out, accumulate);

@@ -311,3 +311,55 @@ def test_device_gaussian_distribution(cuda):
     assert abs(float(x.mean())) < 3e-3 and abs(float(x.std()) - 1) < 3e-3
     h = configs.host_gaussian(4, 1000)
     np.testing.assert_allclose(x[:1000].cpu().numpy(), h.astype(np.float32), rtol=1e-6, atol=1e-6)
+
+
+# ---------------------------------------------------- fp32 fixed-point path
+def _f32_case(x, J=300, D=3, seed=5):
+    fams = st.families_for(list(x.shape), st.EstimatorConfig(J, D, seed))
+    got = st.fcs_dense_batched(st.DenseTensor.from_array(x), fams).cpu().numpy()
+    want = []
+    for f in fams:
+        b, s, j = oracle_family(f)
+        want.append(O.fcs_dense(x.astype(np.float64), b, s, j))
+    return got, np.stack(want)
+
+
+def test_dense_f32_outlier_fallback(cuda):
+    """An outlier the scale sample misses overflows the int32 fixed point; the
+    CTA must detect it and redo its chunk with float accumulation."""
+    rng = np.random.default_rng(21)
+    x = rng.standard_normal((256, 64, 48)).astype(np.float32)
+    x[17, 33, 40] = 3.0e9
+    x[200, 5, 1] = -7.5e8
+    got, want = _f32_case(x)
+    rel_close(got, want, RTOL32)
+
+
+def test_dense_f32_biased_data(cuda):
+    """All-positive data (mean 100): the sampled scale must keep partials in range."""
+    rng = np.random.default_rng(22)
+    x = (100.0 + rng.standard_normal((512, 32, 40))).astype(np.float32)
+    got, want = _f32_case(x, J=64)
+    rel_close(got, want, RTOL32)
+
+
+def test_dense_f32_nan_propagates(cuda):
+    x = np.ones((128, 8, 8), np.float32)
+    x[3, 4, 5] = np.nan
+    got, want = _f32_case(x, J=50, D=2)
+    assert (np.isnan(got) == np.isnan(want)).all()
+    rel_close(np.nan_to_num(got), np.nan_to_num(want), RTOL32)
+
+
+def test_dense_f32_unaligned_pointer(cuda):
+    """An fp32 tensor that is not 16-byte aligned takes the generic kernel."""
+    rng = np.random.default_rng(23)
+    base = torch.from_numpy(rng.standard_normal(64 * 16 * 8 + 1).astype(np.float32)).cuda()
+    flat = base[1:]
+    t = st.DenseTensor([64, 16, 8], flat)
+    fams = st.families_for([64, 16, 8], st.EstimatorConfig(40, 2, 3))
+    got = st.fcs_dense_batched(t, fams).cpu().numpy()
+    x = flat.cpu().numpy().astype(np.float64).reshape((64, 16, 8), order="F")
+    for d, f in enumerate(fams):
+        b, s, j = oracle_family(f)
+        rel_close(got[d], O.fcs_dense(x, b, s, j), RTOL32)

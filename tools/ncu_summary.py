@@ -1,0 +1,40 @@
+"""Summarise an ncu report: duration, DRAM/L2/L1 throughput, smem wavefronts, stalls."""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+        "lts__t_bytes.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+        "smsp__inst_executed.sum", "smsp__inst_executed_op_shared_ld.sum",
+        "smsp__inst_executed_op_shared_st.sum", "smsp__inst_executed_op_shared_atom.sum",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+        "launch__grid_size", "launch__block_size"]
+
+
+def main(path):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    for row in rows[2:]:
+        d = dict(zip(hdr, row))
+        print("kernel:", d.get("Kernel Name", "?")[:100])
+        for k in KEYS:
+            if k in d:
+                print(f"  {k:75s} {d[k]:>18s} {units[hdr.index(k)]}")
+        stalls = [(k, float(v)) for k, v in d.items()
+                  if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith(
+                      "_per_issue_active.ratio") and v not in ("", "n/a")]
+        stalls.sort(key=lambda x: -x[1])
+        print("  top stalls (warps per issue):",
+              ", ".join(f"{k[34:-23]}={v:.2f}" for k, v in stalls[:6]))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
