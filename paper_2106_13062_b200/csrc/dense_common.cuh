@@ -14,6 +14,7 @@ struct DenseArgs {
   uint32_t jt;                     // composed length J~
   uint32_t last_begin;             // first i_{N-1} of this slab
   uint32_t i0_shift;               // mode-0 table shift (order-1 slabs only)
+  uint32_t inv_d1;                 // floor(2^32 / dims[1]) for fast division (order 3)
   uint64_t fibers;                 // mode-0 fibers in this slab
   uint64_t fibers_per_chunk;
 };

@@ -134,7 +134,9 @@ __device__ __forceinline__ void fiber_offset_fast(const DenseArgs& a, const uint
                                                   uint64_t f, uint32_t& c, uint32_t& sbit) {
   if (a.order == 3 && a.fibers < 0xffffffffull) {
     const uint32_t ff = static_cast<uint32_t>(f);
-    const uint32_t i1 = ff % a.dims[1], i2 = ff / a.dims[1] + a.last_begin;
+    const uint32_t i2r = __umulhi(ff, a.inv_d1);  // ff / dims[1] (exact: ff < 2^32 / dims[1])
+    const uint32_t q2 = ff - i2r * a.dims[1] >= a.dims[1] ? i2r + 1 : i2r;
+    const uint32_t i1 = ff - q2 * a.dims[1], i2 = q2 + a.last_begin;
     const uint32_t e1 = __ldg(tab + a.tab_off[1] + i1), e2 = __ldg(tab + a.tab_off[2] + i2);
     c = (e1 & 0x7fffffffu) + (e2 & 0x7fffffffu);
     sbit = (e1 ^ e2) & 0x80000000u;
@@ -186,31 +188,48 @@ __global__ void __launch_bounds__(512, 1) fcs_dense_fx_kernel(DenseArgs a,
   };
   uint64_t f = f_begin + warp;
   if (f < f_end) load(f, cur);
-  for (; f < f_end; f += nwarps) {
-    if (f + nwarps < f_end) load(f + nwarps, nxt);
+  const uint32_t sk_base = static_cast<uint32_t>(__cvta_generic_to_shared(sk));
+  uint32_t ovf_acc = 0;  // bit 31: a partial overflowed
+  uint32_t rng_acc = 0;  // bits >= 23: a converted element was out of range / non-finite
+  // One fiber: the fiber sign goes into the scale; the byte address of bucket
+  // h0 + c is base + 4c + (entry << 2), the shift discarding the entry's sign bit.
+  auto scatter = [&](const float4* vals, uint64_t fib) {
     uint32_t c, sbit;
-    fiber_offset_fast(a, tab, f, c, sbit);
+    fiber_offset_fast(a, tab, fib, c, sbit);
+    const float scale_f = sbit ? -scale : scale;
+    const uint32_t base_c = sk_base + 4u * c;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       if (lane + 32 * j < nvec) {
-        const float* x = reinterpret_cast<const float*>(&cur[j]);
+        const float* x = reinterpret_cast<const float*>(&vals[j]);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const uint32_t e = e0[j][k];
-          const float y =
-              __uint_as_float(__float_as_uint(x[k]) ^ ((e ^ sbit) & 0x80000000u)) * scale;
-          ovf |= !(fabsf(y) < 4194304.0f);  // |y| < 2^22 (also catches NaN / Inf)
-          // round-to-nearest int via the 1.5 * 2^23 magic number (exact for |y| < 2^22)
-          const int32_t q = __float_as_int(y + 12582912.0f) - 0x4B400000;
-          const int32_t old = atomicAdd(&sk[(e & 0x7fffffffu) + c], q);
+          const float xs = __uint_as_float(__float_as_uint(x[k]) ^ (e & 0x80000000u));
+          // round-to-nearest int via the 1.5 * 2^23 magic number: exact while the
+          // scaled value is below 2^22 in magnitude, i.e. while t < 2^23 below
+          const uint32_t t = __float_as_uint(fmaf(xs, scale_f, 12582912.0f)) - 0x4B000000u;
+          rng_acc |= t;
+          const int32_t q = static_cast<int32_t>(t) - 0x400000;
+          int32_t old;
+          asm volatile("atom.shared.add.s32 %0, [%1], %2;"
+                       : "=r"(old)
+                       : "r"(base_c + (e << 2)), "r"(q));
           const int32_t now = old + q;
-          ovf |= ((old ^ now) & (q ^ now)) < 0;  // signed overflow of the partial
+          ovf_acc |= static_cast<uint32_t>((old ^ now) & (q ^ now));
         }
       }
     }
-#pragma unroll
-    for (int j = 0; j < NV; ++j) cur[j] = nxt[j];
+  };
+  // Ping-pong between the two register buffers (no copies).
+  for (; f < f_end; f += 2 * nwarps) {
+    if (f + nwarps < f_end) load(f + nwarps, nxt);
+    scatter(cur, f);
+    if (f + nwarps >= f_end) break;
+    if (f + 2 * nwarps < f_end) load(f + 2 * nwarps, cur);
+    scatter(nxt, f + nwarps);
   }
+  ovf = (ovf_acc >> 31) | ((rng_acc >> 23) != 0);
 
   const bool overflowed = __syncthreads_or(ovf);
   if (overflowed) {
@@ -390,6 +409,8 @@ int fill_args(size_t order, const size_t* dims, size_t last_begin, size_t last_c
   FCS_CHECK_ARG(last_begin + last_count <= dims[order - 1], "fcs_sketch: slab out of range");
   a->fam_stride = static_cast<uint32_t>(sum_dims);
   a->jt = static_cast<uint32_t>(sum_j - order + 1);
+  if (order >= 2)
+    a->inv_d1 = dims[1] > 1 ? static_cast<uint32_t>((1ull << 32) / dims[1]) : 0xffffffffu;
   a->last_begin = static_cast<uint32_t>(last_begin);
   uint64_t fibers = last_count;
   for (size_t n = 1; n + 1 < order; ++n) fibers *= dims[n];
