@@ -256,9 +256,9 @@ def run_gpu(args):
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_kind": peak_kind, "kernel_ms": k_ms,
                          "algorithmic_bytes_per_launch": alg,
-                         "kernel": "fcs_dense_smem_kernel<float,float> + reduce_partials"},
+                         "kernel": "fcs_dense_fx_kernel<8> (+ fx_sample, fx_scale, reduce_fx)"},
             "e2e": e2e,
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": 4 * args.steps,  # sample, scale, fx scatter, reduce per step
             "clocks": clk.summary(),
         }
     if world == 1 and not args.no_secondary:

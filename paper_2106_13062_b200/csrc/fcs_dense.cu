@@ -149,8 +149,8 @@ __device__ __forceinline__ void fiber_offset_fast(const DenseArgs& a, const uint
 // warp per fiber, lane-owned mode-0 indices with their table entries in
 // registers, NV 128-bit loads per lane with the next fiber prefetched,
 // int32 fixed-point shared-memory accumulation with exact overflow detection.
-template <int NV>
-__global__ void __launch_bounds__(512, 1) fcs_dense_fx_kernel(DenseArgs a,
+template <int NV, int SPLIT, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
                                                               const float* __restrict__ t,
                                                               const uint32_t* __restrict__ packed,
                                                               const FxStats* __restrict__ st,
@@ -164,13 +164,17 @@ __global__ void __launch_bounds__(512, 1) fcs_dense_fx_kernel(DenseArgs a,
   const float scale = ldexpf(1.0f, st->S);
   for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) sk[b] = 0;
 
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  // SPLIT warps share a fiber: warp w takes part w % SPLIT (32*NV vectors) of
+  // fiber group w / SPLIT.
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int warp = wid / SPLIT, nwarps = (blockDim.x >> 5) / SPLIT;
+  const uint32_t vbase = static_cast<uint32_t>(wid % SPLIT) * 32u * NV;
   const uint32_t i0n = a.dims[0];
   const uint32_t nvec = i0n / 4;
   uint32_t e0[NV][4];  // packed mode-0 entries (bucket | sign << 31)
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
-    const uint32_t v = lane + 32 * j;
+    const uint32_t v = vbase + lane + 32 * j;
 #pragma unroll
     for (int k = 0; k < 4; ++k) e0[j][k] = v < nvec ? __ldg(tab + a.i0_shift + v * 4 + k) : 0u;
   }
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(512, 1) fcs_dense_fx_kernel(DenseArgs a,
     const float4* src = reinterpret_cast<const float4*>(t + fib * i0n);
 #pragma unroll
     for (int j = 0; j < NV; ++j)
-      if (lane + 32 * j < nvec) dst[j] = __ldcs(src + lane + 32 * j);
+      if (vbase + lane + 32 * j < nvec) dst[j] = __ldcs(src + vbase + lane + 32 * j);
   };
   uint64_t f = f_begin + warp;
   if (f < f_end) load(f, cur);
@@ -200,7 +204,7 @@ __global__ void __launch_bounds__(512, 1) fcs_dense_fx_kernel(DenseArgs a,
     const uint32_t base_c = sk_base + 4u * c;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      if (lane + 32 * j < nvec) {
+      if (vbase + lane + 32 * j < nvec) {
         const float* x = reinterpret_cast<const float*>(&vals[j]);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -237,7 +241,8 @@ __global__ void __launch_bounds__(512, 1) fcs_dense_fx_kernel(DenseArgs a,
     float* skf = reinterpret_cast<float*>(smem_raw);
     for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) skf[b] = 0.f;
     __syncthreads();
-    for (uint64_t g = f_begin + warp; g < f_end; g += nwarps) {
+    const int wall = threadIdx.x >> 5, nwall = blockDim.x >> 5;
+    for (uint64_t g = f_begin + wall; g < f_end; g += nwall) {
       uint32_t c, sbit;
       fiber_offset(a, tab, g, c, sbit);
       for (uint32_t i = lane; i < i0n; i += 32) {
@@ -324,23 +329,27 @@ struct Plan {
   size_t ws = 0;
 };
 
-// Vectors per lane for the fx kernel (0: not applicable to this shape).
+// fx kernel variant for this shape (0: not applicable): 1..3 = one warp per
+// fiber with 1/2/4/8 vectors per lane (512 threads). (Splitting a fiber over
+// two warps at 1024 threads measured slower on B200: 3.5 vs 2.9 ms at config 4,
+// the 64-register cap spills.)
 int fx_nv(const DenseArgs& a) {
   if (a.dims[0] % 4 != 0) return 0;
   const uint32_t per_lane = (a.dims[0] / 4 + 31) / 32;
   if (per_lane == 0 || per_lane > 8) return 0;
-  return per_lane <= 1 ? 1 : per_lane <= 2 ? 2 : per_lane <= 4 ? 4 : 8;
+  return per_lane <= 1 ? 1 : per_lane <= 2 ? 2 : per_lane <= 4 ? 3 : 4;
 }
 
 using FxKernel = void (*)(DenseArgs, const float*, const uint32_t*, const FxStats*, int32_t*, int*);
-FxKernel fx_kernel(int nv) {
-  switch (nv) {
-    case 1: return fcs_dense_fx_kernel<1>;
-    case 2: return fcs_dense_fx_kernel<2>;
-    case 4: return fcs_dense_fx_kernel<4>;
-    default: return fcs_dense_fx_kernel<8>;
+FxKernel fx_kernel(int v) {
+  switch (v) {
+    case 1: return fcs_dense_fx_kernel<1, 1, 512>;
+    case 2: return fcs_dense_fx_kernel<2, 1, 512>;
+    case 3: return fcs_dense_fx_kernel<4, 1, 512>;
+    default: return fcs_dense_fx_kernel<8, 1, 512>;
   }
 }
+inline int fx_threads(int) { return 512; }
 
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
@@ -362,7 +371,7 @@ int make_plan(const DenseArgs& a, Plan* p) {
   p->nv = sizeof(Tin) == 4 ? fx_nv(a) : 0;
   if (p->nv) {
     p->path = Path::Fx;
-    p->threads = 512;
+    p->threads = fx_threads(p->nv);
     auto k = fx_kernel(p->nv);
     FCS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(p->smem_bytes)));
