@@ -205,7 +205,7 @@ def run_gpu(args):
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("c4_fcs_dense_smem_kernel_bytes_per_launch")
+            traffic = json.load(open(prof)).get("c4_fcs_dense_fx_kernel_bytes_per_launch")
         except Exception:
             traffic = None
 
