@@ -215,17 +215,18 @@ def run_gpu(args):
     host = torch.empty(elems_local, dtype=torch.float32, pin_memory=True)
     host.copy_(x)
     hout = np.empty((C4_D, jt), np.float64)
-    slab_dims = L.size_array([dims[0], dims[1], hi - lo])
     seeds_a = L.u64_array(seeds)
-    for _ in range(1):
-        L.check(lib.st_fcs_dense_host(L.ST_F32, C.c_void_p(host.data_ptr()), 3, slab_dims, C4_D,
-                                      seeds_a, lens_a, hout.ctypes.data_as(C.c_void_p)))
+
+    def e2e_call():
+        L.check(lib.st_fcs_dense_host(L.ST_F32, C.c_void_p(host.data_ptr()), 3, dims_a, lo, hi - lo,
+                                      C4_D, seeds_a, lens_a, hout.ctypes.data_as(C.c_void_p)))
+
+    e2e_call()  # warm-up: device buffers are cached across calls
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        L.check(lib.st_fcs_dense_host(L.ST_F32, C.c_void_p(host.data_ptr()), 3, slab_dims, C4_D,
-                                      seeds_a, lens_a, hout.ctypes.data_as(C.c_void_p)))
+        e2e_call()
         if world > 1:
             tmp = torch.from_numpy(hout).cuda()
             dist.all_reduce(tmp)

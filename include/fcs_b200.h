@@ -102,13 +102,17 @@ int st_fcs_dense(int dtype, const void* tensor, size_t order, const size_t* dims
                  const uint32_t* packed, const size_t* hash_lens, double* out, int accumulate,
                  void* workspace, size_t workspace_bytes, void* stream);
 
-/* HOST-buffer convenience: H2D of the tensor (pinned or pageable), K0 on the
- * device from the seeds, K1, D2H of the D x J~ result, synchronised. The
- * end-to-end call a reference caller makes.
+/* HOST-buffer convenience: K0 on the device from the seeds, then the host
+ * tensor (the slab [last_begin, last_begin + last_count) of the last mode of
+ * `dims`; pass 0 / dims[N-1] for the whole tensor) is copied H2D in chunks on
+ * one stream while K1 sketches the previous chunk on another, then the
+ * D x J~ result is copied D2H; synchronised. Device buffers are cached per
+ * device between calls. With pinned host memory the copies run at full link
+ * speed. The end-to-end call a reference caller makes.
  * Replaces D x fcs_sketch(DenseTensor(dims, data), HashFamily(dims, J, seeds[d])). */
 int st_fcs_dense_host(int dtype, const void* host_tensor, size_t order, const size_t* dims,
-                      size_t sketch_count, const uint64_t* master_seeds, const size_t* hash_lens,
-                      double* host_out);
+                      size_t last_begin, size_t last_count, size_t sketch_count,
+                      const uint64_t* master_seeds, const size_t* hash_lens, double* host_out);
 
 /* Count sketch of R columns (cs_sketch_columns, sketch.cpp:118-133; R = 1 is
  * cs_sketch, sketch.cpp:105-116): u is I x R column-major (device), table is

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <numbers>
@@ -71,6 +72,52 @@ struct DevBuf {
 
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+// Grow-only device buffer.
+struct GrowBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t need) {
+    if (need <= bytes && p) return ST_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, need ? need : 1);
+    if (e != cudaSuccess) return fail(ST_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    bytes = need;
+    return ST_OK;
+  }
+};
+
+// Per-device state of the host-buffer entry: a copy stream, a compute stream,
+// double-buffered staging and cached tables / output / workspace.
+struct HostCtx {
+  std::mutex mu;
+  cudaStream_t copy = nullptr, comp = nullptr;
+  cudaEvent_t copied[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
+  GrowBuf buf[2], tab, out, ws;
+};
+
+int host_ctx(HostCtx** out) {
+  static std::mutex mu;
+  static HostCtx* ctx[64] = {};
+  int dev = 0;
+  FCS_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(ST_ECUDA, "device index out of range");
+  std::lock_guard<std::mutex> lock(mu);
+  if (!ctx[dev]) {
+    auto* c = new HostCtx();
+    FCS_CUDA_TRY(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    FCS_CUDA_TRY(cudaStreamCreateWithFlags(&c->comp, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      FCS_CUDA_TRY(cudaEventCreateWithFlags(&c->copied[b], cudaEventDisableTiming));
+      FCS_CUDA_TRY(cudaEventCreateWithFlags(&c->done[b], cudaEventDisableTiming));
+    }
+    ctx[dev] = c;
+  }
+  *out = ctx[dev];
+  return ST_OK;
+}
+
 }  // namespace fcs
 
 using namespace fcs;
@@ -79,7 +126,7 @@ extern "C" {
 
 const char* st_last_error(void) { return g_last_error.c_str(); }
 
-int st_abi_version(void) { return 1; }
+int st_abi_version(void) { return 2; }
 
 int st_device_query(int* sm_count, size_t* smem_optin, size_t* l2_bytes) {
   DeviceInfo di;
@@ -138,43 +185,61 @@ int st_fcs_dense(int dtype, const void* tensor, size_t order, const size_t* dims
 }
 
 int st_fcs_dense_host(int dtype, const void* host_tensor, size_t order, const size_t* dims,
-                      size_t sketch_count, const uint64_t* master_seeds, const size_t* hash_lens,
-                      double* host_out) {
+                      size_t last_begin, size_t last_count, size_t sketch_count,
+                      const uint64_t* master_seeds, const size_t* hash_lens, double* host_out) {
   FCS_CHECK_ARG(dtype == ST_F32 || dtype == ST_F64, "st_fcs_dense_host: unknown dtype");
   FCS_CHECK_ARG(order >= 1 && order <= ST_MAX_ORDER, "fcs_sketch: unsupported tensor order");
-  size_t total = 1, sum_dims = 0, sum_j = 0;
+  FCS_CHECK_ARG(sketch_count >= 1, "EstimatorConfig: hash_len and sketch_count must be >= 1");
+  size_t per_slab = 1, sum_dims = 0, sum_j = 0;
   for (size_t n = 0; n < order; ++n) {
     FCS_CHECK_ARG(dims[n] > 0 && hash_lens[n] > 0, "HashPair: dimensions must be positive");
-    total *= dims[n];
+    if (n + 1 < order) per_slab *= dims[n];
     sum_dims += dims[n];
     sum_j += hash_lens[n];
   }
+  FCS_CHECK_ARG(last_begin + last_count <= dims[order - 1], "fcs_sketch: slab out of range");
   const size_t jt = sum_j - order + 1;
   const size_t esz = dtype == ST_F32 ? 4 : 8;
-  cudaStream_t st;
-  FCS_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  struct StreamGuard {
-    cudaStream_t s;
-    ~StreamGuard() { cudaStreamDestroy(s); }
-  } guard{st};
-  DevBuf dt, dtab, dout, dws;
-  if (int rc = dt.alloc(total * esz)) return rc;
-  if (int rc = dtab.alloc(sketch_count * sum_dims * sizeof(uint32_t))) return rc;
-  if (int rc = dout.alloc(sketch_count * jt * sizeof(double))) return rc;
-  const size_t ws =
-      st_fcs_dense_workspace(dtype, order, dims, dims[order - 1], sketch_count, hash_lens);
-  if (int rc = dws.alloc(ws)) return rc;
-  FCS_CUDA_TRY(cudaMemcpyAsync(dt.p, host_tensor, total * esz, cudaMemcpyHostToDevice, st));
+  HostCtx* hc = nullptr;
+  if (int rc = host_ctx(&hc)) return rc;
+  std::lock_guard<std::mutex> lock(hc->mu);
+  // chunking of the slab along the last mode (order 1: a single chunk)
+  const size_t nchunks = order == 1 ? 1 : std::min<size_t>(8, std::max<size_t>(1, last_count));
+  const size_t per_chunk = (last_count + nchunks - 1) / nchunks;
+  const size_t chunk_elems = (order == 1 ? last_count : per_chunk * per_slab);
+  size_t ws = st_fcs_dense_workspace(dtype, order, dims, std::max<size_t>(per_chunk, 1),
+                                     sketch_count, hash_lens);
+  if (int rc = hc->buf[0].ensure(chunk_elems * esz)) return rc;
+  if (int rc = hc->buf[1].ensure(chunk_elems * esz)) return rc;
+  if (int rc = hc->tab.ensure(sketch_count * sum_dims * sizeof(uint32_t))) return rc;
+  if (int rc = hc->out.ensure(sketch_count * jt * sizeof(double))) return rc;
+  if (int rc = hc->ws.ensure(ws)) return rc;
+  double* dout = static_cast<double*>(hc->out.p);
   if (int rc = st_family_tables(order, dims, hash_lens, sketch_count, master_seeds,
-                                static_cast<uint32_t*>(dtab.p), st))
+                                static_cast<uint32_t*>(hc->tab.p), hc->comp))
     return rc;
-  if (int rc = st_fcs_dense(dtype, dt.p, order, dims, 0, dims[order - 1], sketch_count,
-                            static_cast<uint32_t*>(dtab.p), hash_lens,
-                            static_cast<double*>(dout.p), 0, dws.p, ws, st))
-    return rc;
-  FCS_CUDA_TRY(cudaMemcpyAsync(host_out, dout.p, sketch_count * jt * sizeof(double),
-                               cudaMemcpyDeviceToHost, st));
-  FCS_CUDA_TRY(cudaStreamSynchronize(st));
+  if (last_count == 0)
+    FCS_CUDA_TRY(cudaMemsetAsync(dout, 0, sketch_count * jt * sizeof(double), hc->comp));
+  const char* src = static_cast<const char*>(host_tensor);
+  for (size_t k = 0; k * per_chunk < last_count; ++k) {
+    const size_t lo = k * per_chunk, cnt = std::min(per_chunk, last_count - lo);
+    const int b = static_cast<int>(k & 1);
+    const size_t bytes = (order == 1 ? cnt : cnt * per_slab) * esz;
+    // the copy may overwrite buffer b only after the sketch that used it finished
+    FCS_CUDA_TRY(cudaStreamWaitEvent(hc->copy, hc->done[b], 0));
+    FCS_CUDA_TRY(cudaMemcpyAsync(hc->buf[b].p, src + (order == 1 ? lo : lo * per_slab) * esz,
+                                 bytes, cudaMemcpyHostToDevice, hc->copy));
+    FCS_CUDA_TRY(cudaEventRecord(hc->copied[b], hc->copy));
+    FCS_CUDA_TRY(cudaStreamWaitEvent(hc->comp, hc->copied[b], 0));
+    if (int rc = st_fcs_dense(dtype, hc->buf[b].p, order, dims, last_begin + lo, cnt, sketch_count,
+                              static_cast<uint32_t*>(hc->tab.p), hash_lens, dout, k > 0 ? 1 : 0,
+                              hc->ws.p, ws, hc->comp))
+      return rc;
+    FCS_CUDA_TRY(cudaEventRecord(hc->done[b], hc->comp));
+  }
+  FCS_CUDA_TRY(cudaMemcpyAsync(host_out, dout, sketch_count * jt * sizeof(double),
+                               cudaMemcpyDeviceToHost, hc->comp));
+  FCS_CUDA_TRY(cudaStreamSynchronize(hc->comp));
   return ST_OK;
 }
 

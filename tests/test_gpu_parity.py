@@ -403,3 +403,29 @@ def test_rtpm_well_conditioned_vs_oracle(cuda):
     rel_close(cp.weights, w, 1e-8)
     rel_close(cp._factors_cm[0].t(), f, 1e-8)
     assert np.allclose(np.sort(w)[::-1], [3.0, 2.0, 1.5], atol=0.15)
+
+
+def test_dense_host_entry_slabs(cuda):
+    """st_fcs_dense_host (host buffers, chunked H2D/compute pipeline) on a slab
+    [lo, hi) of the last mode equals the device path's partial for that slab."""
+    import ctypes as C
+    from paper_2106_13062_b200 import _lib as L
+    from paper_2106_13062_b200 import dist
+    rng = np.random.default_rng(41)
+    dims = [128, 24, 40]
+    x = rng.standard_normal(dims).astype(np.float32)
+    fams = st.families_for(dims, st.EstimatorConfig(300, 3, 12))
+    t = st.DenseTensor.from_array(x)
+    lens = L.size_array([300] * 3)
+    seeds = L.u64_array([f.master_seed() for f in fams])
+    for rank, world in ((0, 1), (1, 3), (2, 3)):
+        lo, hi = dist.shard_range(dims[-1], rank, world)
+        host = np.ascontiguousarray(x[:, :, lo:hi].ravel(order="F"))
+        out = np.empty((3, 898), np.float64)
+        L.check(L.lib().st_fcs_dense_host(L.ST_F32, host.ctypes.data_as(C.c_void_p), 3,
+                                          L.size_array(dims), lo, hi - lo, 3, seeds, lens,
+                                          out.ctypes.data_as(C.c_void_p)))
+        xs = np.zeros_like(x, dtype=np.float64)
+        xs[:, :, lo:hi] = x[:, :, lo:hi]
+        want = np.stack([O.fcs_dense(xs, *oracle_family(f)) for f in fams])
+        rel_close(out, want, RTOL32)

@@ -71,6 +71,11 @@ __global__ void __launch_bounds__(512, 1) scatter(const float* __restrict__ t, c
         } else if (MODE == 1) {
           const int q = __float2int_rn(val * 1048576.f);
           asm volatile("red.shared.add.s32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(sk + idx)), "r"(q));
+        } else if (MODE == 5) {  // same instruction stream, conflict-free banks (upper bound)
+          const int q = __float2int_rn(val * 1048576.f);
+          const uint32_t cf = ((idx & ~31u) | lane) % JT;
+          const int old = atomicAdd(sk + cf, q);
+          ovf |= (old ^ (old + q)) & (q ^ (old + q));
         } else if (MODE == 4) {
           const int q = __float2int_rn(val * 1048576.f);
           const int old = atomicAdd(sk + idx, q);
@@ -122,5 +127,6 @@ int main() {
   run<1>("red.shared.add.s32 fixed point", t, tab, out, sms);
   run<2>("plain RMW (racy bound)", t, tab, out, sms);
   run<4>("atom.shared.add.s32 + overflow check", t, tab, out, sms);
+  run<5>("same, conflict-free banks (bound)", t, tab, out, sms);
   return 0;
 }
