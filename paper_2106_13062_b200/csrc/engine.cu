@@ -140,7 +140,7 @@ size_t st_fcs_cp_workspace(size_t order, const size_t* dims, size_t rank, size_t
   for (size_t n = 0; n < order; ++n) sum_j += hash_lens[n];
   FftPlan pl;
   if (get_fft_plan(sum_j - order + 1, &pl) != ST_OK) return 0;
-  return std::max<size_t>(1, rank) * sketch_count * pl.P * sizeof(double2);
+  return (std::max<size_t>(1, rank) + 1) * sketch_count * pl.P * sizeof(double2);
 }
 
 int st_fcs_cp(const double* weights, size_t rank, size_t order, const size_t* dims,
@@ -168,7 +168,7 @@ int st_fcs_cp(const double* weights, size_t rank, size_t order, const size_t* di
   const size_t jt = sum_j - order + 1;
   FftPlan pl;
   if (int rc = get_fft_plan(jt, &pl)) return rc;
-  const size_t need = std::max<size_t>(1, r_count) * sketch_count * pl.P * sizeof(double2);
+  const size_t need = (std::max<size_t>(1, r_count) + 1) * sketch_count * pl.P * sizeof(double2);
   FCS_CHECK_ARG(workspace && workspace_bytes >= need, "st_fcs_cp: workspace too small");
   return launch_cp(pl, a, static_cast<int>(sketch_count), packed,
                    static_cast<double2*>(workspace), out, static_cast<int>(jt), accumulate,

@@ -39,7 +39,10 @@ struct FftPlan {
   const int* f2p;              // device: slot position of frequency k, k in [0, P)
 };
 
-__device__ __forceinline__ uint32_t swz(uint32_t s) { return s ^ ((s >> 4) & 7u); }
+// XOR swizzle of 16-byte slots: the low 3 bits (slot within a 128-byte
+// wavefront) are XORed with bits 3-5, so stride-1, -8 and -16 slot patterns of
+// the butterfly passes land on distinct bank groups.
+__device__ __forceinline__ uint32_t swz(uint32_t s) { return s ^ ((s >> 3) & 7u); }
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));

@@ -12,12 +12,13 @@ namespace fcs {
 
 namespace {
 
-// Smallest M >= n (M even, M = 2^a 3^b with b <= 2) not above kMaxFftM.
+// Smallest M >= n (M = 2^a 3^b with a >= 4, b <= 2) not above kMaxFftM. a >= 4
+// keeps P = M/2 a multiple of 8, which the slot swizzle (groups of 8) needs.
 int choose_m(size_t n) {
   int best = 0;
   for (int b3 = 1; b3 <= 9; b3 *= 3) {
-    for (long m = 2L * b3; m <= kMaxFftM; m *= 2) {
-      if (m >= static_cast<long>(n) && m >= 32 && (best == 0 || m < best)) best = static_cast<int>(m);
+    for (long m = 16L * b3; m <= kMaxFftM; m *= 2) {
+      if (m >= static_cast<long>(n) && (best == 0 || m < best)) best = static_cast<int>(m);
     }
   }
   return best;

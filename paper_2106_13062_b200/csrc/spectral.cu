@@ -146,23 +146,32 @@ __global__ void __launch_bounds__(kFftThreads) cp_rank_kernel(FftPlan pl, CpArgs
   }
 }
 
-// K4-K5: fixed-order sum over ranks per family, one inverse transform, first J~ values.
+// K4: fixed-order sum over ranks, parallel over (slot, family): acc[d][s] =
+// sum_{r: w_r != 0} Q[d][r][s] (convolved_cp_sketch sums per rank, sketch.cpp:73-84;
+// here in the frequency domain by linearity).
+__global__ void cp_rank_sum_kernel(const double2* __restrict__ Q, const double* __restrict__ weights,
+                                   int r_begin, int r_count, int P, double2* __restrict__ acc) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  const int d = blockIdx.y;
+  if (s >= P) return;
+  double2 a = make_double2(0.0, 0.0);
+  const double2* q = Q + static_cast<size_t>(d) * r_count * P + s;
+  for (int rl = 0; rl < r_count; ++rl) {
+    if (weights[r_begin + rl] == 0.0) continue;
+    a = cadd(a, q[static_cast<size_t>(rl) * P]);
+  }
+  acc[static_cast<size_t>(d) * P + s] = a;
+}
+
+// K5: one inverse transform per family, first J~ values into out.
 __global__ void __launch_bounds__(kFftThreads) cp_sum_kernel(FftPlan pl,
-                                                             const double2* __restrict__ Q,
-                                                             const double* weights, int r_begin,
-                                                             int r_count, double* out, int jt,
-                                                             int accumulate) {
+                                                             const double2* __restrict__ acc,
+                                                             double* out, int jt, int accumulate) {
   const Smem sm = carve(pl);
   load_twiddles(sm.tw, pl);
   const int d = blockIdx.x;
-  for (int s = tid(); s < pl.P; s += blockDim.x) {
-    double2 acc = make_double2(0.0, 0.0);
-    for (int rl = 0; rl < r_count; ++rl) {
-      if (weights[r_begin + rl] == 0.0) continue;
-      acc = cadd(acc, Q[(static_cast<size_t>(d) * r_count + rl) * pl.P + s]);
-    }
-    sm.buf[swz(s)] = acc;
-  }
+  const double2* a = acc + static_cast<size_t>(d) * pl.P;
+  for (int s = tid(); s < pl.P; s += blockDim.x) sm.buf[swz(s)] = a[s];
   irfft_in_place(sm, pl);
   const double inv = 1.0 / pl.P;
   double* o = out + static_cast<size_t>(d) * jt;
@@ -405,9 +414,14 @@ int launch_cp(const FftPlan& pl, const CpArgs& a, int D, const uint32_t* packed,
     cp_rank_kernel<<<dim3(a.r_count, D), kFftThreads, sm, st>>>(pl, a, packed, Q);
     FCS_CUDA_TRY(cudaGetLastError());
   }
+  // The summed spectra go to their own region after Q (st_fcs_cp_workspace
+  // reserves D*P extra slots).
+  double2* acc = Q + static_cast<size_t>(D) * std::max(a.r_count, 1) * pl.P;
+  cp_rank_sum_kernel<<<dim3(ceil_div(pl.P, 256), D), 256, 0, st>>>(Q, a.weights, a.r_begin,
+                                                                   a.r_count, pl.P, acc);
+  FCS_CUDA_TRY(cudaGetLastError());
   if (int rc = prep(cp_sum_kernel, pl, &sm)) return rc;
-  cp_sum_kernel<<<D, kFftThreads, sm, st>>>(pl, Q, a.weights, a.r_begin, a.r_count, out, jt,
-                                            accumulate);
+  cp_sum_kernel<<<D, kFftThreads, sm, st>>>(pl, acc, out, jt, accumulate);
   FCS_CUDA_TRY(cudaGetLastError());
   return ST_OK;
 }
