@@ -157,6 +157,50 @@ int st_fcs_kron(const double* a, size_t ra, size_t ca, const double* b, size_t r
                 size_t sketch_count, const uint32_t* packed, const size_t* hash_lens,
                 double* out, void* stream);
 
+/* ------------------------------------------------------ TS and HCS sketches */
+
+/* Tensor sketch of a dense tensor: bucket (sum_n h_n) mod J, all J_n equal
+ * (else ST_EINVAL "ts_sketch: all hash lengths must be equal"); out is D x J.
+ * Computed as the J-periodic fold of the dense FCS.
+ * Replaces ts_sketch(const DenseTensor&, const HashFamily&), sketch.cpp:135-149. */
+size_t st_ts_dense_workspace(int dtype, size_t order, const size_t* dims, size_t last_count,
+                             size_t sketch_count, const size_t* hash_lens);
+int st_ts_dense(int dtype, const void* tensor, size_t order, const size_t* dims, size_t last_begin,
+                size_t last_count, size_t sketch_count, const uint32_t* packed,
+                const size_t* hash_lens, double* out, int accumulate, void* workspace,
+                size_t workspace_bytes, void* stream);
+
+/* Tensor sketch of a CP tensor: circular convolution at length J of the
+ * factor count sketches (= fold of the CP-form FCS); out is D x J.
+ * Replaces ts_sketch(const CpTensor&, const HashFamily&), sketch.cpp:151-155. */
+size_t st_ts_cp_workspace(size_t order, const size_t* dims, size_t rank, size_t sketch_count,
+                          const size_t* hash_lens);
+int st_ts_cp(const double* weights, size_t rank, size_t order, const size_t* dims,
+             const double* const* factors /* HOST array of device ptrs */, size_t r_begin,
+             size_t r_count, size_t sketch_count, const uint32_t* packed,
+             const size_t* hash_lens, double* out, int accumulate, void* workspace,
+             size_t workspace_bytes, void* stream);
+
+/* Higher-order count sketch of a dense tensor into a J_0 x ... x J_{N-1}
+ * column-major tensor per family (D x prod J_n doubles, prod J_n < 2^31).
+ * Replaces hcs_sketch(const DenseTensor&, const HashFamily&), sketch.cpp:157-173. */
+size_t st_hcs_dense_workspace(int dtype, size_t order, const size_t* dims, size_t last_count,
+                              size_t sketch_count, const size_t* hash_lens);
+int st_hcs_dense(int dtype, const void* tensor, size_t order, const size_t* dims,
+                 size_t last_begin, size_t last_count, size_t sketch_count, const uint32_t* packed,
+                 const size_t* hash_lens, double* out, int accumulate, void* workspace,
+                 size_t workspace_bytes, void* stream);
+
+/* Higher-order count sketch of a CP tensor: sum_r w_r CS_0(u_r) o ... o CS_{N-1}(u_r)
+ * (zero weights skipped), D x prod J_n.
+ * Replaces hcs_sketch(const CpTensor&, const HashFamily&), sketch.cpp:175-185. */
+size_t st_hcs_cp_workspace(size_t order, const size_t* dims, size_t rank, size_t sketch_count,
+                           const size_t* hash_lens);
+int st_hcs_cp(const double* weights, size_t rank, size_t order, const size_t* dims,
+              const double* const* factors /* HOST array of device ptrs */, size_t sketch_count,
+              const uint32_t* packed, const size_t* hash_lens, double* out, int accumulate,
+              void* workspace, size_t workspace_bytes, void* stream);
+
 /* --------------------------------------------- sketched contraction engine */
 
 typedef struct st_engine st_engine;

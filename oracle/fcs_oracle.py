@@ -477,3 +477,27 @@ def gaussian_stream(seed: int, n: int) -> np.ndarray:  # noqa: D401
     out[0::2] = radius * np.cos(angle)
     out[1::2] = radius * np.sin(angle)
     return out[:n]
+
+
+def ts_cp(weights, factors, buckets, signs, hash_lens) -> np.ndarray:
+    """ts_sketch(CpTensor) (sketch.cpp:151-155): circular convolution at length J."""
+    if len(set(hash_lens)) != 1:
+        raise ValueError("ts_sketch: all hash lengths must be equal")
+    _check_family(tuple(f.shape[0] for f in factors), buckets, "ts_sketch")
+    return convolved_cp_sketch(weights, factors, buckets, signs, hash_lens, hash_lens[0])
+
+
+def hcs_cp(weights, factors, buckets, signs, hash_lens) -> np.ndarray:
+    """hcs_sketch(CpTensor) (sketch.cpp:175-185): densify of the count-sketched
+    factors (tensor.cpp:86-115, zero weights skipped); returns J_0 x ... array."""
+    _check_family(tuple(f.shape[0] for f in factors), buckets, "hcs_sketch")
+    cs = [cs_sketch_columns(f, b, s, j) for f, b, s, j in zip(factors, buckets, signs, hash_lens)]
+    out = np.zeros(tuple(hash_lens))
+    for r, w in enumerate(np.asarray(weights, np.float64)):
+        if w == 0.0:
+            continue
+        term = np.asarray(w, np.float64)
+        for c in cs:
+            term = np.multiply.outer(term, c[:, r])
+        out += term
+    return out

@@ -366,3 +366,49 @@ def residual_norm_sym(t: np.ndarray, weights, factor) -> float:
     _check(lib().ref_residual_norm_sym(_ptr(data), _sz(dim), _ptr(w), _sz(len(w)), _ptr(f),
                                        C.byref(out)))
     return out.value
+
+
+def ts_dense_tables(t: np.ndarray, buckets, signs, hash_lens) -> np.ndarray:
+    """ts_sketch(DenseTensor, HashFamily) (sketch.cpp:135-149)."""
+    dims = _dims(t.shape)
+    data = np.ascontiguousarray(np.asarray(t, np.float64).ravel(order="F"))
+    b, s = _pack_tables(buckets, signs)
+    hl = _dims(hash_lens)
+    out = np.empty(int(hl[0]), np.float64)
+    _check(lib().ref_ts_dense_tables(_ptr(data), _sz(len(dims)), _ptr(dims), _ptr(b), _ptr(s),
+                                     _ptr(hl), _ptr(out)))
+    return out
+
+
+def ts_cp_tables(weights, factors, buckets, signs, hash_lens) -> np.ndarray:
+    """ts_sketch(CpTensor, HashFamily) (sketch.cpp:151-155)."""
+    w, dims, fs = _pack_cp(weights, factors)
+    b, s = _pack_tables(buckets, signs)
+    hl = _dims(hash_lens)
+    out = np.empty(int(hl[0]), np.float64)
+    _check(lib().ref_ts_cp_tables(_ptr(w), _sz(len(w)), _sz(len(dims)), _ptr(dims), _ptr(fs),
+                                  _ptr(b), _ptr(s), _ptr(hl), _ptr(out)))
+    return out
+
+
+def hcs_dense_tables(t: np.ndarray, buckets, signs, hash_lens) -> np.ndarray:
+    """hcs_sketch(DenseTensor, HashFamily) (sketch.cpp:157-173); J_0 x ... array."""
+    dims = _dims(t.shape)
+    data = np.ascontiguousarray(np.asarray(t, np.float64).ravel(order="F"))
+    b, s = _pack_tables(buckets, signs)
+    hl = _dims(hash_lens)
+    out = np.empty(int(np.prod(hl)), np.float64)
+    _check(lib().ref_hcs_dense_tables(_ptr(data), _sz(len(dims)), _ptr(dims), _ptr(b), _ptr(s),
+                                      _ptr(hl), _ptr(out)))
+    return out.reshape(tuple(int(x) for x in hl), order="F")
+
+
+def hcs_cp_tables(weights, factors, buckets, signs, hash_lens) -> np.ndarray:
+    """hcs_sketch(CpTensor, HashFamily) (sketch.cpp:175-185)."""
+    w, dims, fs = _pack_cp(weights, factors)
+    b, s = _pack_tables(buckets, signs)
+    hl = _dims(hash_lens)
+    out = np.empty(int(np.prod(hl)), np.float64)
+    _check(lib().ref_hcs_cp_tables(_ptr(w), _sz(len(w)), _sz(len(dims)), _ptr(dims), _ptr(fs),
+                                   _ptr(b), _ptr(s), _ptr(hl), _ptr(out)))
+    return out.reshape(tuple(int(x) for x in hl), order="F")

@@ -368,3 +368,51 @@ int ref_residual_norm_sym(const double* data, std::size_t dim, const double* wei
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- TS / HCS
+extern "C" {
+
+// ts_sketch(DenseTensor, explicit HashFamily) (sketch.cpp:135-149).
+int ref_ts_dense_tables(const double* data, std::size_t order, const std::size_t* dims,
+                        const std::uint32_t* buckets, const std::int8_t* signs,
+                        const std::size_t* hash_lens, double* out) {
+  return guarded([&] {
+    DenseTensor t = make_tensor(data, order, dims);
+    copy_out(ts_sketch(t, make_family(order, dims, buckets, signs, hash_lens)).values, out);
+  });
+}
+
+// ts_sketch(CpTensor, explicit HashFamily) (sketch.cpp:151-155).
+int ref_ts_cp_tables(const double* weights, std::size_t rank, std::size_t order,
+                     const std::size_t* dims, const double* factors, const std::uint32_t* buckets,
+                     const std::int8_t* signs, const std::size_t* hash_lens, double* out) {
+  return guarded([&] {
+    CpTensor cp = make_cp(weights, rank, order, dims, factors);
+    copy_out(ts_sketch(cp, make_family(order, dims, buckets, signs, hash_lens)).values, out);
+  });
+}
+
+// hcs_sketch(DenseTensor, explicit HashFamily) (sketch.cpp:157-173); out is prod J (col-major).
+int ref_hcs_dense_tables(const double* data, std::size_t order, const std::size_t* dims,
+                         const std::uint32_t* buckets, const std::int8_t* signs,
+                         const std::size_t* hash_lens, double* out) {
+  return guarded([&] {
+    DenseTensor t = make_tensor(data, order, dims);
+    SketchTensor s = hcs_sketch(t, make_family(order, dims, buckets, signs, hash_lens));
+    std::memcpy(out, s.values.data().data(), sizeof(double) * s.values.size());
+  });
+}
+
+// hcs_sketch(CpTensor, explicit HashFamily) (sketch.cpp:175-185).
+int ref_hcs_cp_tables(const double* weights, std::size_t rank, std::size_t order,
+                      const std::size_t* dims, const double* factors,
+                      const std::uint32_t* buckets, const std::int8_t* signs,
+                      const std::size_t* hash_lens, double* out) {
+  return guarded([&] {
+    CpTensor cp = make_cp(weights, rank, order, dims, factors);
+    SketchTensor s = hcs_sketch(cp, make_family(order, dims, buckets, signs, hash_lens));
+    std::memcpy(out, s.values.data().data(), sizeof(double) * s.values.size());
+  });
+}
+
+}  // extern "C"

@@ -6,7 +6,8 @@ sm_100a CUDA kernels behind the C-ABI in ``include/fcs_b200.h``
 compute call loads the library and fails loudly if it or the GPU is missing.
 """
 from .sketchtensor import (CpTensor, DenseTensor, EstimatorConfig, HashFamily, HashPair,  # noqa
-                           SketchKind, SketchVec, convolve_pairs, cs_sketch, cs_sketch_columns,
+                           SketchKind, SketchTensor, SketchVec, convolve_pairs, cs_sketch,
+                           cs_sketch_columns,
                            families_for, family_seed, fcs_cp_batched, fcs_dense_batched,
                            fcs_kron, fcs_sketch, hcs_sketch, median_reduce, packed_families,
                            ts_sketch)

@@ -37,6 +37,14 @@ SIGNATURES = {
     "st_fcs_cp": (i32, [p, sz, sz, p, p, sz, sz, sz, p, p, p, i32, p, sz, p]),
     "st_convolve_pairs": (i32, [p, sz, p, sz, sz, p, p]),
     "st_fcs_kron": (i32, [p, sz, sz, p, sz, sz, sz, p, p, p, p]),
+    "st_ts_dense_workspace": (sz, [i32, sz, p, sz, sz, p]),
+    "st_ts_dense": (i32, [i32, p, sz, p, sz, sz, sz, p, p, p, i32, p, sz, p]),
+    "st_ts_cp_workspace": (sz, [sz, p, sz, sz, p]),
+    "st_ts_cp": (i32, [p, sz, sz, p, p, sz, sz, sz, p, p, p, i32, p, sz, p]),
+    "st_hcs_dense_workspace": (sz, [i32, sz, p, sz, sz, p]),
+    "st_hcs_dense": (i32, [i32, p, sz, p, sz, sz, sz, p, p, p, i32, p, sz, p]),
+    "st_hcs_cp_workspace": (sz, [sz, p, sz, sz, p]),
+    "st_hcs_cp": (i32, [p, sz, sz, p, p, sz, p, p, p, i32, p, sz, p]),
     "st_engine_create": (i32, [p, i32, p, p, sz, sz, u64, p]),
     "st_engine_destroy": (i32, [p]),
     "st_engine_composed_len": (sz, [p]),

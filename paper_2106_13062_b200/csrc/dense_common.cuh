@@ -1,17 +1,22 @@
-// Shared pieces of the dense-FCS kernels (fcs_dense.cu, fcs_round.cu).
+// Shared pieces of the dense sketch kernels (fcs_dense.cu).
 #pragma once
 
 #include "common.cuh"
 
 namespace fcs {
 
+// A dense sketch launch. The composed bucket of multi-index (i_0..i_{N-1}) is
+// sum_n mult[n] * h_n(i_n) with mult[0] = 1:
+//   FCS (sketch.cpp:187-201): mult[n] = 1, out length J~ = sum J_n - N + 1;
+//   HCS (sketch.cpp:157-173): mult[n] = J_0 * ... * J_{n-1}, out length prod J_n.
 struct DenseArgs {
   int order;
   int D;
   uint32_t dims[ST_MAX_ORDER];
   uint32_t tab_off[ST_MAX_ORDER];  // start of mode n inside one family's tables
+  uint32_t mult[ST_MAX_ORDER];     // bucket multiplier of mode n (mult[0] = 1)
   uint32_t fam_stride;             // sum(dims): distance between families
-  uint32_t jt;                     // composed length J~
+  uint32_t jt;                     // output length per family (J~ for FCS)
   uint32_t last_begin;             // first i_{N-1} of this slab
   uint32_t i0_shift;               // mode-0 table shift (order-1 slabs only)
   uint32_t inv_d1;                 // floor(2^32 / dims[1]) for fast division (order 3)
@@ -33,7 +38,7 @@ __device__ __forceinline__ void fiber_offset(const DenseArgs& a, const uint32_t*
       i = f + a.last_begin;
     }
     const uint32_t e = __ldg(tab + a.tab_off[n] + i);
-    c += e & 0x7fffffffu;
+    c += (e & 0x7fffffffu) * a.mult[n];
     sbit ^= e & 0x80000000u;
   }
 }
@@ -41,17 +46,6 @@ __device__ __forceinline__ void fiber_offset(const DenseArgs& a, const uint32_t*
 template <typename Tacc>
 __device__ __forceinline__ Tacc signed_val(Tacc v, uint32_t sbit) {
   return sbit ? -v : v;
-}
-
-// One shared-memory compare-and-swap of the bit pattern; true if `desired`
-// was stored (the word still held `expected`).
-__device__ __forceinline__ bool cas_update(float* p, float expected, float desired) {
-  const unsigned e = __float_as_uint(expected);
-  return atomicCAS(reinterpret_cast<unsigned*>(p), e, __float_as_uint(desired)) == e;
-}
-__device__ __forceinline__ bool cas_update(double* p, double expected, double desired) {
-  const unsigned long long e = __double_as_longlong(expected);
-  return atomicCAS(reinterpret_cast<unsigned long long*>(p), e, __double_as_longlong(desired)) == e;
 }
 
 }  // namespace fcs

@@ -33,10 +33,10 @@ int launch_normalize_rows(double*, int, int, cudaStream_t);
 int launch_refine_update(double*, const double*, int, int*, cudaStream_t);
 int launch_family_tables(size_t, const size_t*, const size_t*, size_t, const uint64_t*,
                          uint32_t*, cudaStream_t);
-size_t dense_workspace(int, size_t, const size_t*, size_t, size_t, const size_t*);
+size_t dense_workspace(int, size_t, const size_t*, size_t, size_t, const size_t*, int kind = 0);
 int launch_fcs_dense(int, const void*, size_t, const size_t*, size_t, size_t, size_t,
                      const uint32_t*, const size_t*, double*, int, void*, size_t, cudaStream_t,
-                     size_t fam_stride);
+                     size_t fam_stride = 0, int kind = 0);
 
 namespace {
 

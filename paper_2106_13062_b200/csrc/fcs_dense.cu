@@ -138,7 +138,7 @@ __device__ __forceinline__ void fiber_offset_fast(const DenseArgs& a, const uint
     const uint32_t q2 = ff - i2r * a.dims[1] >= a.dims[1] ? i2r + 1 : i2r;
     const uint32_t i1 = ff - q2 * a.dims[1], i2 = q2 + a.last_begin;
     const uint32_t e1 = __ldg(tab + a.tab_off[1] + i1), e2 = __ldg(tab + a.tab_off[2] + i2);
-    c = (e1 & 0x7fffffffu) + (e2 & 0x7fffffffu);
+    c = (e1 & 0x7fffffffu) * a.mult[1] + (e2 & 0x7fffffffu) * a.mult[2];
     sbit = (e1 ^ e2) & 0x80000000u;
   } else {
     fiber_offset(a, tab, f, c, sbit);
@@ -396,28 +396,32 @@ int make_plan(const DenseArgs& a, Plan* p) {
   return ST_OK;
 }
 
+// kind 0: FCS (bucket sum), kind 1: HCS (mixed-radix bucket, sketch.cpp:157-173).
 int fill_args(size_t order, const size_t* dims, size_t last_begin, size_t last_count, size_t D,
-              const size_t* hash_lens, DenseArgs* a) {
+              const size_t* hash_lens, DenseArgs* a, int kind = 0) {
   FCS_CHECK_ARG(order >= 1 && order <= ST_MAX_ORDER, "fcs_sketch: unsupported tensor order");
   FCS_CHECK_ARG(D >= 1, "EstimatorConfig: hash_len and sketch_count must be >= 1");
   *a = DenseArgs{};
   a->order = static_cast<int>(order);
   a->D = static_cast<int>(D);
-  uint64_t sum_dims = 0, sum_j = 0;
+  uint64_t sum_dims = 0, sum_j = 0, prod_j = 1;
   for (size_t n = 0; n < order; ++n) {
     FCS_CHECK_ARG(dims[n] > 0 && hash_lens[n] > 0, "HashPair: dimensions must be positive");
     FCS_CHECK_ARG(dims[n] < (1u << 31) && hash_lens[n] < (1u << 30),
                   "fcs_sketch: dimension too large");
     a->dims[n] = static_cast<uint32_t>(dims[n]);
     a->tab_off[n] = static_cast<uint32_t>(sum_dims);
+    a->mult[n] = kind == 1 ? static_cast<uint32_t>(prod_j) : 1u;
     sum_dims += dims[n];
     sum_j += hash_lens[n];
+    prod_j *= hash_lens[n];
+    FCS_CHECK_ARG(kind == 0 || prod_j < (1ull << 31), "hcs_sketch: sketch tensor too large");
   }
   FCS_CHECK_ARG(sum_dims < (1ull << 32) && sum_j - order + 1 < (1ull << 31),
                 "fcs_sketch: family too large");
   FCS_CHECK_ARG(last_begin + last_count <= dims[order - 1], "fcs_sketch: slab out of range");
   a->fam_stride = static_cast<uint32_t>(sum_dims);
-  a->jt = static_cast<uint32_t>(sum_j - order + 1);
+  a->jt = static_cast<uint32_t>(kind == 1 ? prod_j : sum_j - order + 1);
   if (order >= 2)
     a->inv_d1 = dims[1] > 1 ? static_cast<uint32_t>((1ull << 32) / dims[1]) : 0xffffffffu;
   a->last_begin = static_cast<uint32_t>(last_begin);
@@ -497,9 +501,9 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
 }  // namespace
 
 size_t dense_workspace(int dtype, size_t order, const size_t* dims, size_t last_count, size_t D,
-                       const size_t* hash_lens) {
+                       const size_t* hash_lens, int kind) {
   DenseArgs a;
-  if (fill_args(order, dims, 0, last_count, D, hash_lens, &a) != ST_OK) return 0;
+  if (fill_args(order, dims, 0, last_count, D, hash_lens, &a, kind) != ST_OK) return 0;
   Plan p;
   const int rc = dtype == ST_F32 ? make_plan<float, float>(a, &p) : make_plan<double, double>(a, &p);
   return rc == ST_OK ? p.ws : 0;
@@ -508,9 +512,9 @@ size_t dense_workspace(int dtype, size_t order, const size_t* dims, size_t last_
 int launch_fcs_dense(int dtype, const void* t, size_t order, const size_t* dims, size_t last_begin,
                      size_t last_count, size_t D, const uint32_t* packed, const size_t* hash_lens,
                      double* out, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st,
-                     size_t fam_stride) {
+                     size_t fam_stride, int kind) {
   DenseArgs a;
-  if (int rc = fill_args(order, dims, last_begin, last_count, D, hash_lens, &a)) return rc;
+  if (int rc = fill_args(order, dims, last_begin, last_count, D, hash_lens, &a, kind)) return rc;
   if (fam_stride) a.fam_stride = static_cast<uint32_t>(fam_stride);
   if (dtype == ST_F32)
     return run_dense<float, float>(a, static_cast<const float*>(t), packed, out, accumulate, ws,

@@ -402,15 +402,86 @@ def cs_sketch(x, pair: HashPair) -> SketchVec:
     return SketchVec(vals, HashFamily(pairs=[pair]), SketchKind.CS)
 
 
+class SketchTensor:
+    """SketchTensor (sketch.hpp:24-29; shape contract sketch.cpp:98-103): a
+    J_0 x ... x J_{N-1} sketch (``values``: ndarray-indexable torch tensor)."""
+
+    def __init__(self, values: torch.Tensor, family: HashFamily):
+        if list(values.shape) != family.hash_lens():
+            raise ValueError("SketchTensor: shape does not match hash lengths")
+        self.values = values
+        self.family = family
+
+
+def _cp_call(fn_ws, fn, cp: CpTensor, fams, out_len, ranks=True):
+    dims = cp.shape()
+    lens = fams[0].hash_lens()
+    packed = packed_families(fams)
+    out = torch.empty((len(fams), out_len), dtype=torch.float64, device=_dev())
+    ws_bytes = fn_ws(len(dims), L.size_array(dims), cp.rank(), len(fams), L.size_array(lens))
+    if ws_bytes == 0:
+        _check(L.ST_EINVAL)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=_dev())
+    fptrs = (C.c_void_p * len(dims))(*[f.data_ptr() for f in cp._factors_cm])
+    if ranks:
+        _check(fn(_ptr(cp.weights), cp.rank(), len(dims), L.size_array(dims), fptrs, 0, cp.rank(),
+                  len(fams), _ptr(packed), L.size_array(lens), _ptr(out), 0, _ptr(ws), ws_bytes,
+                  _stream()))
+    else:
+        _check(fn(_ptr(cp.weights), cp.rank(), len(dims), L.size_array(dims), fptrs, len(fams),
+                  _ptr(packed), L.size_array(lens), _ptr(out), 0, _ptr(ws), ws_bytes, _stream()))
+    return out
+
+
+def _dense_call(fn_ws, fn, t: DenseTensor, fams, out_len):
+    dims = t.shape()
+    lens = fams[0].hash_lens()
+    packed = packed_families(fams)
+    out = torch.empty((len(fams), out_len), dtype=torch.float64, device=_dev())
+    ws_bytes = fn_ws(t.st_dtype, len(dims), L.size_array(dims), dims[-1], len(fams),
+                     L.size_array(lens))
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=_dev())
+    _check(fn(t.st_dtype, _ptr(t.flat), len(dims), L.size_array(dims), 0, dims[-1], len(fams),
+              _ptr(packed), L.size_array(lens), _ptr(out), 0, _ptr(ws), ws_bytes, _stream()))
+    return out
+
+
 def ts_sketch(t, family: HashFamily) -> SketchVec:
-    """ts_sketch (sketch.hpp:40,44): kept in the API; the B200 implementation
-    is the next scope row."""
-    raise NotImplementedError("ts_sketch: not on the B200 hot path yet (SURVEY.md §8(f))")
+    """ts_sketch(DenseTensor|CpTensor, HashFamily) (sketch.hpp:40,44;
+    sketch.cpp:135-155): buckets compose by modular sum; equal J required."""
+    lens = family.hash_lens()
+    if any(j != lens[0] for j in lens):
+        raise ValueError("ts_sketch: all hash lengths must be equal")
+    lib = L.lib()
+    if isinstance(t, CpTensor):
+        _require_family(t.shape(), family, "ts_sketch")
+        vals = _cp_call(lib.st_ts_cp_workspace, lib.st_ts_cp, t, [family], lens[0])[0]
+    else:
+        if not isinstance(t, DenseTensor):
+            t = DenseTensor.from_array(t)
+        _require_family(t.shape(), family, "ts_sketch")
+        vals = _dense_call(lib.st_ts_dense_workspace, lib.st_ts_dense, t, [family], lens[0])[0]
+    return SketchVec(vals, family, SketchKind.TS)
 
 
-def hcs_sketch(t, family: HashFamily):
-    """hcs_sketch (sketch.hpp:47,51): kept in the API; next scope row."""
-    raise NotImplementedError("hcs_sketch: not on the B200 hot path yet (SURVEY.md §8(f))")
+def hcs_sketch(t, family: HashFamily) -> SketchTensor:
+    """hcs_sketch(DenseTensor|CpTensor, HashFamily) (sketch.hpp:47,51;
+    sketch.cpp:157-185): per-mode buckets into a J_0 x ... x J_{N-1} tensor."""
+    lens = family.hash_lens()
+    n_out = int(np.prod(lens))
+    lib = L.lib()
+    if isinstance(t, CpTensor):
+        _require_family(t.shape(), family, "hcs_sketch")
+        flat = _cp_call(lib.st_hcs_cp_workspace, lib.st_hcs_cp, t, [family], n_out,
+                        ranks=False)[0]
+    else:
+        if not isinstance(t, DenseTensor):
+            t = DenseTensor.from_array(t)
+        _require_family(t.shape(), family, "hcs_sketch")
+        flat = _dense_call(lib.st_hcs_dense_workspace, lib.st_hcs_dense, t, [family], n_out)[0]
+    # column-major flat -> tensor indexed [j_0, ..., j_{N-1}]
+    vals = flat.reshape(list(reversed(lens))).permute(*reversed(range(len(lens))))
+    return SketchTensor(vals, family)
 
 
 def convolve_pairs(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:

@@ -64,6 +64,19 @@ def main():
         g[f"cp_f{i}"] = f
     g["cp_sketch"] = ref.fcs_cp(w, fs, 9, ref.family_seed(4, 2))
     g["cp_dense_sketch"] = ref.fcs_dense(ref.densify(w, fs), 9, ref.family_seed(4, 2))
+    # TS / HCS (sketch.cpp:135-185), explicit 3-mode family over 6x5x4, J=7
+    bt, st_, _ = ref.hash_family([6, 5, 4], 7, ref.family_seed(6, 0))
+    g["ts_dense"] = ref.ts_dense_tables(x, bt, st_, [7, 7, 7])
+    g["hcs_dense"] = ref.hcs_dense_tables(x, bt, st_, [7, 7, 7])
+    facs = [ref.gaussian(19, 6 * 3).reshape((6, 3), order="F"),
+            ref.gaussian(20, 5 * 3).reshape((5, 3), order="F"),
+            ref.gaussian(21, 4 * 3).reshape((4, 3), order="F")]
+    wts = np.array([0.5, 0.0, -1.25])
+    for i, f in enumerate(facs):
+        g[f"tscp_f{i}"] = f
+    g["tscp_w"] = wts
+    g["ts_cp"] = ref.ts_cp_tables(wts, facs, bt, st_, [7, 7, 7])
+    g["hcs_cp"] = ref.hcs_cp_tables(wts, facs, bt, st_, [7, 7, 7])
     # FFT helpers
     g["conv_12_20"] = ref.fft_convolve([[1, 2], [2, 0]], 3)
     # Engine: symmetric 8x8x8, J=6, D=3, seed 5

@@ -429,3 +429,45 @@ def test_dense_host_entry_slabs(cuda):
         xs[:, :, lo:hi] = x[:, :, lo:hi]
         want = np.stack([O.fcs_dense(xs, *oracle_family(f)) for f in fams])
         rel_close(out, want, RTOL32)
+
+
+# ------------------------------------------------------------ TS / HCS (§8(f))
+def test_ts_hcs_golden(cuda):
+    x = GOLD["dense_small_x"]
+    fam = st.HashFamily([6, 5, 4], 7, st.family_seed(6, 0))
+    rel_close(st.ts_sketch(x, fam).values, GOLD["ts_dense"], RTOL64)
+    rel_close(st.hcs_sketch(x, fam).values, GOLD["hcs_dense"], RTOL64)
+    fs = [GOLD[f"tscp_f{i}"] for i in range(3)]
+    cp = st.CpTensor(GOLD["tscp_w"], fs)
+    rel_close(st.ts_sketch(cp, fam).values, GOLD["ts_cp"], RTOL64)
+    rel_close(st.hcs_sketch(cp, fam).values, GOLD["hcs_cp"], RTOL64)
+    with pytest.raises(ValueError):
+        st.ts_sketch(x, st.HashFamily([6, 5, 4], [7, 7, 8], 3))
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_ts_hcs_dense_vs_oracle(cuda, dtype):
+    rng = np.random.default_rng(51)
+    x = rng.standard_normal((96, 40, 30)).astype(dtype)
+    fam = st.HashFamily([96, 40, 30], 25, st.family_seed(8, 2))
+    b, s, j = oracle_family(fam)
+    tol = RTOL64 if dtype == np.float64 else RTOL32
+    xd = x.astype(np.float64)
+    rel_close(st.ts_sketch(x, fam).values, O.ts_sketch(xd, b, s, j), tol)
+    rel_close(st.hcs_sketch(x, fam).values, O.hcs_sketch(xd, b, s, j), tol)
+
+
+def test_ts_hcs_cp_vs_oracle(cuda):
+    rng = np.random.default_rng(52)
+    fs = [rng.standard_normal((d, 6)) for d in (50, 40, 30)]
+    w = rng.standard_normal(6)
+    w[2] = 0.0
+    fam = st.HashFamily([50, 40, 30], 20, st.family_seed(9, 0))
+    b, s, j = oracle_family(fam)
+    cp = st.CpTensor(w, fs)
+    rel_close(st.ts_sketch(cp, fam).values, O.ts_cp(w, fs, b, s, j), RTOL64)
+    rel_close(st.hcs_sketch(cp, fam).values, O.hcs_cp(w, fs, b, s, j), RTOL64)
+    # path identities: TS/HCS of CP == TS/HCS of the densified tensor
+    dense = configs.densify(w, fs)
+    rel_close(st.ts_sketch(cp, fam).values, st.ts_sketch(dense, fam).values.cpu().numpy(), 1e-9)
+    rel_close(st.hcs_sketch(cp, fam).values, st.hcs_sketch(dense, fam).values.cpu().numpy(), 1e-9)

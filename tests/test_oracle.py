@@ -159,3 +159,15 @@ def test_restatement_vs_reference_errors():
         ref.hash_pair(1, 0, 4)
     with pytest.raises(ValueError):
         ref.median([])
+
+
+def test_golden_ts_hcs():
+    x = GOLD["dense_small_x"]
+    b, s, j = O.hash_family([6, 5, 4], 7, O.family_seed(6, 0))
+    assert rel_close(O.ts_sketch(x, b, s, j), GOLD["ts_dense"], 1e-13)
+    assert rel_close(O.hcs_sketch(x, b, s, j), GOLD["hcs_dense"], 1e-13)
+    fs = [GOLD[f"tscp_f{i}"] for i in range(3)]
+    assert rel_close(O.ts_cp(GOLD["tscp_w"], fs, b, s, j), GOLD["ts_cp"], 1e-12)
+    assert rel_close(O.hcs_cp(GOLD["tscp_w"], fs, b, s, j), GOLD["hcs_cp"], 1e-12)
+    with pytest.raises(ValueError):
+        O.ts_sketch(x, b, s, [7, 7, 8])
