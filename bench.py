@@ -264,7 +264,7 @@ def run_gpu(args):
         }
     if world == 1 and not args.no_secondary:
         try:
-            line["secondary"] = secondary()
+            line["secondary"] = secondary(x)
         except Exception as e:  # never lose the headline
             line["secondary"] = {"error": repr(e)}
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -279,8 +279,10 @@ def run_gpu(args):
         print(json.dumps(line), flush=True)
 
 
-def secondary():
-    """Configs 2, 3, 5 (and c1) on one GPU: device-resident inputs, CUDA events."""
+def secondary(x=None):
+    """Configs 2, 3, 5 (and c1) on one GPU: device-resident inputs, CUDA events;
+    plus K1 on the config-4 tensor `x` for D = 1, 2, 4 (the update-throughput
+    picture behind the headline's roofline fraction)."""
     import torch
 
     import paper_2106_13062_b200 as st
@@ -299,6 +301,20 @@ def secondary():
         return a.elapsed_time(b) / reps
 
     res = {}
+    if x is not None:
+        peak, _ = hbm_peak()
+        t4 = st.DenseTensor(list(C4_DIMS), x)
+        sweep = []
+        for D in (1, 2, 4):
+            fams = st.families_for(list(C4_DIMS), st.EstimatorConfig(C4_J, D, C4_SEED))
+            packed = st.packed_families(fams)
+            out = st.fcs_dense_batched(t4, fams, packed=packed)
+            ms = timeit(lambda: st.fcs_dense_batched(t4, fams, packed=packed, out=out), 10)
+            alg = algorithmic_bytes(x.numel(), C4_DIMS, D, C4_J)
+            sweep.append({"D": D, "ms": ms, "elements_per_sec": x.numel() / (ms * 1e-3),
+                          "hbm_frac": alg / (ms * 1e-3) / 1e9 / peak,
+                          "updates_per_sec": D * x.numel() / (ms * 1e-3)})
+        res["c4_family_sweep"] = sweep
     c = configs.C1
     x = st.DenseTensor.from_array(configs.c1_tensor(c))
     fams = st.families_for(list(c.dims), st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))

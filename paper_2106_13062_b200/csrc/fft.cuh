@@ -202,6 +202,60 @@ __device__ __forceinline__ void fft_forward(double2* buf, const FftPlan& pl, con
   }
 }
 
+// Two independent forward transforms in one sweep: the butterflies of b0 and
+// b1 at the same position share their twiddles, and because the buffers are
+// distinct (__restrict__) the loads of one overlap the arithmetic and stores
+// of the other — twice the instruction-level parallelism of fft_pass.
+template <int R>
+__device__ __forceinline__ void fft_pass2(double2* __restrict__ b0, double2* __restrict__ b1,
+                                          const double2* tw, int hi_off, int M, int P, int L) {
+  const int stride = L / R;
+  const int nbfly = P / R;
+  const uint32_t tw_scale = static_cast<uint32_t>(M / L);
+  for (int b = threadIdx.x; b < nbfly; b += blockDim.x) {
+    const int blk = b / stride;
+    const int j = b - blk * stride;
+    const int base = blk * L + j;
+    double2 x[R], y[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      x[r] = b0[swz(base + r * stride)];
+      y[r] = b1[swz(base + r * stride)];
+    }
+    RegDft<R>::run(x, -1.0);
+    RegDft<R>::run(y, -1.0);
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      const uint32_t e = static_cast<uint32_t>(j * r) * tw_scale;
+      if (e) {
+        const double2 w = twiddle(tw, hi_off, e);
+        x[r] = cmul(x[r], w);
+        y[r] = cmul(y[r], w);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      b0[swz(base + r * stride)] = x[r];
+      b1[swz(base + r * stride)] = y[r];
+    }
+  }
+}
+
+__device__ __forceinline__ void fft_forward2(double2* __restrict__ b0, double2* __restrict__ b1,
+                                             const FftPlan& pl, const double2* tw) {
+  const int hi = 1 << kTwLoBits;
+  for (int p = 0; p < pl.npass; ++p) {
+    switch (pl.radix[p]) {
+      case 16: fft_pass2<16>(b0, b1, tw, hi, pl.M, pl.P, pl.len[p]); break;
+      case 8: fft_pass2<8>(b0, b1, tw, hi, pl.M, pl.P, pl.len[p]); break;
+      case 4: fft_pass2<4>(b0, b1, tw, hi, pl.M, pl.P, pl.len[p]); break;
+      case 3: fft_pass2<3>(b0, b1, tw, hi, pl.M, pl.P, pl.len[p]); break;
+      default: fft_pass2<2>(b0, b1, tw, hi, pl.M, pl.P, pl.len[p]); break;
+    }
+    __syncthreads();
+  }
+}
+
 // Digit-reversed spectrum -> natural order (unnormalised, e^{+i}).
 __device__ __forceinline__ void fft_inverse(double2* buf, const FftPlan& pl, const double2* tw) {
   for (int p = pl.npass - 1; p >= 0; --p) {
@@ -210,55 +264,83 @@ __device__ __forceinline__ void fft_inverse(double2* buf, const FftPlan& pl, con
   }
 }
 
-// Packed P-point spectrum Z -> Hermitian half spectrum X of the M-point real
-// transform (in place, pairs (k, P-k) per thread; slot pos(0) = (X0, XP)).
-__device__ __forceinline__ void r2c_post(double2* buf, const FftPlan& pl, const double2* tw) {
+// Shared-memory table region: twiddles (lo, hi) then the frequency -> slot
+// table (P ints), padded to whole double2 slots.
+__host__ __device__ inline int table_slots(const FftPlan& pl) {
+  return (1 << kTwLoBits) + pl.hi_count + (pl.P + 3) / 4;
+}
+__device__ __forceinline__ const int* smem_f2p(const double2* tw, const FftPlan& pl) {
+  return reinterpret_cast<const int*>(tw + (1 << kTwLoBits) + pl.hi_count);
+}
+
+// Pair pass over (k, P-k), k = 0..P/2, in place; each thread handles kB pairs
+// per step with all loads issued before any store (the pairs are disjoint, so
+// this is safe and exposes kB independent chains).
+//   kPost (r2c_post): packed P-point spectrum Z -> Hermitian half spectrum X
+//     of the M-point real transform; slot pos(0) = (X0, XP).
+//   !kPost (c2r_pre): the inverse map; after fft_inverse slot j holds
+//     P*(x[2j] + i x[2j+1]).
+template <bool kPost>
+__device__ __forceinline__ void pair_pass(double2* buf, const FftPlan& pl, const double2* tw) {
+  const int* f2p = smem_f2p(tw, pl);
   const int hi_off = 1 << kTwLoBits;
   const int half = pl.P / 2;
-  for (int k = threadIdx.x; k <= half; k += blockDim.x) {
-    if (k == 0) {
-      const uint32_t s0 = swz(__ldg(pl.f2p));
-      const double2 z = buf[s0];
-      buf[s0] = make_double2(z.x + z.y, z.x - z.y);
-      continue;
+  if (threadIdx.x == 0) {
+    const uint32_t s0 = swz(f2p[0]);
+    const double2 z = buf[s0];
+    buf[s0] = kPost ? make_double2(z.x + z.y, z.x - z.y)
+                    : make_double2(0.5 * (z.x + z.y), 0.5 * (z.x - z.y));
+  }
+  constexpr int kB = 4;
+  for (int k0 = 1 + threadIdx.x; k0 <= half; k0 += kB * blockDim.x) {
+    uint32_t sa[kB], sb[kB];
+    double2 va[kB], vb[kB];
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const int k = k0 + j * blockDim.x;
+      if (k <= half) {
+        sa[j] = swz(f2p[k]);
+        sb[j] = swz(f2p[pl.P - k]);
+        va[j] = buf[sa[j]];
+        vb[j] = buf[sb[j]];
+      }
     }
-    const int kn = pl.P - k;
-    const uint32_t sa = swz(__ldg(pl.f2p + k)), sb = swz(__ldg(pl.f2p + kn));
-    const double2 za = buf[sa], zb = buf[sb];
-    // E = (Z[k] + conj Z[P-k]) / 2, O = (Z[k] - conj Z[P-k]) / (2i)
-    const double2 e = make_double2(0.5 * (za.x + zb.x), 0.5 * (za.y - zb.y));
-    const double2 o = make_double2(0.5 * (za.y + zb.y), -0.5 * (za.x - zb.x));
-    const double2 wo = cmul(twiddle(tw, hi_off, static_cast<uint32_t>(k)), o);
-    const double2 xa = cadd(e, wo);              // X[k]
-    const double2 xb = cconj(csub(e, wo));       // X[P-k]
-    buf[sa] = xa;
-    if (kn != k) buf[sb] = xb;
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const int k = k0 + j * blockDim.x;
+      if (k > half) continue;
+      const double2 w = twiddle(tw, hi_off, static_cast<uint32_t>(k));
+      const double2 xa = va[j], xb = vb[j];
+      if (kPost) {
+        // E = (Z[k] + conj Z[P-k]) / 2, O = (Z[k] - conj Z[P-k]) / (2i)
+        const double2 e = make_double2(0.5 * (xa.x + xb.x), 0.5 * (xa.y - xb.y));
+        const double2 o = make_double2(0.5 * (xa.y + xb.y), -0.5 * (xa.x - xb.x));
+        const double2 wo = cmul(w, o);
+        va[j] = cadd(e, wo);          // X[k]
+        vb[j] = cconj(csub(e, wo));   // X[P-k]
+      } else {
+        const double2 e = make_double2(0.5 * (xa.x + xb.x), 0.5 * (xa.y - xb.y));
+        const double2 dif = make_double2(0.5 * (xa.x - xb.x), 0.5 * (xa.y + xb.y));
+        const double2 o = cmul(dif, cconj(w));
+        va[j] = make_double2(e.x - o.y, e.y + o.x);   // Z[k] = E + i O
+        vb[j] = make_double2(e.x + o.y, -e.y + o.x);  // Z[P-k] = conj(E) + i conj(O)
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const int k = k0 + j * blockDim.x;
+      if (k > half) continue;
+      buf[sa[j]] = va[j];
+      if (pl.P - k != k) buf[sb[j]] = vb[j];
+    }
   }
 }
 
-// Inverse of r2c_post: Hermitian half spectrum X -> packed Z with
-// Z = DFT_P(x_even + i x_odd); after fft_inverse, slot j holds P*(x[2j] + i x[2j+1]).
+__device__ __forceinline__ void r2c_post(double2* buf, const FftPlan& pl, const double2* tw) {
+  pair_pass<true>(buf, pl, tw);
+}
 __device__ __forceinline__ void c2r_pre(double2* buf, const FftPlan& pl, const double2* tw) {
-  const int hi_off = 1 << kTwLoBits;
-  const int half = pl.P / 2;
-  for (int k = threadIdx.x; k <= half; k += blockDim.x) {
-    if (k == 0) {
-      const uint32_t s0 = swz(__ldg(pl.f2p));
-      const double2 x = buf[s0];  // (X0, XP), both real
-      const double e = 0.5 * (x.x + x.y), o = 0.5 * (x.x - x.y);
-      buf[s0] = make_double2(e, o);
-      continue;
-    }
-    const int kn = pl.P - k;
-    const uint32_t sa = swz(__ldg(pl.f2p + k)), sb = swz(__ldg(pl.f2p + kn));
-    const double2 xa = buf[sa], xb = buf[sb];
-    const double2 e = make_double2(0.5 * (xa.x + xb.x), 0.5 * (xa.y - xb.y));  // (X[k] + conj X[P-k]) / 2
-    const double2 dif = make_double2(0.5 * (xa.x - xb.x), 0.5 * (xa.y + xb.y)); // (X[k] - conj X[P-k]) / 2
-    const double2 o = cmul(dif, cconj(twiddle(tw, hi_off, static_cast<uint32_t>(k))));
-    // Z[k] = E + i O ; Z[P-k] = conj(E) + i conj(O)
-    buf[sa] = make_double2(e.x - o.y, e.y + o.x);
-    if (kn != k) buf[sb] = make_double2(e.x + o.y, -e.y + o.x);
-  }
+  pair_pass<false>(buf, pl, tw);
 }
 
 // Zero the P packed slots.
@@ -272,10 +354,13 @@ __device__ __forceinline__ double& packed_real(double2* buf, uint32_t t) {
   return (t & 1u) ? s.y : s.x;
 }
 
-// Loads the twiddle table into shared memory (lo then hi).
+// Loads the twiddle table (lo then hi) and the frequency -> slot table into
+// shared memory.
 __device__ __forceinline__ void load_twiddles(double2* sm_tw, const FftPlan& pl) {
   const int n = (1 << kTwLoBits) + pl.hi_count;
   for (int i = threadIdx.x; i < n; i += blockDim.x) sm_tw[i] = pl.tw[i];
+  int* f2p = reinterpret_cast<int*>(sm_tw + n);
+  for (int i = threadIdx.x; i < pl.P; i += blockDim.x) f2p[i] = __ldg(pl.f2p + i);
 }
 
 // Pointwise helpers on the half-spectrum slot layout (slot 0 holds two reals).
@@ -286,8 +371,7 @@ __device__ __forceinline__ double2 hconj(double2 a, bool slot0) { return slot0 ?
 
 // Shared-memory bytes a spectral kernel with this plan needs (buffer + twiddles).
 inline size_t fft_smem_bytes(const FftPlan& pl) {
-  return static_cast<size_t>(pl.P) * sizeof(double2) +
-         static_cast<size_t>((1 << kTwLoBits) + pl.hi_count) * sizeof(double2);
+  return static_cast<size_t>(pl.P + table_slots(pl)) * sizeof(double2);
 }
 
 // Host: plan for the smallest supported M >= min_len (cached per device).

@@ -16,40 +16,65 @@ namespace {
 
 __device__ __forceinline__ int tid() { return threadIdx.x; }
 
-// Shared memory carve-up: twiddles, then the P-slot FFT buffer, then a
+// Shared memory carve-up: twiddles, then one or two P-slot FFT buffers, then a
 // 32-double reduction scratch.
 struct Smem {
   double2* tw;
   double2* buf;
+  double2* buf2;  // second buffer (two-buffer kernels only)
   double* red;
 };
 
-__device__ __forceinline__ Smem carve(const FftPlan& pl) {
+__device__ __forceinline__ Smem carve(const FftPlan& pl, int nbuf = 1) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem s;
   s.tw = reinterpret_cast<double2*>(smem_raw);
-  s.buf = s.tw + (1 << kTwLoBits) + pl.hi_count;
-  s.red = reinterpret_cast<double*>(s.buf + pl.P);
+  s.buf = s.tw + table_slots(pl);
+  s.buf2 = nbuf > 1 ? s.buf + pl.P : nullptr;
+  s.red = reinterpret_cast<double*>(s.buf + static_cast<size_t>(nbuf) * pl.P);
   return s;
 }
 
 // Count sketch of vec[0..I) under a packed pair, scattered into the packed
-// real buffer (cs_sketch, sketch.cpp:105-116: zeros skipped), then the
-// length-M real transform -> half spectrum in slot order.
-__device__ void rfft_of_cs(const Smem& sm, const FftPlan& pl, const double* __restrict__ vec,
-                           int I, const uint32_t* __restrict__ tab) {
-  zero_slots(sm.buf, pl.P);
-  __syncthreads();
+// real buffer (cs_sketch, sketch.cpp:105-116: zeros skipped).
+__device__ void scatter_cs(double2* buf, const double* __restrict__ vec, int I,
+                           const uint32_t* __restrict__ tab) {
   for (int i = tid(); i < I; i += blockDim.x) {
     const double v = vec[i];
     if (v != 0.0) {
       const uint32_t e = __ldg(tab + i);
-      atomicAdd(&packed_real(sm.buf, e & 0x7fffffffu), (e >> 31) ? -v : v);
+      atomicAdd(&packed_real(buf, e & 0x7fffffffu), (e >> 31) ? -v : v);
     }
   }
+}
+
+// Count sketch then the length-M real transform -> half spectrum in slot order.
+__device__ void rfft_of_cs(const Smem& sm, double2* buf, const FftPlan& pl,
+                           const double* __restrict__ vec, int I,
+                           const uint32_t* __restrict__ tab) {
+  zero_slots(buf, pl.P);
   __syncthreads();
-  fft_forward(sm.buf, pl, sm.tw);
+  scatter_cs(buf, vec, I, tab);
+  __syncthreads();
+  fft_forward(buf, pl, sm.tw);
+  r2c_post(buf, pl, sm.tw);
+  __syncthreads();
+}
+
+// Two count sketches transformed together (sm.buf <- a, sm.buf2 <- b).
+__device__ void rfft_of_cs2(const Smem& sm, const FftPlan& pl, const double* __restrict__ va,
+                            int Ia, const uint32_t* __restrict__ ta,
+                            const double* __restrict__ vb, int Ib,
+                            const uint32_t* __restrict__ tb) {
+  zero_slots(sm.buf, pl.P);
+  zero_slots(sm.buf2, pl.P);
+  __syncthreads();
+  scatter_cs(sm.buf, va, Ia, ta);
+  scatter_cs(sm.buf2, vb, Ib, tb);
+  __syncthreads();
+  fft_forward2(sm.buf, sm.buf2, pl, sm.tw);
   r2c_post(sm.buf, pl, sm.tw);
+  r2c_post(sm.buf2, pl, sm.tw);
   __syncthreads();
 }
 
@@ -125,7 +150,7 @@ __global__ void __launch_bounds__(kFftThreads) real_from_spec_kernel(FftPlan pl,
 __global__ void __launch_bounds__(kFftThreads) cp_rank_kernel(FftPlan pl, CpArgs a,
                                                               const uint32_t* __restrict__ packed,
                                                               double2* __restrict__ Q) {
-  const Smem sm = carve(pl);
+  const Smem sm = carve(pl, 2);
   load_twiddles(sm.tw, pl);
   const int rl = blockIdx.x, d = blockIdx.y;
   const int r = a.r_begin + rl;
@@ -133,17 +158,29 @@ __global__ void __launch_bounds__(kFftThreads) cp_rank_kernel(FftPlan pl, CpArgs
   double2* q = Q + (static_cast<size_t>(d) * a.r_count + rl) * pl.P;
   const uint32_t* tab = packed + static_cast<size_t>(d) * a.fam_stride;
   if (w == 0.0) return;  // convolved_cp_sketch skips zero weights (sketch.cpp:75)
-  for (int n = 0; n < a.order; ++n) {
+  auto col = [&](int n) { return a.factors[n] + static_cast<size_t>(r) * a.dims[n]; };
+  // modes 0 and 1 together, then the product accumulates in sm.buf and every
+  // further mode is transformed in sm.buf2
+  int n = 1;
+  if (a.order >= 2) {
     __syncthreads();
-    rfft_of_cs(sm, pl, a.factors[n] + static_cast<size_t>(r) * a.dims[n], a.dims[n],
-               tab + a.tab_off[n]);
-    for (int s = tid(); s < pl.P; s += blockDim.x) {
-      const double2 v = sm.buf[swz(s)];
-      double2 acc = n == 0 ? v : hmul(q[s], v, s == 0);
-      if (n == a.order - 1) acc = cscale(acc, w);
-      q[s] = acc;
-    }
+    rfft_of_cs2(sm, pl, col(0), a.dims[0], tab + a.tab_off[0], col(1), a.dims[1],
+                tab + a.tab_off[1]);
+    for (int s = tid(); s < pl.P; s += blockDim.x)
+      sm.buf[swz(s)] = hmul(sm.buf[swz(s)], sm.buf2[swz(s)], s == 0);
+    n = 2;
+  } else {
+    __syncthreads();
+    rfft_of_cs(sm, sm.buf, pl, col(0), a.dims[0], tab + a.tab_off[0]);
   }
+  for (; n < a.order; ++n) {
+    __syncthreads();
+    rfft_of_cs(sm, sm.buf2, pl, col(n), a.dims[n], tab + a.tab_off[n]);
+    for (int s = tid(); s < pl.P; s += blockDim.x)
+      sm.buf[swz(s)] = hmul(sm.buf[swz(s)], sm.buf2[swz(s)], s == 0);
+  }
+  __syncthreads();
+  for (int s = tid(); s < pl.P; s += blockDim.x) q[s] = cscale(sm.buf[swz(s)], w);
 }
 
 // K4: fixed-order sum over ranks, parallel over (slot, family): acc[d][s] =
@@ -208,21 +245,19 @@ __global__ void __launch_bounds__(kFftThreads) conv_kernel(FftPlan pl, const dou
 __global__ void __launch_bounds__(kFftThreads) iuv_kernel(FftPlan pl, EngArgs e, const double* A,
                                                           const double* B, int c1, int c2, int f,
                                                           double2* scratch, double* est) {
-  const Smem sm = carve(pl);
+  (void)scratch;
+  const Smem sm = carve(pl, 2);
   load_twiddles(sm.tw, pl);
   __syncthreads();
   const int b = blockIdx.x, d = blockIdx.y;
   const size_t item = static_cast<size_t>(b) * e.D + d;
-  double2* scr = scratch + item * pl.P;
   const uint32_t* tab = e.packed + static_cast<size_t>(d) * e.fam_stride;
   const double2* S = e.spec + static_cast<size_t>(d) * pl.P;
-  rfft_of_cs(sm, pl, A + static_cast<size_t>(b) * e.dims[c1], e.dims[c1], tab + e.tab_off[c1]);
-  for (int s = tid(); s < pl.P; s += blockDim.x) scr[s] = sm.buf[swz(s)];
-  __syncthreads();
-  rfft_of_cs(sm, pl, B + static_cast<size_t>(b) * e.dims[c2], e.dims[c2], tab + e.tab_off[c2]);
+  rfft_of_cs2(sm, pl, A + static_cast<size_t>(b) * e.dims[c1], e.dims[c1], tab + e.tab_off[c1],
+              B + static_cast<size_t>(b) * e.dims[c2], e.dims[c2], tab + e.tab_off[c2]);
   for (int s = tid(); s < pl.P; s += blockDim.x) {
     const bool s0 = s == 0;
-    const double2 ab = hmul(scr[s], sm.buf[swz(s)], s0);
+    const double2 ab = hmul(sm.buf[swz(s)], sm.buf2[swz(s)], s0);
     sm.buf[swz(s)] = hmul(S[s], hconj(ab, s0), s0);
   }
   irfft_in_place(sm, pl);
@@ -242,34 +277,27 @@ __global__ void __launch_bounds__(kFftThreads) iuv_kernel(FftPlan pl, EngArgs e,
 __global__ void __launch_bounds__(kFftThreads) uvw_kernel(FftPlan pl, EngArgs e, const double* U,
                                                           const double* V, const double* W,
                                                           double2* scratch, double* est) {
-  const Smem sm = carve(pl);
+  (void)scratch;
+  const Smem sm = carve(pl, 2);
   load_twiddles(sm.tw, pl);
   __syncthreads();
   const int b = blockIdx.x, d = blockIdx.y;
   const size_t item = static_cast<size_t>(b) * e.D + d;
-  double2* scr = scratch + item * pl.P;
   const uint32_t* tab = e.packed + static_cast<size_t>(d) * e.fam_stride;
   const double2* S = e.spec + static_cast<size_t>(d) * pl.P;
-  const double* vecs[3] = {U + static_cast<size_t>(b) * e.dims[0],
-                           V + static_cast<size_t>(b) * e.dims[1],
-                           W + static_cast<size_t>(b) * e.dims[2]};
+  rfft_of_cs2(sm, pl, U + static_cast<size_t>(b) * e.dims[0], e.dims[0], tab + e.tab_off[0],
+              V + static_cast<size_t>(b) * e.dims[1], e.dims[1], tab + e.tab_off[1]);
+  for (int s = tid(); s < pl.P; s += blockDim.x)
+    sm.buf[swz(s)] = hmul(sm.buf[swz(s)], sm.buf2[swz(s)], s == 0);
+  __syncthreads();
+  rfft_of_cs(sm, sm.buf2, pl, W + static_cast<size_t>(b) * e.dims[2], e.dims[2],
+             tab + e.tab_off[2]);
   double acc = 0.0;
-  for (int n = 0; n < 3; ++n) {
-    __syncthreads();
-    rfft_of_cs(sm, pl, vecs[n], e.dims[n], tab + e.tab_off[n]);
-    for (int s = tid(); s < pl.P; s += blockDim.x) {
-      const double2 v = sm.buf[swz(s)];
-      if (n == 0) {
-        scr[s] = v;
-      } else if (n == 1) {
-        scr[s] = hmul(scr[s], v, s == 0);
-      } else {
-        const double2 g = hmul(scr[s], v, s == 0);
-        const double2 sd = S[s];
-        const double re = sd.x * g.x + sd.y * g.y;  // Re(S conj(G)) / (X0*G0 + XP*GP at slot 0)
-        acc += s == 0 ? re : 2.0 * re;
-      }
-    }
+  for (int s = tid(); s < pl.P; s += blockDim.x) {
+    const double2 g = hmul(sm.buf[swz(s)], sm.buf2[swz(s)], s == 0);
+    const double2 sd = S[s];
+    const double re = sd.x * g.x + sd.y * g.y;  // Re(S conj(G)) / (X0*G0 + XP*GP at slot 0)
+    acc += s == 0 ? re : 2.0 * re;
   }
   const double tot = block_sum(acc, sm.red);
   if (threadIdx.x == 0) est[item] = tot / pl.M;
@@ -280,28 +308,21 @@ __global__ void __launch_bounds__(kFftThreads) deflate_kernel(FftPlan pl, EngArg
                                                               const double* U, const double* V,
                                                               const double* W, double2* scratch,
                                                               double2* spec) {
-  const Smem sm = carve(pl);
+  (void)scratch;
+  const Smem sm = carve(pl, 2);
   load_twiddles(sm.tw, pl);
   __syncthreads();
   const int d = blockIdx.x;
-  double2* scr = scratch + static_cast<size_t>(d) * pl.P;
   const uint32_t* tab = e.packed + static_cast<size_t>(d) * e.fam_stride;
   double2* S = spec + static_cast<size_t>(d) * pl.P;
-  const double* vecs[3] = {U, V, W};
-  for (int n = 0; n < 3; ++n) {
-    __syncthreads();
-    rfft_of_cs(sm, pl, vecs[n], e.dims[n], tab + e.tab_off[n]);
-    for (int s = tid(); s < pl.P; s += blockDim.x) {
-      const double2 v = sm.buf[swz(s)];
-      if (n == 0) {
-        scr[s] = v;
-      } else if (n == 1) {
-        scr[s] = hmul(scr[s], v, s == 0);
-      } else {
-        const double2 g = hmul(scr[s], v, s == 0);
-        S[s] = csub(S[s], cscale(g, weight));
-      }
-    }
+  rfft_of_cs2(sm, pl, U, e.dims[0], tab + e.tab_off[0], V, e.dims[1], tab + e.tab_off[1]);
+  for (int s = tid(); s < pl.P; s += blockDim.x)
+    sm.buf[swz(s)] = hmul(sm.buf[swz(s)], sm.buf2[swz(s)], s == 0);
+  __syncthreads();
+  rfft_of_cs(sm, sm.buf2, pl, W, e.dims[2], tab + e.tab_off[2]);
+  for (int s = tid(); s < pl.P; s += blockDim.x) {
+    const double2 g = hmul(sm.buf[swz(s)], sm.buf2[swz(s)], s == 0);
+    S[s] = csub(S[s], cscale(g, weight));
   }
 }
 
@@ -379,8 +400,9 @@ __global__ void refine_update_kernel(double* __restrict__ best, const double* __
 namespace {
 
 template <typename K>
-int prep(K kernel, const FftPlan& pl, size_t* smem) {
-  *smem = fft_smem_bytes(pl) + 32 * sizeof(double);
+int prep(K kernel, const FftPlan& pl, size_t* smem, int nbuf = 1) {
+  *smem = fft_smem_bytes(pl) + static_cast<size_t>(nbuf - 1) * pl.P * sizeof(double2) +
+          32 * sizeof(double);
   FCS_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(*smem)));
   return ST_OK;
@@ -409,7 +431,7 @@ int launch_real_from_spec(const FftPlan& pl, const double2* spec, int items, dou
 int launch_cp(const FftPlan& pl, const CpArgs& a, int D, const uint32_t* packed, double2* Q,
               double* out, int jt, int accumulate, cudaStream_t st) {
   size_t sm;
-  if (int rc = prep(cp_rank_kernel, pl, &sm)) return rc;
+  if (int rc = prep(cp_rank_kernel, pl, &sm, 2)) return rc;
   if (a.r_count > 0) {
     cp_rank_kernel<<<dim3(a.r_count, D), kFftThreads, sm, st>>>(pl, a, packed, Q);
     FCS_CUDA_TRY(cudaGetLastError());
@@ -438,7 +460,7 @@ int launch_conv(const FftPlan& pl, const double* a, int la, size_t lda, const do
 int launch_iuv(const FftPlan& pl, const EngArgs& e, int batch, const double* A, const double* B,
                int c1, int c2, int f, double2* scratch, double* est, cudaStream_t st) {
   size_t sm;
-  if (int rc = prep(iuv_kernel, pl, &sm)) return rc;
+  if (int rc = prep(iuv_kernel, pl, &sm, 2)) return rc;
   iuv_kernel<<<dim3(batch, e.D), kFftThreads, sm, st>>>(pl, e, A, B, c1, c2, f, scratch, est);
   FCS_CUDA_TRY(cudaGetLastError());
   return ST_OK;
@@ -447,7 +469,7 @@ int launch_iuv(const FftPlan& pl, const EngArgs& e, int batch, const double* A, 
 int launch_uvw(const FftPlan& pl, const EngArgs& e, int batch, const double* U, const double* V,
                const double* W, double2* scratch, double* est, cudaStream_t st) {
   size_t sm;
-  if (int rc = prep(uvw_kernel, pl, &sm)) return rc;
+  if (int rc = prep(uvw_kernel, pl, &sm, 2)) return rc;
   uvw_kernel<<<dim3(batch, e.D), kFftThreads, sm, st>>>(pl, e, U, V, W, scratch, est);
   FCS_CUDA_TRY(cudaGetLastError());
   return ST_OK;
@@ -457,7 +479,7 @@ int launch_deflate(const FftPlan& pl, const EngArgs& e, double weight, const dou
                    const double* V, const double* W, double2* scratch, double2* spec,
                    cudaStream_t st) {
   size_t sm;
-  if (int rc = prep(deflate_kernel, pl, &sm)) return rc;
+  if (int rc = prep(deflate_kernel, pl, &sm, 2)) return rc;
   deflate_kernel<<<e.D, kFftThreads, sm, st>>>(pl, e, weight, U, V, W, scratch, spec);
   FCS_CUDA_TRY(cudaGetLastError());
   return ST_OK;
