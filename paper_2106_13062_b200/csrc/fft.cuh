@@ -358,9 +358,21 @@ __device__ __forceinline__ double& packed_real(double2* buf, uint32_t t) {
 // shared memory.
 __device__ __forceinline__ void load_twiddles(double2* sm_tw, const FftPlan& pl) {
   const int n = (1 << kTwLoBits) + pl.hi_count;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) sm_tw[i] = pl.tw[i];
-  int* f2p = reinterpret_cast<int*>(sm_tw + n);
-  for (int i = threadIdx.x; i < pl.P; i += blockDim.x) f2p[i] = __ldg(pl.f2p + i);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sm_tw[i] = __ldg(pl.tw + i);
+  // P is a multiple of 8: copy the table as int4 with all loads in flight
+  int4* f2p = reinterpret_cast<int4*>(sm_tw + n);
+  const int4* src = reinterpret_cast<const int4*>(pl.f2p);
+  const int n4 = pl.P / 4;
+  constexpr int kU = 8;
+  for (int i0 = threadIdx.x; i0 < n4; i0 += kU * blockDim.x) {
+    int4 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (i0 + u * blockDim.x < n4) v[u] = __ldg(src + i0 + u * blockDim.x);
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (i0 + u * blockDim.x < n4) f2p[i0 + u * blockDim.x] = v[u];
+  }
 }
 
 // Pointwise helpers on the half-spectrum slot layout (slot 0 holds two reals).

@@ -255,10 +255,22 @@ __global__ void __launch_bounds__(kFftThreads) iuv_kernel(FftPlan pl, EngArgs e,
   const double2* S = e.spec + static_cast<size_t>(d) * pl.P;
   rfft_of_cs2(sm, pl, A + static_cast<size_t>(b) * e.dims[c1], e.dims[c1], tab + e.tab_off[c1],
               B + static_cast<size_t>(b) * e.dims[c2], e.dims[c2], tab + e.tab_off[c2]);
-  for (int s = tid(); s < pl.P; s += blockDim.x) {
-    const bool s0 = s == 0;
-    const double2 ab = hmul(sm.buf[swz(s)], sm.buf2[swz(s)], s0);
-    sm.buf[swz(s)] = hmul(S[s], hconj(ab, s0), s0);
+  constexpr int kU = 6;  // S loads of kU slots in flight
+  for (int s0 = tid(); s0 < pl.P; s0 += kU * blockDim.x) {
+    double2 sv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int s = s0 + u * blockDim.x;
+      if (s < pl.P) sv[u] = __ldg(S + s);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int s = s0 + u * blockDim.x;
+      if (s >= pl.P) continue;
+      const bool z = s == 0;
+      const double2 ab = hmul(sm.buf[swz(s)], sm.buf2[swz(s)], z);
+      sm.buf[swz(s)] = hmul(sv[u], hconj(ab, z), z);
+    }
   }
   irfft_in_place(sm, pl);
   const double inv = 1.0 / pl.P;
