@@ -44,6 +44,15 @@ enum {
 
 enum { ST_F32 = 0, ST_F64 = 1 };
 
+/* SketchBackend (cpd.hpp:13), same order. The B200 engine provides TS and FCS. */
+enum {
+  ST_BACKEND_PLAIN = 0,
+  ST_BACKEND_CS = 1,
+  ST_BACKEND_TS = 2,
+  ST_BACKEND_HCS = 3,
+  ST_BACKEND_FCS = 4
+};
+
 #define ST_MAX_ORDER 8
 
 /* Thread-local text of the last failure. */
@@ -211,8 +220,18 @@ typedef struct st_engine st_engine;
  * once and not retained. */
 int st_engine_create(st_engine** engine, int dtype, const void* tensor, const size_t* dims,
                      size_t hash_len, size_t sketch_count, uint64_t seed, void* stream);
+/* make_contraction_engine(t, backend, cfg) (cpd.cpp:220-232) for backend
+ * ST_BACKEND_FCS (FcsEngine, cpd.cpp:61-94) or ST_BACKEND_TS (TsEngine,
+ * cpd.cpp:96-126: D tensor sketches of length J, estimates by circular
+ * correlation at length J, estimators.cpp:209-233). Other backends return
+ * ST_EINVAL. st_engine_create == backend ST_BACKEND_FCS. */
+int st_engine_create_backend(st_engine** engine, int backend, int dtype, const void* tensor,
+                             const size_t* dims, size_t hash_len, size_t sketch_count,
+                             uint64_t seed, void* stream);
 int st_engine_destroy(st_engine* engine);
-/* J~ and the current D x J~ sketch values (device out). */
+int st_engine_backend(const st_engine* engine);
+/* Sketch length (J~ for FCS, J for TS) and the current D x length sketch
+ * values (device out). */
 size_t st_engine_composed_len(const st_engine* engine);
 int st_engine_sketches(st_engine* engine, double* out, void* stream);
 
@@ -247,6 +266,38 @@ int st_engine_deflate(st_engine* engine, double weight, const double* u, const d
 int st_rtpm(int dtype, const void* tensor, size_t dim, size_t rank, size_t num_inits,
             size_t num_iters, size_t hash_len, size_t sketch_count, uint64_t seed,
             double* weights, double* factor, void* stream);
+/* HOST. st_rtpm with RtpmConfig::backend (ST_BACKEND_FCS or ST_BACKEND_TS). */
+int st_rtpm_backend(int backend, int dtype, const void* tensor, size_t dim, size_t rank,
+                    size_t num_inits, size_t num_iters, size_t hash_len, size_t sketch_count,
+                    uint64_t seed, double* weights, double* factor, void* stream);
+
+/* HOST. Alternating rank-1 power method for a general order-3 device tensor
+ * (rtpm_asym, cpd.cpp:279-335): restarts batched in lockstep, each sweep
+ * three engine iuv calls (free modes 0, 1, 2) with row normalisation, argmax
+ * of |T(u,v,w)| (strict >), refinement, sign absorbed into the first factor,
+ * deflation. Init stream SplitMix64(mix(seed ^ 0x72743161)). Outputs host
+ * weights[rank] and factors packed as dims[0] x rank, dims[1] x rank,
+ * dims[2] x rank (each column-major). */
+int st_rtpm_asym(int backend, int dtype, const void* tensor, const size_t* dims, size_t rank,
+                 size_t num_inits, size_t num_iters, size_t hash_len, size_t sketch_count,
+                 uint64_t seed, double* weights, double* factors, void* stream);
+
+/* HOST. Alternating least squares (als, cpd.cpp:337-383): MTTKRP columns from
+ * one batched engine iuv per mode, exact Gram (F_o1^T F_o1 .* F_o2^T F_o2),
+ * minimum-norm solve, column normalisation into the weights, and the device
+ * residual_norm each sweep with the |prev - residual| < tol stop. Init stream
+ * SplitMix64(mix(seed ^ 0x616c73)). Outputs as st_rtpm_asym; *sweeps (may be
+ * NULL) receives the number of sweeps run. */
+int st_als(int backend, int dtype, const void* tensor, const size_t* dims, size_t rank,
+           size_t max_iters, double tol, size_t hash_len, size_t sketch_count, uint64_t seed,
+           double* weights, double* factors, size_t* sweeps, void* stream);
+
+/* || T - densify(cp) ||_F / || T ||_F (residual_norm, cpd.cpp:385-392) for an
+ * order-3 device tensor and a device CP (weights[rank], factors packed as in
+ * st_rtpm_asym). *out is a HOST double; 0 when both norms are 0, +inf when
+ * only ||T|| is. */
+int st_residual_norm(int dtype, const void* tensor, const size_t* dims, const double* weights,
+                     size_t rank, const double* factors, double* out, void* stream);
 
 /* ---------------------------------------------------------- synthetic data */
 

@@ -412,3 +412,57 @@ def hcs_cp_tables(weights, factors, buckets, signs, hash_lens) -> np.ndarray:
     _check(lib().ref_hcs_cp_tables(_ptr(w), _sz(len(w)), _sz(len(dims)), _ptr(dims), _ptr(fs),
                                    _ptr(b), _ptr(s), _ptr(hl), _ptr(out)))
     return out.reshape(tuple(int(x) for x in hl), order="F")
+
+
+BACKEND_TS = 2
+
+
+def _pack_factors(factors):
+    return np.ascontiguousarray(np.concatenate(
+        [np.asarray(f, np.float64).ravel(order="F") for f in factors]))
+
+
+def _unpack_factors(f, dims, rank):
+    out, off = [], 0
+    for n in dims:
+        out.append(f[off:off + n * rank].reshape((n, rank), order="F"))
+        off += n * rank
+    return out
+
+
+def rtpm_asym(t: np.ndarray, rank: int, num_inits: int, num_iters: int, hash_len: int,
+              sketch_count: int, seed: int, backend: int = BACKEND_FCS):
+    """rtpm_asym (cpd.cpp:279-335); returns (weights, [F0, F1, F2])."""
+    dims = _dims(t.shape)
+    data = np.ascontiguousarray(np.asarray(t, np.float64).ravel(order="F"))
+    w = np.empty(rank, np.float64)
+    f = np.empty(int(dims.sum()) * rank, np.float64)
+    _check(lib().ref_rtpm_asym(_ptr(data), _ptr(dims), _sz(rank), _sz(num_inits), _sz(num_iters),
+                               C.c_int(backend), _sz(hash_len), _sz(sketch_count), _u64(seed),
+                               _ptr(w), _ptr(f)))
+    return w, _unpack_factors(f, [int(x) for x in dims], rank)
+
+
+def als(t: np.ndarray, rank: int, max_iters: int, tol: float, hash_len: int, sketch_count: int,
+        seed: int, backend: int = BACKEND_FCS):
+    """als (cpd.cpp:337-383); returns (weights, [F0, F1, F2])."""
+    dims = _dims(t.shape)
+    data = np.ascontiguousarray(np.asarray(t, np.float64).ravel(order="F"))
+    w = np.empty(rank, np.float64)
+    f = np.empty(int(dims.sum()) * rank, np.float64)
+    _check(lib().ref_als(_ptr(data), _ptr(dims), _sz(rank), _sz(max_iters), _d(tol),
+                         C.c_int(backend), _sz(hash_len), _sz(sketch_count), _u64(seed),
+                         _ptr(w), _ptr(f)))
+    return w, _unpack_factors(f, [int(x) for x in dims], rank)
+
+
+def residual_norm(t: np.ndarray, weights, factors) -> float:
+    """residual_norm (cpd.cpp:385-392) for an order-3 CP."""
+    dims = _dims(t.shape)
+    data = np.ascontiguousarray(np.asarray(t, np.float64).ravel(order="F"))
+    w = np.ascontiguousarray(np.asarray(weights, np.float64))
+    f = _pack_factors(factors)
+    out = _d(0)
+    _check(lib().ref_residual_norm(_ptr(data), _ptr(dims), _ptr(w), _sz(len(w)), _ptr(f),
+                                   C.byref(out)))
+    return out.value

@@ -416,3 +416,67 @@ int ref_hcs_cp_tables(const double* weights, std::size_t rank, std::size_t order
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------- CPD drivers
+extern "C" {
+
+namespace {
+void copy_factors(const CpTensor& cp, double* out) {
+  std::size_t off = 0;
+  for (const Eigen::MatrixXd& f : cp.factors) {
+    std::memcpy(out + off, f.data(), sizeof(double) * f.size());
+    off += static_cast<std::size_t>(f.size());
+  }
+}
+}  // namespace
+
+// rtpm_asym (cpd.cpp:279-335); factors packed dims[0] x rank, dims[1] x rank, dims[2] x rank.
+int ref_rtpm_asym(const double* data, const std::size_t* dims, std::size_t rank,
+                  std::size_t num_inits, std::size_t num_iters, int backend, std::size_t hash_len,
+                  std::size_t sketch_count, std::uint64_t seed, double* weights, double* factors) {
+  return guarded([&] {
+    DenseTensor t = make_tensor(data, 3, dims);
+    RtpmConfig cfg;
+    cfg.target_rank = rank;
+    cfg.num_inits = num_inits;
+    cfg.num_power_iters = num_iters;
+    cfg.backend = static_cast<SketchBackend>(backend);
+    cfg.estimator.hash_len = hash_len;
+    cfg.estimator.sketch_count = sketch_count;
+    cfg.estimator.seed = seed;
+    CpTensor cp = rtpm_asym(t, cfg);
+    copy_out(cp.weights, weights);
+    copy_factors(cp, factors);
+  });
+}
+
+// als (cpd.cpp:337-383); same packing.
+int ref_als(const double* data, const std::size_t* dims, std::size_t rank, std::size_t max_iters,
+            double tol, int backend, std::size_t hash_len, std::size_t sketch_count,
+            std::uint64_t seed, double* weights, double* factors) {
+  return guarded([&] {
+    DenseTensor t = make_tensor(data, 3, dims);
+    AlsConfig cfg;
+    cfg.target_rank = rank;
+    cfg.max_iters = max_iters;
+    cfg.tol = tol;
+    cfg.backend = static_cast<SketchBackend>(backend);
+    cfg.estimator.hash_len = hash_len;
+    cfg.estimator.sketch_count = sketch_count;
+    cfg.estimator.seed = seed;
+    CpTensor cp = als(t, cfg);
+    copy_out(cp.weights, weights);
+    copy_factors(cp, factors);
+  });
+}
+
+// residual_norm (cpd.cpp:385-392) of an order-3 CP (packed factors) against t.
+int ref_residual_norm(const double* data, const std::size_t* dims, const double* weights,
+                      std::size_t rank, const double* factors, double* out) {
+  return guarded([&] {
+    DenseTensor t = make_tensor(data, 3, dims);
+    *out = residual_norm(t, make_cp(weights, rank, 3, dims, factors));
+  });
+}
+
+}  // extern "C"

@@ -16,6 +16,7 @@ HEADER = os.path.join(os.path.dirname(_PKG), "include", "fcs_b200.h")
 
 ST_OK, ST_EINVAL, ST_ENUMERIC, ST_ECUDA, ST_ENCCL, ST_ENOMEM = range(6)
 ST_F32, ST_F64 = 0, 1
+ST_BACKEND_PLAIN, ST_BACKEND_CS, ST_BACKEND_TS, ST_BACKEND_HCS, ST_BACKEND_FCS = range(5)
 MAX_ORDER = 8
 
 p, sz, u64, i32, dbl = C.c_void_p, C.c_size_t, C.c_uint64, C.c_int, C.c_double
@@ -46,13 +47,19 @@ SIGNATURES = {
     "st_hcs_cp_workspace": (sz, [sz, p, sz, sz, p]),
     "st_hcs_cp": (i32, [p, sz, sz, p, p, sz, p, p, p, i32, p, sz, p]),
     "st_engine_create": (i32, [p, i32, p, p, sz, sz, u64, p]),
+    "st_engine_create_backend": (i32, [p, i32, i32, p, p, sz, sz, u64, p]),
     "st_engine_destroy": (i32, [p]),
+    "st_engine_backend": (i32, [p]),
     "st_engine_composed_len": (sz, [p]),
     "st_engine_sketches": (i32, [p, p, p]),
     "st_engine_iuv": (i32, [p, sz, p, p, sz, p, i32, p]),
     "st_engine_uvw": (i32, [p, sz, p, p, p, p, i32, p]),
     "st_engine_deflate": (i32, [p, dbl, p, p, p, p]),
     "st_rtpm": (i32, [i32, p, sz, sz, sz, sz, sz, sz, u64, p, p, p]),
+    "st_rtpm_backend": (i32, [i32, i32, p, sz, sz, sz, sz, sz, sz, u64, p, p, p]),
+    "st_rtpm_asym": (i32, [i32, i32, p, p, sz, sz, sz, sz, sz, u64, p, p, p]),
+    "st_als": (i32, [i32, i32, p, p, sz, sz, dbl, sz, sz, u64, p, p, p, p]),
+    "st_residual_norm": (i32, [i32, p, p, p, sz, p, p, p]),
     "st_host_gaussian": (i32, [u64, sz, p, i32]),
     "st_device_gaussian": (i32, [i32, u64, sz, p, p]),
 }

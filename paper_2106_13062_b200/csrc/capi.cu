@@ -126,7 +126,7 @@ extern "C" {
 
 const char* st_last_error(void) { return g_last_error.c_str(); }
 
-int st_abi_version(void) { return 2; }
+int st_abi_version(void) { return 3; }
 
 int st_device_query(int* sm_count, size_t* smem_optin, size_t* l2_bytes) {
   DeviceInfo di;

@@ -1,128 +1,42 @@
-// Host side of the spectral paths: CP-form FCS, convolution / Kronecker,
-// the FCS contraction engine (FcsEngine, cpd.cpp:61-94) and the batched
-// robust tensor power method driver (rtpm, cpd.cpp:234-277).
+// Host side of the spectral paths: CP-form FCS, convolution / Kronecker and
+// the contraction engine (FcsEngine cpd.cpp:61-94, TsEngine cpd.cpp:96-126).
+// The CPD drivers built on the engine live in cpd.cu.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <limits>
-#include <numbers>
 #include <string>
 #include <vector>
 
-#include "fft.cuh"
+#include "engine.cuh"
 
 namespace fcs {
 
-int launch_spec_from_real(const FftPlan&, const double*, size_t, int, int, double2*, cudaStream_t);
-int launch_real_from_spec(const FftPlan&, const double2*, int, double*, size_t, int, int,
-                          cudaStream_t);
-int launch_cp(const FftPlan&, const CpArgs&, int, const uint32_t*, double2*, double*, int, int,
-              cudaStream_t);
-int launch_conv(const FftPlan&, const double*, int, size_t, const double*, int, size_t, int,
-                double2*, double*, size_t, cudaStream_t);
-int launch_iuv(const FftPlan&, const EngArgs&, int, const double*, const double*, int, int, int,
-               double2*, double*, cudaStream_t);
-int launch_uvw(const FftPlan&, const EngArgs&, int, const double*, const double*, const double*,
-               double2*, double*, cudaStream_t);
-int launch_deflate(const FftPlan&, const EngArgs&, double, const double*, const double*,
-                   const double*, double2*, double2*, cudaStream_t);
-int launch_median(const double*, int, int, int, double*, cudaStream_t);
-int launch_cs_columns(const double*, int, int, const uint32_t*, int, double*, cudaStream_t);
-int launch_normalize_rows(double*, int, int, cudaStream_t);
-int launch_refine_update(double*, const double*, int, int*, cudaStream_t);
-int launch_family_tables(size_t, const size_t*, const size_t*, size_t, const uint64_t*,
-                         uint32_t*, cudaStream_t);
-size_t dense_workspace(int, size_t, const size_t*, size_t, size_t, const size_t*, int kind = 0);
-int launch_fcs_dense(int, const void*, size_t, const size_t*, size_t, size_t, size_t,
-                     const uint32_t*, const size_t*, double*, int, void*, size_t, cudaStream_t,
-                     size_t fam_stride = 0, int kind = 0);
-
-namespace {
-
-inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
-
-// Stream-ordered scratch that only grows.
-struct Scratch {
-  void* p = nullptr;
-  size_t bytes = 0;
-  int ensure(size_t need, cudaStream_t st) {
-    if (need <= bytes) return ST_OK;
-    if (p) FCS_CUDA_TRY(cudaFreeAsync(p, st));
-    p = nullptr;
-    bytes = 0;
-    FCS_CUDA_TRY(cudaMallocAsync(&p, need, st));
-    bytes = need;
-    return ST_OK;
-  }
-  void release(cudaStream_t st) {
-    if (p) cudaFreeAsync(p, st);
-    p = nullptr;
-    bytes = 0;
-  }
-};
-
-// contracted_modes (estimators.cpp:23-29)
-void contracted(size_t f, int* c1, int* c2) {
-  *c1 = f == 0 ? 1 : 0;
-  *c2 = f == 2 ? 1 : 2;
+__global__ void ts_extend_kernel(const double* __restrict__ in, int D, int jt, int J,
+                                 double* __restrict__ ext, double scale, int accumulate) {
+  const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<size_t>(D) * jt) return;
+  const int d = static_cast<int>(i / jt);
+  const int k = static_cast<int>(i - static_cast<size_t>(d) * jt);
+  const double* row = in + static_cast<size_t>(d) * jt;
+  double acc = 0.0;
+  for (int m = k % J; m < jt; m += J) acc += row[m];  // TS bucket (sum h) mod J, sketch.cpp:141
+  ext[i] = accumulate ? ext[i] + scale * acc : scale * acc;
 }
 
-// Host SplitMix64 with the Box-Muller spare (rng.hpp:12-48, rng.cpp:8-21).
-struct HostRng {
-  uint64_t state;
-  double spare = 0.0;
-  bool has_spare = false;
-  explicit HostRng(uint64_t s) : state(s) {}
-  uint64_t next() {
-    state += kGamma;
-    return fmix64(state);
-  }
-  double gaussian() {
-    if (has_spare) {
-      has_spare = false;
-      return spare;
-    }
-    const double u1 = static_cast<double>((next() >> 11) + 1) * 0x1.0p-53;
-    const double u2 = static_cast<double>(next() >> 11) * 0x1.0p-53;
-    const double radius = std::sqrt(-2.0 * std::log(u1));
-    const double angle = 2.0 * std::numbers::pi * u2;
-    spare = radius * std::sin(angle);
-    has_spare = true;
-    return radius * std::cos(angle);
-  }
-};
+int launch_ts_extend(const double* in, int D, int jt, int J, double* ext, double scale,
+                     int accumulate, cudaStream_t st) {
+  const size_t n = static_cast<size_t>(D) * jt;
+  if (n == 0) return ST_OK;
+  ts_extend_kernel<<<ceil_div(n, 256), 256, 0, st>>>(in, D, jt, J, ext, scale, accumulate);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
 
-}  // namespace
 }  // namespace fcs
 
 using namespace fcs;
-
-struct st_engine {
-  int device = 0;
-  size_t dims[3] = {0, 0, 0};
-  size_t hash_len = 0;
-  size_t D = 0;
-  size_t jt = 0;
-  FftPlan plan{};
-  uint32_t* packed = nullptr;  // D x sum(dims)
-  double2* spec = nullptr;     // D x P
-  Scratch scratch, est, vec;
-  EngArgs args() const {
-    EngArgs e{};
-    size_t off = 0;
-    for (int n = 0; n < 3; ++n) {
-      e.dims[n] = static_cast<int>(dims[n]);
-      e.tab_off[n] = static_cast<int>(off);
-      off += dims[n];
-    }
-    e.fam_stride = static_cast<int>(off);
-    e.D = static_cast<int>(D);
-    e.packed = packed;
-    e.spec = spec;
-    return e;
-  }
-};
 
 extern "C" {
 
@@ -219,20 +133,28 @@ int st_fcs_kron(const double* a, size_t ra, size_t ca, const double* b, size_t r
   return rc;
 }
 
-int st_engine_create(st_engine** engine, int dtype, const void* tensor, const size_t* dims,
-                     size_t hash_len, size_t sketch_count, uint64_t seed, void* stream) {
+int st_engine_create_backend(st_engine** engine, int backend, int dtype, const void* tensor,
+                             const size_t* dims, size_t hash_len, size_t sketch_count,
+                             uint64_t seed, void* stream) {
   FCS_CHECK_ARG(engine != nullptr, "st_engine_create: null engine pointer");
+  FCS_CHECK_ARG(backend >= ST_BACKEND_PLAIN && backend <= ST_BACKEND_FCS,
+                "make_contraction_engine: unknown backend");
+  FCS_CHECK_ARG(backend == ST_BACKEND_FCS || backend == ST_BACKEND_TS,
+                "make_contraction_engine: backend not provided by the B200 engine (fcs, ts)");
   FCS_CHECK_ARG(dtype == ST_F32 || dtype == ST_F64, "st_engine_create: unknown dtype");
   FCS_CHECK_ARG(hash_len > 0 && sketch_count > 0,
                 "EstimatorConfig: hash_len and sketch_count must be >= 1");
   for (int n = 0; n < 3; ++n) FCS_CHECK_ARG(dims[n] > 0, "DenseTensor: zero dimension");
+  *engine = nullptr;
   cudaStream_t st = as_stream(stream);
   auto* e = new st_engine();
   FCS_CUDA_TRY(cudaGetDevice(&e->device));
+  e->backend = backend;
   for (int n = 0; n < 3; ++n) e->dims[n] = dims[n];
   e->hash_len = hash_len;
   e->D = sketch_count;
   e->jt = 3 * hash_len - 2;
+  e->slen = backend == ST_BACKEND_TS ? hash_len : e->jt;
   int rc = get_fft_plan(e->jt, &e->plan);
   if (rc) {
     delete e;
@@ -246,13 +168,22 @@ int st_engine_create(st_engine** engine, int dtype, const void* tensor, const si
   double* vals = nullptr;
   void* ws = nullptr;
   const size_t wsb = dense_workspace(dtype, 3, dims, dims[2], sketch_count, hl);
-  if (cudaMallocAsync(reinterpret_cast<void**>(&e->packed),
-                      sketch_count * sum_dims * sizeof(uint32_t), st) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&e->spec),
-                      sketch_count * e->plan.P * sizeof(double2), st) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&vals), sketch_count * e->jt * sizeof(double), st) !=
-          cudaSuccess ||
-      cudaMallocAsync(&ws, std::max<size_t>(1, wsb), st) != cudaSuccess) {
+  const size_t vbytes = sketch_count * e->jt * sizeof(double);
+  bool ok = cudaMallocAsync(reinterpret_cast<void**>(&e->packed),
+                            sketch_count * sum_dims * sizeof(uint32_t), st) == cudaSuccess &&
+            cudaMallocAsync(reinterpret_cast<void**>(&e->spec),
+                            sketch_count * e->plan.P * sizeof(double2), st) == cudaSuccess &&
+            cudaMallocAsync(reinterpret_cast<void**>(&vals), vbytes, st) == cudaSuccess &&
+            cudaMallocAsync(&ws, std::max<size_t>(1, wsb), st) == cudaSuccess;
+  if (ok && backend == ST_BACKEND_TS) {
+    const double one = 1.0;
+    ok = cudaMalloc(reinterpret_cast<void**>(&e->ext), vbytes) == cudaSuccess &&
+         cudaMalloc(reinterpret_cast<void**>(&e->one), sizeof(double)) == cudaSuccess &&
+         cudaMemcpy(e->one, &one, sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess;
+  }
+  if (!ok) {
+    if (vals) cudaFreeAsync(vals, st);
+    if (ws) cudaFreeAsync(ws, st);
     st_engine_destroy(e);
     return fail(ST_ENOMEM, "st_engine_create: device allocation failed");
   }
@@ -260,8 +191,14 @@ int st_engine_create(st_engine** engine, int dtype, const void* tensor, const si
   if (!rc)
     rc = launch_fcs_dense(dtype, tensor, 3, dims, 0, dims[2], sketch_count, e->packed, hl, vals,
                           0, ws, wsb, st, 0);
+  const double* src = vals;
+  if (!rc && backend == ST_BACKEND_TS) {  // TS = (FCS) mod J, kept as its periodic extension
+    rc = launch_ts_extend(vals, static_cast<int>(sketch_count), static_cast<int>(e->jt),
+                          static_cast<int>(hash_len), e->ext, 1.0, 0, st);
+    src = e->ext;
+  }
   if (!rc)
-    rc = launch_spec_from_real(e->plan, vals, e->jt, static_cast<int>(e->jt),
+    rc = launch_spec_from_real(e->plan, src, e->jt, static_cast<int>(e->jt),
                                static_cast<int>(sketch_count), e->spec, st);
   cudaFreeAsync(vals, st);
   cudaFreeAsync(ws, st);
@@ -273,11 +210,19 @@ int st_engine_create(st_engine** engine, int dtype, const void* tensor, const si
   return ST_OK;
 }
 
+int st_engine_create(st_engine** engine, int dtype, const void* tensor, const size_t* dims,
+                     size_t hash_len, size_t sketch_count, uint64_t seed, void* stream) {
+  return st_engine_create_backend(engine, ST_BACKEND_FCS, dtype, tensor, dims, hash_len,
+                                  sketch_count, seed, stream);
+}
+
 int st_engine_destroy(st_engine* e) {
   if (!e) return ST_OK;
   cudaDeviceSynchronize();
   if (e->packed) cudaFree(e->packed);
   if (e->spec) cudaFree(e->spec);
+  if (e->ext) cudaFree(e->ext);
+  if (e->one) cudaFree(e->one);
   e->scratch.release(nullptr);
   e->est.release(nullptr);
   e->vec.release(nullptr);
@@ -286,10 +231,18 @@ int st_engine_destroy(st_engine* e) {
   return ST_OK;
 }
 
-size_t st_engine_composed_len(const st_engine* e) { return e ? e->jt : 0; }
+int st_engine_backend(const st_engine* e) { return e ? e->backend : -1; }
+
+size_t st_engine_composed_len(const st_engine* e) { return e ? e->slen : 0; }
 
 int st_engine_sketches(st_engine* e, double* out, void* stream) {
   FCS_CHECK_ARG(e != nullptr, "st_engine_sketches: null engine");
+  if (e->backend == ST_BACKEND_TS) {
+    FCS_CUDA_TRY(cudaMemcpy2DAsync(out, e->slen * sizeof(double), e->ext, e->jt * sizeof(double),
+                                   e->slen * sizeof(double), e->D, cudaMemcpyDeviceToDevice,
+                                   as_stream(stream)));
+    return ST_OK;
+  }
   return launch_real_from_spec(e->plan, e->spec, static_cast<int>(e->D), out, e->jt,
                                static_cast<int>(e->jt), 0, as_stream(stream));
 }
@@ -341,87 +294,39 @@ int st_engine_deflate(st_engine* e, double weight, const double* u, const double
                       const double* w, void* stream) {
   FCS_CHECK_ARG(e != nullptr, "st_engine_deflate: null engine");
   cudaStream_t st = as_stream(stream);
+  if (e->backend == ST_BACKEND_TS) {
+    // TsEngine::deflate (cpd.cpp:115-122): TS -= ts_sketch(w u o v o w) =
+    // ((CP-form FCS of u o v o w) mod J), then the spectra are rebuilt.
+    const size_t qbytes = 2 * e->D * e->plan.P * sizeof(double2);
+    if (int rc = e->scratch.ensure(qbytes + e->D * e->jt * sizeof(double), st)) return rc;
+    auto* q = static_cast<double2*>(e->scratch.p);
+    auto* c = reinterpret_cast<double*>(static_cast<char*>(e->scratch.p) + qbytes);
+    CpArgs a{};
+    a.order = 3;
+    const EngArgs ea = e->args();
+    for (int n = 0; n < 3; ++n) {
+      a.dims[n] = ea.dims[n];
+      a.tab_off[n] = ea.tab_off[n];
+    }
+    a.fam_stride = ea.fam_stride;
+    a.factors[0] = u;
+    a.factors[1] = v;
+    a.factors[2] = w;
+    a.weights = e->one;
+    a.r_begin = 0;
+    a.r_count = 1;
+    if (int rc = launch_cp(e->plan, a, static_cast<int>(e->D), e->packed, q, c,
+                           static_cast<int>(e->jt), 0, st))
+      return rc;
+    if (int rc = launch_ts_extend(c, static_cast<int>(e->D), static_cast<int>(e->jt),
+                                  static_cast<int>(e->hash_len), e->ext, -weight, 1, st))
+      return rc;
+    return launch_spec_from_real(e->plan, e->ext, e->jt, static_cast<int>(e->jt),
+                                 static_cast<int>(e->D), e->spec, st);
+  }
   if (int rc = e->scratch.ensure(e->D * e->plan.P * sizeof(double2), st)) return rc;
   return launch_deflate(e->plan, e->args(), weight, u, v, w, static_cast<double2*>(e->scratch.p),
                         e->spec, st);
-}
-
-int st_rtpm(int dtype, const void* tensor, size_t dim, size_t rank, size_t num_inits,
-            size_t num_iters, size_t hash_len, size_t sketch_count, uint64_t seed,
-            double* weights, double* factor, void* stream) {
-  FCS_CHECK_ARG(dim > 0, "DenseTensor: zero dimension");
-  FCS_CHECK_ARG(rank > 0 && num_inits > 0 && num_iters > 0,
-                "rtpm: rank, inits, and iterations must be >= 1");
-  cudaStream_t st = as_stream(stream);
-  const size_t dims[3] = {dim, dim, dim};
-  st_engine* e = nullptr;
-  if (int rc = st_engine_create(&e, dtype, tensor, dims, hash_len, sketch_count, seed, st))
-    return rc;
-  struct Guard {
-    st_engine* e;
-    ~Guard() { st_engine_destroy(e); }
-  } guard{e};
-  const size_t L = num_inits;
-  // device: U (L x dim), Y (L x dim), best, next, values, stopped flag
-  if (int rc = e->vec.ensure((2 * L + 2) * dim * sizeof(double) + (L + 1) * sizeof(double) + 16, st))
-    return rc;
-  double* U = static_cast<double*>(e->vec.p);
-  double* Y = U + L * dim;
-  double* best = Y + L * dim;
-  double* next = best + dim;
-  double* vals = next + dim;
-  int* stopped = reinterpret_cast<int*>(vals + L + 1);
-  std::vector<double> hU(L * dim), hvals(L);
-  // init_rng = SplitMix64(mix(seed ^ 0x7274706d)) (cpd.cpp:245)
-  HostRng rng(splitmix_draw(seed ^ 0x7274706dULL, 1));
-  for (size_t r = 0; r < rank; ++r) {
-    for (size_t l = 0; l < L; ++l) {  // random_unit (cpd.cpp:199-204), same draw order
-      double* u = hU.data() + l * dim;
-      double sq = 0.0;
-      for (size_t i = 0; i < dim; ++i) {
-        u[i] = rng.gaussian();
-      }
-      for (size_t i = 0; i < dim; ++i) sq += u[i] * u[i];
-      const double norm = std::sqrt(sq);
-      if (norm > 0)
-        for (size_t i = 0; i < dim; ++i) u[i] /= norm;
-    }
-    FCS_CUDA_TRY(cudaMemcpyAsync(U, hU.data(), L * dim * sizeof(double), cudaMemcpyHostToDevice, st));
-    // L restarts advance in lockstep; a row whose norm underflows stays zero,
-    // exactly like the reference's early break (iuu(0) = 0).
-    for (size_t it = 0; it < num_iters; ++it) {
-      if (int rc = st_engine_iuv(e, L, U, U, 0, Y, 1, st)) return rc;
-      if (int rc = launch_normalize_rows(Y, static_cast<int>(L), static_cast<int>(dim), st)) return rc;
-      std::swap(U, Y);
-    }
-    if (int rc = st_engine_uvw(e, L, U, U, U, vals, 1, st)) return rc;
-    FCS_CUDA_TRY(cudaMemcpyAsync(hvals.data(), vals, L * sizeof(double), cudaMemcpyDeviceToHost, st));
-    FCS_CUDA_TRY(cudaStreamSynchronize(st));
-    double best_value = -std::numeric_limits<double>::infinity();
-    long arg = -1;
-    for (size_t l = 0; l < L; ++l) {
-      if (hvals[l] > best_value) {  // strict >, first wins (cpd.cpp:260)
-        best_value = hvals[l];
-        arg = static_cast<long>(l);
-      }
-    }
-    if (arg < 0) return fail(ST_ENUMERIC, "rtpm: no candidate with a finite contraction value");
-    FCS_CUDA_TRY(cudaMemcpyAsync(best, U + arg * dim, dim * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    FCS_CUDA_TRY(cudaMemsetAsync(stopped, 0, sizeof(int), st));
-    for (size_t it = 0; it < num_iters; ++it) {  // refinement (cpd.cpp:266-270)
-      if (int rc = st_engine_iuv(e, 1, best, best, 0, next, 1, st)) return rc;
-      if (int rc = launch_refine_update(best, next, static_cast<int>(dim), stopped, st)) return rc;
-    }
-    if (int rc = st_engine_uvw(e, 1, best, best, best, vals, 1, st)) return rc;
-    double weight = 0.0;
-    FCS_CUDA_TRY(cudaMemcpyAsync(&weight, vals, sizeof(double), cudaMemcpyDeviceToHost, st));
-    FCS_CUDA_TRY(cudaMemcpyAsync(factor + r * dim, best, dim * sizeof(double), cudaMemcpyDeviceToHost, st));
-    FCS_CUDA_TRY(cudaStreamSynchronize(st));
-    weights[r] = weight;
-    if (int rc = st_engine_deflate(e, weight, best, best, best, st)) return rc;
-  }
-  FCS_CUDA_TRY(cudaStreamSynchronize(st));
-  return ST_OK;
 }
 
 }  // extern "C"

@@ -1,10 +1,12 @@
 """ContractionEngine plug-in and the sketched RTPM driver over the B200 C-ABI.
 
 Mirrors ``cpd.hpp:12-84``: ``SketchBackend``, ``ContractionEngine``
-(uvw / iuv / deflate / uuu / iuu / shape), ``make_contraction_engine`` and
-``rtpm``. Only the FCS backend exists on the B200 path (the north star's
-scope); Plain/CS/TS/HCS raise ValueError naming the missing backend, which is
-the reference's own error class for an unusable backend (cpd.cpp:27).
+(uvw / iuv / deflate / uuu / iuu / shape), ``make_contraction_engine``,
+``rtpm``, ``rtpm_asym``, ``als`` and ``residual_norm``. The B200 engine
+provides the FCS backend (the north star) and the TS backend (SURVEY.md §8(f)
+rank 1, the equal-hash baseline); Plain/CS/HCS raise ValueError naming the
+missing backend, the reference's own error class for an unusable backend
+(cpd.cpp:27).
 
 The engine keeps the D sketches' spectra resident on the device
 (``st_engine_*``); batched entry points (``iuv_batch`` / ``uvw_batch``) are
@@ -76,10 +78,12 @@ class ContractionEngine:
         raise NotImplementedError
 
 
-class FcsEngine(ContractionEngine):
-    """FcsEngine (cpd.cpp:61-94) on the device: D = cfg.sketch_count families
-    from families_for (estimators.cpp:104-115), sketches built once by K1 and
-    their spectra cached (precompute_fcs, estimators.cpp:140-149)."""
+class _DeviceEngine(ContractionEngine):
+    """A sketch engine on the device: D = cfg.sketch_count families from
+    families_for (estimators.cpp:104-115), sketches built once by K1 and their
+    spectra cached (st_engine_create_backend)."""
+
+    BACKEND: SketchBackend = SketchBackend.FCS
 
     def __init__(self, t: DenseTensor, cfg: EstimatorConfig):
         if not isinstance(t, DenseTensor):
@@ -91,10 +95,9 @@ class FcsEngine(ContractionEngine):
         self._shape = t.shape()
         self.cfg = cfg
         h = C.c_void_p()
-        _check(L.lib().st_engine_create(C.byref(h), t.st_dtype, _ptr(t.flat),
-                                        L.size_array(self._shape), cfg.hash_len,
-                                        cfg.sketch_count, C.c_uint64(cfg.seed & ((1 << 64) - 1)),
-                                        _stream()))
+        _check(L.lib().st_engine_create_backend(
+            C.byref(h), self.BACKEND.value, t.st_dtype, _ptr(t.flat), L.size_array(self._shape),
+            cfg.hash_len, cfg.sketch_count, C.c_uint64(cfg.seed & ((1 << 64) - 1)), _stream()))
         self._h = h
 
     def __del__(self):
@@ -107,10 +110,11 @@ class FcsEngine(ContractionEngine):
         return list(self._shape)
 
     def composed_len(self) -> int:
+        """Sketch length: J~ = 3J - 2 (FCS) or J (TS)."""
         return int(L.lib().st_engine_composed_len(self._h))
 
     def sketches(self) -> torch.Tensor:
-        """Current D x J~ sketch values (after any deflations)."""
+        """Current D x composed_len() sketch values (after any deflations)."""
         out = torch.empty((self.cfg.sketch_count, self.composed_len()), dtype=torch.float64,
                           device=_dev())
         _check(L.lib().st_engine_sketches(self._h, _ptr(out), _stream()))
@@ -161,21 +165,44 @@ class FcsEngine(ContractionEngine):
                                          _stream()))
 
 
+class FcsEngine(_DeviceEngine):
+    """FcsEngine (cpd.cpp:61-94): spectra of the D fast count sketches
+    (precompute_fcs, estimators.cpp:140-149)."""
+    BACKEND = SketchBackend.FCS
+
+
+class TsEngine(_DeviceEngine):
+    """TsEngine (cpd.cpp:96-126): D tensor sketches of length J (ts_sketch,
+    sketch.cpp:135-149) and the circular-correlation estimates of
+    estimators.cpp:209-233, computed by the FCS kernels on the sketch's
+    J-periodic extension."""
+    BACKEND = SketchBackend.TS
+
+
+_ENGINES = {SketchBackend.FCS: FcsEngine, SketchBackend.TS: TsEngine}
+
+
+def _engine_backend(backend: SketchBackend) -> int:
+    if backend not in _ENGINES:
+        raise ValueError(f"make_contraction_engine: backend '{backend_name(backend)}' is not "
+                         "provided by the B200 library (fcs, ts)")
+    return backend.value
+
+
 def make_contraction_engine(t, backend: SketchBackend, cfg: EstimatorConfig) -> ContractionEngine:
     """make_contraction_engine (cpd.cpp:220-232)."""
     if not isinstance(t, DenseTensor):
         t = DenseTensor.from_array(t)
     if t.order() != 3:
         raise ValueError("make_contraction_engine: order-3 tensor required")
-    if backend == SketchBackend.FCS:
-        return FcsEngine(t, cfg)
-    raise ValueError(f"make_contraction_engine: backend '{backend_name(backend)}' is not "
-                     "provided by the B200 FCS library")
+    _engine_backend(backend)
+    return _ENGINES[backend](t, cfg)
 
 
 @dataclass
 class RtpmConfig:
-    """RtpmConfig (cpd.hpp:49-55)."""
+    """RtpmConfig (cpd.hpp:49-55). The default backend is FCS here (the
+    reference defaults to Plain, which the B200 library does not provide)."""
     target_rank: int = 1
     num_inits: int = 15
     num_power_iters: int = 20
@@ -183,28 +210,106 @@ class RtpmConfig:
     estimator: EstimatorConfig = field(default_factory=EstimatorConfig)
 
 
-def rtpm(t, cfg: RtpmConfig) -> CpTensor:
-    """rtpm (cpd.cpp:234-277) with the FCS backend: restarts batched on the
-    device (st_rtpm); same initial-vector stream, argmax rule and deflation."""
+@dataclass
+class AlsConfig:
+    """AlsConfig (cpd.hpp:57-63)."""
+    target_rank: int = 1
+    max_iters: int = 50
+    backend: SketchBackend = SketchBackend.FCS
+    estimator: EstimatorConfig = field(default_factory=EstimatorConfig)
+    tol: float = 1e-8
+
+
+def _order3(t, op: str) -> DenseTensor:
     if not isinstance(t, DenseTensor):
         t = DenseTensor.from_array(t)
     if t.order() != 3:
-        raise ValueError("rtpm: order-3 tensor required")
+        raise ValueError(f"{op}: order-3 tensor required")
+    return t
+
+
+def _seed(e: EstimatorConfig):
+    return C.c_uint64(e.seed & ((1 << 64) - 1))
+
+
+def _unpack_factors(f: np.ndarray, dims, R: int):
+    out, off = [], 0
+    for n in dims:
+        out.append(f[off:off + n * R].reshape((R, n)).T.copy())
+        off += n * R
+    return out
+
+
+def rtpm(t, cfg: RtpmConfig) -> CpTensor:
+    """rtpm (cpd.cpp:234-277): restarts batched on the device (st_rtpm_backend);
+    same initial-vector stream, argmax rule and deflation."""
+    t = _order3(t, "rtpm")
     dims = t.shape()
     if dims[0] != dims[1] or dims[1] != dims[2]:
         raise ValueError("rtpm: cubical tensor required")
-    if cfg.backend != SketchBackend.FCS:
-        raise ValueError(f"make_contraction_engine: backend '{backend_name(cfg.backend)}' is not "
-                         "provided by the B200 FCS library")
     if cfg.target_rank == 0 or cfg.num_inits == 0 or cfg.num_power_iters == 0:
         raise ValueError("rtpm: rank, inits, and iterations must be >= 1")
+    backend = _engine_backend(cfg.backend)
     dim, R = dims[0], cfg.target_rank
     w = np.empty(R, np.float64)
     f = np.empty(dim * R, np.float64)
     e = cfg.estimator
-    _check(L.lib().st_rtpm(t.st_dtype, _ptr(t.flat), dim, R, cfg.num_inits, cfg.num_power_iters,
-                           e.hash_len, e.sketch_count, C.c_uint64(e.seed & ((1 << 64) - 1)),
-                           w.ctypes.data_as(C.c_void_p), f.ctypes.data_as(C.c_void_p),
-                           _stream()))
+    _check(L.lib().st_rtpm_backend(backend, t.st_dtype, _ptr(t.flat), dim, R, cfg.num_inits,
+                                   cfg.num_power_iters, e.hash_len, e.sketch_count, _seed(e),
+                                   w.ctypes.data_as(C.c_void_p), f.ctypes.data_as(C.c_void_p),
+                                   _stream()))
     factor = f.reshape((R, dim)).T
     return CpTensor(w, [factor, factor, factor])
+
+
+def rtpm_asym(t, cfg: RtpmConfig) -> CpTensor:
+    """rtpm_asym (cpd.cpp:279-335) for a general order-3 tensor (st_rtpm_asym)."""
+    t = _order3(t, "rtpm_asym")
+    if cfg.target_rank == 0 or cfg.num_inits == 0 or cfg.num_power_iters == 0:
+        raise ValueError("rtpm_asym: rank, inits, and iterations must be >= 1")
+    backend = _engine_backend(cfg.backend)
+    dims, R = t.shape(), cfg.target_rank
+    w = np.empty(R, np.float64)
+    f = np.empty(sum(dims) * R, np.float64)
+    e = cfg.estimator
+    _check(L.lib().st_rtpm_asym(backend, t.st_dtype, _ptr(t.flat), L.size_array(dims), R,
+                                cfg.num_inits, cfg.num_power_iters, e.hash_len, e.sketch_count,
+                                _seed(e), w.ctypes.data_as(C.c_void_p),
+                                f.ctypes.data_as(C.c_void_p), _stream()))
+    return CpTensor(w, _unpack_factors(f, dims, R))
+
+
+def als(t, cfg: AlsConfig, return_sweeps: bool = False):
+    """als (cpd.cpp:337-383): engine MTTKRP columns (one batched iuv per mode),
+    exact Gram solves, device residual each sweep (st_als)."""
+    t = _order3(t, "als")
+    if cfg.target_rank == 0 or cfg.max_iters == 0:
+        raise ValueError("als: rank and iterations must be >= 1")
+    backend = _engine_backend(cfg.backend)
+    dims, R = t.shape(), cfg.target_rank
+    w = np.empty(R, np.float64)
+    f = np.empty(sum(dims) * R, np.float64)
+    sweeps = C.c_size_t(0)
+    e = cfg.estimator
+    _check(L.lib().st_als(backend, t.st_dtype, _ptr(t.flat), L.size_array(dims), R,
+                          cfg.max_iters, C.c_double(cfg.tol), e.hash_len, e.sketch_count,
+                          _seed(e), w.ctypes.data_as(C.c_void_p), f.ctypes.data_as(C.c_void_p),
+                          C.byref(sweeps), _stream()))
+    cp = CpTensor(w, _unpack_factors(f, dims, R))
+    return (cp, int(sweeps.value)) if return_sweeps else cp
+
+
+def residual_norm(t, cp: CpTensor) -> float:
+    """residual_norm (cpd.cpp:385-392): ||t - densify(cp)||_F / ||t||_F on the
+    device (st_residual_norm), order-3."""
+    t = _order3(t, "residual_norm")
+    dims = t.shape()
+    if cp.order() != 3 or cp.shape() != list(dims):
+        raise ValueError("residual_norm: CP shape does not match the tensor")
+    R = cp.rank()
+    packed = torch.cat([f.reshape(-1) for f in cp._factors_cm])
+    w = cp.weights.contiguous()
+    out = C.c_double(0.0)
+    _check(L.lib().st_residual_norm(t.st_dtype, _ptr(t.flat), L.size_array(dims), _ptr(w), R,
+                                    _ptr(packed), C.byref(out), _stream()))
+    return out.value

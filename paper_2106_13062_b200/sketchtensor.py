@@ -286,6 +286,11 @@ class CpTensor:
     def shape(self) -> List[int]:
         return [f.shape[1] for f in self._factors_cm]
 
+    @property
+    def factors(self) -> List[torch.Tensor]:
+        """The I_n x R factor matrices (views of the column-major device copies)."""
+        return [f.t() for f in self._factors_cm]
+
 
 # ------------------------------------------------------------------- sketches
 class SketchKind(enum.Enum):

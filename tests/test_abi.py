@@ -46,7 +46,7 @@ def test_host_calls_without_gpu():
     lib = _lib.lib()
     assert lib.st_family_seed(0, 0) == 0xE220A8397B1DCDAF
     assert lib.st_family_seed(0, 1) == 0x910A2DEC89025CC1
-    assert lib.st_abi_version() == 2
+    assert lib.st_abi_version() == 3
 
 
 def test_host_gaussian_matches_reference_stream():
