@@ -44,6 +44,9 @@ enum {
 
 enum { ST_F32 = 0, ST_F64 = 1 };
 
+/* SketchKind (sketch.hpp:10), same order. */
+enum { ST_SKETCH_CS = 0, ST_SKETCH_TS = 1, ST_SKETCH_FCS = 2 };
+
 /* SketchBackend (cpd.hpp:13), same order. The B200 engine provides TS and FCS. */
 enum {
   ST_BACKEND_PLAIN = 0,
@@ -298,6 +301,52 @@ int st_als(int backend, int dtype, const void* tensor, const size_t* dims, size_
  * only ||T|| is. */
 int st_residual_norm(int dtype, const void* tensor, const size_t* dims, const double* weights,
                      size_t rank, const double* factors, double* out, void* stream);
+
+/* ------------------------------------ inner products, regression, codecs */
+
+/* Sketched inner product <a, b> of two device tensors of the same shape:
+ * D families from families_for(dims, {hash_len, D, seed}); per family the dot
+ * of the two sketches (kind ST_SKETCH_FCS: inner_once, estimators.cpp:193-196;
+ * ST_SKETCH_TS: inner_once_ts, estimators.cpp:235-239), then median_reduce
+ * (estimate_inner, estimators.cpp:198-207). estimates (device, D doubles) and
+ * out (HOST, the median) may each be NULL. */
+int st_estimate_inner(int kind, int dtype, const void* a, const void* b, size_t order,
+                      const size_t* dims, size_t hash_len, size_t sketch_count, uint64_t seed,
+                      double* estimates, double* out, void* stream);
+/* out[k] = <a_k, b_k> for `count` device sketch rows of length len (fixed
+ * summation order): the dot of inner_once / inner_once_ts for any family. */
+int st_sketch_dots(size_t count, size_t len, const double* a, const double* b, double* out,
+                   void* stream);
+
+/* Sketched regression-layer forward map (Eq. 20):
+ * Y[b][c] = median_d <FCS_d(X_b), FCS_d(W_c)> + bias[c], with X batch rows and
+ * W classes rows, each row an order-`order` tensor of shape dims (column-major,
+ * rows contiguous: x is batch x prod(dims), w is classes x prod(dims)). All
+ * rows of one family are sketched by one K1 launch. bias (device) may be NULL;
+ * y is device batch x classes. */
+int st_regression_forward(int dtype, const void* x, size_t batch, const void* w, size_t classes,
+                          const double* bias, size_t order, const size_t* dims, size_t hash_len,
+                          size_t sketch_count, uint64_t seed, double* y, void* stream);
+
+/* compress_contraction: FCS of A (x)_{3,1} B for device
+ * tensors A (dims_a = I1, I2, L) and B (dims_b = L, I3, I4) without forming
+ * the order-4 result: sum_l FCS(A(:,:,l); pairs 0,1) * FCS(B(l,:,:); pairs 2,3)
+ * through the FFT. packed: D families of 4 pairs (I1, I2, I3, I4 entries,
+ * st_family_tables layout); out D x (sum J_n - 3). L = 1 is compress_kron. */
+int st_fcs_contraction(int dtype, const void* a, const size_t* dims_a, const void* b,
+                       const size_t* dims_b, size_t sketch_count, const uint32_t* packed,
+                       const size_t* hash_lens, double* out, void* stream);
+
+/* decompress_kron / decompress_contraction:
+ * out[q] = median_d prod_n s_n(i_n) * sketch_d[(sum_n h_n(i_n)) mod len] for
+ * `count` device multi-indices idx (count x order, uint32), order <= 4. */
+int st_sketch_decompress(const double* sketch, size_t sketch_count, size_t len,
+                         const uint32_t* packed, size_t order, const size_t* dims, size_t count,
+                         const uint32_t* idx, double* out, void* stream);
+/* Full Kronecker reconstruction: out is the (I1 I3) x (I2 I4) column-major
+ * estimate of A (x) B, row = I3 i1 + i3, col = I4 i2 + i4 (dims4 = I1..I4). */
+int st_kron_decompress_all(const double* sketch, size_t sketch_count, size_t len,
+                           const uint32_t* packed, const size_t* dims4, double* out, void* stream);
 
 /* ---------------------------------------------------------- synthetic data */
 

@@ -501,3 +501,194 @@ def hcs_cp(weights, factors, buckets, signs, hash_lens) -> np.ndarray:
             term = np.multiply.outer(term, c[:, r])
         out += term
     return out
+
+
+# ------------------------------------------------ TS engine, CPD drivers (§8(f))
+class PrecomputedTs(PrecomputedFcs):
+    """PrecomputedTs (estimators.cpp:209-215): TS sketch + its J-point DFT."""
+
+    def __init__(self, values, buckets, signs, hash_lens):
+        self.values = np.asarray(values, np.float64)
+        self.buckets, self.signs, self.hash_lens = buckets, signs, hash_lens
+        self.n = hash_lens[0]
+        if len(self.values) != self.n:
+            raise ValueError("PrecomputedTs: TS sketch required")
+        self.spectrum = dft(self.values, self.n)
+
+
+class TsEngine(FcsEngine):
+    """TsEngine (cpd.cpp:96-126): estimates by circular correlation at length J
+    (estimate_uvw / estimate_iuv over PrecomputedTs, estimators.cpp:221-233)."""
+
+    def __init__(self, t: np.ndarray, hash_len: int, sketch_count: int, seed: int):
+        self.shape = t.shape
+        self.pres = []
+        for b, s, j in families_for(t.shape, hash_len, sketch_count, seed):
+            self.pres.append(PrecomputedTs(ts_sketch(t, b, s, j), b, s, j))
+
+    def deflate(self, weight: float, u, v, w):
+        """cpd.cpp:115-122: values -= ts_sketch(rank_one(weight, {u,v,w}))."""
+        facs = [np.asarray(x, np.float64).reshape(-1, 1) for x in (u, v, w)]
+        for i, p in enumerate(self.pres):
+            comp = ts_cp([weight], facs, p.buckets, p.signs, p.hash_lens)
+            self.pres[i] = PrecomputedTs(p.values - comp, p.buckets, p.signs, p.hash_lens)
+
+
+def rtpm_asym(engine, dims, rank: int, num_inits: int, num_iters: int, seed: int):
+    """rtpm_asym (cpd.cpp:279-335) over any engine with iuv/uvw/deflate."""
+    if rank == 0 or num_inits == 0 or num_iters == 0:
+        raise ValueError("rtpm_asym: rank, inits, and iterations must be >= 1")
+    init_rng = SplitMix64(mix(seed ^ 0x72743161))
+    weights = np.zeros(rank)
+    factors = [np.zeros((n, rank)) for n in dims]
+
+    def sweep(vecs):
+        for m in range(3):
+            c1, c2 = _contracted_modes(m, "estimate_iuv")
+            vecs[m], _ = normalize_or_zero(engine.iuv(vecs[c1], vecs[c2], m))
+
+    for r in range(rank):
+        best, best_value = None, -math.inf
+        for _ in range(num_inits):
+            vecs = [random_unit(init_rng, n) for n in dims]
+            for _ in range(num_iters):
+                sweep(vecs)
+            value = abs(engine.uvw(*vecs))
+            if value > best_value:
+                best_value, best = value, list(vecs)
+        for _ in range(num_iters):
+            sweep(best)
+        weight = engine.uvw(*best)
+        if weight < 0:
+            best[0], weight = -best[0], -weight
+        weights[r] = weight
+        for n in range(3):
+            factors[n][:, r] = best[n]
+        engine.deflate(weight, *best)
+    return weights, factors
+
+
+def min_norm_solve(G: np.ndarray, B: np.ndarray) -> np.ndarray:
+    """completeOrthogonalDecomposition().solve (Eigen semantics, cpd.cpp:369-370):
+    column-pivoted QR, numerical rank #{|r_ii| > eps n max|r_kk|}, then the
+    minimum-norm solution of the rank-r trapezoidal system."""
+    import scipy.linalg
+    n = G.shape[0]
+    Q, R, P = scipy.linalg.qr(G, pivoting=True)
+    d = np.abs(np.diag(R))
+    r = int(np.sum(d > np.finfo(np.float64).eps * n * d.max(initial=0.0)))
+    X = np.zeros((n, B.shape[1]))
+    if r == 0:
+        return X
+    c = (Q.T @ B)[:r]
+    y = np.linalg.lstsq(R[:r], c, rcond=None)[0]  # minimum-norm for the full-row-rank r x n
+    X[P] = y
+    return X
+
+
+def residual_norm(t: np.ndarray, weights, factors) -> float:
+    """residual_norm (cpd.cpp:385-392)."""
+    a, b, c = factors
+    diff = np.einsum("r,ir,jr,kr->ijk", np.asarray(weights, np.float64), a, b, c) - t
+    den = float(np.sqrt(np.sum(t * t)))
+    num = float(np.sqrt(np.sum(diff * diff)))
+    if den == 0.0:
+        return 0.0 if num == 0.0 else math.inf
+    return num / den
+
+
+def als(engine, t: np.ndarray, rank: int, max_iters: int, tol: float, seed: int):
+    """als (cpd.cpp:337-383); returns (weights, factors, sweeps)."""
+    if rank == 0 or max_iters == 0:
+        raise ValueError("als: rank and iterations must be >= 1")
+    dims = t.shape
+    init_rng = SplitMix64(mix(seed ^ 0x616C73))
+    factors = [np.stack([random_unit(init_rng, n) for _ in range(rank)], axis=1) for n in dims]
+    weights = np.ones(rank)
+    prev, sweeps = math.inf, 0
+    for sweep in range(max_iters):
+        for mode in range(3):
+            o1, o2 = _contracted_modes(mode, "als")
+            mttkrp = np.stack([engine.iuv(factors[o1][:, r], factors[o2][:, r], mode)
+                               for r in range(rank)], axis=1)
+            gram = (factors[o1].T @ factors[o1]) * (factors[o2].T @ factors[o2])
+            f = min_norm_solve(gram, mttkrp.T).T
+            for r in range(rank):
+                norm = math.sqrt(float(f[:, r] @ f[:, r]))
+                weights[r] = norm
+                if norm > 1e-150:
+                    f[:, r] /= norm
+            factors[mode] = f
+        residual = residual_norm(t, weights, factors)
+        sweeps = sweep + 1
+        if abs(prev - residual) < tol:
+            break
+        prev = residual
+    return weights.copy(), factors, sweeps
+
+
+# ------------------------------------------ inner products, regression, codecs
+def inner_once(a, b, buckets, signs, hash_lens) -> float:
+    """inner_once (estimators.cpp:193-196)."""
+    if a.shape != b.shape:
+        raise ValueError("inner_once: shape mismatch")
+    return float(fcs_dense(a, buckets, signs, hash_lens) @ fcs_dense(b, buckets, signs, hash_lens))
+
+
+def inner_once_ts(a, b, buckets, signs, hash_lens) -> float:
+    """inner_once_ts (estimators.cpp:235-239)."""
+    if a.shape != b.shape:
+        raise ValueError("inner_once_ts: shape mismatch")
+    return float(ts_sketch(a, buckets, signs, hash_lens) @ ts_sketch(b, buckets, signs, hash_lens))
+
+
+def estimate_inner(a, b, hash_len: int, sketch_count: int, seed: int) -> float:
+    """estimate_inner (estimators.cpp:198-207)."""
+    if a.shape != b.shape:
+        raise ValueError("estimate_inner: shape mismatch")
+    return float(median_reduce([inner_once(a, b, *f) for f in
+                                families_for(a.shape, hash_len, sketch_count, seed)]))
+
+
+def regression_forward(x_rows, w_rows, bias, dims, hash_len: int, sketch_count: int,
+                       seed: int) -> np.ndarray:
+    """Y = median_d FCS_d(X rows) FCS_d(W rows)^T + b (PAPER.md
+    Eq. 20); rows are column-major order-N tensors of shape dims."""
+    dims = tuple(int(d) for d in dims)
+    X = np.asarray(x_rows, np.float64).reshape(-1, int(np.prod(dims)))
+    W = np.asarray(w_rows, np.float64).reshape(-1, int(np.prod(dims)))
+    ests = []
+    for f in families_for(dims, hash_len, sketch_count, seed):
+        sx = np.stack([fcs_dense(x.reshape(dims, order="F"), *f) for x in X])
+        sw = np.stack([fcs_dense(w.reshape(dims, order="F"), *f) for w in W])
+        ests.append(sx @ sw.T)
+    y = median_reduce(ests)
+    return y + (0.0 if bias is None else np.asarray(bias, np.float64)[None, :])
+
+
+def kron_tensor(a, b) -> np.ndarray:
+    """A (x) B as the order-4 tensor K[i1, i2, i3, i4] = A[i1, i2] B[i3, i4]
+    (the Kronecker matrix entry at row I3 i1 + i3, col I4 i2 + i4)."""
+    return np.einsum("ij,kl->ijkl", np.asarray(a, np.float64), np.asarray(b, np.float64))
+
+
+def contraction_tensor(a, b) -> np.ndarray:
+    """A (x)_{3,1} B: C[i1, i2, i3, i4] = sum_l A[i1, i2, l] B[l, i3, i4]."""
+    return np.einsum("ijl,lkm->ijkm", np.asarray(a, np.float64), np.asarray(b, np.float64))
+
+
+def compress_tensor4(t4, hash_len: int, sketch_count: int, seed: int) -> np.ndarray:
+    """The defining identity of compress_kron / compress_contraction
+    (SPEC.md:403-404): fcs_dense of the materialised order-4 tensor per family."""
+    return np.stack([fcs_dense(t4, *f) for f in
+                     families_for(t4.shape, hash_len, sketch_count, seed)])
+
+
+def decompress4(sk, fams, i1, i2, i3, i4) -> float:
+    """median_d s1 s2 s3 s4 sk_d[(h1+h2+h3+h4) mod len]."""
+    vals = []
+    for d, (bk, sg, _) in enumerate(fams):
+        h = sum(int(bk[n][i]) for n, i in enumerate((i1, i2, i3, i4)))
+        s = int(np.prod([int(sg[n][i]) for n, i in enumerate((i1, i2, i3, i4))]))
+        vals.append(s * sk[d][h % sk.shape[1]])
+    return float(median_reduce(vals))

@@ -466,3 +466,30 @@ def residual_norm(t: np.ndarray, weights, factors) -> float:
     _check(lib().ref_residual_norm(_ptr(data), _ptr(dims), _ptr(w), _sz(len(w)), _ptr(f),
                                    C.byref(out)))
     return out.value
+
+
+def estimate_inner(a: np.ndarray, b: np.ndarray, hash_len: int, sketch_count: int,
+                   seed: int) -> float:
+    """estimate_inner (estimators.cpp:198-207)."""
+    dims = _dims(a.shape)
+    da = np.ascontiguousarray(np.asarray(a, np.float64).ravel(order="F"))
+    db = np.ascontiguousarray(np.asarray(b, np.float64).ravel(order="F"))
+    out = _d(0)
+    _check(lib().ref_estimate_inner(_ptr(da), _ptr(db), _sz(len(dims)), _ptr(dims),
+                                    _sz(hash_len), _sz(sketch_count), _u64(seed), C.byref(out)))
+    return out.value
+
+
+def inner_once_tables(a: np.ndarray, b: np.ndarray, buckets, signs, hash_lens,
+                      ts: bool = False) -> float:
+    """inner_once / inner_once_ts (estimators.cpp:193-196, 235-239)."""
+    dims = _dims(a.shape)
+    da = np.ascontiguousarray(np.asarray(a, np.float64).ravel(order="F"))
+    db = np.ascontiguousarray(np.asarray(b, np.float64).ravel(order="F"))
+    bk, sg = _pack_tables(buckets, signs)
+    hl = _dims(hash_lens)
+    out = _d(0)
+    _check(lib().ref_inner_once_tables(C.c_int(1 if ts else 0), _ptr(da), _ptr(db),
+                                       _sz(len(dims)), _ptr(dims), _ptr(bk), _ptr(sg), _ptr(hl),
+                                       C.byref(out)))
+    return out.value

@@ -480,3 +480,32 @@ int ref_residual_norm(const double* data, const std::size_t* dims, const double*
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------ inner products
+extern "C" {
+
+// estimate_inner (estimators.cpp:198-207).
+int ref_estimate_inner(const double* a, const double* b, std::size_t order,
+                       const std::size_t* dims, std::size_t hash_len, std::size_t sketch_count,
+                       std::uint64_t seed, double* out) {
+  return guarded([&] {
+    EstimatorConfig cfg;
+    cfg.hash_len = hash_len;
+    cfg.sketch_count = sketch_count;
+    cfg.seed = seed;
+    *out = estimate_inner(make_tensor(a, order, dims), make_tensor(b, order, dims), cfg);
+  });
+}
+
+// inner_once / inner_once_ts (estimators.cpp:193-196, 235-239) with an explicit family.
+int ref_inner_once_tables(int ts, const double* a, const double* b, std::size_t order,
+                          const std::size_t* dims, const std::uint32_t* buckets,
+                          const std::int8_t* signs, const std::size_t* hash_lens, double* out) {
+  return guarded([&] {
+    HashFamily fam = make_family(order, dims, buckets, signs, hash_lens);
+    DenseTensor ta = make_tensor(a, order, dims), tb = make_tensor(b, order, dims);
+    *out = ts ? inner_once_ts(ta, tb, fam) : inner_once(ta, tb, fam);
+  });
+}
+
+}  // extern "C"

@@ -15,4 +15,9 @@ from .engine import (AlsConfig, ContractionEngine, FcsEngine, RtpmConfig, Sketch
                      TsEngine, als, backend_from_name, backend_name, make_contraction_engine,
                      residual_norm, rtpm, rtpm_asym)
 
+from .codecs import (KronSketch, compress_contraction, compress_kron, compression_ratio,  # noqa
+                     decompress_contraction, decompress_kron, estimate_inner, hash_memory,
+                     hash_memory_long_pair, inner_once, inner_once_ts, reconstruct_kron,
+                     sketched_regression_forward)
+
 __all__ = [n for n in dir() if not n.startswith("_")]

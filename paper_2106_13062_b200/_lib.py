@@ -17,6 +17,7 @@ HEADER = os.path.join(os.path.dirname(_PKG), "include", "fcs_b200.h")
 ST_OK, ST_EINVAL, ST_ENUMERIC, ST_ECUDA, ST_ENCCL, ST_ENOMEM = range(6)
 ST_F32, ST_F64 = 0, 1
 ST_BACKEND_PLAIN, ST_BACKEND_CS, ST_BACKEND_TS, ST_BACKEND_HCS, ST_BACKEND_FCS = range(5)
+ST_SKETCH_CS, ST_SKETCH_TS, ST_SKETCH_FCS = range(3)
 MAX_ORDER = 8
 
 p, sz, u64, i32, dbl = C.c_void_p, C.c_size_t, C.c_uint64, C.c_int, C.c_double
@@ -60,6 +61,12 @@ SIGNATURES = {
     "st_rtpm_asym": (i32, [i32, i32, p, p, sz, sz, sz, sz, sz, u64, p, p, p]),
     "st_als": (i32, [i32, i32, p, p, sz, sz, dbl, sz, sz, u64, p, p, p, p]),
     "st_residual_norm": (i32, [i32, p, p, p, sz, p, p, p]),
+    "st_estimate_inner": (i32, [i32, i32, p, p, sz, p, sz, sz, u64, p, p, p]),
+    "st_sketch_dots": (i32, [sz, sz, p, p, p, p]),
+    "st_regression_forward": (i32, [i32, p, sz, p, sz, p, sz, p, sz, sz, u64, p, p]),
+    "st_fcs_contraction": (i32, [i32, p, p, p, p, sz, p, p, p, p]),
+    "st_sketch_decompress": (i32, [p, sz, sz, p, sz, p, sz, p, p, p]),
+    "st_kron_decompress_all": (i32, [p, sz, sz, p, p, p, p]),
     "st_host_gaussian": (i32, [u64, sz, p, i32]),
     "st_device_gaussian": (i32, [i32, u64, sz, p, p]),
 }

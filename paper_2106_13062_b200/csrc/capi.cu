@@ -51,10 +51,6 @@ int launch_family_tables(size_t, const size_t*, const size_t*, size_t, const uin
                          uint32_t*, cudaStream_t);
 int launch_pack_tables(size_t, const uint32_t*, const int8_t*, uint32_t*, cudaStream_t);
 int launch_device_gaussian(int, uint64_t, size_t, void*, cudaStream_t);
-size_t dense_workspace(int, size_t, const size_t*, size_t, size_t, const size_t*, int kind = 0);
-int launch_fcs_dense(int, const void*, size_t, const size_t*, size_t, size_t, size_t,
-                     const uint32_t*, const size_t*, double*, int, void*, size_t, cudaStream_t,
-                     size_t fam_stride = 0, int kind = 0);
 
 // RAII device buffer for the host-buffer conveniences.
 struct DevBuf {

@@ -72,4 +72,15 @@ int device_info(DeviceInfo* out);
 
 inline unsigned ceil_div(size_t a, size_t b) { return static_cast<unsigned>((a + b - 1) / b); }
 
+// K1 launch (fcs_dense.cu). kind 0: FCS bucket sum, 1: HCS mixed radix.
+// out_len != 0 overrides the per-family output length (kind 0 only): the
+// row-batched sketches (codecs.cu) bake a row offset r * J~ into one mode's
+// table entries and write rows x J~ values per family.
+size_t dense_workspace(int dtype, size_t order, const size_t* dims, size_t last_count, size_t D,
+                       const size_t* hash_lens, int kind = 0, size_t out_len = 0);
+int launch_fcs_dense(int dtype, const void* t, size_t order, const size_t* dims, size_t last_begin,
+                     size_t last_count, size_t D, const uint32_t* packed, const size_t* hash_lens,
+                     double* out, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st,
+                     size_t fam_stride = 0, int kind = 0, size_t out_len = 0);
+
 }  // namespace fcs

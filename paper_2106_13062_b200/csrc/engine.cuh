@@ -31,10 +31,6 @@ int launch_normalize_rows(double*, int, int, cudaStream_t);
 int launch_refine_update(double*, const double*, int, int*, cudaStream_t);
 int launch_family_tables(size_t, const size_t*, const size_t*, size_t, const uint64_t*,
                          uint32_t*, cudaStream_t);
-size_t dense_workspace(int, size_t, const size_t*, size_t, size_t, const size_t*, int kind = 0);
-int launch_fcs_dense(int, const void*, size_t, const size_t*, size_t, size_t, size_t,
-                     const uint32_t*, const size_t*, double*, int, void*, size_t, cudaStream_t,
-                     size_t fam_stride = 0, int kind = 0);
 // ext[d][k] (+)= scale * sum_{m = k mod J, m < jt} in[d][m]   (engine.cu)
 int launch_ts_extend(const double* in, int D, int jt, int J, double* ext, double scale,
                      int accumulate, cudaStream_t st);

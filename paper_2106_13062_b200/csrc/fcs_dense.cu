@@ -398,7 +398,7 @@ int make_plan(const DenseArgs& a, Plan* p) {
 
 // kind 0: FCS (bucket sum), kind 1: HCS (mixed-radix bucket, sketch.cpp:157-173).
 int fill_args(size_t order, const size_t* dims, size_t last_begin, size_t last_count, size_t D,
-              const size_t* hash_lens, DenseArgs* a, int kind = 0) {
+              const size_t* hash_lens, DenseArgs* a, int kind = 0, size_t out_len = 0) {
   FCS_CHECK_ARG(order >= 1 && order <= ST_MAX_ORDER, "fcs_sketch: unsupported tensor order");
   FCS_CHECK_ARG(D >= 1, "EstimatorConfig: hash_len and sketch_count must be >= 1");
   *a = DenseArgs{};
@@ -422,6 +422,10 @@ int fill_args(size_t order, const size_t* dims, size_t last_begin, size_t last_c
   FCS_CHECK_ARG(last_begin + last_count <= dims[order - 1], "fcs_sketch: slab out of range");
   a->fam_stride = static_cast<uint32_t>(sum_dims);
   a->jt = static_cast<uint32_t>(kind == 1 ? prod_j : sum_j - order + 1);
+  if (out_len) {
+    FCS_CHECK_ARG(kind == 0 && out_len < (1ull << 31), "fcs_sketch: batched output too large");
+    a->jt = static_cast<uint32_t>(out_len);
+  }
   if (order >= 2)
     a->inv_d1 = dims[1] > 1 ? static_cast<uint32_t>((1ull << 32) / dims[1]) : 0xffffffffu;
   a->last_begin = static_cast<uint32_t>(last_begin);
@@ -501,9 +505,9 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
 }  // namespace
 
 size_t dense_workspace(int dtype, size_t order, const size_t* dims, size_t last_count, size_t D,
-                       const size_t* hash_lens, int kind) {
+                       const size_t* hash_lens, int kind, size_t out_len) {
   DenseArgs a;
-  if (fill_args(order, dims, 0, last_count, D, hash_lens, &a, kind) != ST_OK) return 0;
+  if (fill_args(order, dims, 0, last_count, D, hash_lens, &a, kind, out_len) != ST_OK) return 0;
   Plan p;
   const int rc = dtype == ST_F32 ? make_plan<float, float>(a, &p) : make_plan<double, double>(a, &p);
   return rc == ST_OK ? p.ws : 0;
@@ -512,9 +516,10 @@ size_t dense_workspace(int dtype, size_t order, const size_t* dims, size_t last_
 int launch_fcs_dense(int dtype, const void* t, size_t order, const size_t* dims, size_t last_begin,
                      size_t last_count, size_t D, const uint32_t* packed, const size_t* hash_lens,
                      double* out, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st,
-                     size_t fam_stride, int kind) {
+                     size_t fam_stride, int kind, size_t out_len) {
   DenseArgs a;
-  if (int rc = fill_args(order, dims, last_begin, last_count, D, hash_lens, &a, kind)) return rc;
+  if (int rc = fill_args(order, dims, last_begin, last_count, D, hash_lens, &a, kind, out_len))
+    return rc;
   if (fam_stride) a.fam_stride = static_cast<uint32_t>(fam_stride);
   if (dtype == ST_F32)
     return run_dense<float, float>(a, static_cast<const float*>(t), packed, out, accumulate, ws,

@@ -17,10 +17,6 @@
 
 namespace fcs {
 
-size_t dense_workspace(int, size_t, const size_t*, size_t, size_t, const size_t*, int kind = 0);
-int launch_fcs_dense(int, const void*, size_t, const size_t*, size_t, size_t, size_t,
-                     const uint32_t*, const size_t*, double*, int, void*, size_t, cudaStream_t,
-                     size_t fam_stride = 0, int kind = 0);
 
 namespace {
 
@@ -114,6 +110,14 @@ size_t composed(size_t order, const size_t* hash_lens) {
 }
 
 }  // namespace
+
+// out[d][b] = sum_q in[d][b + qJ] (TS = FCS mod J), for codecs.cu.
+int st_ts_fold(const double* in, int D, uint32_t jt, uint32_t J, double* out, cudaStream_t st) {
+  fold_kernel<<<ceil_div(static_cast<size_t>(D) * J, 256), 256, 0, st>>>(in, D, jt, J, out, 0);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
 }  // namespace fcs
 
 using namespace fcs;

@@ -99,6 +99,30 @@ def main():
     g["rtpm_t"] = tr
     wr, fr = ref.rtpm(tr, 2, 3, 5, 12, 3, 21)
     g["rtpm_weights"], g["rtpm_factor"] = wr, fr
+    # TS engine (cpd.cpp:96-126, estimators.cpp:209-233) on the engine tensor
+    te = ref.Engine(t, 6, 3, 5, backend=ref.BACKEND_TS)
+    g["ts_eng_iuu"] = te.iuu(u)
+    g["ts_eng_iuv1"] = te.iuv(u, v, 1)
+    g["ts_eng_iuv2"] = te.iuv(u, v, 2)
+    g["ts_eng_uvw"] = np.array([te.uvw(u, v, ww)])
+    te.deflate(0.7, u, v, ww)
+    g["ts_eng_defl_iuu"] = te.iuu(u)
+    g["ts_eng_defl_uvw"] = np.array([te.uvw(u, v, ww)])
+    # rtpm_asym / als / residual_norm: rank-2 8x7x6 + noise, J=40, D=3
+    qa = [np.linalg.qr(ref.gaussian(30 + n, 2 * I).reshape((I, 2), order="F"))[0]
+          for n, I in enumerate((8, 7, 6))]
+    ta = np.einsum("r,ir,jr,kr->ijk", np.array([3.0, 1.5]), *qa)
+    ta = ta + 1e-3 * ref.gaussian(33, ta.size).reshape(ta.shape, order="F")
+    g["asym_t"] = ta
+    wa, fa = ref.rtpm_asym(ta, 2, 3, 4, 40, 3, 9)
+    g["asym_weights"] = wa
+    g["asym_f0"], g["asym_f1"], g["asym_f2"] = fa
+    wl, fl = ref.als(ta, 2, 5, 1e-12, 40, 3, 9)
+    g["als_weights"] = wl
+    g["als_f0"], g["als_f1"], g["als_f2"] = fl
+    g["als_residual"] = np.array([ref.residual_norm(ta, wl, fl)])
+    wt, ft = ref.als(ta, 2, 5, 1e-12, 40, 3, 9, backend=ref.BACKEND_TS)
+    g["als_ts_weights"] = wt
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **g)
     print("wrote", len(g), "arrays")
 

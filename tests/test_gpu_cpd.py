@@ -9,6 +9,8 @@ single estimates (the B200 TS path correlates at length 3J-2 instead of J:
 same sums, different FFT rounding) and 1e-7 for whole decompositions (a few
 hundred chained estimates and solves).
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -189,3 +191,35 @@ def test_residual_norm_vs_reference(cuda, dtype):
     z = np.zeros(dims)
     assert st.residual_norm(st.DenseTensor.from_array(z), st.CpTensor(w, F)) == np.inf
     assert st.residual_norm(st.DenseTensor.from_array(z), st.CpTensor(0 * w, F)) == 0.0
+
+
+# ------------------------------------------------------------ golden vectors
+GOLD = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden.npz"))
+
+
+def test_golden_ts_engine(cuda):
+    eng = st.TsEngine(st.DenseTensor.from_array(GOLD["eng_t"]), st.EstimatorConfig(6, 3, 5))
+    u, v, w = GOLD["eng_u"], GOLD["eng_v"], GOLD["eng_w"]
+    rel_close(eng.iuu(u), GOLD["ts_eng_iuu"], 1e-10)
+    rel_close(eng.iuv(u, v, 1), GOLD["ts_eng_iuv1"], 1e-10)
+    rel_close(eng.iuv(u, v, 2), GOLD["ts_eng_iuv2"], 1e-10)
+    rel_close(eng.uvw(u, v, w), GOLD["ts_eng_uvw"][0], 1e-10)
+    eng.deflate(0.7, u, v, w)
+    rel_close(eng.iuu(u), GOLD["ts_eng_defl_iuu"], 1e-10)
+    rel_close(eng.uvw(u, v, w), GOLD["ts_eng_defl_uvw"][0], 1e-10)
+
+
+def test_golden_rtpm_asym_als(cuda):
+    t = st.DenseTensor.from_array(GOLD["asym_t"])
+    est = st.EstimatorConfig(40, 3, 9)
+    cp = st.rtpm_asym(t, st.RtpmConfig(2, 3, 4, FCS, est))
+    rel_close(cp.weights, GOLD["asym_weights"], 1e-8)
+    for n in range(3):
+        rel_close(cp.factors[n], GOLD[f"asym_f{n}"], 1e-8)
+    cp = st.als(t, st.AlsConfig(2, 5, FCS, est, 1e-12))
+    rel_close(cp.weights, GOLD["als_weights"], 1e-8)
+    for n in range(3):
+        rel_close(cp.factors[n], GOLD[f"als_f{n}"], 1e-8)
+    assert abs(st.residual_norm(t, cp) - GOLD["als_residual"][0]) <= 1e-8 * GOLD["als_residual"][0]
+    cp = st.als(t, st.AlsConfig(2, 5, TS, est, 1e-12))
+    rel_close(cp.weights, GOLD["als_ts_weights"], 1e-8)

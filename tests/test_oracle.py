@@ -171,3 +171,82 @@ def test_golden_ts_hcs():
     assert rel_close(O.hcs_cp(GOLD["tscp_w"], fs, b, s, j), GOLD["hcs_cp"], 1e-12)
     with pytest.raises(ValueError):
         O.ts_sketch(x, b, s, [7, 7, 8])
+
+
+# ---------------------------------------- §8(f): TS engine and CPD drivers
+def test_golden_ts_engine():
+    t = GOLD["eng_t"]
+    eng = O.TsEngine(t, 6, 3, 5)
+    u, v, w = GOLD["eng_u"], GOLD["eng_v"], GOLD["eng_w"]
+    assert rel_close(eng.iuu(u), GOLD["ts_eng_iuu"], 1e-10)
+    assert rel_close(eng.iuv(u, v, 1), GOLD["ts_eng_iuv1"], 1e-10)
+    assert rel_close(eng.iuv(u, v, 2), GOLD["ts_eng_iuv2"], 1e-10)
+    assert rel_close(eng.uvw(u, v, w), GOLD["ts_eng_uvw"][0], 1e-10)
+    eng.deflate(0.7, u, v, w)
+    assert rel_close(eng.iuu(u), GOLD["ts_eng_defl_iuu"], 1e-10)
+    assert rel_close(eng.uvw(u, v, w), GOLD["ts_eng_defl_uvw"][0], 1e-10)
+
+
+def test_golden_rtpm_asym():
+    t = GOLD["asym_t"]
+    w, f = O.rtpm_asym(O.FcsEngine(t, 40, 3, 9), t.shape, 2, 3, 4, 9)
+    assert rel_close(w, GOLD["asym_weights"], 1e-8)
+    for n in range(3):
+        assert rel_close(f[n], GOLD[f"asym_f{n}"], 1e-8)
+    assert (w >= 0).all()
+
+
+def test_golden_als_and_residual():
+    t = GOLD["asym_t"]
+    w, f, sweeps = O.als(O.FcsEngine(t, 40, 3, 9), t, 2, 5, 1e-12, 9)
+    assert sweeps == 5
+    assert rel_close(w, GOLD["als_weights"], 1e-8)
+    for n in range(3):
+        assert rel_close(f[n], GOLD[f"als_f{n}"], 1e-8)
+    assert rel_close(O.residual_norm(t, GOLD["als_weights"],
+                                     [GOLD[f"als_f{n}"] for n in range(3)]),
+                     GOLD["als_residual"][0], 1e-12)
+    wt, _, _ = O.als(O.TsEngine(t, 40, 3, 9), t, 2, 5, 1e-12, 9)
+    assert rel_close(wt, GOLD["als_ts_weights"], 1e-8)
+
+
+def test_min_norm_solve_matches_pinv():
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((7, 3))
+    G = A @ A.T  # rank 3
+    B = rng.standard_normal((7, 4))
+    np.testing.assert_allclose(O.min_norm_solve(G, B), np.linalg.pinv(G, rcond=1e-12) @ B,
+                               atol=1e-10)
+    assert (O.min_norm_solve(np.zeros((3, 3)), np.ones((3, 2))) == 0).all()
+
+
+def test_inner_products_vs_reference():
+    rng = np.random.default_rng(1)
+    a, b = rng.standard_normal((5, 4, 3)), rng.standard_normal((5, 4, 3))
+    assert rel_close(O.estimate_inner(a, b, 7, 5, 3), ref.estimate_inner(a, b, 7, 5, 3), 1e-12)
+    for f in O.families_for(a.shape, 7, 3, 3):
+        assert rel_close(O.inner_once(a, b, *f), ref.inner_once_tables(a, b, *f), 1e-12)
+        assert rel_close(O.inner_once_ts(a, b, *f), ref.inner_once_tables(a, b, *f, ts=True),
+                         1e-12)
+    with pytest.raises(ValueError):
+        ref.estimate_inner(a, b, 0, 5, 3)
+
+
+def test_regression_and_codec_oracle_identities():
+    rng = np.random.default_rng(2)
+    dims = (2, 3, 2)
+    X, w, bias = rng.standard_normal((4, 12)), rng.standard_normal((1, 12)), rng.standard_normal(3)
+    y0 = O.regression_forward(X, np.zeros((3, 12)), bias, dims, 5, 5, 4)
+    assert (y0 == np.broadcast_to(bias, (4, 3))).all()
+    y1 = O.regression_forward(X[:1], w, bias[:1], dims, 5, 5, 4)
+    est = O.estimate_inner(X[0].reshape(dims, order="F"), w[0].reshape(dims, order="F"), 5, 5, 4)
+    assert rel_close(y1[0, 0], est + bias[0], 1e-12)
+    # Kronecker: the order-4 tensor's entries are the Kronecker matrix's
+    a, b = rng.standard_normal((3, 4)), rng.standard_normal((4, 5))
+    K4, K = O.kron_tensor(a, b), np.kron(a, b)
+    assert K4[2, 3, 1, 4] == K[4 * 2 + 1, 5 * 3 + 4]
+    sk = O.compress_tensor4(O.kron_tensor([[2.0]], [[3.0]]), 1, 1, 0)
+    assert abs(sk[0, 0]) == 6.0
+    # contraction with L = 1 is the Kronecker tensor of the two slices
+    A, B = rng.standard_normal((3, 4, 1)), rng.standard_normal((1, 4, 5))
+    assert np.allclose(O.contraction_tensor(A, B), O.kron_tensor(A[:, :, 0], B[0]))
