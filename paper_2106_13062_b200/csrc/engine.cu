@@ -54,6 +54,7 @@ size_t st_fcs_cp_workspace(size_t order, const size_t* dims, size_t rank, size_t
   for (size_t n = 0; n < order; ++n) sum_j += hash_lens[n];
   FftPlan pl;
   if (get_fft_plan(sum_j - order + 1, &pl) != ST_OK) return 0;
+  if (pl.large_p1) return 1;  // the two-level path allocates its own scratch
   return (std::max<size_t>(1, rank) + 1) * sketch_count * pl.P * sizeof(double2);
 }
 
@@ -71,6 +72,7 @@ int st_fcs_cp(const double* weights, size_t rank, size_t order, const size_t* di
     FCS_CHECK_ARG(dims[n] > 0 && hash_lens[n] > 0, "HashPair: dimensions must be positive");
     a.dims[n] = static_cast<int>(dims[n]);
     a.tab_off[n] = static_cast<int>(off);
+    a.hash_lens[n] = static_cast<int>(hash_lens[n]);
     a.factors[n] = factors[n];
     off += dims[n];
     sum_j += hash_lens[n];
@@ -82,7 +84,8 @@ int st_fcs_cp(const double* weights, size_t rank, size_t order, const size_t* di
   const size_t jt = sum_j - order + 1;
   FftPlan pl;
   if (int rc = get_fft_plan(jt, &pl)) return rc;
-  const size_t need = (std::max<size_t>(1, r_count) + 1) * sketch_count * pl.P * sizeof(double2);
+  const size_t need =
+      pl.large_p1 ? 1 : (std::max<size_t>(1, r_count) + 1) * sketch_count * pl.P * sizeof(double2);
   FCS_CHECK_ARG(workspace && workspace_bytes >= need, "st_fcs_cp: workspace too small");
   return launch_cp(pl, a, static_cast<int>(sketch_count), packed,
                    static_cast<double2*>(workspace), out, static_cast<int>(jt), accumulate,
@@ -307,6 +310,7 @@ int st_engine_deflate(st_engine* e, double weight, const double* u, const double
     for (int n = 0; n < 3; ++n) {
       a.dims[n] = ea.dims[n];
       a.tab_off[n] = ea.tab_off[n];
+      a.hash_lens[n] = ea.hash_len;
     }
     a.fam_stride = ea.fam_stride;
     a.factors[0] = u;

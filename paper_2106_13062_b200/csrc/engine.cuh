@@ -132,6 +132,7 @@ struct st_engine {
     }
     e.fam_stride = static_cast<int>(off);
     e.D = static_cast<int>(D);
+    e.hash_len = static_cast<int>(hash_len);
     e.packed = packed;
     e.spec = spec;
     return e;

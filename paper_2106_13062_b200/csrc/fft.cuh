@@ -37,6 +37,15 @@ struct FftPlan {
   int hi_count;                // entries of the hi table (= M >> kTwLoBits, rounded up)
   const double2* tw;           // device: lo[64] then hi[hi_count]
   const int* f2p;              // device: slot position of frequency k, k in [0, P)
+  int large_p1;                // 0: one-CTA plan; else P = large_p1 * P2 two-level plan
+};                             // (spectral_large.cu; npass, tw, f2p unused)
+
+// Two-level plan for M > kMaxFftM: P = P1 * P2 with shared-memory sub-plans
+// a (P1-point column transforms) and b (P2-point row transforms).
+struct LargeFft {
+  int M, P, P1, P2;
+  FftPlan a, b;
+  const int* p2f_a;  // device: slot -> frequency of plan a
 };
 
 // XOR swizzle of 16-byte slots: the low 3 bits (slot within a 128-byte
@@ -386,14 +395,17 @@ inline size_t fft_smem_bytes(const FftPlan& pl) {
   return static_cast<size_t>(pl.P + table_slots(pl)) * sizeof(double2);
 }
 
-// Host: plan for the smallest supported M >= min_len (cached per device).
+// Host: plan for the smallest supported M >= min_len (cached per device):
+// one-CTA shared-memory plans up to kMaxFftM, two-level plans beyond.
 int get_fft_plan(size_t min_len, FftPlan* out);
+int get_large_fft(const FftPlan& pl, LargeFft* out);
 
 // Kernel argument blocks shared by spectral.cu (kernels) and engine.cu (host).
 struct CpArgs {
   int order;
   int dims[ST_MAX_ORDER];
   int tab_off[ST_MAX_ORDER];
+  int hash_lens[ST_MAX_ORDER];
   int fam_stride;
   const double* factors[ST_MAX_ORDER];  // I_n x R column-major
   const double* weights;
@@ -406,8 +418,27 @@ struct EngArgs {
   int tab_off[3];
   int fam_stride;
   int D;
+  int hash_len;            // J of every mode
   const uint32_t* packed;  // D families x 3 modes, packed tables
   const double2* spec;     // D x P cached spectra S_d (slot order)
 };
+
+// Two-level counterparts of the spectral launchers (spectral_large.cu).
+int large_rfft(const FftPlan& pl, const double* x, size_t ldx, int64_t len, int items,
+               double2* spec, cudaStream_t st);
+int large_irfft(const FftPlan& pl, double2* spec, int items, double* out, size_t ldo,
+                int64_t out_len, int accumulate, cudaStream_t st);
+int large_real_from_spec(const FftPlan& pl, const double2* spec, int items, double* out,
+                         size_t ldo, int out_len, int accumulate, cudaStream_t st);
+int large_conv(const FftPlan& pl, const double* a, int la, size_t lda, const double* b, int lb,
+               size_t ldb, int items, double* out, size_t ldo, cudaStream_t st);
+int large_iuv(const FftPlan& pl, const EngArgs& e, int batch, const double* A, const double* B,
+              int c1, int c2, int f, int J, double* est, cudaStream_t st);
+int large_uvw(const FftPlan& pl, const EngArgs& e, int batch, const double* U, const double* V,
+              const double* W, int J, double* est, cudaStream_t st);
+int large_deflate(const FftPlan& pl, const EngArgs& e, double weight, const double* U,
+                  const double* V, const double* W, int J, double2* spec, cudaStream_t st);
+int large_cp(const FftPlan& pl, const CpArgs& a, int D, const uint32_t* packed, const int* J,
+             double* out, int jt, int accumulate, cudaStream_t st);
 
 }  // namespace fcs

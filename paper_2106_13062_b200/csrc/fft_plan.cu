@@ -35,11 +35,36 @@ int freq_of(int p, const std::vector<int>& radix, size_t level, int L) {
 
 }  // namespace
 
+// Two-level plan: the smallest P = P1 * P2 >= ceil(min_len / 2) over the
+// one-CTA sizes, ties broken toward balanced factors (P1 <= P2).
+int large_plan(size_t min_len, FftPlan* out) {
+  std::vector<long> sizes;
+  for (int b3 = 1; b3 <= 9; b3 *= 3)
+    for (long m = 16L * b3; m <= kMaxFftM; m *= 2) sizes.push_back(m / 2);
+  const long need = static_cast<long>((min_len + 1) / 2);
+  long best = 0, b1 = 0;
+  for (long p1 : sizes)
+    for (long p2 : sizes) {
+      if (p1 > p2 || p1 * p2 < need) continue;
+      const long p = p1 * p2;
+      if (best == 0 || p < best || (p == best && p2 - p1 < best / b1 - b1)) {
+        best = p;
+        b1 = p1;
+      }
+    }
+  if (best == 0 || best > (1L << 30))
+    return fail(ST_EINVAL, "fft: composed length " + std::to_string(min_len) + " is too large");
+  FftPlan pl{};
+  pl.M = static_cast<int>(2 * best);
+  pl.P = static_cast<int>(best);
+  pl.large_p1 = static_cast<int>(b1);
+  *out = pl;
+  return ST_OK;
+}
+
 int get_fft_plan(size_t min_len, FftPlan* out) {
   const int M = choose_m(min_len);
-  if (M == 0)
-    return fail(ST_EINVAL, "fft: composed length " + std::to_string(min_len) +
-                               " exceeds the shared-memory FFT limit " + std::to_string(kMaxFftM));
+  if (M == 0) return large_plan(min_len, out);
   int dev = 0;
   FCS_CUDA_TRY(cudaGetDevice(&dev));
   static std::mutex mu;

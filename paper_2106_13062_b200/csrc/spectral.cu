@@ -424,6 +424,7 @@ int prep(K kernel, const FftPlan& pl, size_t* smem, int nbuf = 1) {
 
 int launch_spec_from_real(const FftPlan& pl, const double* x, size_t ldx, int len, int items,
                           double2* spec, cudaStream_t st) {
+  if (pl.large_p1) return large_rfft(pl, x, ldx, len, items, spec, st);
   size_t sm;
   if (int rc = prep(spec_from_real_kernel, pl, &sm)) return rc;
   spec_from_real_kernel<<<items, kFftThreads, sm, st>>>(pl, x, ldx, len, spec);
@@ -433,6 +434,7 @@ int launch_spec_from_real(const FftPlan& pl, const double* x, size_t ldx, int le
 
 int launch_real_from_spec(const FftPlan& pl, const double2* spec, int items, double* out,
                           size_t ldo, int out_len, int accumulate, cudaStream_t st) {
+  if (pl.large_p1) return large_real_from_spec(pl, spec, items, out, ldo, out_len, accumulate, st);
   size_t sm;
   if (int rc = prep(real_from_spec_kernel, pl, &sm)) return rc;
   real_from_spec_kernel<<<items, kFftThreads, sm, st>>>(pl, spec, out, ldo, out_len, accumulate);
@@ -442,6 +444,7 @@ int launch_real_from_spec(const FftPlan& pl, const double2* spec, int items, dou
 
 int launch_cp(const FftPlan& pl, const CpArgs& a, int D, const uint32_t* packed, double2* Q,
               double* out, int jt, int accumulate, cudaStream_t st) {
+  if (pl.large_p1) return large_cp(pl, a, D, packed, a.hash_lens, out, jt, accumulate, st);
   size_t sm;
   if (int rc = prep(cp_rank_kernel, pl, &sm, 2)) return rc;
   if (a.r_count > 0) {
@@ -462,6 +465,7 @@ int launch_cp(const FftPlan& pl, const CpArgs& a, int D, const uint32_t* packed,
 
 int launch_conv(const FftPlan& pl, const double* a, int la, size_t lda, const double* b, int lb,
                 size_t ldb, int items, double2* scratch, double* out, size_t ldo, cudaStream_t st) {
+  if (pl.large_p1) return large_conv(pl, a, la, lda, b, lb, ldb, items, out, ldo, st);
   size_t sm;
   if (int rc = prep(conv_kernel, pl, &sm)) return rc;
   conv_kernel<<<items, kFftThreads, sm, st>>>(pl, a, la, lda, b, lb, ldb, scratch, out, ldo);
@@ -471,6 +475,7 @@ int launch_conv(const FftPlan& pl, const double* a, int la, size_t lda, const do
 
 int launch_iuv(const FftPlan& pl, const EngArgs& e, int batch, const double* A, const double* B,
                int c1, int c2, int f, double2* scratch, double* est, cudaStream_t st) {
+  if (pl.large_p1) return large_iuv(pl, e, batch, A, B, c1, c2, f, e.hash_len, est, st);
   size_t sm;
   if (int rc = prep(iuv_kernel, pl, &sm, 2)) return rc;
   iuv_kernel<<<dim3(batch, e.D), kFftThreads, sm, st>>>(pl, e, A, B, c1, c2, f, scratch, est);
@@ -480,6 +485,7 @@ int launch_iuv(const FftPlan& pl, const EngArgs& e, int batch, const double* A, 
 
 int launch_uvw(const FftPlan& pl, const EngArgs& e, int batch, const double* U, const double* V,
                const double* W, double2* scratch, double* est, cudaStream_t st) {
+  if (pl.large_p1) return large_uvw(pl, e, batch, U, V, W, e.hash_len, est, st);
   size_t sm;
   if (int rc = prep(uvw_kernel, pl, &sm, 2)) return rc;
   uvw_kernel<<<dim3(batch, e.D), kFftThreads, sm, st>>>(pl, e, U, V, W, scratch, est);
@@ -490,6 +496,7 @@ int launch_uvw(const FftPlan& pl, const EngArgs& e, int batch, const double* U, 
 int launch_deflate(const FftPlan& pl, const EngArgs& e, double weight, const double* U,
                    const double* V, const double* W, double2* scratch, double2* spec,
                    cudaStream_t st) {
+  if (pl.large_p1) return large_deflate(pl, e, weight, U, V, W, e.hash_len, spec, st);
   size_t sm;
   if (int rc = prep(deflate_kernel, pl, &sm, 2)) return rc;
   deflate_kernel<<<e.D, kFftThreads, sm, st>>>(pl, e, weight, U, V, W, scratch, spec);
