@@ -25,15 +25,17 @@ void cuda_check(cudaError_t e, const char* what) {
 }  // namespace
 
 GpuFcsEngine::GpuFcsEngine(const sketchtensor::DenseTensor& t,
-                           const sketchtensor::EstimatorConfig& cfg)
+                           const sketchtensor::EstimatorConfig& cfg,
+                           sketchtensor::SketchBackend backend)
     : shape_(t.shape()) {
   if (t.order() != 3) throw std::invalid_argument("make_contraction_engine: order-3 tensor required");
   void* dt = nullptr;
   cuda_check(cudaMalloc(&dt, t.size() * sizeof(double)), "cudaMalloc");
   cuda_check(cudaMemcpy(dt, t.data().data(), t.size() * sizeof(double), cudaMemcpyHostToDevice),
              "cudaMemcpy");
-  const int rc = st_engine_create(&eng_, ST_F64, dt, shape_.data(), cfg.hash_len,
-                                  cfg.sketch_count, cfg.seed, nullptr);
+  const int rc = st_engine_create_backend(&eng_, static_cast<int>(backend), ST_F64, dt,
+                                          shape_.data(), cfg.hash_len, cfg.sketch_count, cfg.seed,
+                                          nullptr);
   cudaFree(dt);
   check(rc);
   dev_len_ = *std::max_element(shape_.begin(), shape_.end());
@@ -93,7 +95,8 @@ void GpuFcsEngine::deflate(double weight, const Eigen::VectorXd& u, const Eigen:
 std::unique_ptr<sketchtensor::ContractionEngine> make_contraction_engine(
     const sketchtensor::DenseTensor& t, sketchtensor::SketchBackend backend,
     const sketchtensor::EstimatorConfig& cfg) {
-  if (backend == sketchtensor::SketchBackend::FCS) return std::make_unique<GpuFcsEngine>(t, cfg);
+  if (backend == sketchtensor::SketchBackend::FCS || backend == sketchtensor::SketchBackend::TS)
+    return std::make_unique<GpuFcsEngine>(t, cfg, backend);
   return sketchtensor::make_contraction_engine(t, backend, cfg);
 }
 

@@ -17,9 +17,11 @@ namespace sketchtensor_b200 {
 
 class GpuFcsEngine final : public sketchtensor::ContractionEngine {
  public:
-  // FcsEngine ctor semantics (cpd.cpp:63-67): D = cfg.sketch_count families
-  // from families_for(t.shape(), cfg); the tensor is consumed once.
-  GpuFcsEngine(const sketchtensor::DenseTensor& t, const sketchtensor::EstimatorConfig& cfg);
+  // FcsEngine / TsEngine ctor semantics (cpd.cpp:63-67, 98-102): D =
+  // cfg.sketch_count families from families_for(t.shape(), cfg); the tensor
+  // is consumed once. backend: SketchBackend::FCS or SketchBackend::TS.
+  GpuFcsEngine(const sketchtensor::DenseTensor& t, const sketchtensor::EstimatorConfig& cfg,
+               sketchtensor::SketchBackend backend = sketchtensor::SketchBackend::FCS);
   ~GpuFcsEngine() override;
   GpuFcsEngine(const GpuFcsEngine&) = delete;
   GpuFcsEngine& operator=(const GpuFcsEngine&) = delete;
@@ -39,8 +41,8 @@ class GpuFcsEngine final : public sketchtensor::ContractionEngine {
   std::size_t dev_len_ = 0;
 };
 
-// make_contraction_engine (cpd.cpp:220-232) with FCS routed to the GPU; other
-// backends are delegated to the reference factory.
+// make_contraction_engine (cpd.cpp:220-232) with FCS and TS routed to the GPU;
+// other backends are delegated to the reference factory.
 std::unique_ptr<sketchtensor::ContractionEngine> make_contraction_engine(
     const sketchtensor::DenseTensor& t, sketchtensor::SketchBackend backend,
     const sketchtensor::EstimatorConfig& cfg);

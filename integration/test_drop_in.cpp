@@ -88,6 +88,17 @@ int main() {
   a[0] = gpu->uvw(u, v, w);
   b[0] = ref->uvw(u, v, w);
   worst = std::max(worst, rel_err(a, b));
+  // the TS backend through the same factory (TsEngine, cpd.cpp:96-126)
+  auto ref_ts = sketchtensor::make_contraction_engine(t, SketchBackend::TS, cfg);
+  auto gpu_ts = sketchtensor_b200::make_contraction_engine(t, SketchBackend::TS, cfg);
+  worst = std::max(worst, rel_err(gpu_ts->iuv(v, w, 0), ref_ts->iuv(v, w, 0)));
+  worst = std::max(worst, rel_err(gpu_ts->iuv(u, w, 1), ref_ts->iuv(u, w, 1)));
+  a[0] = gpu_ts->uvw(u, v, w);
+  b[0] = ref_ts->uvw(u, v, w);
+  worst = std::max(worst, rel_err(a, b));
+  ref_ts->deflate(0.5, u, v, w);
+  gpu_ts->deflate(0.5, u, v, w);
+  worst = std::max(worst, rel_err(gpu_ts->iuv(u, v, 2), ref_ts->iuv(u, v, 2)));
   bool threw = false;
   try {
     gpu->iuv(u, v, 3);
