@@ -149,7 +149,7 @@ __device__ __forceinline__ void fiber_offset_fast(const DenseArgs& a, const uint
 // warp per fiber, lane-owned mode-0 indices with their table entries in
 // registers, NV 128-bit loads per lane with the next fiber prefetched,
 // int32 fixed-point shared-memory accumulation with exact overflow detection.
-template <int NV, int SPLIT, int THREADS>
+template <int NV, int SPLIT, int THREADS, bool kFull>
 __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
                                                               const float* __restrict__ t,
                                                               const uint32_t* __restrict__ packed,
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
   uint64_t f = f_begin + warp;
   if (f < f_end) load(f, cur);
   const uint32_t sk_base = static_cast<uint32_t>(__cvta_generic_to_shared(sk));
-  uint32_t ovf_acc = 0;  // bit 31: a partial overflowed
+  uint32_t ovf_acc = 0;  // bit 31: some partial reached |old| >= 2^30 (wrap guard)
   uint32_t rng_acc = 0;  // bits >= 23: a converted element was out of range / non-finite
   // One fiber: the fiber sign goes into the scale; the byte address of bucket
   // h0 + c is base + 4c + (entry << 2), the shift discarding the entry's sign bit.
@@ -201,26 +201,37 @@ __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
     uint32_t c, sbit;
     fiber_offset_fast(a, tab, fib, c, sbit);
     const float scale_f = sbit ? -scale : scale;
-    const uint32_t base_c = sk_base + 4u * c;
+    uint32_t base_c = sk_base + 4u * c;
+    // opaque to the optimiser: keeps the per-element address a single
+    // LEA(entry, base_c) instead of (c + entry) * 4 + a rematerialised window base
+    asm volatile("" : "+r"(base_c));
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      if (vbase + lane + 32 * j < nvec) {
+      if (kFull || vbase + lane + 32 * j < nvec) {  // kFull: every lane owns whole vectors
         const float* x = reinterpret_cast<const float*>(&vals[j]);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const uint32_t e = e0[j][k];
-          const float xs = __uint_as_float(__float_as_uint(x[k]) ^ (e & 0x80000000u));
-          // round-to-nearest int via the 1.5 * 2^23 magic number: exact while the
-          // scaled value is below 2^22 in magnitude, i.e. while t < 2^23 below
-          const uint32_t t = __float_as_uint(fmaf(xs, scale_f, 12582912.0f)) - 0x4B000000u;
-          rng_acc |= t;
-          const int32_t q = static_cast<int32_t>(t) - 0x400000;
+          // x ^ (e & sign): one LOP3 per use (volatile: a hoisted e & sign
+          // would double the 4*NV live table registers and spill)
+          uint32_t xsb;
+          asm volatile("lop3.b32 %0, %1, %2, 0x80000000, 0x78;"
+                       : "=r"(xsb)
+                       : "r"(__float_as_uint(x[k])), "r"(e));
+          const float xs = __uint_as_float(xsb);
+          // round-to-nearest int via the 1.5 * 2^23 magic number: for |y| < 2^22
+          // the sum's bits are 0x4B400000 + round(y), exponent 0x96; any other
+          // exponent (out of range, Inf, NaN) leaves bits >= 23 in bits ^ 0x4B000000
+          const uint32_t bits = __float_as_uint(fmaf(xs, scale_f, 12582912.0f));
+          rng_acc |= bits ^ 0x4B000000u;
+          const int32_t q = static_cast<int32_t>(bits - 0x4B400000u);
           int32_t old;
           asm volatile("atom.shared.add.s32 %0, [%1], %2;"
                        : "=r"(old)
                        : "r"(base_c + (e << 2)), "r"(q));
-          const int32_t now = old + q;
-          ovf_acc |= static_cast<uint32_t>((old ^ now) & (q ^ now));
+          // guard band: |q| < 2^22, so a partial can only wrap after passing
+          // through |old| >= 2^30, which sets bit 31 of old + 2^30
+          ovf_acc |= static_cast<uint32_t>(old) + 0x40000000u;
         }
       }
     }
@@ -337,16 +348,22 @@ int fx_nv(const DenseArgs& a) {
   if (a.dims[0] % 4 != 0) return 0;
   const uint32_t per_lane = (a.dims[0] / 4 + 31) / 32;
   if (per_lane == 0 || per_lane > 8) return 0;
-  return per_lane <= 1 ? 1 : per_lane <= 2 ? 2 : per_lane <= 4 ? 3 : 4;
+  const int v = per_lane <= 1 ? 1 : per_lane <= 2 ? 2 : per_lane <= 4 ? 3 : 4;
+  // 5..8: the same kernels without the per-vector guard when I_0 = 128 NV
+  return a.dims[0] == (128u << (v - 1)) ? v + 4 : v;
 }
 
 using FxKernel = void (*)(DenseArgs, const float*, const uint32_t*, const FxStats*, int32_t*, int*);
 FxKernel fx_kernel(int v) {
   switch (v) {
-    case 1: return fcs_dense_fx_kernel<1, 1, 512>;
-    case 2: return fcs_dense_fx_kernel<2, 1, 512>;
-    case 3: return fcs_dense_fx_kernel<4, 1, 512>;
-    default: return fcs_dense_fx_kernel<8, 1, 512>;
+    case 1: return fcs_dense_fx_kernel<1, 1, 512, false>;
+    case 2: return fcs_dense_fx_kernel<2, 1, 512, false>;
+    case 3: return fcs_dense_fx_kernel<4, 1, 512, false>;
+    case 4: return fcs_dense_fx_kernel<8, 1, 512, false>;
+    case 5: return fcs_dense_fx_kernel<1, 1, 512, true>;
+    case 6: return fcs_dense_fx_kernel<2, 1, 512, true>;
+    case 7: return fcs_dense_fx_kernel<4, 1, 512, true>;
+    default: return fcs_dense_fx_kernel<8, 1, 512, true>;
   }
 }
 inline int fx_threads(int) { return 512; }
