@@ -284,6 +284,44 @@ __global__ void __launch_bounds__(kFftThreads) iuv_kernel(FftPlan pl, EngArgs e,
   }
 }
 
+// K6, one-buffer form: F cs_a goes through a global scratch slot instead of a
+// second shared buffer, halving shared memory so two CTAs fit per SM. Used when
+// the batch is slightly above one wave of the two-buffer kernel (config 3:
+// 15 x 10 = 150 items on 148 SMs), where it removes the nearly empty second wave.
+__global__ void __launch_bounds__(kFftThreads) iuv1_kernel(FftPlan pl, EngArgs e, const double* A,
+                                                           const double* B, int c1, int c2, int f,
+                                                           double2* scratch, double* est) {
+  const Smem sm = carve(pl, 1);
+  load_twiddles(sm.tw, pl);
+  __syncthreads();
+  const int b = blockIdx.x, d = blockIdx.y;
+  const size_t item = static_cast<size_t>(b) * e.D + d;
+  const uint32_t* tab = e.packed + static_cast<size_t>(d) * e.fam_stride;
+  const double2* S = e.spec + static_cast<size_t>(d) * pl.P;
+  double2* scr = scratch + item * pl.P;
+  rfft_of_cs(sm, sm.buf, pl, A + static_cast<size_t>(b) * e.dims[c1], e.dims[c1],
+             tab + e.tab_off[c1]);
+  for (int s = tid(); s < pl.P; s += blockDim.x) scr[s] = sm.buf[swz(s)];
+  __syncthreads();
+  rfft_of_cs(sm, sm.buf, pl, B + static_cast<size_t>(b) * e.dims[c2], e.dims[c2],
+             tab + e.tab_off[c2]);
+  for (int s = tid(); s < pl.P; s += blockDim.x) {
+    const bool z = s == 0;
+    const double2 ab = hmul(scr[s], sm.buf[swz(s)], z);
+    sm.buf[swz(s)] = hmul(__ldg(S + s), hconj(ab, z), z);
+  }
+  irfft_in_place(sm, pl);
+  const double inv = 1.0 / pl.P;
+  const int nf = e.dims[f];
+  const uint32_t* tf = tab + e.tab_off[f];
+  double* o = est + item * nf;
+  for (int i = tid(); i < nf; i += blockDim.x) {
+    const uint32_t t = __ldg(tf + i);
+    const double z = packed_real(sm.buf, t & 0x7fffffffu) * inv;
+    o[i] = (t >> 31) ? -z : z;
+  }
+}
+
 // K7: (1/M) sum_k Re(S_d conj(F cs_u F cs_v F cs_w)) (uvw_spectral + spectral_dot,
 // estimators.cpp:38-64). Grid (batch, D); est[b][d].
 __global__ void __launch_bounds__(kFftThreads) uvw_kernel(FftPlan pl, EngArgs e, const double* U,
@@ -476,9 +514,23 @@ int launch_conv(const FftPlan& pl, const double* a, int la, size_t lda, const do
 int launch_iuv(const FftPlan& pl, const EngArgs& e, int batch, const double* A, const double* B,
                int c1, int c2, int f, double2* scratch, double* est, cudaStream_t st) {
   if (pl.large_p1) return large_iuv(pl, e, batch, A, B, c1, c2, f, e.hash_len, est, st);
-  size_t sm;
-  if (int rc = prep(iuv_kernel, pl, &sm, 2)) return rc;
-  iuv_kernel<<<dim3(batch, e.D), kFftThreads, sm, st>>>(pl, e, A, B, c1, c2, f, scratch, est);
+  size_t sm2, sm1;
+  if (int rc = prep(iuv_kernel, pl, &sm2, 2)) return rc;
+  if (int rc = prep(iuv1_kernel, pl, &sm1, 1)) return rc;
+  // waves of each form; the one-buffer kernel (scratch: batch x D x P slots)
+  // wins when it fits the batch in fewer waves
+  int occ2 = 0, occ1 = 0;
+  FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, iuv_kernel, kFftThreads, sm2));
+  FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, iuv1_kernel, kFftThreads, sm1));
+  DeviceInfo di;
+  if (int rc = device_info(&di)) return rc;
+  const long items = static_cast<long>(batch) * e.D;
+  const long w2 = (items + std::max(occ2, 1) * di.sm_count - 1) / (std::max(occ2, 1) * di.sm_count);
+  const long w1 = (items + std::max(occ1, 1) * di.sm_count - 1) / (std::max(occ1, 1) * di.sm_count);
+  if (scratch != nullptr && w1 < w2)
+    iuv1_kernel<<<dim3(batch, e.D), kFftThreads, sm1, st>>>(pl, e, A, B, c1, c2, f, scratch, est);
+  else
+    iuv_kernel<<<dim3(batch, e.D), kFftThreads, sm2, st>>>(pl, e, A, B, c1, c2, f, scratch, est);
   FCS_CUDA_TRY(cudaGetLastError());
   return ST_OK;
 }
