@@ -19,6 +19,7 @@
 // detected exactly, and a CTA that overflowed redoes its chunk with float
 // atomics. Rounding error per element <= 2^-(S+1) (K1).
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "dense_common.cuh"
@@ -130,6 +131,61 @@ __global__ void fx_scale_kernel(FxStats* st, double n_center) {
   st->S = max(-60, min(30, S));
 }
 
+// Bank-aware load order for the fx kernel (one warp per family). A warp's
+// fiber is 4*NV 128-byte lines; load step j brings 4 whole lines (coalesced)
+// and issues 4 ATOMS instructions, instruction k taking element k of every
+// lane's float4. The ATOMS bank of element i is (h0(i) + c) mod 32 with c
+// common to the whole fiber, so the bank conflicts of an instruction depend
+// on h0 alone: grouping lines whose per-k bank histograms complement each
+// other cuts the shared-memory wavefronts (random h0: ~113 -> ~94 per
+// 1024-element fiber). Greedy: per step, seed with the worst remaining line,
+// then add the line that minimises sum_k max_bank of the group.
+// groups[d][j][q] = line of slot q (lanes 8q..8q+7) at step j.
+__global__ void fx_group_kernel(const uint32_t* __restrict__ packed, uint32_t fam_stride,
+                                uint32_t i0_shift, int nsteps, uint8_t* __restrict__ groups) {
+  __shared__ uint8_t lh[32][4][32];  // [line][k][bank] element counts
+  const int d = blockIdx.x, lane = threadIdx.x;
+  const uint32_t* tab = packed + static_cast<uint64_t>(d) * fam_stride + i0_shift;
+  const int nlines = 4 * nsteps;
+  for (int l = 0; l < nlines; ++l) {
+    const uint32_t bank = __ldg(tab + 32 * l + lane) & 31u;  // element t = lane, k = t & 3
+    for (int k = 0; k < 4; ++k) {
+      // count of elements t = k (mod 4) of line l that land in bank `lane`
+      int cnt = 0;
+      for (int t = k; t < 32; t += 4) cnt += (__shfl_sync(0xffffffffu, bank, t) == static_cast<uint32_t>(lane));
+      lh[l][k][lane] = static_cast<uint8_t>(cnt);
+    }
+  }
+  __syncwarp();
+  auto wmax = [](int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+  };
+  uint32_t used = 0;
+  for (int j = 0; j < nsteps; ++j) {
+    int h[4] = {0, 0, 0, 0};
+    for (int pick = 0; pick < 4; ++pick) {
+      int best = -1, best_cost = 1 << 30;
+      for (int l = 0; l < nlines; ++l) {
+        if (used >> l & 1u) continue;
+        int cost = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) cost += wmax(h[k] + lh[l][k][lane]);
+        // the first pick seeds the group with the worst line (largest self cost)
+        if (pick == 0 ? (best < 0 || cost > -best_cost) : cost < best_cost) {
+          best = l;
+          best_cost = pick == 0 ? -cost : cost;
+        }
+      }
+      used |= 1u << best;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) h[k] += lh[best][k][lane];
+      if (lane == 0) groups[(static_cast<size_t>(d) * nsteps + j) * 4 + pick] = static_cast<uint8_t>(best);
+    }
+  }
+}
+
 __device__ __forceinline__ void fiber_offset_fast(const DenseArgs& a, const uint32_t* tab,
                                                   uint64_t f, uint32_t& c, uint32_t& sbit) {
   if (a.order == 3 && a.fibers < 0xffffffffull) {
@@ -155,7 +211,8 @@ __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
                                                               const uint32_t* __restrict__ packed,
                                                               const FxStats* __restrict__ st,
                                                               int32_t* __restrict__ part,
-                                                              int* __restrict__ flags) {
+                                                              int* __restrict__ flags,
+                                                              const uint8_t* __restrict__ groups) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int32_t* sk = reinterpret_cast<int32_t*>(smem_raw);
   const int d = blockIdx.x % a.D;
@@ -171,10 +228,26 @@ __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
   const uint32_t vbase = static_cast<uint32_t>(wid % SPLIT) * 32u * NV;
   const uint32_t i0n = a.dims[0];
   const uint32_t nvec = i0n / 4;
+  // Vector this lane loads at step j: lane + 32 j, or with the bank-aware
+  // grouping (kFull only) 8 * line + (lane & 7), line = groups[d][j][lane / 8];
+  // the indices are kept packed four per register (vmap).
+  constexpr bool kMapped = kFull && SPLIT == 1;  // vector map in vmap (identity if no groups)
+  const bool grouped = kMapped && groups != nullptr;
+  uint32_t vmap[(NV + 3) / 4];
+#pragma unroll
+  for (int w = 0; w < (NV + 3) / 4; ++w) vmap[w] = 0;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const uint32_t v = grouped ? 8u * groups[(static_cast<size_t>(d) * NV + j) * 4 + (lane >> 3)] +
+                                     (lane & 7u)
+                               : static_cast<uint32_t>(lane + 32 * j);
+    vmap[j / 4] |= (v & 0xffu) << (8 * (j % 4));
+  }
   uint32_t e0[NV][4];  // packed mode-0 entries (bucket | sign << 31)
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
-    const uint32_t v = vbase + lane + 32 * j;
+    const uint32_t v = kMapped ? ((vmap[j / 4] >> (8 * (j % 4))) & 0xffu)
+                               : vbase + lane + 32 * j;
 #pragma unroll
     for (int k = 0; k < 4; ++k) e0[j][k] = v < nvec ? __ldg(tab + a.i0_shift + v * 4 + k) : 0u;
   }
@@ -186,9 +259,14 @@ __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
   float4 cur[NV], nxt[NV];
   auto load = [&](uint64_t fib, float4* dst) {
     const float4* src = reinterpret_cast<const float4*>(t + fib * i0n);
+    if constexpr (kMapped) {
 #pragma unroll
-    for (int j = 0; j < NV; ++j)
-      if (vbase + lane + 32 * j < nvec) dst[j] = __ldcs(src + vbase + lane + 32 * j);
+      for (int j = 0; j < NV; ++j) dst[j] = __ldcs(src + ((vmap[j / 4] >> (8 * (j % 4))) & 0xffu));
+    } else {
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+        if (vbase + lane + 32 * j < nvec) dst[j] = __ldcs(src + vbase + lane + 32 * j);
+    }
   };
   uint64_t f = f_begin + warp;
   if (f < f_end) load(f, cur);
@@ -353,7 +431,8 @@ int fx_nv(const DenseArgs& a) {
   return a.dims[0] == (128u << (v - 1)) ? v + 4 : v;
 }
 
-using FxKernel = void (*)(DenseArgs, const float*, const uint32_t*, const FxStats*, int32_t*, int*);
+using FxKernel = void (*)(DenseArgs, const float*, const uint32_t*, const FxStats*, int32_t*, int*,
+                          const uint8_t*);
 FxKernel fx_kernel(int v) {
   switch (v) {
     case 1: return fcs_dense_fx_kernel<1, 1, 512, false>;
@@ -409,7 +488,8 @@ int make_plan(const DenseArgs& a, Plan* p) {
   nchunk = std::min<uint64_t>(nchunk, std::max<uint64_t>(1, a.fibers / 16));
   p->nchunk = nchunk;
   p->part_bytes = nchunk * a.D * static_cast<size_t>(a.jt) * sizeof(Tacc);
-  p->ws = align_up(p->part_bytes) + align_up(nchunk * a.D * sizeof(int)) + align_up(sizeof(FxStats));
+  p->ws = align_up(p->part_bytes) + align_up(nchunk * a.D * sizeof(int)) +
+          align_up(sizeof(FxStats)) + align_up(static_cast<size_t>(a.D) * 32);
   return ST_OK;
 }
 
@@ -494,8 +574,20 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
     const double per_cta = static_cast<double>(a.fibers_per_chunk) * a.dims[0];
     fx_scale_kernel<<<1, 1, 0, st>>>(stats, 3.0 * per_cta / a.jt + 16.0);
     FCS_CUDA_TRY(cudaGetLastError());
+    // bank-aware load order for the full-vector kernels (I_0 = 128 NV, NV >= 2);
+    // ST_FX_NOGROUP=1 keeps the identity order (A/B probe)
+    static const bool no_group = std::getenv("ST_FX_NOGROUP") != nullptr;
+    uint8_t* groups = nullptr;
+    const int nv_full = p.nv >= 6 ? 1 << (p.nv - 5) : 0;
+    if (nv_full && !no_group) {
+      groups = reinterpret_cast<uint8_t*>(base + align_up(p.part_bytes) +
+                                          align_up(p.nchunk * a.D * sizeof(int)) +
+                                          align_up(sizeof(FxStats)));
+      fx_group_kernel<<<a.D, 32, 0, st>>>(packed, a.fam_stride, a.i0_shift, nv_full, groups);
+      FCS_CUDA_TRY(cudaGetLastError());
+    }
     fx_kernel(p.nv)<<<static_cast<unsigned>(nchunk * a.D), p.threads, p.smem_bytes, st>>>(
-        a, reinterpret_cast<const float*>(t), packed, stats, part, flags);
+        a, reinterpret_cast<const float*>(t), packed, stats, part, flags, groups);
     FCS_CUDA_TRY(cudaGetLastError());
     reduce_fx_kernel<<<ceil_div(out_elems, 256), 256, 0, st>>>(part, flags, nchunk, a.D, a.jt,
                                                                stats, out, accumulate);
