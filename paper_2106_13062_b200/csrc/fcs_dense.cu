@@ -205,7 +205,7 @@ __device__ __forceinline__ void fiber_offset_fast(const DenseArgs& a, const uint
 // warp per fiber, lane-owned mode-0 indices with their table entries in
 // registers, NV 128-bit loads per lane with the next fiber prefetched,
 // int32 fixed-point shared-memory accumulation with exact overflow detection.
-template <int NV, int SPLIT, int THREADS, bool kFull>
+template <int NV, int SPLIT, int THREADS, bool kFull, bool kGroup = false>
 __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
                                                               const float* __restrict__ t,
                                                               const uint32_t* __restrict__ packed,
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
   // Vector this lane loads at step j: lane + 32 j, or with the bank-aware
   // grouping (kFull only) 8 * line + (lane & 7), line = groups[d][j][lane / 8];
   // the indices are kept packed four per register (vmap).
-  constexpr bool kMapped = kFull && SPLIT == 1;  // vector map in vmap (identity if no groups)
+  constexpr bool kMapped = kGroup && kFull && SPLIT == 1;  // vector map in vmap
   const bool grouped = kMapped && groups != nullptr;
   uint32_t vmap[(NV + 3) / 4];
 #pragma unroll
@@ -410,6 +410,7 @@ enum class Path { Global, Smem, Fx };
 
 struct Plan {
   Path path = Path::Global;
+  bool group = false;  // fx: bank-aware load order
   size_t smem_bytes = 0;
   int threads = 0;
   int nv = 0;
@@ -433,7 +434,15 @@ int fx_nv(const DenseArgs& a) {
 
 using FxKernel = void (*)(DenseArgs, const float*, const uint32_t*, const FxStats*, int32_t*, int*,
                           const uint8_t*);
-FxKernel fx_kernel(int v) {
+FxKernel fx_kernel(int v, bool group) {
+  if (group) {  // full-vector kernels with the bank-aware load order
+    switch (v) {
+      case 6: return fcs_dense_fx_kernel<2, 1, 512, true, true>;
+      case 7: return fcs_dense_fx_kernel<4, 1, 512, true, true>;
+      case 8: return fcs_dense_fx_kernel<8, 1, 512, true, true>;
+      default: break;
+    }
+  }
   switch (v) {
     case 1: return fcs_dense_fx_kernel<1, 1, 512, false>;
     case 2: return fcs_dense_fx_kernel<2, 1, 512, false>;
@@ -468,7 +477,13 @@ int make_plan(const DenseArgs& a, Plan* p) {
   if (p->nv) {
     p->path = Path::Fx;
     p->threads = fx_threads(p->nv);
-    auto k = fx_kernel(p->nv);
+    // the bank-aware order pays off when atomics bind (measured at D = 4: -2..3 %;
+    // D = 2: none); with one family
+    // the kernel is load-bound and keeps the immediate-offset loads.
+    // ST_FX_NOGROUP=1 keeps the identity order (A/B probe).
+    static const bool no_group = std::getenv("ST_FX_NOGROUP") != nullptr;
+    p->group = p->nv >= 6 && a.D >= 3 && !no_group;
+    auto k = fx_kernel(p->nv, p->group);
     FCS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(p->smem_bytes)));
     FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
@@ -574,19 +589,17 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
     const double per_cta = static_cast<double>(a.fibers_per_chunk) * a.dims[0];
     fx_scale_kernel<<<1, 1, 0, st>>>(stats, 3.0 * per_cta / a.jt + 16.0);
     FCS_CUDA_TRY(cudaGetLastError());
-    // bank-aware load order for the full-vector kernels (I_0 = 128 NV, NV >= 2);
-    // ST_FX_NOGROUP=1 keeps the identity order (A/B probe)
-    static const bool no_group = std::getenv("ST_FX_NOGROUP") != nullptr;
+    // bank-aware load order for the full-vector kernels (I_0 = 128 NV, NV >= 2)
     uint8_t* groups = nullptr;
     const int nv_full = p.nv >= 6 ? 1 << (p.nv - 5) : 0;
-    if (nv_full && !no_group) {
+    if (p.group) {
       groups = reinterpret_cast<uint8_t*>(base + align_up(p.part_bytes) +
                                           align_up(p.nchunk * a.D * sizeof(int)) +
                                           align_up(sizeof(FxStats)));
       fx_group_kernel<<<a.D, 32, 0, st>>>(packed, a.fam_stride, a.i0_shift, nv_full, groups);
       FCS_CUDA_TRY(cudaGetLastError());
     }
-    fx_kernel(p.nv)<<<static_cast<unsigned>(nchunk * a.D), p.threads, p.smem_bytes, st>>>(
+    fx_kernel(p.nv, p.group)<<<static_cast<unsigned>(nchunk * a.D), p.threads, p.smem_bytes, st>>>(
         a, reinterpret_cast<const float*>(t), packed, stats, part, flags, groups);
     FCS_CUDA_TRY(cudaGetLastError());
     reduce_fx_kernel<<<ceil_div(out_elems, 256), 256, 0, st>>>(part, flags, nchunk, a.D, a.jt,

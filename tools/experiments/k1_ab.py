@@ -15,7 +15,8 @@ n = 1 << 30
 x = torch.empty(n, dtype=torch.float32, device="cuda")
 lib = L.lib()
 L.check(lib.st_device_gaussian(L.ST_F32, 4, n, C.c_void_p(x.data_ptr()), None))
-fams = st.families_for(dims, st.EstimatorConfig(16384, 4, 4))
+D = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+fams = st.families_for(dims, st.EstimatorConfig(16384, D, 4))
 packed = st.packed_families(fams)
 t = st.DenseTensor(dims, x)
 out = st.fcs_dense_batched(t, fams, packed=packed)
@@ -29,4 +30,4 @@ for _ in range(reps):
     st.fcs_dense_batched(t, fams, packed=packed, out=out)
 b.record()
 torch.cuda.synchronize()
-print(os.environ.get("K1_TAG", "?"), "ms per call", round(a.elapsed_time(b) / reps, 4))
+print(os.environ.get("K1_TAG", "?"), "D", D, "ms per call", round(a.elapsed_time(b) / reps, 4))
