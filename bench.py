@@ -337,7 +337,7 @@ def secondary(x=None):
     ms_iuv = timeit(lambda: eng.iuv_batch(U, U, 0), 20)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    cpd = st.rtpm(dt, st.RtpmConfig(c.rank, configs.C3_INITS, configs.C3_ITERS,
+    cpd = st.rtpm(dt, st.RtpmConfig(c.rank, configs.C3_INITS, configs.C3_ITERS, st.SketchBackend.FCS,
                                     estimator=st.EstimatorConfig(c.hash_len, c.sketch_count,
                                                                  c.seed)))
     t_rtpm = time.perf_counter() - t0

@@ -47,7 +47,7 @@ enum { ST_F32 = 0, ST_F64 = 1 };
 /* SketchKind (sketch.hpp:10), same order. */
 enum { ST_SKETCH_CS = 0, ST_SKETCH_TS = 1, ST_SKETCH_FCS = 2 };
 
-/* SketchBackend (cpd.hpp:13), same order. The B200 engine provides TS and FCS. */
+/* SketchBackend (cpd.hpp:13), same order. */
 enum {
   ST_BACKEND_PLAIN = 0,
   ST_BACKEND_CS = 1,
@@ -223,18 +223,21 @@ typedef struct st_engine st_engine;
  * once and not retained. */
 int st_engine_create(st_engine** engine, int dtype, const void* tensor, const size_t* dims,
                      size_t hash_len, size_t sketch_count, uint64_t seed, void* stream);
-/* make_contraction_engine(t, backend, cfg) (cpd.cpp:220-232) for backend
- * ST_BACKEND_FCS (FcsEngine, cpd.cpp:61-94) or ST_BACKEND_TS (TsEngine,
+/* make_contraction_engine(t, backend, cfg) (cpd.cpp:220-232), every backend:
+ * ST_BACKEND_FCS (FcsEngine, cpd.cpp:61-94), ST_BACKEND_TS (TsEngine,
  * cpd.cpp:96-126: D tensor sketches of length J, estimates by circular
- * correlation at length J, estimators.cpp:209-233). Other backends return
- * ST_EINVAL. st_engine_create == backend ST_BACKEND_FCS. */
+ * correlation at length J, estimators.cpp:209-233), ST_BACKEND_PLAIN
+ * (PlainEngine, cpd.cpp:36-59: exact contractions of a device copy of the
+ * tensor; D is 1, no median), ST_BACKEND_HCS (HcsEngine, cpd.cpp:128-158:
+ * D J x J x J sketches) and ST_BACKEND_CS (CsEngine, cpd.cpp:160-197: D
+ * long-pair count sketches of vec(T)). st_engine_create == ST_BACKEND_FCS. */
 int st_engine_create_backend(st_engine** engine, int backend, int dtype, const void* tensor,
                              const size_t* dims, size_t hash_len, size_t sketch_count,
                              uint64_t seed, void* stream);
 int st_engine_destroy(st_engine* engine);
 int st_engine_backend(const st_engine* engine);
-/* Sketch length (J~ for FCS, J for TS) and the current D x length sketch
- * values (device out). */
+/* Sketch length (J~ FCS, J TS and CS, J^3 HCS; 0 Plain) and the current
+ * D x length sketch values (device out; ST_EINVAL for Plain). */
 size_t st_engine_composed_len(const st_engine* engine);
 int st_engine_sketches(st_engine* engine, double* out, void* stream);
 
@@ -269,7 +272,7 @@ int st_engine_deflate(st_engine* engine, double weight, const double* u, const d
 int st_rtpm(int dtype, const void* tensor, size_t dim, size_t rank, size_t num_inits,
             size_t num_iters, size_t hash_len, size_t sketch_count, uint64_t seed,
             double* weights, double* factor, void* stream);
-/* HOST. st_rtpm with RtpmConfig::backend (ST_BACKEND_FCS or ST_BACKEND_TS). */
+/* HOST. st_rtpm with RtpmConfig::backend (any ST_BACKEND_*). */
 int st_rtpm_backend(int backend, int dtype, const void* tensor, size_t dim, size_t rank,
                     size_t num_inits, size_t num_iters, size_t hash_len, size_t sketch_count,
                     uint64_t seed, double* weights, double* factor, void* stream);

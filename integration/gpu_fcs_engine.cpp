@@ -95,9 +95,7 @@ void GpuFcsEngine::deflate(double weight, const Eigen::VectorXd& u, const Eigen:
 std::unique_ptr<sketchtensor::ContractionEngine> make_contraction_engine(
     const sketchtensor::DenseTensor& t, sketchtensor::SketchBackend backend,
     const sketchtensor::EstimatorConfig& cfg) {
-  if (backend == sketchtensor::SketchBackend::FCS || backend == sketchtensor::SketchBackend::TS)
-    return std::make_unique<GpuFcsEngine>(t, cfg, backend);
-  return sketchtensor::make_contraction_engine(t, backend, cfg);
+  return std::make_unique<GpuFcsEngine>(t, cfg, backend);  // every backend runs on the GPU
 }
 
 }  // namespace sketchtensor_b200

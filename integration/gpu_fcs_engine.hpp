@@ -17,9 +17,9 @@ namespace sketchtensor_b200 {
 
 class GpuFcsEngine final : public sketchtensor::ContractionEngine {
  public:
-  // FcsEngine / TsEngine ctor semantics (cpd.cpp:63-67, 98-102): D =
-  // cfg.sketch_count families from families_for(t.shape(), cfg); the tensor
-  // is consumed once. backend: SketchBackend::FCS or SketchBackend::TS.
+  // Engine ctor semantics of the chosen backend (cpd.cpp:36-197): sketch
+  // backends build D = cfg.sketch_count sketches from families_for(t.shape(),
+  // cfg) and drop the tensor; Plain keeps a device copy of it.
   GpuFcsEngine(const sketchtensor::DenseTensor& t, const sketchtensor::EstimatorConfig& cfg,
                sketchtensor::SketchBackend backend = sketchtensor::SketchBackend::FCS);
   ~GpuFcsEngine() override;
@@ -41,8 +41,7 @@ class GpuFcsEngine final : public sketchtensor::ContractionEngine {
   std::size_t dev_len_ = 0;
 };
 
-// make_contraction_engine (cpd.cpp:220-232) with FCS and TS routed to the GPU;
-// other backends are delegated to the reference factory.
+// make_contraction_engine (cpd.cpp:220-232) with every backend on the GPU.
 std::unique_ptr<sketchtensor::ContractionEngine> make_contraction_engine(
     const sketchtensor::DenseTensor& t, sketchtensor::SketchBackend backend,
     const sketchtensor::EstimatorConfig& cfg);

@@ -99,6 +99,20 @@ int main() {
   ref_ts->deflate(0.5, u, v, w);
   gpu_ts->deflate(0.5, u, v, w);
   worst = std::max(worst, rel_err(gpu_ts->iuv(u, v, 2), ref_ts->iuv(u, v, 2)));
+  // the exact and baseline backends (Plain, HCS, long-pair CS) through the same factory
+  EstimatorConfig small = cfg;
+  small.hash_len = 12;
+  for (SketchBackend bk : {SketchBackend::Plain, SketchBackend::HCS, SketchBackend::CS}) {
+    auto r = sketchtensor::make_contraction_engine(t, bk, small);
+    auto g = sketchtensor_b200::make_contraction_engine(t, bk, small);
+    worst = std::max(worst, rel_err(g->iuv(v, w, 0), r->iuv(v, w, 0)));
+    a[0] = g->uvw(u, v, w);
+    b[0] = r->uvw(u, v, w);
+    worst = std::max(worst, rel_err(a, b));
+    r->deflate(0.5, u, v, w);
+    g->deflate(0.5, u, v, w);
+    worst = std::max(worst, rel_err(g->iuv(u, w, 1), r->iuv(u, w, 1)));
+  }
   bool threw = false;
   try {
     gpu->iuv(u, v, 3);

@@ -11,7 +11,8 @@ from .sketchtensor import (CpTensor, DenseTensor, EstimatorConfig, HashFamily, H
                            families_for, family_seed, fcs_cp_batched, fcs_dense_batched,
                            fcs_kron, fcs_sketch, hcs_sketch, median_reduce, packed_families,
                            ts_sketch)
-from .engine import (AlsConfig, ContractionEngine, FcsEngine, RtpmConfig, SketchBackend,  # noqa
+from .engine import (AlsConfig, ContractionEngine, CsEngine, FcsEngine, HcsEngine,  # noqa
+                     PlainEngine, RtpmConfig, SketchBackend,
                      TsEngine, als, backend_from_name, backend_name, make_contraction_engine,
                      residual_norm, rtpm, rtpm_asym)
 

@@ -142,10 +142,8 @@ int st_engine_create_backend(st_engine** engine, int backend, int dtype, const v
   FCS_CHECK_ARG(engine != nullptr, "st_engine_create: null engine pointer");
   FCS_CHECK_ARG(backend >= ST_BACKEND_PLAIN && backend <= ST_BACKEND_FCS,
                 "make_contraction_engine: unknown backend");
-  FCS_CHECK_ARG(backend == ST_BACKEND_FCS || backend == ST_BACKEND_TS,
-                "make_contraction_engine: backend not provided by the B200 engine (fcs, ts)");
   FCS_CHECK_ARG(dtype == ST_F32 || dtype == ST_F64, "st_engine_create: unknown dtype");
-  FCS_CHECK_ARG(hash_len > 0 && sketch_count > 0,
+  FCS_CHECK_ARG(backend == ST_BACKEND_PLAIN || (hash_len > 0 && sketch_count > 0),
                 "EstimatorConfig: hash_len and sketch_count must be >= 1");
   for (int n = 0; n < 3; ++n) FCS_CHECK_ARG(dims[n] > 0, "DenseTensor: zero dimension");
   *engine = nullptr;
@@ -156,6 +154,36 @@ int st_engine_create_backend(st_engine** engine, int backend, int dtype, const v
   for (int n = 0; n < 3; ++n) e->dims[n] = dims[n];
   e->hash_len = hash_len;
   e->D = sketch_count;
+  if (backend == ST_BACKEND_PLAIN || backend == ST_BACKEND_HCS || backend == ST_BACKEND_CS) {
+    // engines_exact.cu: Plain holds the tensor (D = 1: exact contractions);
+    // HCS the D J^3 sketches (needs the families' tables); CS the D long pairs
+    if (backend == ST_BACKEND_PLAIN) e->D = 1;
+    const size_t sum_dims = dims[0] + dims[1] + dims[2];
+    std::vector<uint64_t> seeds(e->D);
+    for (size_t d = 0; d < e->D; ++d)  // families_for / CsEngine seeds (cpd.cpp:162-166)
+      seeds[d] = splitmix_draw(seed + static_cast<uint64_t>(d), 1);
+    int rc = ST_OK;
+    if (backend == ST_BACKEND_HCS) {
+      const size_t hl[3] = {hash_len, hash_len, hash_len};
+      if (cudaMalloc(reinterpret_cast<void**>(&e->packed), e->D * sum_dims * sizeof(uint32_t)) !=
+          cudaSuccess)
+        rc = fail(ST_ENOMEM, "st_engine_create: device allocation failed");
+      if (!rc) rc = launch_family_tables(3, dims, hl, e->D, seeds.data(), e->packed, st);
+    } else if (backend == ST_BACKEND_CS) {
+      if (cudaMalloc(reinterpret_cast<void**>(&e->seeds), e->D * sizeof(uint64_t)) != cudaSuccess)
+        rc = fail(ST_ENOMEM, "st_engine_create: device allocation failed");
+      if (!rc && cudaMemcpy(e->seeds, seeds.data(), e->D * sizeof(uint64_t),
+                            cudaMemcpyHostToDevice) != cudaSuccess)
+        rc = fail(ST_ECUDA, "st_engine_create: seed upload failed");
+    }
+    if (!rc) rc = exact_create(e, dtype, tensor, st);
+    if (rc) {
+      st_engine_destroy(e);
+      return rc;
+    }
+    *engine = e;
+    return ST_OK;
+  }
   e->jt = 3 * hash_len - 2;
   e->slen = backend == ST_BACKEND_TS ? hash_len : e->jt;
   int rc = get_fft_plan(e->jt, &e->plan);
@@ -226,9 +254,12 @@ int st_engine_destroy(st_engine* e) {
   if (e->spec) cudaFree(e->spec);
   if (e->ext) cudaFree(e->ext);
   if (e->one) cudaFree(e->one);
+  if (e->dense) cudaFree(e->dense);
+  if (e->seeds) cudaFree(e->seeds);
   e->scratch.release(nullptr);
   e->est.release(nullptr);
   e->vec.release(nullptr);
+  e->vec2.release(nullptr);
   cudaDeviceSynchronize();
   delete e;
   return ST_OK;
@@ -240,6 +271,12 @@ size_t st_engine_composed_len(const st_engine* e) { return e ? e->slen : 0; }
 
 int st_engine_sketches(st_engine* e, double* out, void* stream) {
   FCS_CHECK_ARG(e != nullptr, "st_engine_sketches: null engine");
+  FCS_CHECK_ARG(e->backend != ST_BACKEND_PLAIN, "st_engine_sketches: the plain engine has no sketches");
+  if (e->backend == ST_BACKEND_HCS || e->backend == ST_BACKEND_CS) {
+    FCS_CUDA_TRY(cudaMemcpyAsync(out, e->dense, e->D * e->slen * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, as_stream(stream)));
+    return ST_OK;
+  }
   if (e->backend == ST_BACKEND_TS) {
     FCS_CUDA_TRY(cudaMemcpy2DAsync(out, e->slen * sizeof(double), e->ext, e->jt * sizeof(double),
                                    e->slen * sizeof(double), e->D, cudaMemcpyDeviceToDevice,
@@ -259,6 +296,18 @@ int st_engine_iuv(st_engine* e, size_t batch, const double* a, const double* b, 
   int c1, c2;
   contracted(free_mode, &c1, &c2);
   const size_t nf = e->dims[free_mode];
+  if (is_exact(e)) {  // Plain / HCS / CS (engines_exact.cu); Plain is exact: no median
+    const bool med = median && e->backend != ST_BACKEND_PLAIN;
+    double* est = out;
+    if (med) {
+      if (int rc = e->est.ensure(batch * e->D * nf * sizeof(double), st)) return rc;
+      est = static_cast<double*>(e->est.p);
+    }
+    if (int rc = exact_iuv(e, batch, a, b, static_cast<int>(free_mode), est, st)) return rc;
+    return med ? launch_median(est, static_cast<int>(batch), static_cast<int>(e->D),
+                               static_cast<int>(nf), out, st)
+               : ST_OK;
+  }
   if (int rc = e->scratch.ensure(batch * e->D * e->plan.P * sizeof(double2), st)) return rc;
   double* est = out;
   if (median) {
@@ -280,6 +329,17 @@ int st_engine_uvw(st_engine* e, size_t batch, const double* u, const double* v, 
   FCS_CHECK_ARG(e != nullptr, "st_engine_uvw: null engine");
   if (batch == 0) return ST_OK;
   cudaStream_t st = as_stream(stream);
+  if (is_exact(e)) {
+    const bool med = median && e->backend != ST_BACKEND_PLAIN;
+    double* est = out;
+    if (med) {
+      if (int rc = e->est.ensure(batch * e->D * sizeof(double), st)) return rc;
+      est = static_cast<double*>(e->est.p);
+    }
+    if (int rc = exact_uvw(e, batch, u, v, w, est, st)) return rc;
+    return med ? launch_median(est, static_cast<int>(batch), static_cast<int>(e->D), 1, out, st)
+               : ST_OK;
+  }
   if (int rc = e->scratch.ensure(batch * e->D * e->plan.P * sizeof(double2), st)) return rc;
   double* est = out;
   if (median) {
@@ -297,6 +357,7 @@ int st_engine_deflate(st_engine* e, double weight, const double* u, const double
                       const double* w, void* stream) {
   FCS_CHECK_ARG(e != nullptr, "st_engine_deflate: null engine");
   cudaStream_t st = as_stream(stream);
+  if (is_exact(e)) return exact_deflate(e, weight, u, v, w, st);
   if (e->backend == ST_BACKEND_TS) {
     // TsEngine::deflate (cpd.cpp:115-122): TS -= ts_sketch(w u o v o w) =
     // ((CP-form FCS of u o v o w) mod J), then the spectra are rebuilt.

@@ -99,6 +99,18 @@ struct HostRng {
 
 }  // namespace fcs
 
+struct st_engine;
+namespace fcs {
+// Plain / HCS / CS backends (engines_exact.cu)
+int exact_create(st_engine* e, int dtype, const void* tensor, cudaStream_t st);
+int exact_iuv(st_engine* e, size_t batch, const double* a, const double* b, int f, double* est,
+              cudaStream_t st);
+int exact_uvw(st_engine* e, size_t batch, const double* u, const double* v, const double* w,
+              double* est, cudaStream_t st);
+int exact_deflate(st_engine* e, double weight, const double* u, const double* v, const double* w,
+                  cudaStream_t st);
+}  // namespace fcs
+
 // The engine: D families' packed hash tables and the cached half spectra of
 // the sketch each estimate correlates against.
 //  FCS backend: S_d = F(FCS_d(T)), length J~ = 3J - 2 (FcsEngine, cpd.cpp:61-94).
@@ -121,7 +133,9 @@ struct st_engine {
   double2* spec = nullptr;     // D x P
   double* ext = nullptr;       // TS: D x jt periodic extension (real)
   double* one = nullptr;       // TS: device 1.0 (rank-one CP weight)
-  fcs::Scratch scratch, est, vec;
+  double* dense = nullptr;     // Plain: the tensor; HCS: D x J^3 sketches; CS: D x J sketches
+  uint64_t* seeds = nullptr;   // CS: the D long pairs' seeds
+  fcs::Scratch scratch, est, vec, vec2;
   fcs::EngArgs args() const {
     fcs::EngArgs e{};
     size_t off = 0;
@@ -138,3 +152,10 @@ struct st_engine {
     return e;
   }
 };
+
+namespace fcs {
+inline bool is_exact(const st_engine* e) {
+  return e->backend == ST_BACKEND_PLAIN || e->backend == ST_BACKEND_HCS ||
+         e->backend == ST_BACKEND_CS;
+}
+}  // namespace fcs

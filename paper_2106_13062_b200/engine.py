@@ -2,11 +2,11 @@
 
 Mirrors ``cpd.hpp:12-84``: ``SketchBackend``, ``ContractionEngine``
 (uvw / iuv / deflate / uuu / iuu / shape), ``make_contraction_engine``,
-``rtpm``, ``rtpm_asym``, ``als`` and ``residual_norm``. The B200 engine
-provides the FCS backend (the north star) and the TS backend (SURVEY.md §8(f)
-rank 1, the equal-hash baseline); Plain/CS/HCS raise ValueError naming the
-missing backend, the reference's own error class for an unusable backend
-(cpd.cpp:27).
+``rtpm``, ``rtpm_asym``, ``als`` and ``residual_norm``, with all five
+backends of the reference factory (cpd.cpp:220-232): FCS (the north star) and
+TS through the spectral kernels, Plain (exact), HCS and long-pair CS through
+the batched contraction kernels of engines_exact.cu. As in the reference,
+``RtpmConfig`` / ``AlsConfig`` default to the Plain backend.
 
 The engine keeps the D sketches' spectra resident on the device
 (``st_engine_*``); batched entry points (``iuv_batch`` / ``uvw_batch``) are
@@ -79,9 +79,9 @@ class ContractionEngine:
 
 
 class _DeviceEngine(ContractionEngine):
-    """A sketch engine on the device: D = cfg.sketch_count families from
-    families_for (estimators.cpp:104-115), sketches built once by K1 and their
-    spectra cached (st_engine_create_backend)."""
+    """A contraction engine on the device (st_engine_create_backend): for the
+    sketch backends D = cfg.sketch_count families from families_for
+    (estimators.cpp:104-115), sketches built once; Plain keeps the tensor."""
 
     BACKEND: SketchBackend = SketchBackend.FCS
 
@@ -90,8 +90,9 @@ class _DeviceEngine(ContractionEngine):
             t = DenseTensor.from_array(t)
         if t.order() != 3:
             raise ValueError("make_contraction_engine: order-3 tensor required")
-        if cfg.hash_len == 0 or cfg.sketch_count == 0:
+        if self.BACKEND != SketchBackend.Plain and (cfg.hash_len == 0 or cfg.sketch_count == 0):
             raise ValueError("EstimatorConfig: hash_len and sketch_count must be >= 1")
+        self._D = 1 if self.BACKEND == SketchBackend.Plain else cfg.sketch_count
         self._shape = t.shape()
         self.cfg = cfg
         h = C.c_void_p()
@@ -115,7 +116,7 @@ class _DeviceEngine(ContractionEngine):
 
     def sketches(self) -> torch.Tensor:
         """Current D x composed_len() sketch values (after any deflations)."""
-        out = torch.empty((self.cfg.sketch_count, self.composed_len()), dtype=torch.float64,
+        out = torch.empty((self._D, self.composed_len()), dtype=torch.float64,
                           device=_dev())
         _check(L.lib().st_engine_sketches(self._h, _ptr(out), _stream()))
         return out
@@ -132,7 +133,7 @@ class _DeviceEngine(ContractionEngine):
         if A2.shape[0] != B2.shape[0]:
             raise ValueError("estimate_iuv: batch mismatch")
         n = A2.shape[0]
-        shape = (n, self._shape[free_mode]) if median else (n, self.cfg.sketch_count,
+        shape = (n, self._shape[free_mode]) if median else (n, self._D,
                                                             self._shape[free_mode])
         out = torch.empty(shape, dtype=torch.float64, device=_dev())
         _check(L.lib().st_engine_iuv(self._h, n, _ptr(A2), _ptr(B2), free_mode, _ptr(out),
@@ -144,7 +145,7 @@ class _DeviceEngine(ContractionEngine):
         V = _vec(v, self._shape[1], "estimate_uvw").reshape(-1, self._shape[1])
         W = _vec(w, self._shape[2], "estimate_uvw").reshape(-1, self._shape[2])
         n = U.shape[0]
-        out = torch.empty((n,) if median else (n, self.cfg.sketch_count), dtype=torch.float64,
+        out = torch.empty((n,) if median else (n, self._D), dtype=torch.float64,
                           device=_dev())
         _check(L.lib().st_engine_uvw(self._h, n, _ptr(U), _ptr(V), _ptr(W), _ptr(out),
                                      1 if median else 0, _stream()))
@@ -179,13 +180,32 @@ class TsEngine(_DeviceEngine):
     BACKEND = SketchBackend.TS
 
 
-_ENGINES = {SketchBackend.FCS: FcsEngine, SketchBackend.TS: TsEngine}
+class PlainEngine(_DeviceEngine):
+    """PlainEngine (cpd.cpp:36-59): exact contractions of the device-resident
+    tensor (contract3 / contract3_free, tensor.cpp:181-226), exact deflation."""
+    BACKEND = SketchBackend.Plain
+
+
+class HcsEngine(_DeviceEngine):
+    """HcsEngine (cpd.cpp:128-158): D higher-order count sketches J x J x J,
+    contracted with the count sketches of the vectors (estimators.cpp:241-275)."""
+    BACKEND = SketchBackend.HCS
+
+
+class CsEngine(_DeviceEngine):
+    """CsEngine (cpd.cpp:160-197): D long-pair count sketches of vec(T), the
+    pair over all prod I_n indices hashed on the device (estimators.cpp:277-350)."""
+    BACKEND = SketchBackend.CS
+
+
+_ENGINES = {SketchBackend.FCS: FcsEngine, SketchBackend.TS: TsEngine,
+            SketchBackend.Plain: PlainEngine, SketchBackend.HCS: HcsEngine,
+            SketchBackend.CS: CsEngine}
 
 
 def _engine_backend(backend: SketchBackend) -> int:
     if backend not in _ENGINES:
-        raise ValueError(f"make_contraction_engine: backend '{backend_name(backend)}' is not "
-                         "provided by the B200 library (fcs, ts)")
+        raise ValueError("make_contraction_engine: unknown backend")
     return backend.value
 
 
@@ -201,12 +221,11 @@ def make_contraction_engine(t, backend: SketchBackend, cfg: EstimatorConfig) -> 
 
 @dataclass
 class RtpmConfig:
-    """RtpmConfig (cpd.hpp:49-55). The default backend is FCS here (the
-    reference defaults to Plain, which the B200 library does not provide)."""
+    """RtpmConfig (cpd.hpp:49-55)."""
     target_rank: int = 1
     num_inits: int = 15
     num_power_iters: int = 20
-    backend: SketchBackend = SketchBackend.FCS
+    backend: SketchBackend = SketchBackend.Plain
     estimator: EstimatorConfig = field(default_factory=EstimatorConfig)
 
 
@@ -215,7 +234,7 @@ class AlsConfig:
     """AlsConfig (cpd.hpp:57-63)."""
     target_rank: int = 1
     max_iters: int = 50
-    backend: SketchBackend = SketchBackend.FCS
+    backend: SketchBackend = SketchBackend.Plain
     estimator: EstimatorConfig = field(default_factory=EstimatorConfig)
     tol: float = 1e-8
 

@@ -80,11 +80,50 @@ def test_ts_engine_batched_f32(cuda):
         rel_close(got[l], oeng.iuv(A[l], B[l], 0), 1e-4)
 
 
-def test_engine_unsupported_backend(cuda):
-    t = st.DenseTensor.from_array(np.ones((4, 4, 4)))
-    for b in (st.SketchBackend.Plain, st.SketchBackend.CS, st.SketchBackend.HCS):
-        with pytest.raises(ValueError):
-            st.make_contraction_engine(t, b, st.EstimatorConfig(8, 2, 1))
+@pytest.mark.parametrize("backend", [st.SketchBackend.Plain, st.SketchBackend.HCS,
+                                     st.SketchBackend.CS])
+@pytest.mark.parametrize("dims,J,D,seed", [((9, 7, 5), 6, 3, 5), ((40, 30, 20), 16, 5, 11),
+                                           ((24, 24, 24), 40, 4, 2)])
+def test_exact_engines_vs_reference(cuda, backend, dims, J, D, seed):
+    """Plain (exact), HCS and long-pair CS engines (cpd.cpp:36-59,128-197)."""
+    rng = np.random.default_rng(seed)
+    t = rng.standard_normal(dims)
+    eng = st.make_contraction_engine(st.DenseTensor.from_array(t), backend,
+                                     st.EstimatorConfig(J, D, seed))
+    oeng = ref.Engine(t, J, D, seed, backend=backend.value)
+    u, v, w = (rng.standard_normal(n) for n in dims)
+    rel_close(eng.iuv(v, w, 0), oeng.iuv(v, w, 0), 1e-11)
+    rel_close(eng.iuv(u, w, 1), oeng.iuv(u, w, 1), 1e-11)
+    rel_close(eng.iuv(u, v, 2), oeng.iuv(u, v, 2), 1e-11)
+    rel_close(eng.uvw(u, v, w), oeng.uvw(u, v, w), 1e-11)
+    eng.deflate(0.7, u, v, w)
+    oeng.deflate(0.7, u, v, w)
+    rel_close(eng.iuv(v, w, 0), oeng.iuv(v, w, 0), 1e-11)
+    rel_close(eng.iuv(u, v, 2), oeng.iuv(u, v, 2), 1e-11)
+    rel_close(eng.uvw(u, v, w), oeng.uvw(u, v, w), 1e-11)
+    # batches larger than one chunk of 8, zero entries in the vectors
+    A, B = rng.standard_normal((11, dims[1])), rng.standard_normal((11, dims[2]))
+    B[3, :2] = 0.0
+    got = eng.iuv_batch(A, B, 0).cpu().numpy()
+    for l in (0, 3, 10):
+        rel_close(got[l], oeng.iuv(A[l], B[l], 0), 1e-11)
+    U3 = rng.standard_normal((9, dims[0]))
+    vals = eng.uvw_batch(U3, A[:9], B[:9]).cpu().numpy()
+    for l in (0, 8):
+        rel_close(vals[l], oeng.uvw(U3[l], A[l], B[l]), 1e-11)
+
+
+def test_plain_engine_is_exact(cuda):
+    rng = np.random.default_rng(3)
+    t = rng.standard_normal((12, 10, 8))
+    eng = st.PlainEngine(st.DenseTensor.from_array(t.astype(np.float32)),
+                         st.EstimatorConfig(0, 0, 0))
+    u, v, w = (rng.standard_normal(n) for n in t.shape)
+    t32 = t.astype(np.float32).astype(np.float64)
+    rel_close(eng.iuv(v, w, 0), np.einsum("ijk,j,k->i", t32, v, w), 1e-12)
+    rel_close(eng.uvw(u, v, w), np.einsum("ijk,i,j,k->", t32, u, v, w), 1e-12)
+    with pytest.raises(ValueError):
+        eng.sketches()
 
 
 # ------------------------------------------------------------ rtpm / rtpm_asym
@@ -116,6 +155,40 @@ def test_rtpm_asym_recovers_components(cuda):
                       st.RtpmConfig(2, 5, 10, FCS, st.EstimatorConfig(2000, 5, 3)))
     np.testing.assert_allclose(np.sort(cp.weights.cpu().numpy())[::-1], [5.0, 3.0], atol=0.1)
     assert st.residual_norm(st.DenseTensor.from_array(t), cp) < 0.3
+
+
+@pytest.mark.parametrize("backend", [st.SketchBackend.Plain, st.SketchBackend.HCS,
+                                     st.SketchBackend.CS])
+def test_cpd_drivers_exact_backends(cuda, backend):
+    """rtpm / rtpm_asym / als through the Plain, HCS and CS engines vs the reference."""
+    q = np.linalg.qr(np.random.default_rng(5).standard_normal((12, 2)))[0]
+    t = configs.densify([3.0, 1.5], [q, q, q])
+    est = st.EstimatorConfig(10, 3, 9)
+    cp = st.rtpm(st.DenseTensor.from_array(t), st.RtpmConfig(2, 3, 5, backend, est))
+    w, f = ref.rtpm(t, 2, 3, 5, 10, 3, 9, backend=backend.value)
+    rel_close(cp.weights, w, 1e-8)
+    rel_close(cp.factors[0], f, 1e-8)
+    ta, _ = low_rank((10, 8, 6), [2.0, 1.0], 6, noise=1e-3)
+    cp = st.rtpm_asym(st.DenseTensor.from_array(ta), st.RtpmConfig(2, 3, 4, backend, est))
+    w, f = ref.rtpm_asym(ta, 2, 3, 4, 10, 3, 9, backend=backend.value)
+    rel_close(cp.weights, w, 1e-8)
+    for n in range(3):
+        rel_close(cp.factors[n], f[n], 1e-8)
+    cp = st.als(st.DenseTensor.from_array(ta), st.AlsConfig(2, 6, backend, est, 1e-12))
+    w, f = ref.als(ta, 2, 6, 1e-12, 10, 3, 9, backend=backend.value)
+    rel_close(cp.weights, w, 1e-7)
+    for n in range(3):
+        rel_close(cp.factors[n], f[n], 1e-7)
+
+
+def test_rtpm_plain_default_recovers(cuda):
+    """RtpmConfig defaults to the Plain backend, as the reference (cpd.hpp:49-55)."""
+    q = np.linalg.qr(np.random.default_rng(8).standard_normal((30, 3)))[0]
+    t = configs.densify([4.0, 2.0, 1.0], [q, q, q])
+    cp = st.rtpm(st.DenseTensor.from_array(t), st.RtpmConfig(target_rank=3))
+    np.testing.assert_allclose(np.sort(cp.weights.cpu().numpy())[::-1], [4.0, 2.0, 1.0],
+                               atol=1e-6)
+    assert st.residual_norm(st.DenseTensor.from_array(t), cp) < 1e-6
 
 
 # ------------------------------------------------------------ ALS

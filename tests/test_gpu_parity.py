@@ -293,7 +293,7 @@ def test_engine_c3_size(cuda):
 
 
 def test_rtpm_golden(cuda):
-    cfg = st.RtpmConfig(target_rank=2, num_inits=3, num_power_iters=5,
+    cfg = st.RtpmConfig(target_rank=2, num_inits=3, num_power_iters=5, backend=st.SketchBackend.FCS,
                         estimator=st.EstimatorConfig(12, 3, 21))
     cp = st.rtpm(st.DenseTensor.from_array(GOLD["rtpm_t"]), cfg)
     rel_close(cp.weights, GOLD["rtpm_weights"], 1e-8)
@@ -377,7 +377,8 @@ def test_rtpm_c3_per_call(cuda):
     t, lam, V = configs.c3_tensor(c)
     est = st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed)
     cp = st.rtpm(st.DenseTensor.from_array(t),
-                 st.RtpmConfig(c.rank, configs.C3_INITS, configs.C3_ITERS, estimator=est))
+                 st.RtpmConfig(c.rank, configs.C3_INITS, configs.C3_ITERS,
+                                backend=st.SketchBackend.FCS, estimator=est))
     assert np.isfinite(cp.weights.cpu().numpy()).all()
     eng = st.FcsEngine(st.DenseTensor.from_array(t), est)
     oeng = O.FcsEngine(t, c.hash_len, c.sketch_count, c.seed)
@@ -398,7 +399,7 @@ def test_rtpm_well_conditioned_vs_oracle(cuda):
     q, _ = np.linalg.qr(rng.standard_normal((40, 3)))
     t = configs.densify([3.0, 2.0, 1.5], [q, q, q]) + 1e-4 * rng.standard_normal((40, 40, 40))
     est = st.EstimatorConfig(1000, 5, 17)
-    cp = st.rtpm(st.DenseTensor.from_array(t), st.RtpmConfig(3, 5, 10, estimator=est))
+    cp = st.rtpm(st.DenseTensor.from_array(t), st.RtpmConfig(3, 5, 10, st.SketchBackend.FCS, est))
     w, f = O.rtpm(O.FcsEngine(t, 1000, 5, 17), 40, 3, 5, 10, 17)
     rel_close(cp.weights, w, 1e-8)
     rel_close(cp._factors_cm[0].t(), f, 1e-8)
