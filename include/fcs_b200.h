@@ -305,6 +305,18 @@ int st_als(int backend, int dtype, const void* tensor, const size_t* dims, size_
 int st_residual_norm(int dtype, const void* tensor, const size_t* dims, const double* weights,
                      size_t rank, const double* factors, double* out, void* stream);
 
+/* densify(cp) (tensor.cpp:86-115): out (device, prod dims fp64, column-major)
+ * = sum_r w_r u_r^(1) o ... o u_r^(N); factors: HOST array of device I_n x R
+ * column-major matrices, weights device. */
+int st_densify(size_t order, const size_t* dims, size_t rank, const double* weights,
+               const double* const* factors, double* out, void* stream);
+
+/* psnr(reference, estimate) (cpd.cpp:394-403): 10 log10(peak^2 / MSE) with
+ * peak = max |reference|, capped at 99 dB (99 when MSE = 0); n elements of
+ * two device tensors of the same dtype; *out HOST. */
+int st_psnr(int dtype, const void* reference, const void* estimate, size_t n, double* out,
+            void* stream);
+
 /* ------------------------------------ inner products, regression, codecs */
 
 /* Sketched inner product <a, b> of two device tensors of the same shape:

@@ -493,3 +493,13 @@ def inner_once_tables(a: np.ndarray, b: np.ndarray, buckets, signs, hash_lens,
                                        _sz(len(dims)), _ptr(dims), _ptr(bk), _ptr(sg), _ptr(hl),
                                        C.byref(out)))
     return out.value
+
+
+def psnr(a: np.ndarray, b: np.ndarray) -> float:
+    """psnr (cpd.cpp:394-403)."""
+    dims = _dims(a.shape)
+    da = np.ascontiguousarray(np.asarray(a, np.float64).ravel(order="F"))
+    db = np.ascontiguousarray(np.asarray(b, np.float64).ravel(order="F"))
+    out = _d(0)
+    _check(lib().ref_psnr(_ptr(da), _ptr(db), _sz(len(dims)), _ptr(dims), C.byref(out)))
+    return out.value

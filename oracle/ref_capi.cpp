@@ -509,3 +509,11 @@ int ref_inner_once_tables(int ts, const double* a, const double* b, std::size_t 
 }
 
 }  // extern "C"
+
+extern "C" {
+// psnr (cpd.cpp:394-403).
+int ref_psnr(const double* a, const double* b, std::size_t order, const std::size_t* dims,
+             double* out) {
+  return guarded([&] { *out = psnr(make_tensor(a, order, dims), make_tensor(b, order, dims)); });
+}
+}  // extern "C"

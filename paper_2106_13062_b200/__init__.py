@@ -14,7 +14,8 @@ from .sketchtensor import (CpTensor, DenseTensor, EstimatorConfig, HashFamily, H
 from .engine import (AlsConfig, ContractionEngine, CsEngine, FcsEngine, HcsEngine,  # noqa
                      PlainEngine, RtpmConfig, SketchBackend,
                      TsEngine, als, backend_from_name, backend_name, make_contraction_engine,
-                     residual_norm, rtpm, rtpm_asym)
+                     residual_norm, rtpm, rtpm_asym, psnr, densify, rank_one, contract3,
+                     contract3_free, inner)
 
 from .codecs import (KronSketch, compress_contraction, compress_kron, compression_ratio,  # noqa
                      decompress_contraction, decompress_kron, estimate_inner, hash_memory,

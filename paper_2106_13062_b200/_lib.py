@@ -61,6 +61,8 @@ SIGNATURES = {
     "st_rtpm_asym": (i32, [i32, i32, p, p, sz, sz, sz, sz, sz, u64, p, p, p]),
     "st_als": (i32, [i32, i32, p, p, sz, sz, dbl, sz, sz, u64, p, p, p, p]),
     "st_residual_norm": (i32, [i32, p, p, p, sz, p, p, p]),
+    "st_densify": (i32, [sz, p, sz, p, p, p, p]),
+    "st_psnr": (i32, [i32, p, p, sz, p, p]),
     "st_estimate_inner": (i32, [i32, i32, p, p, sz, p, sz, sz, u64, p, p, p]),
     "st_sketch_dots": (i32, [sz, sz, p, p, p, p]),
     "st_regression_forward": (i32, [i32, p, sz, p, sz, p, sz, p, sz, sz, u64, p, p]),

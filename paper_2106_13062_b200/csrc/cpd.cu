@@ -88,6 +88,59 @@ __global__ void residual_final_kernel(const double* __restrict__ part, int n, do
   }
 }
 
+// densify (tensor.cpp:86-115): out[l] = sum_r w_r prod_n U_n[i_n(l), r] for an
+// order-N CP tensor (factors I_n x R column-major), flat column-major l.
+struct DensifyArgs {
+  int order, rank;
+  int dims[ST_MAX_ORDER];
+  const double* factors[ST_MAX_ORDER];
+  const double* weights;
+};
+__global__ void densify_kernel(DensifyArgs a, size_t total, double* __restrict__ out) {
+  for (size_t l = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; l < total;
+       l += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    int idx[ST_MAX_ORDER];
+    size_t rem = l;
+    for (int n = 0; n < a.order; ++n) {
+      idx[n] = static_cast<int>(rem % a.dims[n]);
+      rem /= a.dims[n];
+    }
+    double s = 0.0;
+    for (int r = 0; r < a.rank; ++r) {
+      double p = a.weights[r];
+      for (int n = 0; n < a.order; ++n) p *= a.factors[n][idx[n] + static_cast<size_t>(r) * a.dims[n]];
+      s += p;
+    }
+    out[l] = s;
+  }
+}
+
+// psnr partials (cpd.cpp:394-403): per CTA max |ref| and sum (ref - est)^2.
+template <typename T>
+__global__ void psnr_kernel(const T* __restrict__ ref, const T* __restrict__ est, size_t n,
+                            double* __restrict__ part) {
+  __shared__ double red[32];
+  double mx = 0.0, se = 0.0;
+  for (size_t l = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; l < n;
+       l += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const double r = static_cast<double>(ref[l]), d = r - static_cast<double>(est[l]);
+    mx = fmax(mx, fabs(r));
+    se += d * d;
+  }
+  se = cta_sum(se, red);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  __shared__ double mred[32];
+  if ((threadIdx.x & 31) == 0) mred[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (unsigned w = 0; w < (blockDim.x >> 5); ++w) m = fmax(m, mred[w]);
+    part[2 * blockIdx.x] = m;
+    part[2 * blockIdx.x + 1] = se;
+  }
+}
+
 __global__ void negate_kernel(double* v, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) v[i] = -v[i];
@@ -415,6 +468,59 @@ int st_rtpm_asym(int backend, int dtype, const void* tensor, const size_t* dims,
     if (int rc = st_engine_deflate(e, weight, B[0], B[1], B[2], st)) return rc;
   }
   FCS_CUDA_TRY(cudaStreamSynchronize(st));
+  return ST_OK;
+}
+
+int st_densify(size_t order, const size_t* dims, size_t rank, const double* weights,
+               const double* const* factors, double* out, void* stream) {
+  FCS_CHECK_ARG(order >= 1 && order <= ST_MAX_ORDER, "CpTensor: no factors");
+  DensifyArgs a{};
+  a.order = static_cast<int>(order);
+  a.rank = static_cast<int>(rank);
+  a.weights = weights;
+  size_t total = 1;
+  for (size_t n = 0; n < order; ++n) {
+    FCS_CHECK_ARG(dims[n] > 0, "DenseTensor: zero dimension");
+    a.dims[n] = static_cast<int>(dims[n]);
+    a.factors[n] = factors[n];
+    total *= dims[n];
+  }
+  const unsigned grid = static_cast<unsigned>(std::min<size_t>((total + 255) / 256, 16384));
+  densify_kernel<<<grid, 256, 0, as_stream(stream)>>>(a, total, out);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+int st_psnr(int dtype, const void* reference, const void* estimate, size_t n, double* out,
+            void* stream) {
+  FCS_CHECK_ARG(dtype == ST_F32 || dtype == ST_F64, "psnr: unknown dtype");
+  FCS_CHECK_ARG(n > 0 && out != nullptr, "psnr: empty tensors");
+  cudaStream_t st = as_stream(stream);
+  const int nblk = residual_blocks();
+  double* part = nullptr;
+  FCS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), 2 * nblk * sizeof(double), st));
+  if (dtype == ST_F64)
+    psnr_kernel<double><<<nblk, 256, 0, st>>>(static_cast<const double*>(reference),
+                                              static_cast<const double*>(estimate), n, part);
+  else
+    psnr_kernel<float><<<nblk, 256, 0, st>>>(static_cast<const float*>(reference),
+                                             static_cast<const float*>(estimate), n, part);
+  std::vector<double> h(2 * nblk);
+  const cudaError_t le = cudaGetLastError();
+  const cudaError_t ce =
+      cudaMemcpyAsync(h.data(), part, 2 * nblk * sizeof(double), cudaMemcpyDeviceToHost, st);
+  const cudaError_t se = cudaStreamSynchronize(st);
+  cudaFreeAsync(part, st);
+  FCS_CUDA_TRY(le);
+  FCS_CUDA_TRY(ce);
+  FCS_CUDA_TRY(se);
+  double peak = 0.0, sse = 0.0;
+  for (int b = 0; b < nblk; ++b) {
+    peak = std::max(peak, h[2 * b]);
+    sse += h[2 * b + 1];
+  }
+  const double mse = sse / static_cast<double>(n);
+  *out = mse == 0.0 ? 99.0 : std::min(10.0 * std::log10(peak * peak / mse), 99.0);
   return ST_OK;
 }
 

@@ -332,3 +332,60 @@ def residual_norm(t, cp: CpTensor) -> float:
     _check(L.lib().st_residual_norm(t.st_dtype, _ptr(t.flat), L.size_array(dims), _ptr(w), R,
                                     _ptr(packed), C.byref(out), _stream()))
     return out.value
+
+
+def psnr(reference, estimate) -> float:
+    """psnr (cpd.cpp:394-403): 10 log10(peak^2 / MSE), peak = max|reference|,
+    capped at 99 dB, on the device (st_psnr)."""
+    if not isinstance(reference, DenseTensor):
+        reference = DenseTensor.from_array(reference)
+    if not isinstance(estimate, DenseTensor):
+        estimate = DenseTensor.from_array(estimate)
+    if reference.shape() != estimate.shape():
+        raise ValueError("psnr: shape mismatch")
+    est = estimate.flat.to(reference.flat.dtype).contiguous()
+    out = C.c_double(0.0)
+    _check(L.lib().st_psnr(reference.st_dtype, _ptr(reference.flat), _ptr(est),
+                           reference.size(), C.byref(out), _stream()))
+    return out.value
+
+
+def densify(cp: CpTensor) -> DenseTensor:
+    """densify (tensor.cpp:86-115) on the device (st_densify)."""
+    dims = cp.shape()
+    out = torch.empty(int(np.prod(dims)), dtype=torch.float64, device=_dev())
+    fptrs = (C.c_void_p * len(dims))(*[f.data_ptr() for f in cp._factors_cm])
+    _check(L.lib().st_densify(len(dims), L.size_array(dims), cp.rank(), _ptr(cp.weights), fptrs,
+                              _ptr(out), _stream()))
+    return DenseTensor(dims, out)
+
+
+def rank_one(weight: float, vectors) -> CpTensor:
+    """rank_one (tensor.hpp): weight * v_1 o ... o v_N as a CpTensor."""
+    return CpTensor([weight], [np.asarray(v, np.float64).reshape(-1, 1) if not torch.is_tensor(v)
+                               else v.reshape(-1, 1) for v in vectors])
+
+
+def contract3(t, u, v, w) -> float:
+    """contract3 (tensor.cpp:181-197): T(u, v, w), exact, on the device."""
+    return PlainEngine(_order3(t, "contract3"), EstimatorConfig(0, 0, 0)).uvw(u, v, w)
+
+
+def contract3_free(t, a, b, free_mode: int) -> np.ndarray:
+    """contract3_free (tensor.cpp:199-226): exact T with the identity at free_mode."""
+    return PlainEngine(_order3(t, "contract3_free"), EstimatorConfig(0, 0, 0)).iuv(a, b, free_mode)
+
+
+def inner(a, b) -> float:
+    """inner (tensor.hpp): vec(a)^T vec(b) on the device (fixed-order dot)."""
+    if not isinstance(a, DenseTensor):
+        a = DenseTensor.from_array(a)
+    if not isinstance(b, DenseTensor):
+        b = DenseTensor.from_array(b)
+    if a.shape() != b.shape():
+        raise ValueError("inner: shape mismatch")
+    x = a.flat.to(torch.float64).reshape(1, -1).contiguous()
+    y = b.flat.to(torch.float64).reshape(1, -1).contiguous()
+    out = torch.empty(1, dtype=torch.float64, device=_dev())
+    _check(L.lib().st_sketch_dots(1, x.shape[1], _ptr(x), _ptr(y), _ptr(out), _stream()))
+    return float(out.item())

@@ -296,3 +296,31 @@ def test_golden_rtpm_asym_als(cuda):
     assert abs(st.residual_norm(t, cp) - GOLD["als_residual"][0]) <= 1e-8 * GOLD["als_residual"][0]
     cp = st.als(t, st.AlsConfig(2, 5, TS, est, 1e-12))
     rel_close(cp.weights, GOLD["als_ts_weights"], 1e-8)
+
+
+# ------------------------------------------------------------ tensor utilities
+def test_psnr_densify_contract_inner(cuda):
+    rng = np.random.default_rng(17)
+    a = rng.standard_normal((9, 8, 7))
+    b = a + 0.01 * rng.standard_normal(a.shape)
+    assert abs(st.psnr(a, b) - ref.psnr(a, b)) < 1e-10
+    assert st.psnr(a, a) == ref.psnr(a, a) == 99.0
+    assert abs(st.psnr(a.astype(np.float32), b.astype(np.float32)) -
+               ref.psnr(a.astype(np.float32).astype(np.float64),
+                        b.astype(np.float32).astype(np.float64))) < 1e-4
+    with pytest.raises(ValueError):
+        st.psnr(a, b[:, :, :3])
+    w = rng.standard_normal(3)
+    F = [rng.standard_normal((n, 3)) for n in (5, 4, 3, 2)]
+    dt = st.densify(st.CpTensor(w, F))
+    want = np.einsum("r,ir,jr,kr,lr->ijkl", w, *F)
+    got = dt.flat.cpu().numpy().reshape(dt.shape(), order="F")
+    np.testing.assert_allclose(got, want, rtol=1e-13, atol=1e-13)
+    u, v, x = (rng.standard_normal(n) for n in a.shape)
+    assert abs(st.contract3(a, u, v, x) - np.einsum("ijk,i,j,k->", a, u, v, x)) < 1e-12
+    np.testing.assert_allclose(st.contract3_free(a, u, x, 1), np.einsum("ijk,i,k->j", a, u, x),
+                               rtol=1e-12, atol=1e-12)
+    assert abs(st.inner(a, b) - float((a * b).sum())) < 1e-10
+    r1 = st.rank_one(2.0, [u, v, x])
+    np.testing.assert_allclose(st.densify(r1).flat.cpu().numpy().reshape(a.shape, order="F"),
+                               2.0 * np.einsum("i,j,k->ijk", u, v, x), rtol=1e-13, atol=1e-14)
