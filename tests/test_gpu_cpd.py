@@ -324,3 +324,16 @@ def test_psnr_densify_contract_inner(cuda):
     r1 = st.rank_one(2.0, [u, v, x])
     np.testing.assert_allclose(st.densify(r1).flat.cpu().numpy().reshape(a.shape, order="F"),
                                2.0 * np.einsum("i,j,k->ijk", u, v, x), rtol=1e-13, atol=1e-14)
+
+
+def test_sharded_rtpm_driver_single_process(cuda):
+    """The restart-sharded RTPM driver (dist.sharded_rtpm) on one process with the
+    device engine reproduces st.rtpm (same initial stream, argmax and refinement)."""
+    from paper_2106_13062_b200 import dist as pdist
+    q = np.linalg.qr(np.random.default_rng(23).standard_normal((20, 2)))[0]
+    t = configs.densify([3.0, 1.5], [q, q, q])
+    est = st.EstimatorConfig(200, 3, 5)
+    w, f = pdist.sharded_rtpm(st.FcsEngine(st.DenseTensor.from_array(t), est), 20, 2, 4, 6, 5)
+    cp = st.rtpm(st.DenseTensor.from_array(t), st.RtpmConfig(2, 4, 6, FCS, est))
+    rel_close(w, cp.weights.cpu().numpy(), 1e-9)
+    rel_close(f, cp.factors[0].cpu().numpy(), 1e-9)
