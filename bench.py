@@ -250,7 +250,7 @@ def run_gpu(args):
             "data": "synthetic: seeded SplitMix64/Box-Muller N(0,1) device fill",
             "config": {"workload": "c4: dense FCS 1024x1024x1024 float32, J_n=16384 (J~=49150), "
                                    "D=4", "dims": dims, "hash_len": C4_J, "sketch_count": C4_D,
-                       "composed_len": jt, "parallelism": f"element-shard x{world} + nccl "
+                       "composed_len": jt, "seed": C4_SEED, "parallelism": f"element-shard x{world} + nccl "
                                                          "allreduce" if world > 1 else "single",
                        "l2": "input 4 GiB > L2 126 MB: no flush needed"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -280,79 +280,139 @@ def run_gpu(args):
 
 
 def secondary(x=None):
-    """Configs 2, 3, 5 (and c1) on one GPU: device-resident inputs, CUDA events;
-    plus K1 on the config-4 tensor `x` for D = 1, 2, 4 (the update-throughput
-    picture behind the headline's roofline fraction)."""
+    """Configs 1, 2, 3, 5 on one GPU: device-resident inputs,
+    preallocated outputs and workspaces, the C-ABI calls themselves timed with
+    CUDA events per call, median of >= 10 calls after warm-up; plus K1 on the
+    config-4 tensor `x` for D = 1, 2, 4 (the update-throughput picture behind
+    the headline's roofline fraction)."""
+    import ctypes as C
+
     import torch
 
     import paper_2106_13062_b200 as st
+    from paper_2106_13062_b200 import _lib as L
     from paper_2106_13062_b200 import configs
 
-    def timeit(fn, reps):
-        for _ in range(2):
+    lib = L.lib()
+    stream = torch.cuda.current_stream()
+    sp = C.c_void_p(stream.cuda_stream)
+    peak, _ = hbm_peak()
+
+    def median_ms(fn, reps=12):
+        for _ in range(3):
             fn()
         torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(reps):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(reps)]
+        for a, b in evs:
+            a.record(stream)
             fn()
-        b.record()
+            b.record(stream)
         torch.cuda.synchronize()
-        return a.elapsed_time(b) / reps
+        return statistics.median(a.elapsed_time(b) for a, b in evs)
+
+    def dense_call(t, dims, fams, D, dtype):
+        packed = st.packed_families(fams)
+        lens = fams[0].hash_lens()
+        out = torch.empty((D, fams[0].composed_len()), dtype=torch.float64, device="cuda")
+        dims_a, lens_a = L.size_array(dims), L.size_array(lens)
+        ws_bytes = lib.st_fcs_dense_workspace(dtype, len(dims), dims_a, dims[-1], D, lens_a)
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device="cuda")
+
+        def call():
+            L.check(lib.st_fcs_dense(dtype, C.c_void_p(t.data_ptr()), len(dims), dims_a, 0,
+                                     dims[-1], D, C.c_void_p(packed.data_ptr()), lens_a,
+                                     C.c_void_p(out.data_ptr()), 0, C.c_void_p(ws.data_ptr()),
+                                     ws_bytes, sp))
+        return call
 
     res = {}
     if x is not None:
-        peak, _ = hbm_peak()
-        t4 = st.DenseTensor(list(C4_DIMS), x)
         sweep = []
         for D in (1, 2, 4):
             fams = st.families_for(list(C4_DIMS), st.EstimatorConfig(C4_J, D, C4_SEED))
-            packed = st.packed_families(fams)
-            out = st.fcs_dense_batched(t4, fams, packed=packed)
-            ms = timeit(lambda: st.fcs_dense_batched(t4, fams, packed=packed, out=out), 10)
+            ms = median_ms(dense_call(x, list(C4_DIMS), fams, D, L.ST_F32), 10)
             alg = algorithmic_bytes(x.numel(), C4_DIMS, D, C4_J)
             sweep.append({"D": D, "ms": ms, "elements_per_sec": x.numel() / (ms * 1e-3),
                           "hbm_frac": alg / (ms * 1e-3) / 1e9 / peak,
                           "updates_per_sec": D * x.numel() / (ms * 1e-3)})
         res["c4_family_sweep"] = sweep
+    # c1: dense FCS of 100^3 fp64, D = 1 (the reference's CPU-runnable case)
     c = configs.C1
-    x = st.DenseTensor.from_array(configs.c1_tensor(c))
+    t1 = torch.from_numpy(np.ascontiguousarray(configs.c1_tensor(c).ravel(order="F"))).cuda()
     fams = st.families_for(list(c.dims), st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
-    packed = st.packed_families(fams)
-    ms = timeit(lambda: st.fcs_dense_batched(x, fams, packed=packed), 50)
-    res["c1_dense_fcs"] = {"ms": ms, "elements_per_sec": 1e6 / (ms * 1e-3)}
+    ms = median_ms(dense_call(t1, list(c.dims), fams, c.sketch_count, L.ST_F64))
+    alg = configs.algorithmic_bytes("c1")
+    res["c1_dense_fcs"] = {"ms": ms, "elements_per_sec": t1.numel() / (ms * 1e-3),
+                           "hbm_gbs": alg / (ms * 1e-3) / 1e9, "seed": c.seed}
+    # c2: CP-form FCS, rank 50 400^3, D = 10
     c = configs.C2
     w, fs = configs.c2_cp(c)
     cp = st.CpTensor(w, fs)
     fams = st.families_for(list(c.dims), st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
     packed = st.packed_families(fams)
-    ms = timeit(lambda: st.fcs_cp_batched(cp, fams, packed=packed), 10)
+    dims_a, lens_a = L.size_array(list(c.dims)), L.size_array(fams[0].hash_lens())
+    out2 = torch.empty((c.sketch_count, fams[0].composed_len()), dtype=torch.float64,
+                       device="cuda")
+    ws2 = lib.st_fcs_cp_workspace(3, dims_a, cp.rank(), c.sketch_count, lens_a)
+    wbuf2 = torch.empty(max(ws2, 1), dtype=torch.uint8, device="cuda")
+    fptrs = (C.c_void_p * 3)(*[f.data_ptr() for f in cp._factors_cm])
+
+    def cp_call():
+        L.check(lib.st_fcs_cp(C.c_void_p(cp.weights.data_ptr()), cp.rank(), 3, dims_a, fptrs, 0,
+                              cp.rank(), c.sketch_count, C.c_void_p(packed.data_ptr()), lens_a,
+                              C.c_void_p(out2.data_ptr()), 0, C.c_void_p(wbuf2.data_ptr()), ws2,
+                              sp))
+    ms = median_ms(cp_call)
     res["c2_cp_fcs"] = {"ms": ms, "sketches_per_sec": c.sketch_count / (ms * 1e-3),
+                        "hbm_gbs": configs.algorithmic_bytes("c2") / (ms * 1e-3) / 1e9,
+                        "seed": c.seed,
                         "metric": "CP-FCS sketches/s (D=10 sketches of a rank-50 400^3 CP tensor)"}
+    # c3: one batched T(I,u,u) step (15 restarts x 10 families) and the full RTPM
     c = configs.C3
     t, lam, V = configs.c3_tensor(c)
     dt = st.DenseTensor.from_array(t)
-    eng = st.FcsEngine(dt, st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
+    est = st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed)
+    eng = st.FcsEngine(dt, est)
     U = torch.randn(configs.C3_INITS, 200, dtype=torch.float64, device="cuda")
-    ms_iuv = timeit(lambda: eng.iuv_batch(U, U, 0), 20)
+    Y = torch.empty((configs.C3_INITS, 200), dtype=torch.float64, device="cuda")
+
+    def iuv_call():
+        L.check(lib.st_engine_iuv(eng._h, configs.C3_INITS, C.c_void_p(U.data_ptr()),
+                                  C.c_void_p(U.data_ptr()), 0, C.c_void_p(Y.data_ptr()), 1, sp))
+    ms_iuv = median_ms(iuv_call, 20)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    cpd = st.rtpm(dt, st.RtpmConfig(c.rank, configs.C3_INITS, configs.C3_ITERS, st.SketchBackend.FCS,
-                                    estimator=st.EstimatorConfig(c.hash_len, c.sketch_count,
-                                                                 c.seed)))
+    cpd = st.rtpm(dt, st.RtpmConfig(c.rank, configs.C3_INITS, configs.C3_ITERS,
+                                    st.SketchBackend.FCS, est))
+    torch.cuda.synchronize()
     t_rtpm = time.perf_counter() - t0
     # estimates/s: one batched step gives L restarts x D sketches of T(I,u,u) (median over D
     # gives L estimates). Weights are reported, not scored: at this size the sketch noise
     # dominates and RTPM trajectories are chaotic (DESIGN.md §4).
     res["c3_rtpm"] = {"iuv_step_ms": ms_iuv,
                       "estimates_per_sec": configs.C3_INITS / (ms_iuv * 1e-3),
-                      "rtpm_total_s": t_rtpm,
+                      "step_hbm_gbs": 1517680 / (ms_iuv * 1e-3) / 1e9,
+                      "rtpm_total_s": t_rtpm, "seed": c.seed,
                       "weights": [round(float(x), 6) for x in cpd.weights.cpu().numpy()]}
+    # c5: FCS of A (x) B, 512^2 operands, D = 8 (device-resident operands)
     c = configs.C5
     A, B = configs.c5_matrices(c)
     fams = st.families_for(list(c.dims), st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
-    ms = timeit(lambda: st.fcs_kron(A, B, fams), 10)
-    res["c5_kron"] = {"ms_incl_h2d": ms}
+    packed5 = st.packed_families(fams)
+    lens5 = L.size_array(fams[0].hash_lens())
+    Ad = torch.from_numpy(np.ascontiguousarray(A.ravel(order="F"))).cuda()
+    Bd = torch.from_numpy(np.ascontiguousarray(B.ravel(order="F"))).cuda()
+    out5 = torch.empty((c.sketch_count, fams[0].composed_len()), dtype=torch.float64,
+                       device="cuda")
+
+    def kron_call():
+        L.check(lib.st_fcs_kron(C.c_void_p(Ad.data_ptr()), 512, 512, C.c_void_p(Bd.data_ptr()),
+                                512, 512, c.sketch_count, C.c_void_p(packed5.data_ptr()), lens5,
+                                C.c_void_p(out5.data_ptr()), sp))
+    ms = median_ms(kron_call)
+    res["c5_kron"] = {"ms": ms, "hbm_gbs": configs.algorithmic_bytes("c5") / (ms * 1e-3) / 1e9,
+                      "seed": c.seed}
     return res
 
 

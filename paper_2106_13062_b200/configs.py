@@ -134,6 +134,11 @@ def algorithmic_bytes(cfg_key: str) -> int:
         return int(np.prod(c.dims)) * 4 + c.sketch_count * sum(c.dims) * 5 + c.sketch_count * jt * 4
     if cfg_key == "c1":
         return int(np.prod(c.dims)) * 8 + c.sketch_count * sum(c.dims) * 5 + c.sketch_count * jt * 8
+    if cfg_key == "c2":  # factors + weights + tables + output
+        return 3 * 400 * c.rank * 8 + c.rank * 8 + c.sketch_count * sum(c.dims) * 5 + \
+            c.sketch_count * jt * 8
+    if cfg_key == "c5":  # two 512^2 fp64 operands + tables + output (4J - 3)
+        return 2 * 512 * 512 * 8 + c.sketch_count * sum(c.dims) * 5 + c.sketch_count * jt * 8
     raise KeyError(cfg_key)
 
 

@@ -349,15 +349,27 @@ __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
 }
 
 // Fixed-order fp64 reduction of the chunk partials: out[d][b] (+)= sum_c part[c][d][b].
+// 32 outputs x 32 chunk lanes per CTA: lane y sums chunks y, y + 32, ...
+// (coalesced over the 32 outputs), then the 32 lane sums are added in lane
+// order — a fixed order, with 32x the memory-level parallelism of one thread
+// per output (small tensors have few outputs and many chunks).
 template <typename Tacc>
 __global__ void reduce_partials_kernel(const Tacc* __restrict__ part, uint64_t nchunk,
                                        uint64_t per_chunk, double* __restrict__ out,
                                        int accumulate) {
-  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (i >= per_chunk) return;
-  double acc = accumulate ? out[i] : 0.0;
-  for (uint64_t c = 0; c < nchunk; ++c) acc += static_cast<double>(part[c * per_chunk + i]);
-  out[i] = acc;
+  __shared__ double red[32][33];
+  const uint64_t i = blockIdx.x * 32ull + threadIdx.x;
+  double acc = 0.0;
+  if (i < per_chunk)
+    for (uint64_t c = threadIdx.y; c < nchunk; c += 32)
+      acc += static_cast<double>(part[c * per_chunk + i]);
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && i < per_chunk) {
+    double s = accumulate ? out[i] : 0.0;
+    for (int y = 0; y < 32; ++y) s += red[y][threadIdx.x];
+    out[i] = s;
+  }
 }
 
 // Same for fixed-point partials (flag 0: int32 * 2^-S, flag 1: float bits).
@@ -501,6 +513,12 @@ int make_plan(const DenseArgs& a, Plan* p) {
   const uint64_t resident = static_cast<uint64_t>(per_sm) * di.sm_count;
   uint64_t nchunk = std::max<uint64_t>(1, resident / static_cast<uint64_t>(a.D));
   nchunk = std::min<uint64_t>(nchunk, std::max<uint64_t>(1, a.fibers / 16));
+  // Small tensors: each chunk writes (and the reduction re-reads) a D x J~
+  // partial, so keep the partials to at most the tensor's bytes (config 1:
+  // 592 -> 333 chunks; config 4 is unaffected).
+  const uint64_t elems = a.fibers * a.dims[0];
+  const uint64_t part_per_chunk = static_cast<uint64_t>(a.D) * a.jt * sizeof(Tacc);
+  nchunk = std::min<uint64_t>(nchunk, std::max<uint64_t>(1, elems * sizeof(Tin) / part_per_chunk));
   p->nchunk = nchunk;
   p->part_bytes = nchunk * a.D * static_cast<size_t>(a.jt) * sizeof(Tacc);
   p->ws = align_up(p->part_bytes) + align_up(nchunk * a.D * sizeof(int)) +
@@ -618,8 +636,8 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
   fcs_dense_smem_kernel<Tin, Tacc>
       <<<static_cast<unsigned>(nchunk * a.D), threads, p.smem_bytes, st>>>(a, t, packed, part);
   FCS_CUDA_TRY(cudaGetLastError());
-  reduce_partials_kernel<Tacc><<<ceil_div(out_elems, 256), 256, 0, st>>>(part, nchunk, out_elems,
-                                                                         out, accumulate);
+  reduce_partials_kernel<Tacc><<<ceil_div(out_elems, 32), dim3(32, 32), 0, st>>>(
+      part, nchunk, out_elems, out, accumulate);
   FCS_CUDA_TRY(cudaGetLastError());
   return ST_OK;
 }
