@@ -111,3 +111,28 @@ def test_rtpm_large_hash(cuda):
     w, f = ref.rtpm(t, 2, 3, 5, 5000, 3, 4)
     rel_close(cp.weights, w, 1e-8)
     rel_close(cp.factors[0], f, 1e-8)
+
+
+@pytest.mark.parametrize("n", [12288, 12289, 16, 17, 1])
+def test_plan_boundaries(cuda, n):
+    """Lengths at the one-CTA / two-level boundary and the smallest plans."""
+    rng = np.random.default_rng(n)
+    la = max(1, n // 2)
+    lb = n - la + 1
+    a, b = rng.standard_normal((2, la)), rng.standard_normal((2, lb))
+    got = st.convolve_pairs(torch.from_numpy(a), torch.from_numpy(b))
+    for r in range(2):
+        rel_close(got[r], np.convolve(a[r], b[r]))
+
+
+def test_engine_tiny_hash(cuda):
+    """J = 1 (J~ = 1): every entry lands in bucket 0 for FCS and TS."""
+    rng = np.random.default_rng(2)
+    t = rng.standard_normal((4, 3, 2))
+    u, v, w = (rng.standard_normal(n) for n in t.shape)
+    for backend in (st.SketchBackend.FCS, st.SketchBackend.TS):
+        eng = st.make_contraction_engine(st.DenseTensor.from_array(t), backend,
+                                         st.EstimatorConfig(1, 3, 1))
+        oeng = ref.Engine(t, 1, 3, 1, backend=backend.value)
+        rel_close(eng.iuv(v, w, 0), oeng.iuv(v, w, 0))
+        rel_close(eng.uvw(u, v, w), oeng.uvw(u, v, w))
