@@ -141,47 +141,63 @@ __global__ void fx_scale_kernel(FxStats* st, double n_center) {
 // 1024-element fiber). Greedy: per step, seed with the worst remaining line,
 // then add the line that minimises sum_k max_bank of the group.
 // groups[d][j][q] = line of slot q (lanes 8q..8q+7) at step j.
-__global__ void fx_group_kernel(const uint32_t* __restrict__ packed, uint32_t fam_stride,
-                                uint32_t i0_shift, int nsteps, uint8_t* __restrict__ groups) {
+// One CTA per family, one warp per line: warp l builds line l's histogram and,
+// at every pick, prices adding line l to the current group; thread 0 takes
+// the best (ties: lowest line).
+__global__ void __launch_bounds__(1024) fx_group_kernel(const uint32_t* __restrict__ packed,
+                                                        uint32_t fam_stride, uint32_t i0_shift,
+                                                        int nsteps, uint8_t* __restrict__ groups) {
   __shared__ uint8_t lh[32][4][32];  // [line][k][bank] element counts
-  const int d = blockIdx.x, lane = threadIdx.x;
+  __shared__ int h[4][32];           // current group's counts
+  __shared__ int cost[32];
+  __shared__ uint32_t used;
+  const int d = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t* tab = packed + static_cast<uint64_t>(d) * fam_stride + i0_shift;
   const int nlines = 4 * nsteps;
-  for (int l = 0; l < nlines; ++l) {
-    const uint32_t bank = __ldg(tab + 32 * l + lane) & 31u;  // element t = lane, k = t & 3
+  if (w < nlines) {
+    const uint32_t bank = __ldg(tab + 32 * w + lane) & 31u;  // element t = lane, k = t & 3
+#pragma unroll
     for (int k = 0; k < 4; ++k) {
-      // count of elements t = k (mod 4) of line l that land in bank `lane`
-      int cnt = 0;
+      int cnt = 0;  // elements t = k (mod 4) of line w that land in bank `lane`
+#pragma unroll
       for (int t = k; t < 32; t += 4) cnt += (__shfl_sync(0xffffffffu, bank, t) == static_cast<uint32_t>(lane));
-      lh[l][k][lane] = static_cast<uint8_t>(cnt);
+      lh[w][k][lane] = static_cast<uint8_t>(cnt);
     }
   }
-  __syncwarp();
-  auto wmax = [](int v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-  };
-  uint32_t used = 0;
+  if (threadIdx.x == 0) used = 0;
   for (int j = 0; j < nsteps; ++j) {
-    int h[4] = {0, 0, 0, 0};
+    if (threadIdx.x < 128) h[threadIdx.x >> 5][lane] = 0;
+    __syncthreads();
     for (int pick = 0; pick < 4; ++pick) {
-      int best = -1, best_cost = 1 << 30;
-      for (int l = 0; l < nlines; ++l) {
-        if (used >> l & 1u) continue;
-        int cost = 0;
+      if (w < nlines) {
+        int c = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) cost += wmax(h[k] + lh[l][k][lane]);
-        // the first pick seeds the group with the worst line (largest self cost)
-        if (pick == 0 ? (best < 0 || cost > -best_cost) : cost < best_cost) {
-          best = l;
-          best_cost = pick == 0 ? -cost : cost;
+        for (int k = 0; k < 4; ++k) {
+          int v = h[k][lane] + lh[w][k][lane];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+          c += v;
+        }
+        if (lane == 0) cost[w] = c;
+      }
+      __syncthreads();
+      if (w == 0) {
+        // pick 0 seeds the group with the worst remaining line (largest self
+        // cost), later picks add the line that minimises sum_k max_bank;
+        // warp argmin over key = (signed cost, line): ties go to the lowest line
+        const bool ok = lane < nlines && !(used >> lane & 1u);
+        int key = ok ? ((pick == 0 ? 4096 - cost[lane] : cost[lane]) << 5) | lane : 0x7fffffff;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, o));
+        const int b = key & 31;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) h[k][lane] += lh[b][k][lane];  // warp 0 owns h
+        if (lane == 0) {
+          used |= 1u << b;
+          groups[(static_cast<size_t>(d) * nsteps + j) * 4 + pick] = static_cast<uint8_t>(b);
         }
       }
-      used |= 1u << best;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) h[k] += lh[best][k][lane];
-      if (lane == 0) groups[(static_cast<size_t>(d) * nsteps + j) * 4 + pick] = static_cast<uint8_t>(best);
+      __syncthreads();
     }
   }
 }
@@ -614,7 +630,8 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
       groups = reinterpret_cast<uint8_t*>(base + align_up(p.part_bytes) +
                                           align_up(p.nchunk * a.D * sizeof(int)) +
                                           align_up(sizeof(FxStats)));
-      fx_group_kernel<<<a.D, 32, 0, st>>>(packed, a.fam_stride, a.i0_shift, nv_full, groups);
+      fx_group_kernel<<<a.D, 32 * 4 * nv_full, 0, st>>>(packed, a.fam_stride, a.i0_shift, nv_full,
+                                                       groups);
       FCS_CUDA_TRY(cudaGetLastError());
     }
     fx_kernel(p.nv, p.group)<<<static_cast<unsigned>(nchunk * a.D), p.threads, p.smem_bytes, st>>>(
