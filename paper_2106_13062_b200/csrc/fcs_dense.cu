@@ -25,6 +25,15 @@
 #include "dense_common.cuh"
 
 namespace fcs {
+// Streaming 16-byte load that does not allocate in L1: the tensor is read
+// once per CTA, and L1 shares its SRAM and data pipe with the shared-memory
+// sketch and its atomics (config 4: 2.47 -> 2.33 ms vs __ldg, 2.50 ms __ldcs).
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
 
 // Sampled statistics of the input and the fixed-point exponent derived from them.
 struct FxStats {
@@ -277,11 +286,11 @@ __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
     const float4* src = reinterpret_cast<const float4*>(t + fib * i0n);
     if constexpr (kMapped) {
 #pragma unroll
-      for (int j = 0; j < NV; ++j) dst[j] = __ldcs(src + ((vmap[j / 4] >> (8 * (j % 4))) & 0xffu));
+      for (int j = 0; j < NV; ++j) dst[j] = ld_stream(src + ((vmap[j / 4] >> (8 * (j % 4))) & 0xffu));
     } else {
 #pragma unroll
       for (int j = 0; j < NV; ++j)
-        if (vbase + lane + 32 * j < nvec) dst[j] = __ldcs(src + vbase + lane + 32 * j);
+        if (vbase + lane + 32 * j < nvec) dst[j] = ld_stream(src + vbase + lane + 32 * j);
     }
   };
   uint64_t f = f_begin + warp;

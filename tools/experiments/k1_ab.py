@@ -13,6 +13,8 @@ from paper_2106_13062_b200 import _lib as L  # noqa: E402
 dims = [1024, 1024, 1024]
 n = 1 << 30
 x = torch.empty(n, dtype=torch.float32, device="cuda")
+if os.environ.get("K1_LIB"):
+    L.LIB_PATH = os.environ["K1_LIB"]
 lib = L.lib()
 L.check(lib.st_device_gaussian(L.ST_F32, 4, n, C.c_void_p(x.data_ptr()), None))
 D = int(sys.argv[2]) if len(sys.argv) > 2 else 4
