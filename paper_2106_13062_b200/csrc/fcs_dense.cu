@@ -93,9 +93,13 @@ __global__ void __launch_bounds__(1024) fcs_dense_smem_kernel(DenseArgs a,
   for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) dst[b] = sk[b];
 }
 
-// Sampled max|x|, sum and sum of squares over up to `nsample` evenly spaced fibers.
+// Sampled max|x|, sum and sum of squares over up to `nsample` evenly spaced
+// fibers: one fiber per CTA, a block reduction, then one set of global
+// atomics per CTA (per-warp atomics on four words serialise at L2).
 __global__ void fx_sample_kernel(DenseArgs a, const float* __restrict__ t, uint64_t nsample,
                                  FxStats* __restrict__ st) {
+  __shared__ float smx[32];
+  __shared__ double ss[32], ss2[32], scnt[32];
   const uint32_t i0n = a.dims[0];
   float mx = 0.f;
   double s = 0.0, s2 = 0.0, cnt = 0.0;
@@ -116,7 +120,21 @@ __global__ void fx_sample_kernel(DenseArgs a, const float* __restrict__ t, uint6
     s2 += __shfl_xor_sync(0xffffffffu, s2, o);
     cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
   }
+  const int w = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) {
+    smx[w] = mx;
+    ss[w] = s;
+    ss2[w] = s2;
+    scnt[w] = cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (unsigned q = 1; q < (blockDim.x >> 5); ++q) {
+      mx = fmaxf(mx, smx[q]);
+      s += ss[q];
+      s2 += ss2[q];
+      cnt += scnt[q];
+    }
     atomicMax(&st->maxbits, __float_as_uint(mx));
     atomicAdd(&st->sum, s);
     atomicAdd(&st->sumsq, s2);
@@ -626,7 +644,7 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
                                              align_up(p.nchunk * a.D * sizeof(int)));
     FCS_CUDA_TRY(cudaMemsetAsync(stats, 0, sizeof(FxStats), st));
     const uint64_t nsample = std::min<uint64_t>(a.fibers, 2048);
-    fx_sample_kernel<<<static_cast<unsigned>(std::min<uint64_t>(nsample, 296)), 256, 0, st>>>(
+    fx_sample_kernel<<<static_cast<unsigned>(nsample), 256, 0, st>>>(
         a, reinterpret_cast<const float*>(t), nsample, stats);
     FCS_CUDA_TRY(cudaGetLastError());
     const double per_cta = static_cast<double>(a.fibers_per_chunk) * a.dims[0];
