@@ -503,3 +503,26 @@ def psnr(a: np.ndarray, b: np.ndarray) -> float:
     out = _d(0)
     _check(lib().ref_psnr(_ptr(da), _ptr(db), _sz(len(dims)), _ptr(dims), C.byref(out)))
     return out.value
+
+
+def mode_unfold(t: np.ndarray, mode: int) -> np.ndarray:
+    """mode_unfold (tensor.cpp:117-136)."""
+    dims = _dims(t.shape)
+    data = np.ascontiguousarray(np.asarray(t, np.float64).ravel(order="F"))
+    n = int(dims[mode])
+    out = np.empty(t.size, np.float64)
+    _check(lib().ref_mode_unfold(_ptr(data), _sz(len(dims)), _ptr(dims), _sz(mode), _ptr(out)))
+    return out.reshape((n, t.size // n), order="F")
+
+
+def contract_pair(a: np.ndarray, b: np.ndarray, ma: int, mb: int) -> np.ndarray:
+    """contract_pair (tensor.cpp:238-261); returns the result as an N-d array."""
+    da, db = _dims(a.shape), _dims(b.shape)
+    xa = np.ascontiguousarray(np.asarray(a, np.float64).ravel(order="F"))
+    xb = np.ascontiguousarray(np.asarray(b, np.float64).ravel(order="F"))
+    shape = [int(x) for n, x in enumerate(da) if n != ma] + [int(x) for n, x in enumerate(db)
+                                                               if n != mb]
+    out = np.empty(int(np.prod(shape)), np.float64)
+    _check(lib().ref_contract_pair(_ptr(xa), _sz(len(da)), _ptr(da), _ptr(xb), _sz(len(db)),
+                                   _ptr(db), _sz(ma), _sz(mb), _ptr(out)))
+    return out.reshape(shape, order="F")

@@ -517,3 +517,25 @@ int ref_psnr(const double* a, const double* b, std::size_t order, const std::siz
   return guarded([&] { *out = psnr(make_tensor(a, order, dims), make_tensor(b, order, dims)); });
 }
 }  // extern "C"
+
+extern "C" {
+// mode_unfold (tensor.cpp:117-136): out is dims[mode] x (size / dims[mode]) column-major.
+int ref_mode_unfold(const double* data, std::size_t order, const std::size_t* dims,
+                    std::size_t mode, double* out) {
+  return guarded([&] {
+    Eigen::MatrixXd m = mode_unfold(make_tensor(data, order, dims), mode);
+    std::memcpy(out, m.data(), sizeof(double) * m.size());
+  });
+}
+
+// contract_pair (tensor.cpp:238-261): result data (column-major) of size
+// prod(a rest) * prod(b rest).
+int ref_contract_pair(const double* a, std::size_t oa, const std::size_t* da, const double* b,
+                      std::size_t ob, const std::size_t* db, std::size_t ma, std::size_t mb,
+                      double* out) {
+  return guarded([&] {
+    DenseTensor r = contract_pair(make_tensor(a, oa, da), make_tensor(b, ob, db), ma, mb);
+    std::memcpy(out, r.data().data(), sizeof(double) * r.size());
+  });
+}
+}  // extern "C"

@@ -15,7 +15,8 @@ from .engine import (AlsConfig, ContractionEngine, CsEngine, FcsEngine, HcsEngin
                      PlainEngine, RtpmConfig, SketchBackend,
                      TsEngine, als, backend_from_name, backend_name, make_contraction_engine,
                      residual_norm, rtpm, rtpm_asym, psnr, densify, rank_one, contract3,
-                     contract3_free, inner)
+                     contract3_free, inner, mode_unfold, mode_fold, contract_pair, kron,
+                     tensor_from_matrix)
 
 from .codecs import (KronSketch, compress_contraction, compress_kron, compression_ratio,  # noqa
                      decompress_contraction, decompress_kron, estimate_inner, hash_memory,

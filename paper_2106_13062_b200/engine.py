@@ -389,3 +389,72 @@ def inner(a, b) -> float:
     out = torch.empty(1, dtype=torch.float64, device=_dev())
     _check(L.lib().st_sketch_dots(1, x.shape[1], _ptr(x), _ptr(y), _ptr(out), _stream()))
     return float(out.item())
+
+
+# ------------------------------------------------ tensor utilities (tensor.hpp)
+def _dense_from(t) -> DenseTensor:
+    return t if isinstance(t, DenseTensor) else DenseTensor.from_array(t)
+
+
+def mode_unfold(t, mode: int) -> torch.Tensor:
+    """mode_unfold (tensor.cpp:117-136): the I_mode x prod_{m != mode} I_m
+    matricization, columns in the flat order with mode `mode` removed; a device
+    tensor (row/column indices as in the reference's Eigen matrix)."""
+    t = _dense_from(t)
+    dims = t.shape()
+    if mode >= len(dims):
+        raise ValueError("mode_unfold: mode out of range")
+    inner = int(np.prod(dims[:mode], dtype=np.int64))
+    n = dims[mode]
+    outer = t.size() // (inner * n)
+    # flat = (o * n + i) * inner + k  ->  M[i, o * inner + k]
+    return t.flat.to(torch.float64).reshape(outer, n, inner).permute(1, 0, 2).reshape(n, -1)
+
+
+def mode_fold(m, shape, mode: int) -> DenseTensor:
+    """mode_fold (tensor.cpp:138-160): inverse of mode_unfold for `shape`."""
+    shape = [int(s) for s in shape]
+    if mode >= len(shape):
+        raise ValueError("mode_fold: mode out of range")
+    m = torch.as_tensor(m if torch.is_tensor(m) else np.asarray(m, np.float64),
+                        dtype=torch.float64).to(_dev())
+    inner = int(np.prod(shape[:mode], dtype=np.int64))
+    n = shape[mode]
+    total = int(np.prod(shape, dtype=np.int64))
+    if tuple(m.shape) != (n, total // n):
+        raise ValueError("mode_fold: matrix does not match shape")
+    outer = total // (inner * n)
+    flat = m.reshape(n, outer, inner).permute(1, 0, 2).reshape(-1).contiguous()
+    return DenseTensor(shape, flat)
+
+
+def contract_pair(a, b, mode_a: int, mode_b: int) -> DenseTensor:
+    """contract_pair (tensor.cpp:238-261): contraction of a's mode_a with b's
+    mode_b, result modes a-rest then b-rest (one device GEMM)."""
+    a, b = _dense_from(a), _dense_from(b)
+    if mode_a >= a.order() or mode_b >= b.order():
+        raise ValueError("contract_pair: mode out of range")
+    if a.shape()[mode_a] != b.shape()[mode_b]:
+        raise ValueError("contract_pair: contracted dimensions differ")
+    if a.order() + b.order() < 3:
+        raise ValueError("contract_pair: result would have no modes")
+    prod = mode_unfold(a, mode_a).t() @ mode_unfold(b, mode_b)  # a-rest x b-rest
+    shape = [d for n, d in enumerate(a.shape()) if n != mode_a] + \
+        [d for n, d in enumerate(b.shape()) if n != mode_b]
+    return DenseTensor(shape, prod.t().contiguous().reshape(-1))  # column-major flat
+
+
+def kron(a, b) -> torch.Tensor:
+    """kron (tensor.cpp:228-236): Kronecker product of two matrices (device)."""
+    ta = torch.as_tensor(a if torch.is_tensor(a) else np.asarray(a, np.float64),
+                         dtype=torch.float64).to(_dev())
+    tb = torch.as_tensor(b if torch.is_tensor(b) else np.asarray(b, np.float64),
+                         dtype=torch.float64).to(_dev())
+    return torch.kron(ta, tb)
+
+
+def tensor_from_matrix(m) -> DenseTensor:
+    """tensor_from_matrix (tensor.hpp): order-2 tensor, column-major copy."""
+    tm = torch.as_tensor(m if torch.is_tensor(m) else np.asarray(m, np.float64),
+                         dtype=torch.float64)
+    return DenseTensor(list(tm.shape), tm.t().contiguous().reshape(-1))

@@ -337,3 +337,31 @@ def test_sharded_rtpm_driver_single_process(cuda):
     cp = st.rtpm(st.DenseTensor.from_array(t), st.RtpmConfig(2, 4, 6, FCS, est))
     rel_close(w, cp.weights.cpu().numpy(), 1e-9)
     rel_close(f, cp.factors[0].cpu().numpy(), 1e-9)
+
+
+def test_tensor_layout_utilities(cuda):
+    rng = np.random.default_rng(29)
+    a = rng.standard_normal((3, 4, 5))
+    b = rng.standard_normal((5, 2, 3))
+    for m in range(3):
+        np.testing.assert_array_equal(st.mode_unfold(a, m).cpu().numpy(), ref.mode_unfold(a, m))
+        back = st.mode_fold(st.mode_unfold(a, m), a.shape, m)
+        np.testing.assert_array_equal(back.flat.cpu().numpy(), a.ravel(order="F"))
+    got = st.contract_pair(a, b, 2, 0)
+    want = ref.contract_pair(a, b, 2, 0)
+    assert got.shape() == list(want.shape)
+    np.testing.assert_allclose(got.flat.cpu().numpy(), want.ravel(order="F"), rtol=1e-12,
+                               atol=1e-12)
+    got = st.contract_pair(a, b, 0, 2)
+    np.testing.assert_allclose(got.flat.cpu().numpy(),
+                               ref.contract_pair(a, b, 0, 2).ravel(order="F"), rtol=1e-12,
+                               atol=1e-12)
+    x, y = rng.standard_normal((3, 4)), rng.standard_normal((2, 5))
+    np.testing.assert_allclose(st.kron(x, y).cpu().numpy(), ref.kron(x, y), rtol=1e-15)
+    tm = st.tensor_from_matrix(x)
+    assert tm.shape() == [3, 4]
+    np.testing.assert_array_equal(tm.flat.cpu().numpy(), x.ravel(order="F"))
+    with pytest.raises(ValueError):
+        st.contract_pair(a, b, 1, 0)
+    with pytest.raises(ValueError):
+        st.mode_unfold(a, 3)
