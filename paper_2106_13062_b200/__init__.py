@@ -10,7 +10,7 @@ from .sketchtensor import (CpTensor, DenseTensor, EstimatorConfig, HashFamily, H
                            cs_sketch_columns,
                            families_for, family_seed, fcs_cp_batched, fcs_dense_batched,
                            fcs_kron, fcs_sketch, hcs_sketch, median_reduce, packed_families,
-                           ts_sketch)
+                           ts_sketch, dft, idft_real, fft_convolve)
 from .engine import (AlsConfig, ContractionEngine, CsEngine, FcsEngine, HcsEngine,  # noqa
                      PlainEngine, RtpmConfig, SketchBackend,
                      TsEngine, als, backend_from_name, backend_name, make_contraction_engine,

@@ -531,3 +531,53 @@ def median_reduce(values):
     s = np.sort(v, axis=0)
     n = s.shape[0]
     return s[n // 2] if n % 2 else 0.5 * (s[n // 2 - 1] + s[n // 2])
+
+
+# ------------------------------------------------------------------ fft.hpp
+def dft(x, n: int) -> torch.Tensor:
+    """dft (fft.cpp:42-51): the n-point complex DFT of x zero-padded (or
+    truncated) to n, exact length. A utility of the reference's public API;
+    the library's spectral paths use their own padded transforms (fft.cuh), so
+    this one is a cuFFT call through torch."""
+    if n == 0:
+        raise ValueError("dft: zero length")
+    v = torch.as_tensor(x if torch.is_tensor(x) else np.asarray(x, np.float64),
+                        dtype=torch.float64).reshape(-1).to(_dev())
+    buf = torch.zeros(n, dtype=torch.float64, device=_dev())
+    m = min(n, v.numel())
+    buf[:m] = v[:m]
+    return torch.fft.fft(buf)
+
+
+def idft_real(spectrum) -> torch.Tensor:
+    """idft_real (fft.cpp:53-73): real part of the normalised inverse DFT;
+    RuntimeError when the imaginary residue exceeds 1e-9 of the real norm
+    (+1e-12), as the reference."""
+    s = torch.as_tensor(spectrum if torch.is_tensor(spectrum) else np.asarray(spectrum),
+                        dtype=torch.complex128).reshape(-1).to(_dev())
+    if s.numel() == 0:
+        raise ValueError("idft_real: zero length")
+    z = torch.fft.ifft(s)
+    re, im = z.real, z.imag
+    if float(torch.linalg.norm(im)) > 1e-9 * float(torch.linalg.norm(re)) + 1e-12:
+        raise RuntimeError("idft_real: inverse transform is not real")
+    return re.contiguous()
+
+
+def fft_convolve(inputs, n: int) -> torch.Tensor:
+    """fft_convolve (fft.cpp:75-84): circular convolution at length n of the
+    inputs truncated / zero-padded to n — computed as the linear convolution
+    (the library's shared-memory FFT, st_convolve_pairs) folded mod n."""
+    if len(inputs) == 0:
+        raise ValueError("fft_convolve: no inputs")
+    if n == 0:
+        raise ValueError("dft: zero length")
+    vs = [torch.as_tensor(x if torch.is_tensor(x) else np.asarray(x, np.float64),
+                          dtype=torch.float64).reshape(-1)[:n].to(_dev()) for x in inputs]
+    acc = vs[0] if vs[0].numel() else torch.zeros(1, dtype=torch.float64, device=_dev())
+    for v in vs[1:]:
+        v = v if v.numel() else torch.zeros(1, dtype=torch.float64, device=_dev())
+        acc = convolve_pairs(acc.reshape(1, -1), v.reshape(1, -1))[0]
+    out = torch.zeros(n, dtype=torch.float64, device=_dev())
+    idx = torch.arange(acc.numel(), device=_dev()) % n
+    return out.index_add_(0, idx, acc)

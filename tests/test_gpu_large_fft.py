@@ -136,3 +136,26 @@ def test_engine_tiny_hash(cuda):
         oeng = ref.Engine(t, 1, 3, 1, backend=backend.value)
         rel_close(eng.iuv(v, w, 0), oeng.iuv(v, w, 0))
         rel_close(eng.uvw(u, v, w), oeng.uvw(u, v, w))
+
+
+def test_fft_hpp_utilities(cuda):
+    """dft / idft_real / fft_convolve (fft.cpp:42-84) vs the reference, including
+    circular wrap (n shorter than the linear length) and truncation."""
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(37)
+    for n in (37, 50, 20, 2998):
+        got = st.dft(x, n).cpu().numpy()
+        want = ref.dft(x, n)
+        assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+        back = st.idft_real(st.dft(x, n)).cpu().numpy()
+        np.testing.assert_allclose(back[:min(n, 37)], x[:min(n, 37)], atol=1e-12)
+    with pytest.raises(RuntimeError):
+        st.idft_real(np.array([1.0, 1j, 0.0]))
+    with pytest.raises(ValueError):
+        st.dft(x, 0)
+    a, b, c = rng.standard_normal(30), rng.standard_normal(20), rng.standard_normal(9)
+    for n in (56, 40, 17, 100):
+        rel_close(st.fft_convolve([a, b, c], n), ref.fft_convolve([a, b, c], n))
+    rel_close(st.fft_convolve([a], 30), ref.fft_convolve([a], 30))
+    with pytest.raises(ValueError):
+        st.fft_convolve([], 4)
