@@ -257,9 +257,9 @@ def run_gpu(args):
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_kind": peak_kind, "kernel_ms": k_ms,
                          "algorithmic_bytes_per_launch": alg,
-                         "kernel": "fcs_dense_fx_kernel<8> (+ fx_sample, fx_scale, reduce_fx)"},
+                         "kernel": "fcs_dense_fx_kernel<8> (+ fx_sample, fx_scale, fx_group, reduce_fx)"},
             "e2e": e2e,
-            "gpu_launches": 4 * args.steps,  # sample, scale, fx scatter, reduce per step
+            "gpu_launches": 5 * args.steps,  # sample, scale, group, fx scatter, reduce per step
             "clocks": clk.summary(),
         }
     if world == 1 and not args.no_secondary:

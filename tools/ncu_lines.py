@@ -21,12 +21,19 @@ LIB = os.path.join(ROOT, "paper_2106_13062_b200", "_lib", "libfcs_b200.so")
 
 
 def main(rep, kname, top=30):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                         capture_output=True, text=True).stdout
+    raw = subprocess.run(["ncu", "-i", rep, "-k", "regex:" + kname, "--page", "source", "--csv",
+                          "--print-source", "sass"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr = rows[1]
     iw = hdr.index("Warp Stall Sampling (All Samples)")
-    samples = [float(r[iw] or 0) for r in rows[2:] if len(r) == len(hdr)]
+    samples = []
+    for r in rows[2:]:
+        if len(r) != len(hdr):
+            continue
+        try:
+            samples.append(float(r[iw] or 0))
+        except ValueError:  # a repeated header (several kernels in the report)
+            break
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", LIB], cwd=tmp, capture_output=True)
     lines = None
