@@ -240,7 +240,7 @@ int st_estimate_inner(int kind, int dtype, const void* a, const void* b, size_t 
   FCS_CHECK_ARG(order >= 1 && order <= ST_MAX_ORDER, "fcs_sketch: unsupported tensor order");
   FCS_CHECK_ARG(hash_len > 0 && sketch_count > 0,
                 "EstimatorConfig: hash_len and sketch_count must be >= 1");
-  FCS_CHECK_ARG(sketch_count <= 64, "median_reduce: at most 64 sketches supported");
+  FCS_CHECK_ARG(sketch_count >= 1, "median_reduce: empty input");
   size_t sum_dims = 0;
   for (size_t n = 0; n < order; ++n) {
     FCS_CHECK_ARG(dims[n] > 0, "HashPair: dimensions must be positive");
@@ -307,7 +307,7 @@ int st_regression_forward(int dtype, const void* x, size_t batch, const void* w,
   FCS_CHECK_ARG(order >= 1 && order < ST_MAX_ORDER, "fcs_sketch: unsupported tensor order");
   FCS_CHECK_ARG(hash_len > 0 && sketch_count > 0,
                 "EstimatorConfig: hash_len and sketch_count must be >= 1");
-  FCS_CHECK_ARG(sketch_count <= 64, "median_reduce: at most 64 sketches supported");
+  FCS_CHECK_ARG(sketch_count >= 1, "median_reduce: empty input");
   if (batch == 0 || classes == 0) return ST_OK;
   size_t sum_dims = 0;
   for (size_t n = 0; n < order; ++n) {

@@ -383,6 +383,26 @@ __global__ void median_kernel(const double* __restrict__ est, int batch, int D, 
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= batch * len) return;
   const int b = idx / len, i = idx - b * len;
+  const double* col = est + static_cast<size_t>(b) * D * len + i;  // stride len
+  if (D > 64) {
+    // rank selection without storage (O(D^2)): x_k is the m-th order
+    // statistic iff #less <= m < #less + #equal (std::sort order for finite values)
+    auto order_stat = [&](int m) {
+      for (int k = 0; k < D; ++k) {
+        const double x = col[static_cast<size_t>(k) * len];
+        int less = 0, eq = 0;
+        for (int j = 0; j < D; ++j) {
+          const double y = col[static_cast<size_t>(j) * len];
+          less += y < x;
+          eq += y == x;
+        }
+        if (less <= m && m < less + eq) return x;
+      }
+      return col[0];  // non-finite input: no consistent order
+    };
+    out[idx] = (D & 1) ? order_stat(D / 2) : 0.5 * (order_stat(D / 2 - 1) + order_stat(D / 2));
+    return;
+  }
   double v[64];
   for (int d = 0; d < D; ++d) {
     const double x = est[(static_cast<size_t>(b) * D + d) * len + i];
@@ -557,7 +577,7 @@ int launch_deflate(const FftPlan& pl, const EngArgs& e, double weight, const dou
 }
 
 int launch_median(const double* est, int batch, int D, int len, double* out, cudaStream_t st) {
-  if (D > 64) return fail(ST_EINVAL, "median_reduce: at most 64 sketches supported");
+  FCS_CHECK_ARG(D >= 1, "median_reduce: empty input");
   const int n = batch * len;
   if (n == 0) return ST_OK;
   median_kernel<<<ceil_div(n, 128), 128, 0, st>>>(est, batch, D, len, out);

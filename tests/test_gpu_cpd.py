@@ -365,3 +365,17 @@ def test_tensor_layout_utilities(cuda):
         st.contract_pair(a, b, 1, 0)
     with pytest.raises(ValueError):
         st.mode_unfold(a, 3)
+
+
+def test_engine_many_sketches(cuda):
+    """D > 64 families: the median takes the rank-selection path (no storage)."""
+    rng = np.random.default_rng(31)
+    t = rng.standard_normal((8, 7, 6))
+    for D in (65, 80):
+        eng = st.FcsEngine(st.DenseTensor.from_array(t), st.EstimatorConfig(9, D, 4))
+        oeng = ref.Engine(t, 9, D, 4)
+        u, v, w = (rng.standard_normal(n) for n in t.shape)
+        rel_close(eng.iuv(v, w, 0), oeng.iuv(v, w, 0), 1e-10)
+        rel_close(eng.uvw(u, v, w), oeng.uvw(u, v, w), 1e-10)
+        got, est = st.estimate_inner(t, t, st.EstimatorConfig(9, D, 4), return_estimates=True)
+        assert abs(got - ref.estimate_inner(t, t, 9, D, 4)) <= 1e-10 * abs(got)
