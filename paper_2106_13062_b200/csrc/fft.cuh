@@ -68,6 +68,49 @@ __device__ __forceinline__ double2 twiddle(const double2* tw, int hi_off, uint32
   return cmul(tw[e & ((1u << kTwLoBits) - 1)], tw[hi_off + (e >> kTwLoBits)]);
 }
 
+// x[r] *= w^r, r = 1..R-1, for one butterfly from w = w^1 with powers by a
+// product chain instead of R - 1 table lookups (each two shared-memory loads
+// and a complex product): w2 = w w, w4 = w2 w2, w8 = w4 w4, then for r < 8
+// t_r (at most two products of w, w2, w4) scales x[r] and w8 t_r scales
+// x[r + 8], so only a handful of twiddles are live at a time. Relative error
+// a few ulp beyond the table's, far inside the fp64 FFT's own error budget.
+template <int R, int NB>
+__device__ __forceinline__ void apply_twiddles(double2 (*x)[R], double2 w) {
+  auto mul = [&](int r, double2 t) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) x[b][r] = cmul(x[b][r], t);
+  };
+  mul(1, w);
+  if constexpr (R == 3) mul(2, cmul(w, w));
+  if constexpr (R >= 4) {
+    const double2 w2 = cmul(w, w);
+    const double2 w3 = cmul(w2, w);
+    mul(2, w2);
+    mul(3, w3);
+    if constexpr (R >= 8) {
+      const double2 w4 = cmul(w2, w2);
+      const double2 w5 = cmul(w4, w);
+      const double2 w6 = cmul(w4, w2);
+      const double2 w7 = cmul(w4, w3);
+      mul(4, w4);
+      mul(5, w5);
+      mul(6, w6);
+      mul(7, w7);
+      if constexpr (R == 16) {
+        const double2 w8 = cmul(w4, w4);
+        mul(8, w8);
+        mul(9, cmul(w8, w));
+        mul(10, cmul(w8, w2));
+        mul(11, cmul(w8, w3));
+        mul(12, cmul(w8, w4));
+        mul(13, cmul(w8, w5));
+        mul(14, cmul(w8, w6));
+        mul(15, cmul(w8, w7));
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------ in-register DFTs
 // cos(2 pi k / 16); sin(2 pi k / 16) = cos16(k - 4). Folds to constants once
 // the butterfly loops are unrolled.
@@ -168,26 +211,19 @@ __device__ __forceinline__ void fft_pass(double2* buf, const double2* tw, int hi
     const int blk = b / stride;
     const int j = b - blk * stride;
     const int base = blk * L + j;
-    double2 x[R];
+    double2 x[1][R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) x[r] = buf[swz(base + r * stride)];
+    for (int r = 0; r < R; ++r) x[0][r] = buf[swz(base + r * stride)];
     if (kForward) {
-      RegDft<R>::run(x, -1.0);
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        const uint32_t e = static_cast<uint32_t>(j * r) * tw_scale;
-        if (e) x[r] = cmul(x[r], twiddle(tw, hi_off, e));
-      }
+      RegDft<R>::run(x[0], -1.0);
+      if (j) apply_twiddles<R, 1>(x, twiddle(tw, hi_off, static_cast<uint32_t>(j) * tw_scale));
     } else {
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        const uint32_t e = static_cast<uint32_t>(j * r) * tw_scale;
-        if (e) x[r] = cmul(x[r], cconj(twiddle(tw, hi_off, e)));
-      }
-      RegDft<R>::run(x, +1.0);
+      if (j)
+        apply_twiddles<R, 1>(x, cconj(twiddle(tw, hi_off, static_cast<uint32_t>(j) * tw_scale)));
+      RegDft<R>::run(x[0], +1.0);
     }
 #pragma unroll
-    for (int r = 0; r < R; ++r) buf[swz(base + r * stride)] = x[r];
+    for (int r = 0; r < R; ++r) buf[swz(base + r * stride)] = x[0][r];
   }
 }
 
@@ -225,27 +261,19 @@ __device__ __forceinline__ void fft_pass2(double2* __restrict__ b0, double2* __r
     const int blk = b / stride;
     const int j = b - blk * stride;
     const int base = blk * L + j;
-    double2 x[R], y[R];
+    double2 xy[2][R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      x[r] = b0[swz(base + r * stride)];
-      y[r] = b1[swz(base + r * stride)];
+      xy[0][r] = b0[swz(base + r * stride)];
+      xy[1][r] = b1[swz(base + r * stride)];
     }
-    RegDft<R>::run(x, -1.0);
-    RegDft<R>::run(y, -1.0);
-#pragma unroll
-    for (int r = 1; r < R; ++r) {
-      const uint32_t e = static_cast<uint32_t>(j * r) * tw_scale;
-      if (e) {
-        const double2 w = twiddle(tw, hi_off, e);
-        x[r] = cmul(x[r], w);
-        y[r] = cmul(y[r], w);
-      }
-    }
+    RegDft<R>::run(xy[0], -1.0);
+    RegDft<R>::run(xy[1], -1.0);
+    if (j) apply_twiddles<R, 2>(xy, twiddle(tw, hi_off, static_cast<uint32_t>(j) * tw_scale));
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      b0[swz(base + r * stride)] = x[r];
-      b1[swz(base + r * stride)] = y[r];
+      b0[swz(base + r * stride)] = xy[0][r];
+      b1[swz(base + r * stride)] = xy[1][r];
     }
   }
 }

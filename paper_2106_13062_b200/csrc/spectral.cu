@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kFftThreads) iuv_kernel(FftPlan pl, EngArgs e,
 // second shared buffer, halving shared memory so two CTAs fit per SM. Used when
 // the batch is slightly above one wave of the two-buffer kernel (config 3:
 // 15 x 10 = 150 items on 148 SMs), where it removes the nearly empty second wave.
-__global__ void __launch_bounds__(kFftThreads) iuv1_kernel(FftPlan pl, EngArgs e, const double* A,
+__global__ void __launch_bounds__(kFftThreads, 2) iuv1_kernel(FftPlan pl, EngArgs e, const double* A,
                                                            const double* B, int c1, int c2, int f,
                                                            double2* scratch, double* est) {
   const Smem sm = carve(pl, 1);
