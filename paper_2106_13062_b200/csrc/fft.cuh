@@ -207,8 +207,10 @@ __device__ __forceinline__ void fft_pass(double2* buf, const double2* tw, int hi
   const int stride = L / R;
   const int nbfly = P / R;
   const uint32_t tw_scale = static_cast<uint32_t>(M / L);  // w_L = w_M^{M/L}
+  // b / stride as a multiply-high (stride > 1): exact for every b < P <= 2^13
+  const uint32_t magic = 0xffffffffu / static_cast<uint32_t>(stride) + 1u;
   for (int b = threadIdx.x; b < nbfly; b += blockDim.x) {
-    const int blk = b / stride;
+    const int blk = stride == 1 ? b : static_cast<int>(__umulhi(static_cast<uint32_t>(b), magic));
     const int j = b - blk * stride;
     const int base = blk * L + j;
     double2 x[1][R];
@@ -257,8 +259,9 @@ __device__ __forceinline__ void fft_pass2(double2* __restrict__ b0, double2* __r
   const int stride = L / R;
   const int nbfly = P / R;
   const uint32_t tw_scale = static_cast<uint32_t>(M / L);
+  const uint32_t magic = 0xffffffffu / static_cast<uint32_t>(stride) + 1u;
   for (int b = threadIdx.x; b < nbfly; b += blockDim.x) {
-    const int blk = b / stride;
+    const int blk = stride == 1 ? b : static_cast<int>(__umulhi(static_cast<uint32_t>(b), magic));
     const int j = b - blk * stride;
     const int base = blk * L + j;
     double2 xy[2][R];
