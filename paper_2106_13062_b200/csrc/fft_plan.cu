@@ -78,7 +78,7 @@ int get_fft_plan(size_t min_len, FftPlan* out) {
   FftPlan pl{};
   pl.M = M;
   pl.P = M / 2;
-  // radix schedule: 3s first, then 16s, then the remainder
+  // radix schedule: 3s first, then 16s, then the remainder (16 * 2 as 8 * 4)
   std::vector<int> radix;
   int rem = pl.P;
   while (rem % 3 == 0) {
@@ -88,6 +88,10 @@ int get_fft_plan(size_t min_len, FftPlan* out) {
   while (rem % 16 == 0) {
     radix.push_back(16);
     rem /= 16;
+  }
+  if (rem == 2 && !radix.empty() && radix.back() == 16) {
+    radix.back() = 8;  // 16 * 2 -> 8 * 4: a radix-2 pass has P/2 butterflies
+    rem = 4;
   }
   if (rem > 1) radix.push_back(rem);  // 8, 4 or 2
   pl.npass = static_cast<int>(radix.size());

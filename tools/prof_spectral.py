@@ -9,6 +9,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2106_13062_b200 as st  # noqa: E402
+from paper_2106_13062_b200 import _lib as L  # noqa: E402
 from paper_2106_13062_b200 import configs  # noqa: E402
 
 
@@ -16,7 +17,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--which", default="c2,c3")
+    ap.add_argument("--lib", default=None, help="alternative libfcs_b200.so (A/B runs)")
     args = ap.parse_args()
+    if args.lib:
+        L.LIB_PATH = args.lib
     which = args.which.split(",")
     res = {}
     if "c2" in which:
