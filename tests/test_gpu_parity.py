@@ -125,6 +125,48 @@ def test_dense_f32_wide_sketch(cuda):
         rel_close(got[d], O.fcs_dense(x.astype(np.float64), b, s, j), RTOL32)
 
 
+def test_dense_c4_full_size(cuda):
+    """BASELINE config 4 at full size (1024^3 fp32, J = 16384, D = 4), the bench
+    workload, through size-independent checks: (i) every bucket against an
+    independent kernel — the fp64 global-atomic path on the widened tensor
+    (itself pinned to the oracle in test_dense_global_fallback) — at the fp32
+    rule; (ii) the zeroth and first moments of each sketch against direct
+    contractions of the tensor: sum_b sk[b] = <T, s0 (x) s1 (x) s2> and
+    sum_b b sk[b] = sum_n <T, ... (h_n s_n) ...> (every element lands in bucket
+    h0 + h1 + h2 with sign s0 s1 s2). Moment tolerance 1e-3 ||T||_F (x J~ for
+    the first): the fixed-point rounding sums to ~2e-2 here, a dropped or
+    doubled fiber chunk moves the sum by ~1e3."""
+    import ctypes as C
+    from paper_2106_13062_b200 import _lib as L
+    c = configs.C4
+    n = int(np.prod(c.dims))
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    L.check(L.lib().st_device_gaussian(L.ST_F32, c.seed, n, C.c_void_p(x.data_ptr()), None))
+    fams = st.families_for(list(c.dims), st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
+    got = st.fcs_dense_batched(st.DenseTensor(list(c.dims), x), fams)
+    x64 = x.double()
+    del x
+    ref = st.fcs_dense_batched(st.DenseTensor(list(c.dims), x64), fams)
+    assert got.shape == ref.shape == (4, 49150)
+    rel_close(got, ref.cpu().numpy(), RTOL32)
+    X = x64.view(c.dims[2], c.dims[1], c.dims[0])  # column-major: [i2][i1][i0]
+    norm = float(torch.linalg.vector_norm(x64))
+    jt = got.shape[1]
+    b = torch.arange(jt, dtype=torch.float64, device="cuda")
+    for d, f in enumerate(fams):
+        s = [torch.tensor(f.pair(k).sign_map(), dtype=torch.float64, device="cuda") for k in range(3)]
+        h = [torch.tensor(f.pair(k).bucket_map().astype(np.int64), dtype=torch.float64,
+                          device="cuda") for k in range(3)]
+
+        def con(a0, a1, a2):
+            return float(((X @ a0) @ a1) @ a2)
+        m0 = con(s[0], s[1], s[2])
+        m1 = con(h[0] * s[0], s[1], s[2]) + con(s[0], h[1] * s[1], s[2]) + \
+            con(s[0], s[1], h[2] * s[2])
+        assert abs(float(got[d].sum()) - m0) <= 1e-3 * norm, (d, float(got[d].sum()), m0)
+        assert abs(float(got[d] @ b) - m1) <= 1e-3 * norm * jt, (d, float(got[d] @ b), m1)
+
+
 def test_dense_global_fallback(cuda):
     """fp64 sketch larger than shared memory (J~ = 29998 -> 240 KB): global path."""
     rng = np.random.default_rng(5)
