@@ -37,6 +37,8 @@ struct FftPlan {
   int hi_count;                // entries of the hi table (= M >> kTwLoBits, rounded up)
   const double2* tw;           // device: lo[64] then hi[hi_count]
   const int* f2p;              // device: slot position of frequency k, k in [0, P)
+  const uint2* units;          // device: pair units of the last pass (see last_pass_post)
+  int nunits;
   int large_p1;                // 0: one-CTA plan; else P = large_p1 * P2 two-level plan
 };                             // (spectral_large.cu; npass, tw, f2p unused)
 
@@ -307,10 +309,13 @@ __device__ __forceinline__ void fft_inverse(double2* buf, const FftPlan& pl, con
 // Shared-memory table region: twiddles (lo, hi) then the frequency -> slot
 // table (P ints), padded to whole double2 slots.
 __host__ __device__ inline int table_slots(const FftPlan& pl) {
-  return (1 << kTwLoBits) + pl.hi_count + (pl.P + 3) / 4;
+  return (1 << kTwLoBits) + pl.hi_count + (pl.P + 3) / 4 + (pl.nunits + 1) / 2;
 }
 __device__ __forceinline__ const int* smem_f2p(const double2* tw, const FftPlan& pl) {
   return reinterpret_cast<const int*>(tw + (1 << kTwLoBits) + pl.hi_count);
+}
+__device__ __forceinline__ const uint2* smem_units(const double2* tw, const FftPlan& pl) {
+  return reinterpret_cast<const uint2*>(tw + (1 << kTwLoBits) + pl.hi_count + (pl.P + 3) / 4);
 }
 
 // Pair pass over (k, P-k), k = 0..P/2, in place; each thread handles kB pairs
@@ -383,6 +388,136 @@ __device__ __forceinline__ void c2r_pre(double2* buf, const FftPlan& pl, const d
   pair_pass<false>(buf, pl, tw);
 }
 
+// The same pair maps on two registers: a = Z[k], b = Z[P-k] (post) or
+// a = X[k], b = X[P-k] (pre), w = w_M^k. a and b may alias (k = P/2): both
+// formulas then write the same value twice.
+__device__ __forceinline__ void post_pair(double2& a, double2& b, double2 w) {
+  const double2 e = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+  const double2 o = make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x));
+  const double2 wo = cmul(w, o);
+  a = cadd(e, wo);
+  b = cconj(csub(e, wo));
+}
+__device__ __forceinline__ void pre_pair(double2& a, double2& b, double2 w) {
+  const double2 e = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+  const double2 dif = make_double2(0.5 * (a.x - b.x), 0.5 * (a.y + b.y));
+  const double2 o = cmul(dif, cconj(w));
+  a = make_double2(e.x - o.y, e.y + o.x);
+  b = make_double2(e.x + o.y, -e.y + o.x);
+}
+
+// Last DIF pass fused with r2c_post / first DIT pass fused with c2r_pre.
+// The last pass (radix R, stride 1, no twiddles) transforms groups b of R
+// consecutive slots; slot b R + r holds frequency k = m(b) + r G (G = P / R).
+// The partner P - k of every k in group b sits in the mirror group b' with
+// m(b') = G - m(b), at r' = R - 1 - r; groups with m = 0 or 2m = G pair with
+// themselves. One thread takes a unit (b, b') — both groups in registers — so
+// the (k, P-k) pass needs no extra shared-memory sweep (nor its
+// bank-conflicted frequency-order accesses). units[u] = {b | b' << 16, m(b)}
+// (fft_plan.cu).
+template <int R, bool kForward>
+__device__ __forceinline__ void pair_group_pass(double2* buf, const FftPlan& pl,
+                                                const double2* tw) {
+  const uint2* un = smem_units(tw, pl);
+  const uint32_t G = static_cast<uint32_t>(pl.P / R);
+  const int hi_off = 1 << kTwLoBits;
+  for (int u = threadIdx.x; u < pl.nunits; u += blockDim.x) {
+    const uint2 d = un[u];
+    const uint32_t b = d.x & 0xffffu, bp = d.x >> 16, m = d.y;
+    double2 x[R], y[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r] = buf[swz(b * R + r)];
+    if (bp != b) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) y[r] = buf[swz(bp * R + r)];
+    }
+    if (kForward) RegDft<R>::run(x, -1.0);
+    if (bp != b) {
+      if (kForward) RegDft<R>::run(y, -1.0);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double2 w = twiddle(tw, hi_off, m + r * G);
+        if (kForward) post_pair(x[r], y[R - 1 - r], w);
+        else pre_pair(x[r], y[R - 1 - r], w);
+      }
+      if (!kForward) RegDft<R>::run(y, +1.0);
+#pragma unroll
+      for (int r = 0; r < R; ++r) buf[swz(bp * R + r)] = y[r];
+    } else if (m == 0) {  // k = r G: pairs (r, R - r), r = 0 the (X0, XP) slot
+      const double2 z = x[0];
+      x[0] = kForward ? make_double2(z.x + z.y, z.x - z.y)
+                      : make_double2(0.5 * (z.x + z.y), 0.5 * (z.x - z.y));
+#pragma unroll
+      for (int r = 1; r <= R / 2; ++r) {
+        const double2 w = twiddle(tw, hi_off, r * G);
+        if (kForward) post_pair(x[r], x[R - r], w);
+        else pre_pair(x[r], x[R - r], w);
+      }
+    } else {  // 2m = G: pairs (r, R - 1 - r)
+#pragma unroll
+      for (int r = 0; r <= (R - 1) / 2; ++r) {
+        const double2 w = twiddle(tw, hi_off, m + r * G);
+        if (kForward) post_pair(x[r], x[R - 1 - r], w);
+        else pre_pair(x[r], x[R - 1 - r], w);
+      }
+    }
+    if (!kForward) RegDft<R>::run(x, +1.0);
+#pragma unroll
+    for (int r = 0; r < R; ++r) buf[swz(b * R + r)] = x[r];
+  }
+}
+
+template <bool kForward>
+__device__ __forceinline__ void pair_group_dispatch(double2* buf, const FftPlan& pl,
+                                                    const double2* tw) {
+  switch (pl.radix[pl.npass - 1]) {
+    case 8: pair_group_pass<8, kForward>(buf, pl, tw); break;
+    case 4: pair_group_pass<4, kForward>(buf, pl, tw); break;
+    case 3: pair_group_pass<3, kForward>(buf, pl, tw); break;
+    default: pair_group_pass<2, kForward>(buf, pl, tw); break;
+  }
+}
+
+// fft_forward + r2c_post (no trailing barrier, like r2c_post).
+__device__ __forceinline__ void fft_forward_post(double2* buf, const FftPlan& pl,
+                                                 const double2* tw) {
+  for (int p = 0; p + 1 < pl.npass; ++p) {
+    fft_dispatch<true>(buf, tw, 1 << kTwLoBits, pl.M, pl.P, pl.radix[p], pl.len[p]);
+    __syncthreads();
+  }
+  pair_group_dispatch<true>(buf, pl, tw);
+}
+
+// fft_forward2 + r2c_post on both buffers.
+__device__ __forceinline__ void fft_forward2_post(double2* __restrict__ b0,
+                                                  double2* __restrict__ b1, const FftPlan& pl,
+                                                  const double2* tw) {
+  const int hi = 1 << kTwLoBits;
+  for (int p = 0; p + 1 < pl.npass; ++p) {
+    switch (pl.radix[p]) {
+      case 16: fft_pass2<16>(b0, b1, tw, hi, pl.M, pl.P, pl.len[p]); break;
+      case 8: fft_pass2<8>(b0, b1, tw, hi, pl.M, pl.P, pl.len[p]); break;
+      case 4: fft_pass2<4>(b0, b1, tw, hi, pl.M, pl.P, pl.len[p]); break;
+      case 3: fft_pass2<3>(b0, b1, tw, hi, pl.M, pl.P, pl.len[p]); break;
+      default: fft_pass2<2>(b0, b1, tw, hi, pl.M, pl.P, pl.len[p]); break;
+    }
+    __syncthreads();
+  }
+  pair_group_dispatch<true>(b0, pl, tw);
+  pair_group_dispatch<true>(b1, pl, tw);
+}
+
+// c2r_pre + fft_inverse (ends with a barrier, like fft_inverse).
+__device__ __forceinline__ void fft_inverse_pre(double2* buf, const FftPlan& pl,
+                                                const double2* tw) {
+  pair_group_dispatch<false>(buf, pl, tw);
+  __syncthreads();
+  for (int p = pl.npass - 2; p >= 0; --p) {
+    fft_dispatch<false>(buf, tw, 1 << kTwLoBits, pl.M, pl.P, pl.radix[p], pl.len[p]);
+    __syncthreads();
+  }
+}
+
 // Zero the P packed slots.
 __device__ __forceinline__ void zero_slots(double2* buf, int P) {
   for (int s = threadIdx.x; s < P; s += blockDim.x) buf[s] = make_double2(0.0, 0.0);
@@ -394,8 +529,8 @@ __device__ __forceinline__ double& packed_real(double2* buf, uint32_t t) {
   return (t & 1u) ? s.y : s.x;
 }
 
-// Loads the twiddle table (lo then hi) and the frequency -> slot table into
-// shared memory.
+// Loads the twiddle table (lo then hi), the frequency -> slot table and the
+// last-pass pair units into shared memory.
 __device__ __forceinline__ void load_twiddles(double2* sm_tw, const FftPlan& pl) {
   const int n = (1 << kTwLoBits) + pl.hi_count;
   for (int i = threadIdx.x; i < n; i += blockDim.x) sm_tw[i] = __ldg(pl.tw + i);
@@ -413,6 +548,8 @@ __device__ __forceinline__ void load_twiddles(double2* sm_tw, const FftPlan& pl)
     for (int u = 0; u < kU; ++u)
       if (i0 + u * blockDim.x < n4) f2p[i0 + u * blockDim.x] = v[u];
   }
+  uint2* units = reinterpret_cast<uint2*>(sm_tw + n + (pl.P + 3) / 4);
+  for (int i = threadIdx.x; i < pl.nunits; i += blockDim.x) units[i] = __ldg(pl.units + i);
 }
 
 // Pointwise helpers on the half-spectrum slot layout (slot 0 holds two reals).

@@ -94,6 +94,10 @@ int get_fft_plan(size_t min_len, FftPlan* out) {
     rem = 4;
   }
   if (rem > 1) radix.push_back(rem);  // 8, 4 or 2
+  if (rem == 1 && !radix.empty() && radix.back() == 16) {
+    radix.back() = 4;  // the fused last pass (pair_group_pass) holds 2 R values: R <= 8
+    radix.push_back(4);
+  }
   pl.npass = static_cast<int>(radix.size());
   int L = pl.P;
   for (int p = 0; p < pl.npass; ++p) {
@@ -113,12 +117,36 @@ int get_fft_plan(size_t min_len, FftPlan* out) {
   for (int e = 0; e < pl.hi_count; ++e) tw[(1 << kTwLoBits) + e] = root(static_cast<long>(e) << kTwLoBits);
   std::vector<int> f2p(pl.P);
   for (int p = 0; p < pl.P; ++p) f2p[freq_of(p, radix, 0, pl.P)] = p;
+  // pair units of the fused last pass: group b holds k = m(b) + r G; its
+  // partner group has m = G - m(b) (self for m = 0 and 2m = G)
+  const int R = radix.back(), G = pl.P / R;
+  std::vector<int> m_of(G), b_of(G);
+  for (int b = 0; b < G; ++b) {
+    m_of[b] = freq_of(b * R, radix, 0, pl.P);
+    b_of[m_of[b]] = b;
+  }
+  std::vector<uint2> units;
+  for (int b = 0; b < G; ++b) {
+    const int m = m_of[b];
+    if (m == 0 || 2 * m == G) {
+      units.push_back(make_uint2(static_cast<uint32_t>(b) | (static_cast<uint32_t>(b) << 16), m));
+    } else if (m < G - m) {
+      const int bp = b_of[G - m];
+      units.push_back(make_uint2(static_cast<uint32_t>(b) | (static_cast<uint32_t>(bp) << 16), m));
+    }
+  }
+  pl.nunits = static_cast<int>(units.size());
   double2* dtw = nullptr;
   int* df2p = nullptr;
   FCS_CUDA_TRY(cudaMalloc(&dtw, tw.size() * sizeof(double2)));
   FCS_CUDA_TRY(cudaMalloc(&df2p, f2p.size() * sizeof(int)));
   FCS_CUDA_TRY(cudaMemcpy(dtw, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
   FCS_CUDA_TRY(cudaMemcpy(df2p, f2p.data(), f2p.size() * sizeof(int), cudaMemcpyHostToDevice));
+  uint2* dunits = nullptr;
+  FCS_CUDA_TRY(cudaMalloc(&dunits, units.size() * sizeof(uint2)));
+  FCS_CUDA_TRY(cudaMemcpy(dunits, units.data(), units.size() * sizeof(uint2),
+                          cudaMemcpyHostToDevice));
+  pl.units = dunits;
   pl.tw = dtw;
   pl.f2p = df2p;
   cache[{dev, M}] = pl;

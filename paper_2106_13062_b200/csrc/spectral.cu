@@ -56,8 +56,7 @@ __device__ void rfft_of_cs(const Smem& sm, double2* buf, const FftPlan& pl,
   __syncthreads();
   scatter_cs(buf, vec, I, tab);
   __syncthreads();
-  fft_forward(buf, pl, sm.tw);
-  r2c_post(buf, pl, sm.tw);
+  fft_forward_post(buf, pl, sm.tw);
   __syncthreads();
 }
 
@@ -72,9 +71,7 @@ __device__ void rfft_of_cs2(const Smem& sm, const FftPlan& pl, const double* __r
   scatter_cs(sm.buf, va, Ia, ta);
   scatter_cs(sm.buf2, vb, Ib, tb);
   __syncthreads();
-  fft_forward2(sm.buf, sm.buf2, pl, sm.tw);
-  r2c_post(sm.buf, pl, sm.tw);
-  r2c_post(sm.buf2, pl, sm.tw);
+  fft_forward2_post(sm.buf, sm.buf2, pl, sm.tw);
   __syncthreads();
 }
 
@@ -86,8 +83,7 @@ __device__ void rfft_of_real(const Smem& sm, const FftPlan& pl, const double* __
     sm.buf[swz(s)] = make_double2(t < len ? x[t] : 0.0, t + 1 < len ? x[t + 1] : 0.0);
   }
   __syncthreads();
-  fft_forward(sm.buf, pl, sm.tw);
-  r2c_post(sm.buf, pl, sm.tw);
+  fft_forward_post(sm.buf, pl, sm.tw);
   __syncthreads();
 }
 
@@ -95,9 +91,7 @@ __device__ void rfft_of_real(const Smem& sm, const FftPlan& pl, const double* __
 // (caller divides by P; idft_real's 1/n, fft.cpp:61-66).
 __device__ void irfft_in_place(const Smem& sm, const FftPlan& pl) {
   __syncthreads();
-  c2r_pre(sm.buf, pl, sm.tw);
-  __syncthreads();
-  fft_inverse(sm.buf, pl, sm.tw);
+  fft_inverse_pre(sm.buf, pl, sm.tw);
 }
 
 __device__ double block_sum(double v, double* red) {

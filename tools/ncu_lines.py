@@ -1,6 +1,9 @@
 """Map ncu per-instruction warp-stall samples to CUDA source lines.
 
-  python tools/ncu_lines.py REPORT.ncu-rep KERNEL_SUBSTRING [TOP]
+  python tools/ncu_lines.py REPORT.ncu-rep KERNEL_SUBSTRING [TOP] [COLUMN]
+
+COLUMN defaults to "Warp Stall Sampling (All Samples)"; any numeric column of
+ncu's source page works, e.g. "L1 Wavefronts Shared Excessive".
 
 Extracts the cubins from the library, disassembles the kernel with line info
 (nvdisasm -g), aligns it with ncu's SASS page by instruction order, and prints
@@ -20,18 +23,18 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2106_13062_b200", "_lib", "libfcs_b200.so")
 
 
-def main(rep, kname, top=30):
+def main(rep, kname, top=30, column="Warp Stall Sampling (All Samples)"):
     raw = subprocess.run(["ncu", "-i", rep, "-k", "regex:" + kname, "--page", "source", "--csv",
                           "--print-source", "sass"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr = rows[1]
-    iw = hdr.index("Warp Stall Sampling (All Samples)")
+    iw = hdr.index(column)
     samples = []
     for r in rows[2:]:
         if len(r) != len(hdr):
             continue
         try:
-            samples.append(float(r[iw] or 0))
+            samples.append(float(r[iw].replace(",", "") or 0))
         except ValueError:  # a repeated header (several kernels in the report)
             break
     tmp = tempfile.mkdtemp()
@@ -75,4 +78,5 @@ def main(rep, kname, top=30):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 30)
+    main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 30,
+         *(sys.argv[4:5]))
