@@ -308,14 +308,16 @@ __device__ __forceinline__ void fft_inverse(double2* buf, const FftPlan& pl, con
 
 // Shared-memory table region: twiddles (lo, hi) then the frequency -> slot
 // table (P ints), padded to whole double2 slots.
-__host__ __device__ inline int table_slots(const FftPlan& pl) {
-  return (1 << kTwLoBits) + pl.hi_count + (pl.P + 3) / 4 + (pl.nunits + 1) / 2;
-}
-__device__ __forceinline__ const int* smem_f2p(const double2* tw, const FftPlan& pl) {
-  return reinterpret_cast<const int*>(tw + (1 << kTwLoBits) + pl.hi_count);
+// Layout: twiddles (lo, hi), the last-pass pair units, then (only for kernels
+// that index spectra by frequency, spectral_large.cu) the frequency -> slot table.
+__host__ __device__ inline int table_slots(const FftPlan& pl, bool with_f2p = true) {
+  return (1 << kTwLoBits) + pl.hi_count + (pl.nunits + 1) / 2 + (with_f2p ? (pl.P + 3) / 4 : 0);
 }
 __device__ __forceinline__ const uint2* smem_units(const double2* tw, const FftPlan& pl) {
-  return reinterpret_cast<const uint2*>(tw + (1 << kTwLoBits) + pl.hi_count + (pl.P + 3) / 4);
+  return reinterpret_cast<const uint2*>(tw + (1 << kTwLoBits) + pl.hi_count);
+}
+__device__ __forceinline__ const int* smem_f2p(const double2* tw, const FftPlan& pl) {
+  return reinterpret_cast<const int*>(tw + (1 << kTwLoBits) + pl.hi_count + (pl.nunits + 1) / 2);
 }
 
 // Pair pass over (k, P-k), k = 0..P/2, in place; each thread handles kB pairs
@@ -529,13 +531,17 @@ __device__ __forceinline__ double& packed_real(double2* buf, uint32_t t) {
   return (t & 1u) ? s.y : s.x;
 }
 
-// Loads the twiddle table (lo then hi), the frequency -> slot table and the
-// last-pass pair units into shared memory.
-__device__ __forceinline__ void load_twiddles(double2* sm_tw, const FftPlan& pl) {
+// Loads the twiddle table (lo then hi), the last-pass pair units and, with
+// with_f2p, the frequency -> slot table into shared memory (table_slots layout).
+__device__ __forceinline__ void load_twiddles(double2* sm_tw, const FftPlan& pl,
+                                              bool with_f2p = true) {
   const int n = (1 << kTwLoBits) + pl.hi_count;
   for (int i = threadIdx.x; i < n; i += blockDim.x) sm_tw[i] = __ldg(pl.tw + i);
+  uint2* units = reinterpret_cast<uint2*>(sm_tw + n);
+  for (int i = threadIdx.x; i < pl.nunits; i += blockDim.x) units[i] = __ldg(pl.units + i);
+  if (!with_f2p) return;
   // P is a multiple of 8: copy the table as int4 with all loads in flight
-  int4* f2p = reinterpret_cast<int4*>(sm_tw + n);
+  int4* f2p = reinterpret_cast<int4*>(sm_tw + n + (pl.nunits + 1) / 2);
   const int4* src = reinterpret_cast<const int4*>(pl.f2p);
   const int n4 = pl.P / 4;
   constexpr int kU = 8;
@@ -548,8 +554,6 @@ __device__ __forceinline__ void load_twiddles(double2* sm_tw, const FftPlan& pl)
     for (int u = 0; u < kU; ++u)
       if (i0 + u * blockDim.x < n4) f2p[i0 + u * blockDim.x] = v[u];
   }
-  uint2* units = reinterpret_cast<uint2*>(sm_tw + n + (pl.P + 3) / 4);
-  for (int i = threadIdx.x; i < pl.nunits; i += blockDim.x) units[i] = __ldg(pl.units + i);
 }
 
 // Pointwise helpers on the half-spectrum slot layout (slot 0 holds two reals).
@@ -559,8 +563,8 @@ __device__ __forceinline__ double2 hmul(double2 a, double2 b, bool slot0) {
 __device__ __forceinline__ double2 hconj(double2 a, bool slot0) { return slot0 ? a : cconj(a); }
 
 // Shared-memory bytes a spectral kernel with this plan needs (buffer + twiddles).
-inline size_t fft_smem_bytes(const FftPlan& pl) {
-  return static_cast<size_t>(pl.P + table_slots(pl)) * sizeof(double2);
+inline size_t fft_smem_bytes(const FftPlan& pl, bool with_f2p = true) {
+  return static_cast<size_t>(pl.P + table_slots(pl, with_f2p)) * sizeof(double2);
 }
 
 // Host: plan for the smallest supported M >= min_len (cached per device):

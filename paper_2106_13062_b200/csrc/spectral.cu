@@ -29,7 +29,7 @@ __device__ __forceinline__ Smem carve(const FftPlan& pl, int nbuf = 1) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem s;
   s.tw = reinterpret_cast<double2*>(smem_raw);
-  s.buf = s.tw + table_slots(pl);
+  s.buf = s.tw + table_slots(pl, false);  // no frequency -> slot table here
   s.buf2 = nbuf > 1 ? s.buf + pl.P : nullptr;
   s.red = reinterpret_cast<double*>(s.buf + static_cast<size_t>(nbuf) * pl.P);
   return s;
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kFftThreads) spec_from_real_kernel(FftPlan pl,
                                                                      size_t ldx, int len,
                                                                      double2* spec) {
   const Smem sm = carve(pl);
-  load_twiddles(sm.tw, pl);
+  load_twiddles(sm.tw, pl, false);
   __syncthreads();
   rfft_of_real(sm, pl, x + blockIdx.x * ldx, len);
   double2* o = spec + static_cast<size_t>(blockIdx.x) * pl.P;
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kFftThreads) real_from_spec_kernel(FftPlan pl,
                                                                      double* out, size_t ldo,
                                                                      int out_len, int accumulate) {
   const Smem sm = carve(pl);
-  load_twiddles(sm.tw, pl);
+  load_twiddles(sm.tw, pl, false);
   const double2* in = spec + static_cast<size_t>(blockIdx.x) * pl.P;
   for (int s = tid(); s < pl.P; s += blockDim.x) sm.buf[swz(s)] = in[s];
   irfft_in_place(sm, pl);
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kFftThreads) cp_rank_kernel(FftPlan pl, CpArgs
                                                               const uint32_t* __restrict__ packed,
                                                               double2* __restrict__ Q) {
   const Smem sm = carve(pl, 2);
-  load_twiddles(sm.tw, pl);
+  load_twiddles(sm.tw, pl, false);
   const int rl = blockIdx.x, d = blockIdx.y;
   const int r = a.r_begin + rl;
   const double w = a.weights[r];
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kFftThreads) cp_sum_kernel(FftPlan pl,
                                                              const double2* __restrict__ acc,
                                                              double* out, int jt, int accumulate) {
   const Smem sm = carve(pl);
-  load_twiddles(sm.tw, pl);
+  load_twiddles(sm.tw, pl, false);
   const int d = blockIdx.x;
   const double2* a = acc + static_cast<size_t>(d) * pl.P;
   for (int s = tid(); s < pl.P; s += blockDim.x) sm.buf[swz(s)] = a[s];
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kFftThreads) conv_kernel(FftPlan pl, const dou
                                                            size_t ldb, double2* scratch,
                                                            double* out, size_t ldo) {
   const Smem sm = carve(pl);
-  load_twiddles(sm.tw, pl);
+  load_twiddles(sm.tw, pl, false);
   __syncthreads();
   const int item = blockIdx.x;
   double2* scr = scratch + static_cast<size_t>(item) * pl.P;
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kFftThreads) iuv_kernel(FftPlan pl, EngArgs e,
                                                           double2* scratch, double* est) {
   (void)scratch;
   const Smem sm = carve(pl, 2);
-  load_twiddles(sm.tw, pl);
+  load_twiddles(sm.tw, pl, false);
   __syncthreads();
   const int b = blockIdx.x, d = blockIdx.y;
   const size_t item = static_cast<size_t>(b) * e.D + d;
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kFftThreads, 2) iuv1_kernel(FftPlan pl, EngArg
                                                            const double* B, int c1, int c2, int f,
                                                            double2* scratch, double* est) {
   const Smem sm = carve(pl, 1);
-  load_twiddles(sm.tw, pl);
+  load_twiddles(sm.tw, pl, false);
   __syncthreads();
   const int b = blockIdx.x, d = blockIdx.y;
   const size_t item = static_cast<size_t>(b) * e.D + d;
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(kFftThreads) uvw_kernel(FftPlan pl, EngArgs e,
                                                           double2* scratch, double* est) {
   (void)scratch;
   const Smem sm = carve(pl, 2);
-  load_twiddles(sm.tw, pl);
+  load_twiddles(sm.tw, pl, false);
   __syncthreads();
   const int b = blockIdx.x, d = blockIdx.y;
   const size_t item = static_cast<size_t>(b) * e.D + d;
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(kFftThreads) deflate_kernel(FftPlan pl, EngArg
                                                               double2* spec) {
   (void)scratch;
   const Smem sm = carve(pl, 2);
-  load_twiddles(sm.tw, pl);
+  load_twiddles(sm.tw, pl, false);
   __syncthreads();
   const int d = blockIdx.x;
   const uint32_t* tab = e.packed + static_cast<size_t>(d) * e.fam_stride;
@@ -465,7 +465,7 @@ namespace {
 
 template <typename K>
 int prep(K kernel, const FftPlan& pl, size_t* smem, int nbuf = 1) {
-  *smem = fft_smem_bytes(pl) + static_cast<size_t>(nbuf - 1) * pl.P * sizeof(double2) +
+  *smem = fft_smem_bytes(pl, false) + static_cast<size_t>(nbuf - 1) * pl.P * sizeof(double2) +
           32 * sizeof(double);
   FCS_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(*smem)));
