@@ -8,6 +8,8 @@
 // (K4) so each output needs a single inverse transform (K5).
 #include <algorithm>
 
+#include <math_constants.h>
+
 #include "fft.cuh"
 
 namespace fcs {
@@ -372,12 +374,50 @@ __global__ void __launch_bounds__(kFftThreads) deflate_kernel(FftPlan pl, EngArg
 
 // K8: elementwise median over D (median_reduce, estimators.cpp:117-138):
 // est[b][d][i] -> out[b][i]; even D averages the two middle order statistics.
+// Finite values, D <= N: all D values in registers (fully unrolled, padded
+// with +inf) and the order statistics by rank counting — the same value a
+// sort yields. Returns false (caller falls back) on a non-finite input.
+template <int N>
+__device__ __forceinline__ bool median_regs(const double* col, int D, int len, double* res) {
+  double v[N];
+  bool finite = true;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    v[k] = k < D ? col[static_cast<size_t>(k) * len] : CUDART_INF;
+    if (k < D) finite &= isfinite(v[k]);
+  }
+  if (!finite) return false;
+  const int m1 = (D - 1) / 2, m2 = D / 2;  // equal for odd D
+  double lo = 0.0, hi = 0.0;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    int less = 0, eq = 0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      less += v[j] < v[k];
+      eq += v[j] == v[k];
+    }
+    if (k < D) {
+      if (less <= m1 && m1 < less + eq) lo = v[k];
+      if (less <= m2 && m2 < less + eq) hi = v[k];
+    }
+  }
+  *res = (D & 1) ? hi : 0.5 * (lo + hi);
+  return true;
+}
+
 __global__ void median_kernel(const double* __restrict__ est, int batch, int D, int len,
                               double* __restrict__ out) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= batch * len) return;
   const int b = idx / len, i = idx - b * len;
   const double* col = est + static_cast<size_t>(b) * D * len + i;  // stride len
+  double r;
+  if ((D <= 8 && median_regs<8>(col, D, len, &r)) ||
+      (D > 8 && D <= 16 && median_regs<16>(col, D, len, &r))) {
+    out[idx] = r;
+    return;
+  }
   if (D > 64) {
     // rank selection without storage (O(D^2)): x_k is the m-th order
     // statistic iff #less <= m < #less + #equal (std::sort order for finite values)
