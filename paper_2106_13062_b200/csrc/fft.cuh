@@ -34,6 +34,9 @@ struct FftPlan {
   int npass;
   int radix[kFftMaxPasses];    // DIF order
   int len[kFftMaxPasses];      // sub-transform length L entering each pass
+  unsigned long long rcode;    // radix[p] - 1 in bits 4p..4p+3 (device loops decode this
+                               // instead of indexing radix[] / len[], which would copy the
+                               // plan to local memory)
   int hi_count;                // entries of the hi table (= M >> kTwLoBits, rounded up)
   const double2* tw;           // device: lo[64] then hi[hi_count]
   const int* f2p;              // device: slot position of frequency k, k in [0, P)
@@ -243,11 +246,18 @@ __device__ __forceinline__ void fft_dispatch(double2* buf, const double2* tw, in
   }
 }
 
+__device__ __forceinline__ int pass_radix(const FftPlan& pl, int p) {
+  return static_cast<int>((pl.rcode >> (4 * p)) & 15ull) + 1;
+}
+
 // Natural-order packed input -> digit-reversed spectrum (unnormalised, e^{-i}).
 __device__ __forceinline__ void fft_forward(double2* buf, const FftPlan& pl, const double2* tw) {
+  int L = pl.P;
   for (int p = 0; p < pl.npass; ++p) {
-    fft_dispatch<true>(buf, tw, 1 << kTwLoBits, pl.M, pl.P, pl.radix[p], pl.len[p]);
+    const int R = pass_radix(pl, p);
+    fft_dispatch<true>(buf, tw, 1 << kTwLoBits, pl.M, pl.P, R, L);
     __syncthreads();
+    L /= R;
   }
 }
 
@@ -283,25 +293,38 @@ __device__ __forceinline__ void fft_pass2(double2* __restrict__ b0, double2* __r
   }
 }
 
-__device__ __forceinline__ void fft_forward2(double2* __restrict__ b0, double2* __restrict__ b1,
-                                             const FftPlan& pl, const double2* tw) {
+// The first `npass` paired forward passes (all of them, or all but the last).
+__device__ __forceinline__ void fft_forward2_passes(double2* __restrict__ b0,
+                                                    double2* __restrict__ b1, const FftPlan& pl,
+                                                    const double2* tw, int npass) {
   const int hi = 1 << kTwLoBits;
-  for (int p = 0; p < pl.npass; ++p) {
-    switch (pl.radix[p]) {
-      case 16: fft_pass2<16>(b0, b1, tw, hi, pl.M, pl.P, pl.len[p]); break;
-      case 8: fft_pass2<8>(b0, b1, tw, hi, pl.M, pl.P, pl.len[p]); break;
-      case 4: fft_pass2<4>(b0, b1, tw, hi, pl.M, pl.P, pl.len[p]); break;
-      case 3: fft_pass2<3>(b0, b1, tw, hi, pl.M, pl.P, pl.len[p]); break;
-      default: fft_pass2<2>(b0, b1, tw, hi, pl.M, pl.P, pl.len[p]); break;
+  int L = pl.P;
+  for (int p = 0; p < npass; ++p) {
+    const int R = pass_radix(pl, p);
+    switch (R) {
+      case 16: fft_pass2<16>(b0, b1, tw, hi, pl.M, pl.P, L); break;
+      case 8: fft_pass2<8>(b0, b1, tw, hi, pl.M, pl.P, L); break;
+      case 4: fft_pass2<4>(b0, b1, tw, hi, pl.M, pl.P, L); break;
+      case 3: fft_pass2<3>(b0, b1, tw, hi, pl.M, pl.P, L); break;
+      default: fft_pass2<2>(b0, b1, tw, hi, pl.M, pl.P, L); break;
     }
     __syncthreads();
+    L /= R;
   }
+}
+
+__device__ __forceinline__ void fft_forward2(double2* __restrict__ b0, double2* __restrict__ b1,
+                                             const FftPlan& pl, const double2* tw) {
+  fft_forward2_passes(b0, b1, pl, tw, pl.npass);
 }
 
 // Digit-reversed spectrum -> natural order (unnormalised, e^{+i}).
 __device__ __forceinline__ void fft_inverse(double2* buf, const FftPlan& pl, const double2* tw) {
+  int L = 1;  // len[p] = prod_{q >= p} radix[q]
   for (int p = pl.npass - 1; p >= 0; --p) {
-    fft_dispatch<false>(buf, tw, 1 << kTwLoBits, pl.M, pl.P, pl.radix[p], pl.len[p]);
+    const int R = pass_radix(pl, p);
+    L *= R;
+    fft_dispatch<false>(buf, tw, 1 << kTwLoBits, pl.M, pl.P, R, L);
     __syncthreads();
   }
 }
@@ -472,7 +495,7 @@ __device__ __forceinline__ void pair_group_pass(double2* buf, const FftPlan& pl,
 template <bool kForward>
 __device__ __forceinline__ void pair_group_dispatch(double2* buf, const FftPlan& pl,
                                                     const double2* tw) {
-  switch (pl.radix[pl.npass - 1]) {
+  switch (pass_radix(pl, pl.npass - 1)) {
     case 8: pair_group_pass<8, kForward>(buf, pl, tw); break;
     case 4: pair_group_pass<4, kForward>(buf, pl, tw); break;
     case 3: pair_group_pass<3, kForward>(buf, pl, tw); break;
@@ -483,9 +506,12 @@ __device__ __forceinline__ void pair_group_dispatch(double2* buf, const FftPlan&
 // fft_forward + r2c_post (no trailing barrier, like r2c_post).
 __device__ __forceinline__ void fft_forward_post(double2* buf, const FftPlan& pl,
                                                  const double2* tw) {
+  int L = pl.P;
   for (int p = 0; p + 1 < pl.npass; ++p) {
-    fft_dispatch<true>(buf, tw, 1 << kTwLoBits, pl.M, pl.P, pl.radix[p], pl.len[p]);
+    const int R = pass_radix(pl, p);
+    fft_dispatch<true>(buf, tw, 1 << kTwLoBits, pl.M, pl.P, R, L);
     __syncthreads();
+    L /= R;
   }
   pair_group_dispatch<true>(buf, pl, tw);
 }
@@ -494,17 +520,7 @@ __device__ __forceinline__ void fft_forward_post(double2* buf, const FftPlan& pl
 __device__ __forceinline__ void fft_forward2_post(double2* __restrict__ b0,
                                                   double2* __restrict__ b1, const FftPlan& pl,
                                                   const double2* tw) {
-  const int hi = 1 << kTwLoBits;
-  for (int p = 0; p + 1 < pl.npass; ++p) {
-    switch (pl.radix[p]) {
-      case 16: fft_pass2<16>(b0, b1, tw, hi, pl.M, pl.P, pl.len[p]); break;
-      case 8: fft_pass2<8>(b0, b1, tw, hi, pl.M, pl.P, pl.len[p]); break;
-      case 4: fft_pass2<4>(b0, b1, tw, hi, pl.M, pl.P, pl.len[p]); break;
-      case 3: fft_pass2<3>(b0, b1, tw, hi, pl.M, pl.P, pl.len[p]); break;
-      default: fft_pass2<2>(b0, b1, tw, hi, pl.M, pl.P, pl.len[p]); break;
-    }
-    __syncthreads();
-  }
+  fft_forward2_passes(b0, b1, pl, tw, pl.npass - 1);
   pair_group_dispatch<true>(b0, pl, tw);
   pair_group_dispatch<true>(b1, pl, tw);
 }
@@ -514,8 +530,11 @@ __device__ __forceinline__ void fft_inverse_pre(double2* buf, const FftPlan& pl,
                                                 const double2* tw) {
   pair_group_dispatch<false>(buf, pl, tw);
   __syncthreads();
+  int L = pass_radix(pl, pl.npass - 1);
   for (int p = pl.npass - 2; p >= 0; --p) {
-    fft_dispatch<false>(buf, tw, 1 << kTwLoBits, pl.M, pl.P, pl.radix[p], pl.len[p]);
+    const int R = pass_radix(pl, p);
+    L *= R;
+    fft_dispatch<false>(buf, tw, 1 << kTwLoBits, pl.M, pl.P, R, L);
     __syncthreads();
   }
 }

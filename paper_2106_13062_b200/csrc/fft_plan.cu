@@ -103,6 +103,7 @@ int get_fft_plan(size_t min_len, FftPlan* out) {
   for (int p = 0; p < pl.npass; ++p) {
     pl.radix[p] = radix[p];
     pl.len[p] = L;
+    pl.rcode |= static_cast<unsigned long long>(radix[p] - 1) << (4 * p);
     L /= radix[p];
   }
   pl.hi_count = (M + (1 << kTwLoBits) - 1) >> kTwLoBits;
