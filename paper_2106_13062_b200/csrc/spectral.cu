@@ -7,6 +7,7 @@
 // prologue), and products / sums over rank happen in the frequency domain
 // (K4) so each output needs a single inverse transform (K5).
 #include <algorithm>
+#include <cstdlib>
 
 #include <math_constants.h>
 
@@ -177,6 +178,35 @@ __global__ void __launch_bounds__(kFftThreads) cp_rank_kernel(FftPlan pl, CpArgs
   }
   __syncthreads();
   for (int s = tid(); s < pl.P; s += blockDim.x) q[s] = cscale(sm.buf[swz(s)], w);
+}
+
+// K2-K4, one-buffer form: the product over modes accumulates in the item's Q
+// slot (each thread re-reads only the slots it wrote, L2-resident), so shared
+// memory is one buffer plus the tables and two CTAs fit per SM — fewer waves
+// when the (rank, family) items are several times the SM count (config 2:
+// 500 items of P = 6144).
+__global__ void __launch_bounds__(kFftThreads, 2) cp_rank1_kernel(FftPlan pl, CpArgs a,
+                                                                  const uint32_t* __restrict__ packed,
+                                                                  double2* __restrict__ Q) {
+  const Smem sm = carve(pl, 1);
+  load_twiddles(sm.tw, pl, false);
+  const int rl = blockIdx.x, d = blockIdx.y;
+  const int r = a.r_begin + rl;
+  const double w = a.weights[r];
+  double2* q = Q + (static_cast<size_t>(d) * a.r_count + rl) * pl.P;
+  const uint32_t* tab = packed + static_cast<size_t>(d) * a.fam_stride;
+  if (w == 0.0) return;  // convolved_cp_sketch skips zero weights (sketch.cpp:75)
+  for (int n = 0; n < a.order; ++n) {
+    __syncthreads();
+    rfft_of_cs(sm, sm.buf, pl, a.factors[n] + static_cast<size_t>(r) * a.dims[n], a.dims[n],
+               tab + a.tab_off[n]);
+    const bool last = n + 1 == a.order;
+    for (int s = tid(); s < pl.P; s += blockDim.x) {
+      double2 v = sm.buf[swz(s)];
+      if (n > 0) v = hmul(q[s], v, s == 0);
+      q[s] = last ? cscale(v, w) : v;
+    }
+  }
 }
 
 // K4: fixed-order sum over ranks, parallel over (slot, family): acc[d][s] =
@@ -537,10 +567,24 @@ int launch_real_from_spec(const FftPlan& pl, const double2* spec, int items, dou
 int launch_cp(const FftPlan& pl, const CpArgs& a, int D, const uint32_t* packed, double2* Q,
               double* out, int jt, int accumulate, cudaStream_t st) {
   if (pl.large_p1) return large_cp(pl, a, D, packed, a.hash_lens, out, jt, accumulate, st);
-  size_t sm;
+  size_t sm, sm1;
   if (int rc = prep(cp_rank_kernel, pl, &sm, 2)) return rc;
+  if (int rc = prep(cp_rank1_kernel, pl, &sm1, 1)) return rc;
   if (a.r_count > 0) {
-    cp_rank_kernel<<<dim3(a.r_count, D), kFftThreads, sm, st>>>(pl, a, packed, Q);
+    // the one-buffer form when it needs fewer waves (as launch_iuv)
+    int occ2 = 0, occ1 = 0;
+    FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, cp_rank_kernel, kFftThreads, sm));
+    FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, cp_rank1_kernel, kFftThreads,
+                                                               sm1));
+    DeviceInfo di;
+    if (int rc = device_info(&di)) return rc;
+    const long items = static_cast<long>(a.r_count) * D;
+    const long c2 = static_cast<long>(std::max(occ2, 1)) * di.sm_count;
+    const long c1 = static_cast<long>(std::max(occ1, 1)) * di.sm_count;
+    if ((items + c1 - 1) / c1 < (items + c2 - 1) / c2 && !std::getenv("ST_CP_TWO_BUFFER"))
+      cp_rank1_kernel<<<dim3(a.r_count, D), kFftThreads, sm1, st>>>(pl, a, packed, Q);
+    else
+      cp_rank_kernel<<<dim3(a.r_count, D), kFftThreads, sm, st>>>(pl, a, packed, Q);
     FCS_CUDA_TRY(cudaGetLastError());
   }
   // The summed spectra go to their own region after Q (st_fcs_cp_workspace
