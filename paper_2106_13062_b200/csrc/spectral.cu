@@ -214,20 +214,31 @@ __global__ void __launch_bounds__(kFftThreads, 2) cp_rank1_kernel(FftPlan pl, Cp
 // here in the frequency domain by linearity).
 __global__ void cp_rank_sum_kernel(const double2* __restrict__ Q, const double* __restrict__ weights,
                                    int r_begin, int r_count, int P, double2* __restrict__ acc) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  // 32 slots x 8 rank lanes: lane y sums ranks y, y + 8, ... (several loads in
+  // flight per slot), then the 8 lane sums are added in lane order — a fixed order
+  __shared__ double2 red[8][32];
+  const int s = blockIdx.x * 32 + threadIdx.x;
   const int d = blockIdx.y;
-  if (s >= P) return;
   double2 a = make_double2(0.0, 0.0);
-  const double2* q = Q + static_cast<size_t>(d) * r_count * P + s;
-  for (int rl = 0; rl < r_count; ++rl) {
-    if (weights[r_begin + rl] == 0.0) continue;
-    a = cadd(a, q[static_cast<size_t>(rl) * P]);
+  if (s < P) {
+    const double2* q = Q + static_cast<size_t>(d) * r_count * P + s;
+    for (int rl = threadIdx.y; rl < r_count; rl += 8) {
+      if (weights[r_begin + rl] == 0.0) continue;
+      a = cadd(a, q[static_cast<size_t>(rl) * P]);
+    }
   }
-  acc[static_cast<size_t>(d) * P + s] = a;
+  red[threadIdx.y][threadIdx.x] = a;
+  __syncthreads();
+  if (threadIdx.y == 0 && s < P) {
+    double2 t = red[0][threadIdx.x];
+#pragma unroll
+    for (int y = 1; y < 8; ++y) t = cadd(t, red[y][threadIdx.x]);
+    acc[static_cast<size_t>(d) * P + s] = t;
+  }
 }
 
 // K5: one inverse transform per family, first J~ values into out.
-__global__ void __launch_bounds__(kFftThreads) cp_sum_kernel(FftPlan pl,
+__global__ void __launch_bounds__(2 * kFftThreads, 1) cp_sum_kernel(FftPlan pl,
                                                              const double2* __restrict__ acc,
                                                              double* out, int jt, int accumulate) {
   const Smem sm = carve(pl);
@@ -590,11 +601,12 @@ int launch_cp(const FftPlan& pl, const CpArgs& a, int D, const uint32_t* packed,
   // The summed spectra go to their own region after Q (st_fcs_cp_workspace
   // reserves D*P extra slots).
   double2* acc = Q + static_cast<size_t>(D) * std::max(a.r_count, 1) * pl.P;
-  cp_rank_sum_kernel<<<dim3(ceil_div(pl.P, 256), D), 256, 0, st>>>(Q, a.weights, a.r_begin,
-                                                                   a.r_count, pl.P, acc);
+  cp_rank_sum_kernel<<<dim3(ceil_div(pl.P, 32), D), dim3(32, 8), 0, st>>>(Q, a.weights, a.r_begin,
+                                                                          a.r_count, pl.P, acc);
   FCS_CUDA_TRY(cudaGetLastError());
   if (int rc = prep(cp_sum_kernel, pl, &sm)) return rc;
-  cp_sum_kernel<<<D, kFftThreads, sm, st>>>(pl, acc, out, jt, accumulate);
+  // D CTAs only: twice the threads per CTA shortens the one-transform latency
+  cp_sum_kernel<<<D, 2 * kFftThreads, sm, st>>>(pl, acc, out, jt, accumulate);
   FCS_CUDA_TRY(cudaGetLastError());
   return ST_OK;
 }
