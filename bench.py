@@ -381,10 +381,11 @@ def secondary(x=None):
         L.check(lib.st_engine_iuv(eng._h, configs.C3_INITS, C.c_void_p(U.data_ptr()),
                                   C.c_void_p(U.data_ptr()), 0, C.c_void_p(Y.data_ptr()), 1, sp))
     ms_iuv = median_ms(iuv_call, 20)
+    rcfg = st.RtpmConfig(c.rank, configs.C3_INITS, configs.C3_ITERS, st.SketchBackend.FCS, est)
+    st.rtpm(dt, rcfg)  # warm-up: first launches of the driver's kernels, plans, pools
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    cpd = st.rtpm(dt, st.RtpmConfig(c.rank, configs.C3_INITS, configs.C3_ITERS,
-                                    st.SketchBackend.FCS, est))
+    cpd = st.rtpm(dt, rcfg)
     torch.cuda.synchronize()
     t_rtpm = time.perf_counter() - t0
     # estimates/s: one batched step gives L restarts x D sketches of T(I,u,u) (median over D
@@ -393,7 +394,7 @@ def secondary(x=None):
     res["c3_rtpm"] = {"iuv_step_ms": ms_iuv,
                       "estimates_per_sec": configs.C3_INITS / (ms_iuv * 1e-3),
                       "step_hbm_gbs": 1517680 / (ms_iuv * 1e-3) / 1e9,
-                      "rtpm_total_s": t_rtpm, "seed": c.seed,
+                      "rtpm_total_s": t_rtpm, "rtpm_timing": "second call (warm)", "seed": c.seed,
                       "weights": [round(float(x), 6) for x in cpd.weights.cpu().numpy()]}
     # c5: FCS of A (x) B, 512^2 operands, D = 8 (device-resident operands)
     c = configs.C5
