@@ -9,7 +9,8 @@
 // library (cached tensor spectra, factor spectra, products) lives in that
 // same slot order, so pointwise products never permute; the inverse
 // (decimation-in-time, the exact reverse of the forward passes) returns
-// natural order. r2c_post / c2r_pre convert between the packed P-point
+// natural order. The post / pre pair maps (post_pair / pre_pair, fused into
+// the last forward / first inverse pass) convert between the packed P-point
 // transform and the Hermitian half spectrum X[0..P] of the length-M real
 // transform; slot pos(0) holds the two real bins (X[0], X[P]).
 //
@@ -313,11 +314,6 @@ __device__ __forceinline__ void fft_forward2_passes(double2* __restrict__ b0,
   }
 }
 
-__device__ __forceinline__ void fft_forward2(double2* __restrict__ b0, double2* __restrict__ b1,
-                                             const FftPlan& pl, const double2* tw) {
-  fft_forward2_passes(b0, b1, pl, tw, pl.npass);
-}
-
 // Digit-reversed spectrum -> natural order (unnormalised, e^{+i}).
 __device__ __forceinline__ void fft_inverse(double2* buf, const FftPlan& pl, const double2* tw) {
   int L = 1;  // len[p] = prod_{q >= p} radix[q]
@@ -329,9 +325,7 @@ __device__ __forceinline__ void fft_inverse(double2* buf, const FftPlan& pl, con
   }
 }
 
-// Shared-memory table region: twiddles (lo, hi) then the frequency -> slot
-// table (P ints), padded to whole double2 slots.
-// Layout: twiddles (lo, hi), the last-pass pair units, then (only for kernels
+// Shared-memory table region, in double2 slots. Layout: twiddles (lo, hi), the last-pass pair units, then (only for kernels
 // that index spectra by frequency, spectral_large.cu) the frequency -> slot table.
 __host__ __device__ inline int table_slots(const FftPlan& pl, bool with_f2p = true) {
   return (1 << kTwLoBits) + pl.hi_count + (pl.nunits + 1) / 2 + (with_f2p ? (pl.P + 3) / 4 : 0);
@@ -343,79 +337,14 @@ __device__ __forceinline__ const int* smem_f2p(const double2* tw, const FftPlan&
   return reinterpret_cast<const int*>(tw + (1 << kTwLoBits) + pl.hi_count + (pl.nunits + 1) / 2);
 }
 
-// Pair pass over (k, P-k), k = 0..P/2, in place; each thread handles kB pairs
-// per step with all loads issued before any store (the pairs are disjoint, so
-// this is safe and exposes kB independent chains).
-//   kPost (r2c_post): packed P-point spectrum Z -> Hermitian half spectrum X
-//     of the M-point real transform; slot pos(0) = (X0, XP).
-//   !kPost (c2r_pre): the inverse map; after fft_inverse slot j holds
-//     P*(x[2j] + i x[2j+1]).
-template <bool kPost>
-__device__ __forceinline__ void pair_pass(double2* buf, const FftPlan& pl, const double2* tw) {
-  const int* f2p = smem_f2p(tw, pl);
-  const int hi_off = 1 << kTwLoBits;
-  const int half = pl.P / 2;
-  if (threadIdx.x == 0) {
-    const uint32_t s0 = swz(f2p[0]);
-    const double2 z = buf[s0];
-    buf[s0] = kPost ? make_double2(z.x + z.y, z.x - z.y)
-                    : make_double2(0.5 * (z.x + z.y), 0.5 * (z.x - z.y));
-  }
-  constexpr int kB = 4;
-  for (int k0 = 1 + threadIdx.x; k0 <= half; k0 += kB * blockDim.x) {
-    uint32_t sa[kB], sb[kB];
-    double2 va[kB], vb[kB];
-#pragma unroll
-    for (int j = 0; j < kB; ++j) {
-      const int k = k0 + j * blockDim.x;
-      if (k <= half) {
-        sa[j] = swz(f2p[k]);
-        sb[j] = swz(f2p[pl.P - k]);
-        va[j] = buf[sa[j]];
-        vb[j] = buf[sb[j]];
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < kB; ++j) {
-      const int k = k0 + j * blockDim.x;
-      if (k > half) continue;
-      const double2 w = twiddle(tw, hi_off, static_cast<uint32_t>(k));
-      const double2 xa = va[j], xb = vb[j];
-      if (kPost) {
-        // E = (Z[k] + conj Z[P-k]) / 2, O = (Z[k] - conj Z[P-k]) / (2i)
-        const double2 e = make_double2(0.5 * (xa.x + xb.x), 0.5 * (xa.y - xb.y));
-        const double2 o = make_double2(0.5 * (xa.y + xb.y), -0.5 * (xa.x - xb.x));
-        const double2 wo = cmul(w, o);
-        va[j] = cadd(e, wo);          // X[k]
-        vb[j] = cconj(csub(e, wo));   // X[P-k]
-      } else {
-        const double2 e = make_double2(0.5 * (xa.x + xb.x), 0.5 * (xa.y - xb.y));
-        const double2 dif = make_double2(0.5 * (xa.x - xb.x), 0.5 * (xa.y + xb.y));
-        const double2 o = cmul(dif, cconj(w));
-        va[j] = make_double2(e.x - o.y, e.y + o.x);   // Z[k] = E + i O
-        vb[j] = make_double2(e.x + o.y, -e.y + o.x);  // Z[P-k] = conj(E) + i conj(O)
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < kB; ++j) {
-      const int k = k0 + j * blockDim.x;
-      if (k > half) continue;
-      buf[sa[j]] = va[j];
-      if (pl.P - k != k) buf[sb[j]] = vb[j];
-    }
-  }
-}
-
-__device__ __forceinline__ void r2c_post(double2* buf, const FftPlan& pl, const double2* tw) {
-  pair_pass<true>(buf, pl, tw);
-}
-__device__ __forceinline__ void c2r_pre(double2* buf, const FftPlan& pl, const double2* tw) {
-  pair_pass<false>(buf, pl, tw);
-}
-
-// The same pair maps on two registers: a = Z[k], b = Z[P-k] (post) or
-// a = X[k], b = X[P-k] (pre), w = w_M^k. a and b may alias (k = P/2): both
-// formulas then write the same value twice.
+// The real-transform pair maps on two registers, w = w_M^k:
+//   post (r2c): a = Z[k], b = Z[P-k] of the packed P-point spectrum ->
+//     a = X[k] = E + w O, b = X[P-k] = conj(E - w O) of the Hermitian half
+//     spectrum of the M-point real transform, with E = (Z[k] + conj Z[P-k]) / 2,
+//     O = (Z[k] - conj Z[P-k]) / (2i); slot of k = 0 holds (X0, XP).
+//   pre (c2r): the inverse map (Z[k] = E + i O, Z[P-k] = conj(E) + i conj(O));
+//     after the inverse passes slot j holds P (x[2j] + i x[2j+1]).
+// a and b may alias (k = P/2): both formulas then write the same value twice.
 __device__ __forceinline__ void post_pair(double2& a, double2& b, double2 w) {
   const double2 e = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
   const double2 o = make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x));
@@ -431,7 +360,8 @@ __device__ __forceinline__ void pre_pair(double2& a, double2& b, double2 w) {
   b = make_double2(e.x + o.y, -e.y + o.x);
 }
 
-// Last DIF pass fused with r2c_post / first DIT pass fused with c2r_pre.
+// Last DIF pass fused with the r2c post map / first DIT pass fused with the
+// c2r pre map.
 // The last pass (radix R, stride 1, no twiddles) transforms groups b of R
 // consecutive slots; slot b R + r holds frequency k = m(b) + r G (G = P / R).
 // The partner P - k of every k in group b sits in the mirror group b' with
@@ -503,7 +433,7 @@ __device__ __forceinline__ void pair_group_dispatch(double2* buf, const FftPlan&
   }
 }
 
-// fft_forward + r2c_post (no trailing barrier, like r2c_post).
+// fft_forward + the r2c post map (no trailing barrier).
 __device__ __forceinline__ void fft_forward_post(double2* buf, const FftPlan& pl,
                                                  const double2* tw) {
   int L = pl.P;
@@ -516,7 +446,7 @@ __device__ __forceinline__ void fft_forward_post(double2* buf, const FftPlan& pl
   pair_group_dispatch<true>(buf, pl, tw);
 }
 
-// fft_forward2 + r2c_post on both buffers.
+// Both buffers: paired forward passes + the r2c post map.
 __device__ __forceinline__ void fft_forward2_post(double2* __restrict__ b0,
                                                   double2* __restrict__ b1, const FftPlan& pl,
                                                   const double2* tw) {
@@ -525,7 +455,7 @@ __device__ __forceinline__ void fft_forward2_post(double2* __restrict__ b0,
   pair_group_dispatch<true>(b1, pl, tw);
 }
 
-// c2r_pre + fft_inverse (ends with a barrier, like fft_inverse).
+// The c2r pre map + fft_inverse (ends with a barrier, like fft_inverse).
 __device__ __forceinline__ void fft_inverse_pre(double2* buf, const FftPlan& pl,
                                                 const double2* tw) {
   pair_group_dispatch<false>(buf, pl, tw);

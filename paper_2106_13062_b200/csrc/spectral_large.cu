@@ -10,7 +10,7 @@
 // fft.cuh in its digit-reversed slot order. Z[k] lands at position
 // pos(k) = f2p_a[k mod P1] * P2 + f2p_b[k / P1]; pos(0) = 0. The r2c pair
 // pass then maps (Z[k], Z[P-k]) to the Hermitian half spectrum exactly as
-// fft.cuh's pair_pass does, so every pointwise kernel (products, conjugates,
+// fft.cuh's post / pre pair maps do, so every pointwise kernel (products, conjugates,
 // Parseval sums with the two real bins in slot 0) is layout-agnostic and the
 // inverse runs the passes backwards (DIT rows, conjugate twiddle, DIT columns).
 //
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(kFftThreads) lf_rows_fwd(LargeFft L, double2* 
   for (int s2 = threadIdx.x; s2 < L.P2; s2 += blockDim.x) row[s2] = buf[swz(s2)];
 }
 
-// r2c / c2r pair pass over (k, P-k) (fft.cuh pair_pass), one thread per pair.
+// r2c / c2r pair pass over (k, P-k) (fft.cuh post_pair / pre_pair), one thread per pair.
 template <bool kPost>
 __global__ void lf_pairs(LargeFft L, double2* __restrict__ Z, int items) {
   const int64_t half = L.P / 2;
@@ -91,22 +91,10 @@ __global__ void lf_pairs(LargeFft L, double2* __restrict__ Z, int items) {
     return;
   }
   const size_t pa = lpos(L, k), pb = lpos(L, L.P - k);
-  const double2 xa = z[pa], xb = z[pb];
+  double2 va = z[pa], vb = z[pb];
   const double2 w = root_p(k, L.M);
-  double2 va, vb;
-  if (kPost) {
-    const double2 e = make_double2(0.5 * (xa.x + xb.x), 0.5 * (xa.y - xb.y));
-    const double2 o = make_double2(0.5 * (xa.y + xb.y), -0.5 * (xa.x - xb.x));
-    const double2 wo = cmul(w, o);
-    va = cadd(e, wo);
-    vb = cconj(csub(e, wo));
-  } else {
-    const double2 e = make_double2(0.5 * (xa.x + xb.x), 0.5 * (xa.y - xb.y));
-    const double2 dif = make_double2(0.5 * (xa.x - xb.x), 0.5 * (xa.y + xb.y));
-    const double2 o = cmul(dif, cconj(w));
-    va = make_double2(e.x - o.y, e.y + o.x);
-    vb = make_double2(e.x + o.y, -e.y + o.x);
-  }
+  if (kPost) post_pair(va, vb, w);
+  else pre_pair(va, vb, w);
   z[pa] = va;
   if (pb != pa) z[pb] = vb;
   (void)items;
