@@ -370,6 +370,20 @@ __device__ __forceinline__ void pre_pair(double2& a, double2& b, double2 w) {
 // the (k, P-k) pass needs no extra shared-memory sweep (nor its
 // bank-conflicted frequency-order accesses). units[u] = {b | b' << 16, m(b)}
 // (fft_plan.cu).
+// w_M^{m + rG} for the fused pass (M = 2 R G): w_M^m times the constant
+// w_M^{rG} = exp(-i pi r / R) — one table lookup per group instead of R.
+template <int R>
+__device__ __forceinline__ double2 group_twiddle(double2 wm, int r) {
+  if constexpr (R == 2 || R == 4 || R == 8) {
+    const int q = r * (8 / R);  // angle pi r / R = 2 pi q / 16
+    const double2 c = make_double2(cos16(q), -cos16(q - 4));
+    return r == 0 ? wm : cmul(wm, c);
+  } else {
+    constexpr double kPi = 3.14159265358979323846;
+    return r == 0 ? wm : cmul(wm, make_double2(cos(kPi * r / R), -sin(kPi * r / R)));
+  }
+}
+
 template <int R, bool kForward>
 __device__ __forceinline__ void pair_group_pass(double2* buf, const FftPlan& pl,
                                                 const double2* tw) {
@@ -389,9 +403,10 @@ __device__ __forceinline__ void pair_group_pass(double2* buf, const FftPlan& pl,
     if (kForward) RegDft<R>::run(x, -1.0);
     if (bp != b) {
       if (kForward) RegDft<R>::run(y, -1.0);
+      const double2 wm = twiddle(tw, hi_off, m);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const double2 w = twiddle(tw, hi_off, m + r * G);
+        const double2 w = group_twiddle<R>(wm, r);
         if (kForward) post_pair(x[r], y[R - 1 - r], w);
         else pre_pair(x[r], y[R - 1 - r], w);
       }
@@ -404,14 +419,15 @@ __device__ __forceinline__ void pair_group_pass(double2* buf, const FftPlan& pl,
                       : make_double2(0.5 * (z.x + z.y), 0.5 * (z.x - z.y));
 #pragma unroll
       for (int r = 1; r <= R / 2; ++r) {
-        const double2 w = twiddle(tw, hi_off, r * G);
+        const double2 w = group_twiddle<R>(make_double2(1.0, 0.0), r);
         if (kForward) post_pair(x[r], x[R - r], w);
         else pre_pair(x[r], x[R - r], w);
       }
     } else {  // 2m = G: pairs (r, R - 1 - r)
+      const double2 wm = twiddle(tw, hi_off, m);
 #pragma unroll
       for (int r = 0; r <= (R - 1) / 2; ++r) {
-        const double2 w = twiddle(tw, hi_off, m + r * G);
+        const double2 w = group_twiddle<R>(wm, r);
         if (kForward) post_pair(x[r], x[R - 1 - r], w);
         else pre_pair(x[r], x[R - 1 - r], w);
       }
