@@ -88,7 +88,19 @@ __device__ __forceinline__ void apply_twiddles(double2 (*x)[R], double2 w) {
   };
   mul(1, w);
   if constexpr (R == 3) mul(2, cmul(w, w));
-  if constexpr (R >= 4) {
+  if constexpr (R == 9) {
+    const double2 w2 = cmul(w, w);
+    const double2 w3 = cmul(w2, w);
+    const double2 w4 = cmul(w2, w2);
+    mul(2, w2);
+    mul(3, w3);
+    mul(4, w4);
+    mul(5, cmul(w4, w));
+    mul(6, cmul(w3, w3));
+    mul(7, cmul(w4, w3));
+    mul(8, cmul(w4, w4));
+  }
+  if constexpr (R >= 4 && R != 9) {
     const double2 w2 = cmul(w, w);
     const double2 w3 = cmul(w2, w);
     mul(2, w2);
@@ -204,6 +216,40 @@ struct RegDft<3> {
   }
 };
 
+// 9 = 3 x 3: DFT3 over n1 for each n2 (x[3 n1 + n2]), twiddle w9^{n2 k1},
+// DFT3 over n2 for each k1; output y[k1 + 3 k2] in natural order.
+template <>
+struct RegDft<9> {
+  static __device__ __forceinline__ void run(double2* x, double sign) {
+    // cos / sin(2 pi k / 9), k = 1, 2, 4
+    constexpr double c1 = 0.76604444311897803520, s1 = 0.64278760968653932632;
+    constexpr double c2 = 0.17364817766693034885, s2 = 0.98480775301220805936;
+    constexpr double c4 = -0.93969262078590838405, s4 = 0.34202014332566873304;
+    double2 a[3][3];  // a[n2][k1]
+#pragma unroll
+    for (int n2 = 0; n2 < 3; ++n2) {
+      double2 t[3] = {x[n2], x[3 + n2], x[6 + n2]};
+      RegDft<3>::run(t, sign);
+#pragma unroll
+      for (int k1 = 0; k1 < 3; ++k1) a[n2][k1] = t[k1];
+    }
+    // w9^{n2 k1}: (1,1) -> w, (1,2) and (2,1) -> w^2, (2,2) -> w^4
+    const double2 w1 = make_double2(c1, sign * s1), w2 = make_double2(c2, sign * s2),
+                  w4 = make_double2(c4, sign * s4);
+    a[1][1] = cmul(a[1][1], w1);
+    a[1][2] = cmul(a[1][2], w2);
+    a[2][1] = cmul(a[2][1], w2);
+    a[2][2] = cmul(a[2][2], w4);
+#pragma unroll
+    for (int k1 = 0; k1 < 3; ++k1) {
+      double2 t[3] = {a[0][k1], a[1][k1], a[2][k1]};
+      RegDft<3>::run(t, sign);
+#pragma unroll
+      for (int k2 = 0; k2 < 3; ++k2) x[k1 + 3 * k2] = t[k2];
+    }
+  }
+};
+
 // ----------------------------------------------------- block-wide passes
 // One radix-R pass over all butterflies of sub-transforms of length L.
 // Forward (DIF): DFT then twiddle w_L^{j r'}; inverse (DIT): conj twiddle then DFT.
@@ -242,6 +288,7 @@ __device__ __forceinline__ void fft_dispatch(double2* buf, const double2* tw, in
     case 16: fft_pass<16, kForward>(buf, tw, hi_off, M, P, L); break;
     case 8: fft_pass<8, kForward>(buf, tw, hi_off, M, P, L); break;
     case 4: fft_pass<4, kForward>(buf, tw, hi_off, M, P, L); break;
+    case 9: fft_pass<9, kForward>(buf, tw, hi_off, M, P, L); break;
     case 3: fft_pass<3, kForward>(buf, tw, hi_off, M, P, L); break;
     default: fft_pass<2, kForward>(buf, tw, hi_off, M, P, L); break;
   }
@@ -306,6 +353,7 @@ __device__ __forceinline__ void fft_forward2_passes(double2* __restrict__ b0,
       case 16: fft_pass2<16>(b0, b1, tw, hi, pl.M, pl.P, L); break;
       case 8: fft_pass2<8>(b0, b1, tw, hi, pl.M, pl.P, L); break;
       case 4: fft_pass2<4>(b0, b1, tw, hi, pl.M, pl.P, L); break;
+      case 9: fft_pass2<9>(b0, b1, tw, hi, pl.M, pl.P, L); break;
       case 3: fft_pass2<3>(b0, b1, tw, hi, pl.M, pl.P, L); break;
       default: fft_pass2<2>(b0, b1, tw, hi, pl.M, pl.P, L); break;
     }

@@ -78,10 +78,14 @@ int get_fft_plan(size_t min_len, FftPlan* out) {
   FftPlan pl{};
   pl.M = M;
   pl.P = M / 2;
-  // radix schedule: 3s first, then 16s, then the remainder (16 * 2 as 8 * 4)
+  // radix schedule: 9s and 3s first, then 16s, then the remainder (16 * 2 as 8 * 4)
   std::vector<int> radix;
   int rem = pl.P;
-  while (rem % 3 == 0) {
+  while (rem % 9 == 0) {  // 3 * 3 as one radix-9 pass (one shared-memory sweep fewer)
+    radix.push_back(9);
+    rem /= 9;
+  }
+  if (rem % 3 == 0) {
     radix.push_back(3);
     rem /= 3;
   }
