@@ -167,6 +167,33 @@ def test_dense_c4_full_size(cuda):
         assert abs(float(got[d] @ b) - m1) <= 1e-3 * norm * jt, (d, float(got[d] @ b), m1)
 
 
+def test_dense_beyond_2e32_elements(cuda):
+    """64-bit indexing: a 1024 x 2048 x 2049 fp32 tensor (4.3e9 elements, 17 GB)
+    through the fp32 fixed-point kernel, per bucket against the fp64 kernel on
+    the widened tensor and by the zeroth moment (see test_dense_c4_full_size)."""
+    import ctypes as C
+    from paper_2106_13062_b200 import _lib as L
+    dims = [1024, 2048, 2049]
+    n = int(np.prod(dims))
+    assert n > 2 ** 32
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    L.check(L.lib().st_device_gaussian(L.ST_F32, 77, n, C.c_void_p(x.data_ptr()), None))
+    fams = st.families_for(dims, st.EstimatorConfig(4096, 2, 11))
+    got = st.fcs_dense_batched(st.DenseTensor(dims, x), fams)
+    x64 = x.double()
+    del x
+    ref = st.fcs_dense_batched(st.DenseTensor(dims, x64), fams)
+    rel_close(got, ref.cpu().numpy(), RTOL32)
+    X = x64.view(dims[2], dims[1], dims[0])
+    norm = float(torch.linalg.vector_norm(x64))
+    for d, f in enumerate(fams):
+        s = [torch.tensor(f.pair(k).sign_map(), dtype=torch.float64, device="cuda") for k in range(3)]
+        m0 = float(((X @ s[0]) @ s[1]) @ s[2])
+        assert abs(float(got[d].sum()) - m0) <= 1e-3 * norm, (d, float(got[d].sum()), m0)
+    del x64, X
+    torch.cuda.empty_cache()
+
+
 def test_dense_global_fallback(cuda):
     """fp64 sketch larger than shared memory (J~ = 29998 -> 240 KB): global path."""
     rng = np.random.default_rng(5)
