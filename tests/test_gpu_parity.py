@@ -102,6 +102,22 @@ def test_dense_integer_bitexact(cuda, shape, J, D, dtype):
         assert (got[d] == O.fcs_dense(x.astype(np.float64), b, s, j)).all()
 
 
+@pytest.mark.parametrize("i0", [4, 100, 128, 200, 256, 500, 512, 1000, 1024, 1028, 2048, 6])
+@pytest.mark.parametrize("D", [1, 3])
+def test_dense_f32_kernel_variants(cuda, i0, D):
+    """Every fp32 kernel variant by fiber length: guarded / full-vector fixed
+    point with 1-8 vectors per lane, the bank-grouped order (D >= 3, full
+    vectors), unaligned fibers (I_0 % 4 != 0) and fibers beyond 1024 elements
+    (float-atomic kernel). Integer data: fixed point is exact, so bit-exact."""
+    rng = np.random.default_rng(i0 + D)
+    x = rng.integers(-8, 9, size=(i0, 6, 5)).astype(np.float32)
+    fams = st.families_for([i0, 6, 5], st.EstimatorConfig(300, D, 5))
+    got = st.fcs_dense_batched(st.DenseTensor.from_array(x), fams).cpu().numpy()
+    for d, f in enumerate(fams):
+        b, s_, j = oracle_family(f)
+        assert (got[d] == O.fcs_dense(x.astype(np.float64), b, s_, j)).all(), d
+
+
 def test_dense_c1_full(cuda):
     """BASELINE config 1: 100^3 fp64, J=1000, D=1 -> 2998 buckets."""
     c = configs.C1
