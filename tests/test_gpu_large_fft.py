@@ -125,6 +125,31 @@ def test_plan_boundaries(cuda, n):
         rel_close(got[r], np.convolve(a[r], b[r]))
 
 
+def _one_cta_sizes():
+    out = []
+    for b in range(7):
+        m = 16 * 3 ** b
+        while m <= 12288:
+            out.append(m)
+            m *= 2
+    return sorted(out)
+
+
+@pytest.mark.parametrize("M", _one_cta_sizes())
+def test_every_one_cta_plan(cuda, M):
+    """Every one-CTA transform length M = 16 3^b 2^a <= 12288: all radix
+    schedules (radix-9 / radix-3 head, 16s, the 8 x 4 and 4 x 4 tails) and the
+    fused pair pass with every last radix, through a length-M linear convolution
+    (forward x 2, product, inverse)."""
+    rng = np.random.default_rng(M)
+    la = M // 2 + 1
+    lb = M - la + 1
+    a, b = rng.standard_normal((2, la)), rng.standard_normal((2, lb))
+    got = st.convolve_pairs(torch.from_numpy(a), torch.from_numpy(b))
+    for r in range(2):
+        rel_close(got[r], np.convolve(a[r], b[r]))
+
+
 def test_engine_tiny_hash(cuda):
     """J = 1 (J~ = 1): every entry lands in bucket 0 for FCS and TS."""
     rng = np.random.default_rng(2)
