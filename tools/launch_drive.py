@@ -90,7 +90,7 @@ def main(which):
         st.idft_real(st.dft(rng.standard_normal(40), 45))
         st.median_reduce([rng.standard_normal(10) for _ in range(70)])
     torch.cuda.synchronize()
-    print("sanitize drive ok:", [r for r in ran if r in which or "all" in which])
+    print("launch drive ok:", [r for r in ran if r in which or "all" in which])
 
 
 if __name__ == "__main__":
