@@ -137,10 +137,11 @@ def _one_cta_sizes():
 
 @pytest.mark.parametrize("M", _one_cta_sizes())
 def test_every_one_cta_plan(cuda, M):
-    """Every one-CTA transform length M = 16 3^b 2^a <= 12288: all radix
-    schedules (radix-9 / radix-3 head, 16s, the 8 x 4 and 4 x 4 tails) and the
-    fused pair pass with every last radix, through a length-M linear convolution
-    (forward x 2, product, inverse)."""
+    """Convolution lengths M = 16 3^b 2^a <= 12288, b <= 6: for b <= 2 these are
+    exactly the one-CTA plan lengths (fft_plan.cu choose_m) — every radix
+    schedule (radix-9 / radix-3 head, 16s, the 8 x 4 and 4 x 4 tails) and the
+    fused pair pass with every last radix; larger b exercise the round-up to
+    the next plan. Forward x 2, product, inverse."""
     rng = np.random.default_rng(M)
     la = M // 2 + 1
     lb = M - la + 1
