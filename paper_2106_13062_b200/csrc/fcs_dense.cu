@@ -174,12 +174,13 @@ __global__ void fx_scale_kernel(FxStats* st, double n_center) {
 // permutation before use, so a stale or torn entry can cost speed, never
 // correctness); on a miss (2) greedy construction — per step, seed with the
 // worst remaining line, then add the line that minimises the group cost —
-// then (3) kFxSearchIters rounds of parallel swap search: each warp prices
+// then (3) up to kFxSearchIters rounds of parallel swap search (scaled with
+// the tensor size so the one-off search stays a few % of one sketch): each warp prices
 // one pseudo-random swap of two lines between two steps (lane = bank), the
 // best swap is applied if it does not raise the cost (plateau moves allowed).
 // Config-4 tables: greedy ~2.9, searched ~2.7 wavefronts per ATOMS
 // (random order ~3.6).
-constexpr int kFxSearchIters = 256;
+constexpr int kFxSearchIters = 256;  // search rounds for a 2^30-element tensor (scaled down below)
 constexpr int kFxCacheSlots = 64;
 struct FxGroupEntry {
   unsigned long long fp;
@@ -196,7 +197,8 @@ __device__ __forceinline__ unsigned long long fx_mix(unsigned long long x) {
 
 __global__ void __launch_bounds__(1024) fx_group_kernel(const uint32_t* __restrict__ packed,
                                                         uint32_t fam_stride, uint32_t i0_shift,
-                                                        int nsteps, uint8_t* __restrict__ groups,
+                                                        int nsteps, int iters,
+                                                        uint8_t* __restrict__ groups,
                                                         FxGroupEntry* __restrict__ cache) {
   __shared__ uint8_t lh[32][4][32];  // [line][k][bank] element counts
   __shared__ int h[4][32];           // current group's counts (greedy)
@@ -306,13 +308,16 @@ __global__ void __launch_bounds__(1024) fx_group_kernel(const uint32_t* __restri
     if (lane == 0) cost[w] = c;
   }
   __syncthreads();
-  for (int it = 0; it < (nsteps >= 2 ? kFxSearchIters : 0); ++it) {
+  for (int it = 0; it < (nsteps >= 2 ? iters : 0); ++it) {
     {
-      const unsigned long long r = fx_mix((static_cast<unsigned long long>(d) << 40) ^
-                                          (static_cast<unsigned long long>(it) << 8) ^ w);
-      const int j1 = static_cast<int>(r % nsteps);
-      const int j2 = (j1 + 1 + static_cast<int>((r >> 16) % (nsteps - 1))) % nsteps;
-      const int q1 = static_cast<int>((r >> 32) & 3), q2 = static_cast<int>((r >> 40) & 3);
+      // 32-bit draws; nsteps is a power of two (2, 4 or 8)
+      const uint32_t r = static_cast<uint32_t>(
+          fx_mix((static_cast<unsigned long long>(d) << 40) ^ (static_cast<unsigned long long>(it) << 8) ^
+                 static_cast<unsigned long long>(w)));
+      const int j1 = static_cast<int>(r & static_cast<uint32_t>(nsteps - 1));
+      const int j2 = (j1 + 1 + static_cast<int>((r >> 8) % static_cast<uint32_t>(nsteps - 1))) &
+                     (nsteps - 1);
+      const int q1 = static_cast<int>((r >> 20) & 3), q2 = static_cast<int>((r >> 24) & 3);
       const int a = g[j1][q1], b = g[j2][q2];
       int c1 = 0, c2 = 0;
 #pragma unroll
@@ -820,8 +825,10 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
                                           align_up(sizeof(FxStats)));
       FxGroupEntry* cache = nullptr;
       if (int rc = fx_group_cache(&cache)) return rc;
-      fx_group_kernel<<<a.D, 1024, 0, st>>>(packed, a.fam_stride, a.i0_shift, nv_full, groups,
-                                            cache);
+      const uint64_t elems = a.fibers * a.dims[0];
+      const int iters = static_cast<int>(std::min<uint64_t>(kFxSearchIters, elems >> 22));
+      fx_group_kernel<<<a.D, 1024, 0, st>>>(packed, a.fam_stride, a.i0_shift, nv_full, iters,
+                                            groups, cache);
       FCS_CUDA_TRY(cudaGetLastError());
     }
     fx_kernel(p.nv, p.group)<<<static_cast<unsigned>(nchunk * a.D), p.threads, p.smem_bytes, st>>>(
