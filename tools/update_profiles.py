@@ -32,7 +32,7 @@ def launches(tag):
         if x["Metric Name"] == "gpu__time_duration.sum":
             v = float(x["Metric Value"].replace(",", ""))
             u = x["Metric Unit"]
-            v = v / 1e3 if u == "usecond" else (v / 1e6 if u == "nsecond" else v)
+            v = v / 1e3 if u in ("usecond", "us") else (v / 1e6 if u in ("nsecond", "ns") else v)
             agg[x["Kernel Name"].split("(")[0]].append(v)
     tot = sum(sum(v) for v in agg.values())
     lines = ["ncu --metrics gpu__time_duration.sum --clock-control none, command:",
