@@ -45,6 +45,16 @@ struct FxStats {
   double sumsq;
   double count;
 };
+// Per-CTA partial of the sample (fx_sample_kernel), reduced in a fixed order
+// by fx_scale_kernel: no contended atomics, and the chosen scale (hence the
+// fixed-point rounding) is the same on every run.
+struct FxPart {
+  float mx;
+  float pad;
+  double s, s2, cnt;
+};
+constexpr int kFxSampleCtas = 1024;  // threads of fx_scale_kernel
+constexpr int kFxMaxSample = 2048;   // sampled fibers = sample CTAs = partials
 
 // ------------------------------------------------------------------ kernels
 // Generic block-private kernel (any shape, fp32 or fp64): one family per CTA,
@@ -96,10 +106,10 @@ __global__ void __launch_bounds__(1024) fcs_dense_smem_kernel(DenseArgs a,
 }
 
 // Sampled max|x|, sum and sum of squares over up to `nsample` evenly spaced
-// fibers: one fiber per CTA, a block reduction, then one set of global
-// atomics per CTA (per-warp atomics on four words serialise at L2).
+// fibers: CTA b takes fibers b, b + gridDim.x, ... (one each at the usual
+// grid of nsample CTAs) and writes its partial.
 __global__ void fx_sample_kernel(DenseArgs a, const float* __restrict__ t, uint64_t nsample,
-                                 FxStats* __restrict__ st) {
+                                 FxPart* __restrict__ parts) {
   __shared__ float smx[32];
   __shared__ double ss[32], ss2[32], scnt[32];
   const uint32_t i0n = a.dims[0];
@@ -137,17 +147,59 @@ __global__ void fx_sample_kernel(DenseArgs a, const float* __restrict__ t, uint6
       s2 += ss2[q];
       cnt += scnt[q];
     }
-    atomicMax(&st->maxbits, __float_as_uint(mx));
-    atomicAdd(&st->sum, s);
-    atomicAdd(&st->sumsq, s2);
-    atomicAdd(&st->count, cnt);
+    FxPart pt;
+    pt.mx = mx;
+    pt.pad = 0.f;
+    pt.s = s;
+    pt.s2 = s2;
+    pt.cnt = cnt;
+    parts[blockIdx.x] = pt;
   }
 }
 
 // Fixed-point exponent: the largest S with a comfortable margin between the
 // expected largest per-CTA bucket partial and 2^31 (bias * N + 8 sigma sqrt(N)
 // + max, N = the expected count of elements a CTA adds to its busiest bucket).
-__global__ void fx_scale_kernel(FxStats* st, double n_center) {
+__global__ void __launch_bounds__(kFxSampleCtas) fx_scale_kernel(const FxPart* __restrict__ parts,
+                                                                 int nparts, FxStats* st,
+                                                                 double n_center) {
+  // fixed-order reduction of the sample partials (thread t: part t; xor tree)
+  __shared__ float smx[kFxSampleCtas / 32];
+  __shared__ double ss[kFxSampleCtas / 32], ss2[kFxSampleCtas / 32], scnt[kFxSampleCtas / 32];
+  float pm = 0.f;
+  double ps = 0.0, ps2 = 0.0, pc = 0.0;
+  for (int q = threadIdx.x; q < nparts; q += blockDim.x) {
+    const FxPart pt = parts[q];
+    pm = fmaxf(pm, pt.mx);
+    ps += pt.s;
+    ps2 += pt.s2;
+    pc += pt.cnt;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, o));
+    ps += __shfl_xor_sync(0xffffffffu, ps, o);
+    ps2 += __shfl_xor_sync(0xffffffffu, ps2, o);
+    pc += __shfl_xor_sync(0xffffffffu, pc, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    smx[threadIdx.x >> 5] = pm;
+    ss[threadIdx.x >> 5] = ps;
+    ss2[threadIdx.x >> 5] = ps2;
+    scnt[threadIdx.x >> 5] = pc;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int q = 1; q < static_cast<int>(blockDim.x >> 5); ++q) {
+    pm = fmaxf(pm, smx[q]);
+    ps += ss[q];
+    ps2 += ss2[q];
+    pc += scnt[q];
+  }
+  st->maxbits = __float_as_uint(pm);
+  st->sum = ps;
+  st->sumsq = ps2;
+  st->count = pc;
   const double n = fmax(st->count, 1.0);
   const double mean = st->sum / n;
   const double rms = sqrt(fmax(st->sumsq / n, 0.0));
@@ -574,10 +626,22 @@ __global__ void reduce_fx_kernel(const int32_t* __restrict__ part, const int* __
   const int d = static_cast<int>(i / jt);
   const double inv = ldexp(1.0, -st->S);
   double acc = accumulate ? out[i] : 0.0;
-  for (uint64_t c = 0; c < nchunk; ++c) {
-    const int32_t w = part[c * per + i];
-    acc += flags[c * D + d] ? static_cast<double>(__int_as_float(w)) : static_cast<double>(w) * inv;
+  auto term = [&](int32_t w, int fl) {
+    return fl ? static_cast<double>(__int_as_float(w)) : static_cast<double>(w) * inv;
+  };
+  uint64_t c = 0;
+  for (; c + 4 <= nchunk; c += 4) {  // four partials in flight, summed in chunk order
+    int32_t w[4];
+    int fl[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      w[u] = part[(c + u) * per + i];
+      fl[u] = flags[(c + u) * D + d];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc += term(w[u], fl[u]);
   }
+  for (; c < nchunk; ++c) acc += term(part[c * per + i], flags[c * D + d]);
   out[i] = acc;
 }
 
@@ -731,7 +795,8 @@ int make_plan(const DenseArgs& a, Plan* p) {
   p->nchunk = nchunk;
   p->part_bytes = nchunk * a.D * static_cast<size_t>(a.jt) * sizeof(Tacc);
   p->ws = align_up(p->part_bytes) + align_up(nchunk * a.D * sizeof(int)) +
-          align_up(sizeof(FxStats)) + align_up(static_cast<size_t>(a.D) * 32);
+          align_up(sizeof(FxStats)) + align_up(static_cast<size_t>(a.D) * 32) +
+          align_up(kFxMaxSample * sizeof(FxPart));
   return ST_OK;
 }
 
@@ -808,13 +873,16 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
     auto* flags = reinterpret_cast<int*>(base + align_up(p.part_bytes));
     auto* stats = reinterpret_cast<FxStats*>(base + align_up(p.part_bytes) +
                                              align_up(p.nchunk * a.D * sizeof(int)));
-    FCS_CUDA_TRY(cudaMemsetAsync(stats, 0, sizeof(FxStats), st));
-    const uint64_t nsample = std::min<uint64_t>(a.fibers, 2048);
-    fx_sample_kernel<<<static_cast<unsigned>(nsample), 256, 0, st>>>(
-        a, reinterpret_cast<const float*>(t), nsample, stats);
+    auto* parts = reinterpret_cast<FxPart*>(base + align_up(p.part_bytes) +
+                                            align_up(p.nchunk * a.D * sizeof(int)) +
+                                            align_up(sizeof(FxStats)) +
+                                            align_up(static_cast<size_t>(a.D) * 32));
+    const uint64_t nsample = std::min<uint64_t>(a.fibers, kFxMaxSample);
+    const int nparts = static_cast<int>(nsample);  // one fiber per sample CTA
+    fx_sample_kernel<<<nparts, 256, 0, st>>>(a, reinterpret_cast<const float*>(t), nsample, parts);
     FCS_CUDA_TRY(cudaGetLastError());
     const double per_cta = static_cast<double>(a.fibers_per_chunk) * a.dims[0];
-    fx_scale_kernel<<<1, 1, 0, st>>>(stats, 3.0 * per_cta / a.jt + 16.0);
+    fx_scale_kernel<<<1, kFxSampleCtas, 0, st>>>(parts, nparts, stats, 3.0 * per_cta / a.jt + 16.0);
     FCS_CUDA_TRY(cudaGetLastError());
     // bank-aware load order for the full-vector kernels (I_0 = 128 NV, NV >= 2)
     uint8_t* groups = nullptr;
