@@ -118,6 +118,19 @@ def test_dense_f32_kernel_variants(cuda, i0, D):
         assert (got[d] == O.fcs_dense(x.astype(np.float64), b, s_, j)).all(), d
 
 
+def test_dense_f32_deterministic(cuda):
+    """The fp32 fixed-point path is run-to-run bit-identical: integer shared
+    atomics, a fixed-order sample reduction for the scale and fixed-order
+    partial sums (K1)."""
+    rng = np.random.default_rng(21)
+    x = rng.standard_normal((1024, 40, 24)).astype(np.float32)
+    fams = st.families_for([1024, 40, 24], st.EstimatorConfig(4096, 4, 3))
+    t = st.DenseTensor.from_array(x)
+    first = st.fcs_dense_batched(t, fams)
+    for _ in range(3):
+        assert torch.equal(st.fcs_dense_batched(t, fams), first)
+
+
 def test_dense_c1_full(cuda):
     """BASELINE config 1: 100^3 fp64, J=1000, D=1 -> 2998 buckets."""
     c = configs.C1
