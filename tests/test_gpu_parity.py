@@ -196,6 +196,46 @@ def test_dense_c4_full_size(cuda):
         assert abs(float(got[d] @ b) - m1) <= 1e-3 * norm * jt, (d, float(got[d] @ b), m1)
 
 
+def test_dense_c4_full_vs_reference(cuda):
+    """The bench workload itself (config 4: 1024^3 fp32 device fill, J = 16384,
+    D = 4) against the unmodified reference's fcs_sketch (oracle/_ref) on the
+    same tensor widened to fp64: 64 slabs of 16 i_3-planes per family, each
+    sketched by the reference with the family's last-mode table sliced to the
+    slab (linearity), summed in slab order; all host threads.
+    Every bucket at the fp32 rule."""
+    import concurrent.futures as cf
+    import ctypes as C
+    from oracle import ref
+    from paper_2106_13062_b200 import _lib as L
+    c = configs.C4
+    dims = list(c.dims)
+    n = int(np.prod(dims))
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    L.check(L.lib().st_device_gaussian(L.ST_F32, c.seed, n, C.c_void_p(x.data_ptr()), None))
+    fams = st.families_for(dims, st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
+    got = st.fcs_dense_batched(st.DenseTensor(dims, x), fams).cpu().numpy()
+    host = x.cpu().numpy()
+    del x
+    per = dims[0] * dims[1]
+    tabs = [ref.hash_family(dims, c.hash_len, ref.family_seed(c.seed, d)) for d in range(c.sketch_count)]
+    slab = 16
+
+    def one(task):
+        s0, d = task
+        b, sg, _ = tabs[d]
+        t = host[s0 * per:(s0 + slab) * per].astype(np.float64).reshape(
+            (dims[0], dims[1], slab), order="F")
+        return ref.fcs_dense_tables(t, [b[0], b[1], b[2][s0:s0 + slab]],
+                                    [sg[0], sg[1], sg[2][s0:s0 + slab]], [c.hash_len] * 3)
+    tasks = [(s0, d) for d in range(c.sketch_count) for s0 in range(0, dims[2], slab)]
+    with cf.ThreadPoolExecutor(min(16, os.cpu_count() or 1)) as ex:
+        outs = list(ex.map(one, tasks))
+    want = np.zeros_like(got)
+    for (s0, d), o in zip(tasks, outs):  # slab order per family
+        want[d] += o
+    rel_close(got, want, RTOL32)
+
+
 def test_dense_beyond_2e32_elements(cuda):
     """64-bit indexing: a 1024 x 2048 x 2049 fp32 tensor (4.3e9 elements, 17 GB)
     through the fp32 fixed-point kernel, per bucket against the fp64 kernel on
