@@ -336,6 +336,42 @@ def test_cp_c2_full(cuda):
         rel_close(got[d], O.fcs_cp(w, fs, b, s, j), RTOL64)
 
 
+def test_full_configs_vs_reference(cuda):
+    """BASELINE configs 2, 3 and 5 at full size against the unmodified reference
+    (oracle/_ref, shim FFT): the CP sketch of config 2 (all 10 families), the
+    config-3 engine's T(I,u,u) / T(u,u,u) and deflation, and config 5's
+    Kronecker composition (reference fcs_sketch of each operand with its two
+    pairs, then the reference fft_convolve)."""
+    from oracle import ref
+    c = configs.C2
+    w, fs = configs.c2_cp(c)
+    fams = st.families_for(list(c.dims), st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
+    got = st.fcs_cp_batched(st.CpTensor(w, fs), fams).cpu().numpy()
+    for d in range(c.sketch_count):
+        rel_close(got[d], ref.fcs_cp(w, fs, c.hash_len, ref.family_seed(c.seed, d)), RTOL64)
+    c = configs.C3
+    t, lam, V = configs.c3_tensor(c)
+    eng = st.FcsEngine(st.DenseTensor.from_array(t), st.EstimatorConfig(c.hash_len, c.sketch_count,
+                                                                        c.seed))
+    reng = ref.Engine(t, c.hash_len, c.sketch_count, c.seed)
+    u = V[:, 0] + 0.2 * V[:, 3]
+    rel_close(eng.iuu(u), reng.iuu(u), RTOL64)
+    rel_close(eng.uuu(u), reng.uuu(u), RTOL64)
+    eng.deflate(lam[0], V[:, 0], V[:, 0], V[:, 0])
+    reng.deflate(lam[0], V[:, 0], V[:, 0], V[:, 0])
+    rel_close(eng.iuu(u), reng.iuu(u), RTOL64)
+    c = configs.C5
+    A, B = configs.c5_matrices(c)
+    fams = st.families_for(list(c.dims), st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
+    got = st.fcs_kron(A, B, fams).cpu().numpy()
+    for d in (0, 3, 7):
+        b, sg, _ = ref.hash_family(list(c.dims), c.hash_len, ref.family_seed(c.seed, d))
+        fa = ref.fcs_dense_tables(A, [b[0], b[1]], [sg[0], sg[1]], [c.hash_len] * 2)
+        fb = ref.fcs_dense_tables(B, [b[2], b[3]], [sg[2], sg[3]], [c.hash_len] * 2)
+        want = ref.fft_convolve([fa, fb], len(fa) + len(fb) - 1)
+        rel_close(got[d], want, RTOL64)
+
+
 def test_cp_vs_dense_path(cuda):
     """fcs_cp == fcs_dense(densify) on a random rank-5 10x12x14."""
     rng = np.random.default_rng(3)
