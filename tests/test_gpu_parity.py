@@ -337,12 +337,17 @@ def test_cp_c2_full(cuda):
 
 
 def test_full_configs_vs_reference(cuda):
-    """BASELINE configs 2, 3 and 5 at full size against the unmodified reference
-    (oracle/_ref, shim FFT): the CP sketch of config 2 (all 10 families), the
+    """BASELINE configs 1, 2, 3 and 5 at full size against the unmodified reference
+    (oracle/_ref, shim FFT): the dense sketch of config 1, the CP sketch of config 2 (all 10 families), the
     config-3 engine's T(I,u,u) / T(u,u,u) and deflation, and config 5's
     Kronecker composition (reference fcs_sketch of each operand with its two
     pairs, then the reference fft_convolve)."""
     from oracle import ref
+    c = configs.C1
+    x = configs.c1_tensor(c)
+    fams = st.families_for(list(c.dims), st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
+    got = st.fcs_dense_batched(st.DenseTensor.from_array(x), fams).cpu().numpy()
+    rel_close(got[0], ref.fcs_dense(x, c.hash_len, ref.family_seed(c.seed, 0)), RTOL64)
     c = configs.C2
     w, fs = configs.c2_cp(c)
     fams = st.families_for(list(c.dims), st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
