@@ -17,10 +17,14 @@
 // a scale 2^S chosen from a sampled bound on the partial sums; every
 // accumulate returns the old word, so overflow (and non-finite input) is
 // detected exactly, and a CTA that overflowed redoes its chunk with float
-// atomics. Rounding error per element <= 2^-(S+1) (K1).
+// atomics. Rounding error per element <= 2^-(S+1) (K1). The
+// sample statistics are reduced in a fixed order, so S — and the whole fixed-
+// point result — is the same on every run. For D >= 3 the fiber's 128-byte
+// lines are regrouped per load step to spread each ATOMS over more banks
+// (fx_group_kernel, searched once per table set and cached on the device).
 #include <algorithm>
-#include <mutex>
 #include <map>
+#include <mutex>
 #include <cstdlib>
 #include <cmath>
 
