@@ -766,12 +766,13 @@ int make_plan(const DenseArgs& a, Plan* p) {
   if (p->nv) {
     p->path = Path::Fx;
     p->threads = fx_threads(p->nv);
-    // the bank-aware order pays off when atomics bind (measured at D = 4: -2..3 %;
-    // D = 2: none); with one family
-    // the kernel is load-bound and keeps the immediate-offset loads.
+    // the bank-aware order pays off when atomics bind: with the searched
+    // groups, config-4 geometry D = 2: 1.333 -> 1.155 ms, D = 4: -4 %; with one
+    // family the kernel is load-bound (D = 1: 0.722 vs 0.725 ms) and keeps
+    // the immediate-offset loads.
     // ST_FX_NOGROUP=1 keeps the identity order (A/B probe).
     static const bool no_group = std::getenv("ST_FX_NOGROUP") != nullptr;
-    p->group = p->nv >= 6 && a.D >= 3 && !no_group;
+    p->group = p->nv >= 6 && a.D >= 2 && !no_group;
     auto k = fx_kernel(p->nv, p->group);
     FCS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(p->smem_bytes)));
