@@ -52,11 +52,15 @@ __device__ void scatter_cs(double2* buf, const double* __restrict__ vec, int I,
 }
 
 // Count sketch then the length-M real transform -> half spectrum in slot order.
+// zeroed: the caller already cleared buf (fused into its last read of it) and
+// synchronised.
 __device__ void rfft_of_cs(const Smem& sm, double2* buf, const FftPlan& pl,
                            const double* __restrict__ vec, int I,
-                           const uint32_t* __restrict__ tab) {
-  zero_slots(buf, pl.P);
-  __syncthreads();
+                           const uint32_t* __restrict__ tab, bool zeroed = false) {
+  if (!zeroed) {
+    zero_slots(buf, pl.P);
+    __syncthreads();
+  }
   scatter_cs(buf, vec, I, tab);
   __syncthreads();
   fft_forward_post(buf, pl, sm.tw);
@@ -199,10 +203,11 @@ __global__ void __launch_bounds__(kFftThreads, 2) cp_rank1_kernel(FftPlan pl, Cp
   for (int n = 0; n < a.order; ++n) {
     __syncthreads();
     rfft_of_cs(sm, sm.buf, pl, a.factors[n] + static_cast<size_t>(r) * a.dims[n], a.dims[n],
-               tab + a.tab_off[n]);
+               tab + a.tab_off[n], n > 0);
     const bool last = n + 1 == a.order;
     for (int s = tid(); s < pl.P; s += blockDim.x) {
       double2 v = sm.buf[swz(s)];
+      if (!last) sm.buf[swz(s)] = make_double2(0.0, 0.0);  // cleared for the next mode
       if (n > 0) v = hmul(q[s], v, s == 0);
       q[s] = last ? cscale(v, w) : v;
     }
@@ -338,10 +343,13 @@ __global__ void __launch_bounds__(kFftThreads, 2) iuv1_kernel(FftPlan pl, EngArg
   double2* scr = scratch + item * pl.P;
   rfft_of_cs(sm, sm.buf, pl, A + static_cast<size_t>(b) * e.dims[c1], e.dims[c1],
              tab + e.tab_off[c1]);
-  for (int s = tid(); s < pl.P; s += blockDim.x) scr[s] = sm.buf[swz(s)];
+  for (int s = tid(); s < pl.P; s += blockDim.x) {
+    scr[s] = sm.buf[swz(s)];
+    sm.buf[swz(s)] = make_double2(0.0, 0.0);  // cleared for cs_b
+  }
   __syncthreads();
   rfft_of_cs(sm, sm.buf, pl, B + static_cast<size_t>(b) * e.dims[c2], e.dims[c2],
-             tab + e.tab_off[c2]);
+             tab + e.tab_off[c2], true);
   for (int s = tid(); s < pl.P; s += blockDim.x) {
     const bool z = s == 0;
     const double2 ab = hmul(scr[s], sm.buf[swz(s)], z);
