@@ -19,7 +19,7 @@
 // detected exactly, and a CTA that overflowed redoes its chunk with float
 // atomics. Rounding error per element <= 2^-(S+1) (K1). The
 // sample statistics are reduced in a fixed order, so S — and the whole fixed-
-// point result — is the same on every run. For D >= 3 the fiber's 128-byte
+// point result — is the same on every run. For D >= 2 the fiber's 128-byte
 // lines are regrouped per load step to spread each ATOMS over more banks
 // (fx_group_kernel, searched once per table set and cached on the device).
 #include <algorithm>

@@ -103,10 +103,10 @@ def test_dense_integer_bitexact(cuda, shape, J, D, dtype):
 
 
 @pytest.mark.parametrize("i0", [4, 100, 128, 200, 256, 500, 512, 1000, 1024, 1028, 2048, 6])
-@pytest.mark.parametrize("D", [1, 3])
+@pytest.mark.parametrize("D", [1, 2, 3])
 def test_dense_f32_kernel_variants(cuda, i0, D):
     """Every fp32 kernel variant by fiber length: guarded / full-vector fixed
-    point with 1-8 vectors per lane, the bank-grouped order (D >= 3, full
+    point with 1-8 vectors per lane, the bank-grouped order (D >= 2, full
     vectors), unaligned fibers (I_0 % 4 != 0) and fibers beyond 1024 elements
     (float-atomic kernel). Integer data: fixed point is exact, so bit-exact."""
     rng = np.random.default_rng(i0 + D)
