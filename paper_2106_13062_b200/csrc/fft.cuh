@@ -569,6 +569,25 @@ __device__ __forceinline__ void load_twiddles(double2* sm_tw, const FftPlan& pl,
   }
 }
 
+// load_twiddles without the frequency -> slot table, as asynchronous 16-byte
+// global -> shared copies (cp.async): the caller overlaps the latency with
+// other work and calls cp_async_wait_all() before the first FFT pass.
+__device__ __forceinline__ void load_twiddles_async(double2* sm_tw, const FftPlan& pl) {
+  const int n = (1 << kTwLoBits) + pl.hi_count + (pl.nunits + 1) / 2;  // 16-byte chunks
+  const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(sm_tw));
+  const int ntw = (1 << kTwLoBits) + pl.hi_count;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const void* src = i < ntw ? static_cast<const void*>(pl.tw + i)
+                              : static_cast<const void*>(pl.units + 2 * (i - ntw));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * i), "l"(src)
+                 : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 // Pointwise helpers on the half-spectrum slot layout (slot 0 holds two reals).
 __device__ __forceinline__ double2 hmul(double2 a, double2 b, bool slot0) {
   return slot0 ? make_double2(a.x * b.x, a.y * b.y) : cmul(a, b);

@@ -141,6 +141,7 @@ int get_fft_plan(size_t min_len, FftPlan* out) {
     }
   }
   pl.nunits = static_cast<int>(units.size());
+  if (units.size() & 1) units.push_back(make_uint2(0, 0));  // whole 16-byte chunks (async copy)
   double2* dtw = nullptr;
   int* df2p = nullptr;
   FCS_CUDA_TRY(cudaMalloc(&dtw, tw.size() * sizeof(double2)));

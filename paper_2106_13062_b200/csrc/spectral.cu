@@ -62,6 +62,7 @@ __device__ void rfft_of_cs(const Smem& sm, double2* buf, const FftPlan& pl,
     __syncthreads();
   }
   scatter_cs(buf, vec, I, tab);
+  cp_async_wait_all();  // twiddles of load_twiddles_async (no-op otherwise)
   __syncthreads();
   fft_forward_post(buf, pl, sm.tw);
   __syncthreads();
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(kFftThreads, 2) cp_rank1_kernel(FftPlan pl, Cp
                                                                   const uint32_t* __restrict__ packed,
                                                                   double2* __restrict__ Q) {
   const Smem sm = carve(pl, 1);
-  load_twiddles(sm.tw, pl, false);
+  load_twiddles_async(sm.tw, pl);
   const int rl = blockIdx.x, d = blockIdx.y;
   const int r = a.r_begin + rl;
   const double w = a.weights[r];
@@ -334,8 +335,7 @@ __global__ void __launch_bounds__(kFftThreads, 2) iuv1_kernel(FftPlan pl, EngArg
                                                            const double* B, int c1, int c2, int f,
                                                            double2* scratch, double* est) {
   const Smem sm = carve(pl, 1);
-  load_twiddles(sm.tw, pl, false);
-  __syncthreads();
+  load_twiddles_async(sm.tw, pl);
   const int b = blockIdx.x, d = blockIdx.y;
   const size_t item = static_cast<size_t>(b) * e.D + d;
   const uint32_t* tab = e.packed + static_cast<size_t>(d) * e.fam_stride;
@@ -350,10 +350,26 @@ __global__ void __launch_bounds__(kFftThreads, 2) iuv1_kernel(FftPlan pl, EngArg
   __syncthreads();
   rfft_of_cs(sm, sm.buf, pl, B + static_cast<size_t>(b) * e.dims[c2], e.dims[c2],
              tab + e.tab_off[c2], true);
-  for (int s = tid(); s < pl.P; s += blockDim.x) {
-    const bool z = s == 0;
-    const double2 ab = hmul(scr[s], sm.buf[swz(s)], z);
-    sm.buf[swz(s)] = hmul(__ldg(S + s), hconj(ab, z), z);
+  // kU slots per thread per step with their scr / S loads (L2) in flight together
+  constexpr int kU = 4;
+  for (int s0 = tid(); s0 < pl.P; s0 += kU * blockDim.x) {
+    double2 fa[kU], sv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int s = s0 + u * blockDim.x;
+      if (s < pl.P) {
+        fa[u] = __ldcg(scr + s);
+        sv[u] = __ldg(S + s);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int s = s0 + u * blockDim.x;
+      if (s >= pl.P) continue;
+      const bool z = s == 0;
+      const double2 ab = hmul(fa[u], sm.buf[swz(s)], z);
+      sm.buf[swz(s)] = hmul(sv[u], hconj(ab, z), z);
+    }
   }
   irfft_in_place(sm, pl);
   const double inv = 1.0 / pl.P;
