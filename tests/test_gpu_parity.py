@@ -377,6 +377,29 @@ def test_full_configs_vs_reference(cuda):
         rel_close(got[d], want, RTOL64)
 
 
+def test_ts_hcs_full_size_vs_reference(cuda):
+    """The (f1) sketches at BASELINE sizes against the unmodified reference: TS
+    and HCS of the config-1 tensor (100^3, J = 1000 / 8 per mode), and the TS
+    engine at the config-3 geometry (200^3, J = 3000, D = 10): T(I,u,u), T(u,u,u)."""
+    from oracle import ref
+    c = configs.C1
+    x = configs.c1_tensor(c)
+    fam = st.HashFamily(list(c.dims), c.hash_len, st.family_seed(c.seed, 0))
+    b, sg, j = oracle_family(fam)
+    rel_close(st.ts_sketch(x, fam).values, ref.ts_dense_tables(x, b, sg, j), RTOL64)
+    fam8 = st.HashFamily(list(c.dims), 8, st.family_seed(c.seed, 1))
+    b8, s8, j8 = oracle_family(fam8)
+    rel_close(st.hcs_sketch(x, fam8).values, ref.hcs_dense_tables(x, b8, s8, j8), RTOL64)
+    c = configs.C3
+    t, lam, V = configs.c3_tensor(c)
+    eng = st.make_contraction_engine(st.DenseTensor.from_array(t), st.SketchBackend.TS,
+                                     st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
+    reng = ref.Engine(t, c.hash_len, c.sketch_count, c.seed, backend=ref.BACKEND_TS)
+    u = V[:, 1] - 0.3 * V[:, 2]
+    rel_close(eng.iuu(u), reng.iuu(u), RTOL64)
+    rel_close(eng.uuu(u), reng.uuu(u), RTOL64)
+
+
 def test_cp_vs_dense_path(cuda):
     """fcs_cp == fcs_dense(densify) on a random rank-5 10x12x14."""
     rng = np.random.default_rng(3)
