@@ -378,9 +378,10 @@ def test_full_configs_vs_reference(cuda):
 
 
 def test_ts_hcs_full_size_vs_reference(cuda):
-    """The (f1) sketches at BASELINE sizes against the unmodified reference: TS
-    and HCS of the config-1 tensor (100^3, J = 1000 / 8 per mode), and the TS
-    engine at the config-3 geometry (200^3, J = 3000, D = 10): T(I,u,u), T(u,u,u)."""
+    """The (f1) sketches and engines at BASELINE sizes against the unmodified
+    reference: TS and HCS of the config-1 tensor (100^3, J = 1000 / 8 per mode),
+    the TS and Plain engines at the config-3 geometry (200^3, J = 3000, D = 10):
+    T(I,u,u), T(u,u,u), and TS of the config-2 CP tensor."""
     from oracle import ref
     c = configs.C1
     x = configs.c1_tensor(c)
@@ -398,6 +399,20 @@ def test_ts_hcs_full_size_vs_reference(cuda):
     u = V[:, 1] - 0.3 * V[:, 2]
     rel_close(eng.iuu(u), reng.iuu(u), RTOL64)
     rel_close(eng.uuu(u), reng.uuu(u), RTOL64)
+    # the Plain (exact, the reference factory's default) engine at the same size
+    peng = st.make_contraction_engine(st.DenseTensor.from_array(t), st.SketchBackend.Plain,
+                                      st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
+    rpeng = ref.Engine(t, c.hash_len, c.sketch_count, c.seed, backend=ref.BACKEND_PLAIN)
+    rel_close(peng.iuu(u), rpeng.iuu(u), RTOL64)
+    rel_close(peng.uuu(u), rpeng.uuu(u), RTOL64)
+    # TS of the config-2 CP tensor (all ten families' first and last)
+    c = configs.C2
+    w, fs = configs.c2_cp(c)
+    cp = st.CpTensor(w, fs)
+    for d in (0, 9):
+        fam = st.HashFamily(list(c.dims), c.hash_len, st.family_seed(c.seed, d))
+        b, sg, j = oracle_family(fam)
+        rel_close(st.ts_sketch(cp, fam).values, ref.ts_cp_tables(w, fs, b, sg, j), RTOL64)
 
 
 def test_cp_vs_dense_path(cuda):
