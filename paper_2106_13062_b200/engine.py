@@ -104,7 +104,10 @@ class _DeviceEngine(ContractionEngine):
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            L.lib().st_engine_destroy(h)
+            try:
+                L.lib().st_engine_destroy(h)
+            except (TypeError, AttributeError):  # interpreter teardown: module globals gone
+                pass
             self._h = None
 
     def shape(self) -> List[int]:
