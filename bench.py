@@ -418,90 +418,166 @@ def secondary(x=None):
 
 
 # ------------------------------------------------------------ reference (CPU)
-def cpu_baseline(threads: int, target_s: float = 10.0, slabs: int = None):
-    """The reference's own fcs_sketch(DenseTensor) (oracle/_ref, unmodified
-    sources) on a bounded sample of the config-4 workload: the first `slabs`
-    i_3-slabs (1024 x 1024 x slabs) widened to fp64 (the reference is fp64-only),
-    all D = 4 families. Work is split over (slab chunk, family) tasks when
-    threads > 1 (harness-level, SPEC.md:234)."""
-    import concurrent.futures as cf
+# Both CPU legs run the UNMODIFIED reference sources (oracle/_ref) and import
+# nothing from paper_2106_13062_b200: the data come from the reference's own
+# SplitMix64/next_gaussian (rng.cpp:8-21), rounded through float32 (config 4
+# is fp32; the reference API is fp64-only, tensor.hpp:50-51), held in
+# resident reference DenseTensors built outside the timed region.
 
-    from oracle import ref
-    from paper_2106_13062_b200 import configs
+def _host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
-    lib = ref.lib()
-    seeds = [ref.family_seed(C4_SEED, d) for d in range(C4_D)]
-    per = C4_DIMS[0] * C4_DIMS[1]
 
-    def run(nslab, nthreads):
-        x = configs.host_gaussian(C4_SEED, per * nslab)  # fp64 sample
-        chunks = []
-        step = max(1, nslab // max(1, nthreads // C4_D if nthreads > C4_D else 1))
-        for s0 in range(0, nslab, step):
-            chunks.append((s0, min(nslab, s0 + step)))
-        tasks = [(c, d) for c in chunks for d in range(C4_D)]
-        jt = jt_of(C4_DIMS, C4_J)
+class RefC4:
+    """The config-4 workload on the reference: the 1024 i_3-slabs split into
+    `nchunks` contiguous chunks (each a resident DenseTensor), D = 4 families
+    (families_for(dims, {16384, 4, 4}), estimators.cpp:104-115). One pass =
+    fcs_sketch of every (chunk, family) with the chunk's slice of the family's
+    last-mode table (sharding by linearity), then the per-family
+    sum of the chunk partials."""
 
-        def one(task):
-            (s0, s1), d = task
-            # slab shard of the full 1024^3 family: the tables are the full ones,
-            # the reference needs a tensor whose shape matches the family, so a
-            # slab is sketched with the family over (1024, 1024, s1 - s0) whose
-            # last-mode table is the slice [s0, s1) — via explicit tables.
-            b, s, _ = ref.hash_family(C4_DIMS, C4_J, seeds[d])
-            bs = [b[0], b[1], b[2][s0:s1]]
-            ss = [s[0], s[1], s[2][s0:s1]]
-            t = x[s0 * per:s1 * per].reshape((1024, 1024, s1 - s0), order="F")
-            return ref.fcs_dense_tables(t, bs, ss, [C4_J] * 3)
+    def __init__(self, slabs: int, nchunks: int, threads: int):
+        import concurrent.futures as cf
 
+        from oracle import ref
+        self.ref = ref
+        self.threads = max(1, threads)
+        self.slabs = slabs
+        nchunks = max(1, min(nchunks, slabs))
+        bounds = [slabs * c // nchunks for c in range(nchunks + 1)]
+        self.chunks = [(bounds[c], bounds[c + 1]) for c in range(nchunks)]
+        self.fams = [ref.hash_family(C4_DIMS, C4_J, ref.family_seed(C4_SEED, d))[:2]
+                     for d in range(C4_D)]
+
+        def make(c):
+            s0, s1 = self.chunks[c]
+            return ref.ResidentTensor.gaussian(C4_SEED * 1000003 + s0, (1024, 1024, s1 - s0),
+                                               round_f32=True)
+        with cf.ThreadPoolExecutor(self.threads) as ex:
+            self.tensors = list(ex.map(make, range(nchunks)))
+        self.tasks = [(c, d) for c in range(nchunks) for d in range(C4_D)]
+        self.jt = jt_of(C4_DIMS, C4_J)
+        self.parts = np.zeros((len(self.tasks), self.jt))
+        self.pool = cf.ThreadPoolExecutor(self.threads) if self.threads > 1 else None
+
+    @property
+    def elements(self) -> int:
+        return C4_DIMS[0] * C4_DIMS[1] * self.slabs
+
+    def _one(self, k):
+        c, d = self.tasks[k]
+        s0, s1 = self.chunks[c]
+        b, s = self.fams[d]
+        self.tensors[c].fcs([b[0], b[1], b[2][s0:s1]], [s[0], s[1], s[2][s0:s1]], [C4_J] * 3,
+                            out=self.parts[k])
+
+    def run(self) -> float:
+        """One timed pass (wall clock, seconds); returns the elapsed time."""
         t0 = time.perf_counter()
-        if nthreads == 1:
-            outs = [one(tk) for tk in tasks]
+        if self.pool is None:
+            for k in range(len(self.tasks)):
+                self._one(k)
         else:
-            with cf.ThreadPoolExecutor(nthreads) as ex:
-                outs = list(ex.map(one, tasks))
+            list(self.pool.map(self._one, range(len(self.tasks))))
+        out = self.parts.reshape(len(self.chunks), C4_D, self.jt).sum(axis=0)
         dt = time.perf_counter() - t0
-        assert all(o.shape == (jt,) for o in outs)
+        assert out.shape == (C4_D, self.jt)
         return dt
 
-    if slabs is None:
-        dt1 = run(2, threads)
-        slabs = int(min(256, max(2, target_s / max(dt1, 1e-3) * 2)))
-    dt = run(slabs, threads)
-    elems = per * slabs
-    return {"value": elems / dt, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": f"1024x1024x{slabs} slab of config 4 (fp64-widened, {elems} elements), "
-                      f"D=4 families, reference fcs_sketch(DenseTensor) via oracle/_ref",
+    def close(self):
+        if self.pool is not None:
+            self.pool.shutdown()
+        for t in self.tensors:
+            t.close()
+        self.tensors = []
+
+
+def cpu_baseline(threads: int = 1, target_s: float = 10.0):
+    """The reference's own fcs_sketch(DenseTensor) (oracle/_ref) on a bounded
+    sample of config 4: the first `slabs` i_3-slabs (1024 x 1024 x slabs),
+    all D = 4 families, on `threads` host threads; median of 3 passes."""
+    probe = RefC4(4, 1, threads)
+    dt = probe.run()
+    probe.close()
+    slabs = int(min(256, max(4, target_s / 3.0 / max(dt, 1e-3) * 4)))
+    w = RefC4(slabs, max(1, threads), threads)
+    times = [w.run() for _ in range(3)]
+    w.close()
+    dt = statistics.median(times)
+    return {"value": w.elements / dt, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"1024x1024x{slabs} slab of config 4 ({w.elements} elements, fp32 values "
+                      f"widened to fp64), D=4 families, reference fcs_sketch(DenseTensor) via "
+                      f"oracle/_ref, median of 3",
             "seconds": dt}
 
 
 def run_reference(args):
+    """--impl reference: the reference CPU path on the FULL config-4 workload
+    per step (2^30 elements, D = 4), every host core (harness-level split into
+    slab chunks x families). Rank 0 only under torchrun."""
     rank, world, _ = env_rank()
     if rank != 0:
         return
-    nthreads = os.cpu_count() or 1
-    slabs = args.ref_slabs
+    cores = _host_cores()
+    w = RefC4(C4_DIMS[2], max(16, 2 * cores), cores)
     times = []
-    base = None
     for i in range(max(args.warmup, 0) + args.steps):
-        b = cpu_baseline(threads=nthreads, slabs=slabs)
+        dt = w.run()
         if i >= args.warmup:
-            times.append(b["seconds"])
-            base = b
-    per = C4_DIMS[0] * C4_DIMS[1] * slabs
+            times.append(dt)
+    w.close()
     ms = statistics.mean(times) * 1e3
-    value = per / (ms * 1e-3)
+    value = w.elements / (ms * 1e-3)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: seeded SplitMix64/Box-Muller N(0,1) host stream",
-            "config": {"workload": "c4: dense FCS 1024x1024x1024, J_n=16384, D=4 (bounded "
-                                   f"sample: {slabs} slabs of 1024x1024 per step)"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "reference",
-                             "sample": base["sample"]},
+            "data": "synthetic: seeded SplitMix64/Box-Muller N(0,1) (reference rng), fp32-rounded",
+            "config": {"workload": "c4: dense FCS 1024x1024x1024 float32, J_n=16384 (J~=49150), "
+                                   "D=4", "dims": list(C4_DIMS), "hash_len": C4_J,
+                       "sketch_count": C4_D, "composed_len": jt_of(C4_DIMS, C4_J),
+                       "seed": C4_SEED},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                             "sample": f"the full workload per step: {len(w.chunks)} slab chunks "
+                                       f"x {C4_D} families of fcs_sketch(DenseTensor) "
+                                       "(oracle/_ref, unmodified reference sources), fp64"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def run_probe(args):
+    """--probe (CPU test of the launcher): gloo all-reduce across the spawned
+    ranks, rank 0 prints the world it saw."""
+    import torch
+    import torch.distributed as dist
+    rank, world, _ = env_rank()
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.ones(1)
+        dist.all_reduce(t)
+        seen = int(t.item())
+        dist.destroy_process_group()
+    else:
+        seen = 1
+    if rank == 0:
+        print(json.dumps({"probe": True, "n_gpus": world, "ranks_seen": seen}), flush=True)
+
+
+def spawn(args) -> int:
+    """--gpus N > 1 without a torchrun environment: relaunch this script as N
+    ranks (one process per GPU) under torch.distributed.run on 127.0.0.1."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -512,11 +588,15 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--ref-slabs", type=int, default=16)
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--probe", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(args))
+    if args.probe:
+        run_probe(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_gpu(args)

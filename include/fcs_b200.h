@@ -104,9 +104,16 @@ size_t st_fcs_dense_workspace(int dtype, size_t order, const size_t* dims, size_
  * `tensor` holds the slab i_{N-1} in [last_begin, last_begin + last_count)
  * of the full tensor `dims` (contiguous because the last mode is slowest) —
  * the shard a rank owns under element sharding; pass 0 / dims[N-1] for the
- * whole tensor. dtype ST_F32 accumulates per-block partials in fp32 and
- * reduces them in fp64; ST_F64 is fp64 throughout. accumulate != 0 adds to
- * out instead of overwriting it.
+ * whole tensor. Numerics: dtype ST_F32 with I_0 % 4 == 0, I_0 <= 1024 and a
+ * 16-byte aligned tensor accumulates each CTA's partial sketch in int32 fixed
+ * point, value * 2^S rounded to nearest, with S chosen per call from a
+ * sampled bound on the partials (error <= 2^-(S+1) per element; the same S
+ * and result on every run); an element out of range, a non-finite element,
+ * a partial reaching 2^30, or a CTA whose partials all stay below 2^16 makes
+ * that CTA redo its chunk with fp32 shared-memory atomics (order-dependent
+ * rounding). Other fp32 shapes accumulate in fp32 atomics. ST_F64 accumulates
+ * in fp64. Partials are reduced in fp64 in a fixed order. accumulate != 0
+ * adds to out instead of overwriting it.
  * Replaces fcs_sketch(const DenseTensor&, const HashFamily&), sketch.cpp:187-201
  * (D calls, one per family). */
 int st_fcs_dense(int dtype, const void* tensor, size_t order, const size_t* dims,

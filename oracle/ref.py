@@ -526,3 +526,56 @@ def contract_pair(a: np.ndarray, b: np.ndarray, ma: int, mb: int) -> np.ndarray:
     _check(lib().ref_contract_pair(_ptr(xa), _sz(len(da)), _ptr(da), _ptr(xb), _sz(len(db)),
                                    _ptr(db), _sz(ma), _sz(mb), _ptr(out)))
     return out.reshape(shape, order="F")
+
+
+class ResidentTensor:
+    """A reference DenseTensor held in C++ (built once, outside any timed
+    region): ``fcs(buckets, signs, hash_lens)`` is exactly
+    fcs_sketch(const DenseTensor&, HashFamily(explicit pairs)), sketch.cpp:187-201.
+    ``gaussian`` fills it with SplitMix64(seed).next_gaussian() draws
+    (rng.cpp:8-21), rounded through float32 when ``round_f32``."""
+
+    def __init__(self, handle, dims):
+        if not handle:
+            raise RuntimeError(lib().ref_last_error().decode())
+        self._h = handle
+        self.dims = tuple(int(x) for x in dims)
+
+    @classmethod
+    def gaussian(cls, seed: int, dims, round_f32: bool = False):
+        L = lib()
+        L.ref_dense_gaussian.restype = _p
+        L.ref_dense_gaussian.argtypes = [_u64, _sz, _p, C.c_int]
+        dd = _dims(dims)
+        return cls(L.ref_dense_gaussian(_u64(seed), _sz(len(dd)), _ptr(dd), int(round_f32)), dims)
+
+    @classmethod
+    def from_array(cls, t: np.ndarray):
+        L = lib()
+        L.ref_dense_create.restype = _p
+        L.ref_dense_create.argtypes = [_p, _sz, _p]
+        dd = _dims(t.shape)
+        data = np.ascontiguousarray(np.asarray(t, np.float64).ravel(order="F"))
+        return cls(L.ref_dense_create(_ptr(data), _sz(len(dd)), _ptr(dd)), t.shape)
+
+    def fcs(self, buckets, signs, hash_lens, out: np.ndarray = None) -> np.ndarray:
+        L = lib()
+        fdims = _dims([len(x) for x in buckets])
+        b, s = _pack_tables(buckets, signs)
+        hl = _dims(hash_lens)
+        if out is None:
+            out = np.empty(max(int(hl.sum()) - len(hl) + 1, 1), np.float64)
+        _check(L.ref_fcs_dense_handle(_p(self._h), _sz(len(fdims)), _ptr(fdims), _ptr(b),
+                                      _ptr(s), _ptr(hl), _ptr(out)))
+        return out
+
+    def close(self):
+        if self._h:
+            lib().ref_dense_destroy(_p(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -539,3 +539,55 @@ int ref_contract_pair(const double* a, std::size_t oa, const std::size_t* da, co
   });
 }
 }  // extern "C"
+
+extern "C" {
+// Resident reference tensors for timing (bench.py cpu_baseline / --impl
+// reference): the DenseTensor is built once, outside the timed region, so a
+// timed call is exactly fcs_sketch(const DenseTensor&, const HashFamily&)
+// (sketch.cpp:187-201) plus the HashFamily construction from explicit tables.
+
+// DenseTensor(dims) filled with `count` SplitMix64(seed).next_gaussian()
+// draws (rng.cpp:8-21), optionally rounded to float32 and widened back (the
+// config-4 input is fp32; the reference API is fp64-only, tensor.hpp:50-51).
+void* ref_dense_gaussian(std::uint64_t seed, std::size_t order, const std::size_t* dims,
+                         int round_f32) {
+  try {
+    std::vector<std::size_t> shape = to_dims(order, dims);
+    std::size_t total = 1;
+    for (std::size_t d : shape) total *= d;
+    std::vector<double> v(total);
+    SplitMix64 rng(seed);
+    for (std::size_t i = 0; i < total; ++i) {
+      const double g = rng.next_gaussian();
+      v[i] = round_f32 ? static_cast<double>(static_cast<float>(g)) : g;
+    }
+    return new DenseTensor(std::move(shape), std::move(v));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+void* ref_dense_create(const double* data, std::size_t order, const std::size_t* dims) {
+  try {
+    return new DenseTensor(make_tensor(data, order, dims));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+void ref_dense_destroy(void* t) { delete static_cast<DenseTensor*>(t); }
+
+// fcs_sketch(t, HashFamily(explicit pairs)) on a resident tensor.
+int ref_fcs_dense_handle(const void* t, std::size_t fam_order, const std::size_t* fam_dims,
+                         const std::uint32_t* buckets, const std::int8_t* signs,
+                         const std::size_t* hash_lens, double* out) {
+  return guarded([&] {
+    copy_out(fcs_sketch(*static_cast<const DenseTensor*>(t),
+                        make_family(fam_order, fam_dims, buckets, signs, hash_lens))
+                 .values,
+             out);
+  });
+}
+}  // extern "C"

@@ -211,6 +211,18 @@ int st_fcs_dense_host(int dtype, const void* host_tensor, size_t order, const si
   if (int rc = hc->out.ensure(sketch_count * jt * sizeof(double))) return rc;
   if (int rc = hc->ws.ensure(ws)) return rc;
   double* dout = static_cast<double*>(hc->out.p);
+  // On any error return below, drain both streams before returning: an H2D
+  // copy may still be reading the caller's host buffer.
+  struct DrainOnError {
+    HostCtx* hc;
+    bool armed = true;
+    ~DrainOnError() {
+      if (armed) {
+        cudaStreamSynchronize(hc->copy);
+        cudaStreamSynchronize(hc->comp);
+      }
+    }
+  } drain{hc};
   if (int rc = st_family_tables(order, dims, hash_lens, sketch_count, master_seeds,
                                 static_cast<uint32_t*>(hc->tab.p), hc->comp))
     return rc;
@@ -236,6 +248,7 @@ int st_fcs_dense_host(int dtype, const void* host_tensor, size_t order, const si
   FCS_CUDA_TRY(cudaMemcpyAsync(host_out, dout, sketch_count * jt * sizeof(double),
                                cudaMemcpyDeviceToHost, hc->comp));
   FCS_CUDA_TRY(cudaStreamSynchronize(hc->comp));
+  drain.armed = false;
   return ST_OK;
 }
 

@@ -37,11 +37,30 @@ int launch_ts_extend(const double* in, int D, int jt, int J, double* ext, double
 
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
-// Stream-ordered scratch that only grows.
+// Stream-ordered scratch that only grows. Every use calls ensure() with its
+// stream; when the stream differs from the previous user's, the new stream
+// first waits (event) for the previous stream's work, so neither the buffer's
+// contents nor a cudaFreeAsync on growth can race a kernel still reading it.
 struct Scratch {
   void* p = nullptr;
   size_t bytes = 0;
+  cudaStream_t last = nullptr;
+  bool used = false;
   int ensure(size_t need, cudaStream_t st) {
+    if (used && last != st) {
+      cudaEvent_t ev;
+      bool ok = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess;
+      if (ok) {
+        ok = cudaEventRecord(ev, last) == cudaSuccess && cudaStreamWaitEvent(st, ev, 0) == cudaSuccess;
+        cudaEventDestroy(ev);
+      }
+      if (!ok) {  // the previous stream is gone: order against the whole device
+        cudaGetLastError();
+        FCS_CUDA_TRY(cudaDeviceSynchronize());
+      }
+    }
+    last = st;
+    used = true;
     if (need <= bytes) return ST_OK;
     if (p) FCS_CUDA_TRY(cudaFreeAsync(p, st));
     p = nullptr;

@@ -58,6 +58,12 @@ struct FxPart {
   double s, s2, cnt;
 };
 constexpr int kFxSampleCtas = 1024;  // threads of fx_scale_kernel
+constexpr int kFxMaxS = 120;         // largest fixed-point exponent (2^S finite in fp32)
+// A CTA whose largest |partial| stays below 2^kFxSmallBits (and is not zero)
+// saw data far smaller than the sample predicted: its fixed-point rounding
+// would be coarse relative to its own values, so it redoes its chunk with
+// float atomics, like an overflowing CTA (the c4 N(0,1) partials peak near 2^28).
+constexpr int kFxSmallBits = 16;
 constexpr int kFxMaxSample = 2048;   // sampled fibers = sample CTAs = partials
 
 // ------------------------------------------------------------------ kernels
@@ -209,11 +215,16 @@ __global__ void __launch_bounds__(kFxSampleCtas) fx_scale_kernel(const FxPart* _
   const double rms = sqrt(fmax(st->sumsq / n, 0.0));
   const double mx = static_cast<double>(__uint_as_float(st->maxbits));
   const double bound = fabs(mean) * n_center + 8.0 * rms * sqrt(n_center) + 2.0 * mx;
-  int S = 30;
+  // An all-zero sample gives the top exponent: any element of the tensor
+  // above 2^-(kFxMaxS - 21) then trips the exact range check and its CTA
+  // redoes the chunk with float atomics, so a sample that missed the data
+  // costs time, never accuracy. Small-magnitude data gets a large S (the
+  // scale 2^S stays a finite float up to 2^127).
+  int S = kFxMaxS;
   if (bound > 0.0) S = static_cast<int>(floor(log2(1073741824.0 / bound)));
   // single elements must stay below 2^21 (the kernel's exact-rounding range is 2^22)
   if (mx > 0.0) S = min(S, static_cast<int>(floor(log2(2097152.0 / mx))));
-  st->S = max(-60, min(30, S));
+  st->S = max(-100, min(kFxMaxS, S));
 }
 
 // Bank-aware load order for the fx kernel. A warp's fiber is 4*NV 128-byte
@@ -571,7 +582,18 @@ __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
   }
   ovf = (ovf_acc >> 31) | ((rng_acc >> 23) != 0);
 
-  const bool overflowed = __syncthreads_or(ovf);
+  bool overflowed = __syncthreads_or(ovf);
+  if (!overflowed) {  // precision guard (kFxSmallBits): all partials nonzero-but-tiny
+    int nz = 0, big = 0;
+    for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) {
+      const int32_t v = sk[b];
+      const uint32_t m = static_cast<uint32_t>(v < 0 ? -v : v);
+      nz |= m != 0u;
+      big |= (m >> kFxSmallBits) != 0u;
+    }
+    const bool any_big = __syncthreads_or(big);
+    overflowed = __syncthreads_or(nz) && !any_big;
+  }
   if (overflowed) {
     // Exact fallback for this CTA: float atomics over the same chunk.
     float* skf = reinterpret_cast<float*>(smem_raw);

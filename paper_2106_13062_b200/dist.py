@@ -122,6 +122,13 @@ def sharded_families(partial_fn: Callable[[int, int], torch.Tensor], D: int,
 
 
 # ------------------------------------------------------------- sharded RTPM
+def _comm_device(group=None) -> torch.device:
+    """Device for collective buffers: the current CUDA device under NCCL."""
+    if dist.is_initialized() and dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
 def _np(x):
     import numpy as np
     return x.detach().cpu().numpy() if torch.is_tensor(x) else np.asarray(x, np.float64)
@@ -172,16 +179,19 @@ def sharded_rtpm(engine, dim: int, target_rank: int, num_inits: int, num_iters: 
             for l in np.nonzero(alive)[0]:  # a stopped restart broke out of its loop
                 mine[l], alive[l] = normalize(Y[l])
         vals = _np(engine.uvw_batch(mine, mine, mine)) if hi > lo else np.zeros(0)
-        buf = torch.zeros((per, dim + 1), dtype=torch.float64)
+        # the exchange buffer lives where the process group's backend can
+        # reach it: the rank's GPU under NCCL (which rejects host tensors),
+        # host memory under gloo
+        buf = torch.zeros((per, dim + 1), dtype=torch.float64, device=_comm_device(group))
         buf[: hi - lo, 0] = torch.from_numpy(np.asarray(vals, np.float64).reshape(-1))
         buf[: hi - lo, 1:] = torch.from_numpy(mine)
         bufs = [buf]
-        if world > 1:
+        if dist.is_initialized():  # (also at world 1, so a 1-GPU NCCL run exercises it)
             bufs = [torch.empty_like(buf) for _ in range(world)]
             dist.all_gather(bufs, buf, group=group)
         allv = torch.cat([bufs[q][: shard_range(num_inits, q, world)[1] -
                                   shard_range(num_inits, q, world)[0]]
-                          for q in range(world)]).numpy()
+                          for q in range(world)]).cpu().numpy()
         best, best_value = None, -math.inf
         for l in range(num_inits):  # strict >, first wins (cpd.cpp:260)
             if allv[l, 0] > best_value:

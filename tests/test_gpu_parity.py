@@ -550,6 +550,42 @@ def test_dense_f32_outlier_fallback(cuda):
     x[200, 5, 1] = -7.5e8
     got, want = _f32_case(x)
     rel_close(got, want, RTOL32)
+    # the buckets that receive no outlier, against their own scale (the
+    # outliers' buckets would otherwise set the ||c||_inf pad for all of them)
+    fams = st.families_for(list(x.shape), st.EstimatorConfig(300, 3, 5))
+    mask = np.ones_like(want, bool)
+    for d, f in enumerate(fams):
+        for idx in ((17, 33, 40), (200, 5, 1)):
+            mask[d, sum(int(f.pair(n).bucket_map()[i]) for n, i in enumerate(idx))] = False
+    rel_close(got[mask], want[mask], RTOL32)
+
+
+@pytest.mark.parametrize("sigma", [1e-6, 1e-10, 1e-30])
+def test_dense_f32_small_magnitude(cuda, sigma):
+    """Small-magnitude fp32 data keeps its relative accuracy: the sampled
+    fixed-point exponent grows with 1/sigma (up to 2^120) instead of being
+    capped, so elements are not rounded away (advisor round 1)."""
+    rng = np.random.default_rng(31)
+    x = (sigma * rng.standard_normal((256, 64, 48))).astype(np.float32)
+    got, want = _f32_case(x.astype(np.float32))
+    rel_close(got, want, RTOL32)
+    big = np.abs(want) > 1e-3 * np.abs(want).max()
+    assert np.all(np.abs(got - want)[big] <= 1e-5 * np.abs(want)[big])
+
+
+@pytest.mark.parametrize("sigma", [1.0, 1e-30])
+def test_dense_f32_sample_misses_data(cuda, sigma):
+    """Every sampled fiber is zero (the scale sample reads fibers k * F / 2048,
+    here every 16th fiber): the exponent defaults to the top (2^120), so data
+    of ordinary magnitude trips the exact range check and each CTA redoes its
+    chunk with float atomics; tiny data is represented at full resolution."""
+    rng = np.random.default_rng(32)
+    x = (sigma * rng.standard_normal((128, 512, 64))).astype(np.float32)
+    fib = x.reshape(128, -1, order="F")
+    fib[:, ::16] = 0.0  # the sampled fibers (32768 fibers, 2048 samples)
+    x = fib.reshape(x.shape, order="F")
+    got, want = _f32_case(x, J=200)
+    rel_close(got, want, RTOL32)
 
 
 def test_dense_f32_biased_data(cuda):
