@@ -121,6 +121,15 @@ int st_fcs_dense(int dtype, const void* tensor, size_t order, const size_t* dims
                  const uint32_t* packed, const size_t* hash_lens, double* out, int accumulate,
                  void* workspace, size_t workspace_bytes, void* stream);
 
+/* HOST, synchronous diagnostics of the last ST_F32 st_fcs_dense call that
+ * used `workspace` with this shape: the fixed-point exponent S (INT_MIN when
+ * that call did not take the fixed-point kernel), the number of (chunk,
+ * family) CTAs that fell back to float atomics, and the number of CTAs. */
+int st_fcs_dense_report(size_t order, const size_t* dims, size_t last_count,
+                        size_t sketch_count, const size_t* hash_lens, const void* workspace,
+                        size_t workspace_bytes, int* fx_exponent, size_t* fallback_ctas,
+                        size_t* ctas);
+
 /* HOST-buffer convenience: K0 on the device from the seeds, then the host
  * tensor (the slab [last_begin, last_begin + last_count) of the last mode of
  * `dims`; pass 0 / dims[N-1] for the whole tensor) is copied H2D in chunks on

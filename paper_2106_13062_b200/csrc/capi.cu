@@ -171,6 +171,14 @@ size_t st_fcs_dense_workspace(int dtype, size_t order, const size_t* dims, size_
   return dense_workspace(dtype, order, dims, last_count, sketch_count, hash_lens);
 }
 
+int st_fcs_dense_report(size_t order, const size_t* dims, size_t last_count,
+                        size_t sketch_count, const size_t* hash_lens, const void* workspace,
+                        size_t workspace_bytes, int* fx_exponent, size_t* fallback_ctas,
+                        size_t* ctas) {
+  return dense_fx_report(order, dims, last_count, sketch_count, hash_lens, workspace,
+                         workspace_bytes, fx_exponent, fallback_ctas, ctas);
+}
+
 int st_fcs_dense(int dtype, const void* tensor, size_t order, const size_t* dims,
                  size_t last_begin, size_t last_count, size_t sketch_count,
                  const uint32_t* packed, const size_t* hash_lens, double* out, int accumulate,

@@ -23,6 +23,8 @@
 // lines are regrouped per load step to spread each ATOMS over more banks
 // (fx_group_kernel, searched once per table set and cached on the device).
 #include <algorithm>
+#include <climits>
+#include <vector>
 #include <map>
 #include <mutex>
 #include <cstdlib>
@@ -170,15 +172,56 @@ __global__ void fx_sample_kernel(DenseArgs a, const float* __restrict__ t, uint6
 // Fixed-point exponent: the largest S with a comfortable margin between the
 // expected largest per-CTA bucket partial and 2^31 (bias * N + 8 sigma sqrt(N)
 // + max, N = the expected count of elements a CTA adds to its busiest bucket).
+// The statistics are ROBUST to outliers: the nparts / 64 sampled fibers with
+// the largest |x| are left out, so one huge element (which its CTA handles by
+// the exact range check + float fallback) cannot coarsen the scale for the
+// whole tensor. The excluded set comes from a bitonic sort of the per-fiber
+// maxima with ties broken by index, so S is still the same on every run.
 __global__ void __launch_bounds__(kFxSampleCtas) fx_scale_kernel(const FxPart* __restrict__ parts,
                                                                  int nparts, FxStats* st,
                                                                  double n_center) {
-  // fixed-order reduction of the sample partials (thread t: part t; xor tree)
+  static_assert(kFxMaxSample == 2 * kFxSampleCtas, "two sort keys per thread");
+  __shared__ float key[kFxMaxSample];
+  __shared__ short kidx[kFxMaxSample];
+  __shared__ unsigned char kept[kFxMaxSample];
+  for (int q = threadIdx.x; q < kFxMaxSample; q += blockDim.x) {
+    key[q] = q < nparts ? parts[q].mx : -1.0f;  // NaN maxima are ignored (fmaxf), keys >= 0
+    kidx[q] = static_cast<short>(q);
+    kept[q] = 0;
+  }
+  __syncthreads();
+  // descending by key, ascending index on ties
+  for (int k = 2; k <= kFxMaxSample; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < kFxMaxSample; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool desc = (i & k) == 0;
+          const float ki = key[i], kl = key[l];
+          const bool l_first = kl > ki || (kl == ki && kidx[l] < kidx[i]);
+          if (desc == l_first) {
+            key[i] = kl;
+            key[l] = ki;
+            const short t = kidx[i];
+            kidx[i] = kidx[l];
+            kidx[l] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const int drop = nparts / 64;
+  for (int r = threadIdx.x; r < nparts; r += blockDim.x)
+    if (r >= drop) kept[kidx[r]] = 1;
+  __syncthreads();
+  // fixed-order reduction of the kept sample partials (thread t: parts t, t + 1024; xor tree)
   __shared__ float smx[kFxSampleCtas / 32];
   __shared__ double ss[kFxSampleCtas / 32], ss2[kFxSampleCtas / 32], scnt[kFxSampleCtas / 32];
   float pm = 0.f;
   double ps = 0.0, ps2 = 0.0, pc = 0.0;
   for (int q = threadIdx.x; q < nparts; q += blockDim.x) {
+    if (!kept[q]) continue;
     const FxPart pt = parts[q];
     pm = fmaxf(pm, pt.mx);
     ps += pt.s;
@@ -952,6 +995,36 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
 }
 
 }  // namespace
+
+// Diagnostics of the last fp32 fixed-point call that used `ws` (synchronous):
+// the exponent S, how many (chunk, family) CTAs fell back to float atomics,
+// and how many there were. *S = INT_MIN and counts 0 when the call did not
+// take the fixed-point kernel.
+int dense_fx_report(size_t order, const size_t* dims, size_t last_count, size_t D,
+                    const size_t* hash_lens, const void* ws, size_t ws_bytes, int* S,
+                    size_t* fallback, size_t* ctas) {
+  DenseArgs a;
+  if (int rc = fill_args(order, dims, 0, last_count, D, hash_lens, &a)) return rc;
+  *S = INT32_MIN;
+  *fallback = *ctas = 0;
+  Plan p;
+  if (int rc = make_plan<float, float>(a, &p)) return rc;
+  if (p.path != Path::Fx || a.fibers == 0) return ST_OK;
+  FCS_CHECK_ARG(ws != nullptr && ws_bytes >= p.ws, "st_fcs_dense_report: workspace too small");
+  a.fibers_per_chunk = (a.fibers + p.nchunk - 1) / p.nchunk;
+  const uint64_t nchunk = (a.fibers + a.fibers_per_chunk - 1) / a.fibers_per_chunk;
+  const char* base = static_cast<const char*>(ws);
+  std::vector<int> flags(nchunk * a.D);
+  FCS_CUDA_TRY(cudaMemcpy(flags.data(), base + align_up(p.part_bytes), flags.size() * sizeof(int),
+                          cudaMemcpyDeviceToHost));
+  FxStats stats;
+  FCS_CUDA_TRY(cudaMemcpy(&stats, base + align_up(p.part_bytes) + align_up(p.nchunk * a.D * sizeof(int)),
+                          sizeof(FxStats), cudaMemcpyDeviceToHost));
+  *S = stats.S;
+  *ctas = flags.size();
+  for (int f : flags) *fallback += f != 0;
+  return ST_OK;
+}
 
 size_t dense_workspace(int dtype, size_t order, const size_t* dims, size_t last_count, size_t D,
                        const size_t* hash_lens, int kind, size_t out_len) {

@@ -196,26 +196,36 @@ def test_dense_c4_full_size(cuda):
         assert abs(float(got[d] @ b) - m1) <= 1e-3 * norm * jt, (d, float(got[d] @ b), m1)
 
 
-def test_dense_c4_full_vs_reference(cuda):
-    """The bench workload itself (config 4: 1024^3 fp32 device fill, J = 16384,
-    D = 4) against the unmodified reference's fcs_sketch (oracle/_ref) on the
-    same tensor widened to fp64: 64 slabs of 16 i_3-planes per family, each
-    sketched by the reference with the family's last-mode table sliced to the
-    slab (linearity), summed in slab order; all host threads.
-    Every bucket at the fp32 rule."""
+def _c4_gpu_and_reference(x, report=False):
+    """K1 on the device-resident config-4-geometry tensor x (fp32, flat) and
+    the unmodified reference's fcs_sketch (oracle/_ref) on the same values
+    widened to fp64: 64 slabs of 16 i_3-planes per family, each sketched by the
+    reference with the family's last-mode table sliced to the slab (linearity,
+    SPEC.md:224), summed in slab order; all host threads."""
     import concurrent.futures as cf
     import ctypes as C
     from oracle import ref
     from paper_2106_13062_b200 import _lib as L
     c = configs.C4
     dims = list(c.dims)
-    n = int(np.prod(dims))
-    x = torch.empty(n, dtype=torch.float32, device="cuda")
-    L.check(L.lib().st_device_gaussian(L.ST_F32, c.seed, n, C.c_void_p(x.data_ptr()), None))
     fams = st.families_for(dims, st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
-    got = st.fcs_dense_batched(st.DenseTensor(dims, x), fams).cpu().numpy()
+    lib = L.lib()
+    packed = st.packed_families(fams)
+    dims_a, lens_a = L.size_array(dims), L.size_array([c.hash_len] * 3)
+    ws_bytes = lib.st_fcs_dense_workspace(L.ST_F32, 3, dims_a, dims[2], c.sketch_count, lens_a)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    out = torch.empty((c.sketch_count, fams[0].composed_len()), dtype=torch.float64,
+                      device="cuda")
+    L.check(lib.st_fcs_dense(L.ST_F32, C.c_void_p(x.data_ptr()), 3, dims_a, 0, dims[2],
+                             c.sketch_count, C.c_void_p(packed.data_ptr()), lens_a,
+                             C.c_void_p(out.data_ptr()), 0, C.c_void_p(ws.data_ptr()), ws_bytes,
+                             None))
+    got = out.cpu().numpy()
+    S, fb, ctas = C.c_int(0), C.c_size_t(0), C.c_size_t(0)
+    L.check(lib.st_fcs_dense_report(3, dims_a, dims[2], c.sketch_count, lens_a,
+                                    C.c_void_p(ws.data_ptr()), ws_bytes, C.byref(S), C.byref(fb),
+                                    C.byref(ctas)))
     host = x.cpu().numpy()
-    del x
     per = dims[0] * dims[1]
     tabs = [ref.hash_family(dims, c.hash_len, ref.family_seed(c.seed, d)) for d in range(c.sketch_count)]
     slab = 16
@@ -233,7 +243,61 @@ def test_dense_c4_full_vs_reference(cuda):
     want = np.zeros_like(got)
     for (s0, d), o in zip(tasks, outs):  # slab order per family
         want[d] += o
+    return got, want, {"S": S.value, "fallback_ctas": fb.value, "ctas": ctas.value}
+
+
+def precision(got, want):
+    """max |g-c| / ||c||_inf and the pure relative error on the buckets with
+    |c| > 1e-3 ||c||_inf (per family)."""
+    inf = np.abs(want).max(axis=-1, keepdims=True)
+    big = np.abs(want) > 1e-3 * inf
+    err = np.abs(got - want)
+    return float((err / inf).max()), float((err[big] / np.abs(want[big])).max())
+
+
+def test_dense_c4_full_vs_reference(cuda):
+    """The bench workload itself (config 4: 1024^3 fp32 device fill, J = 16384,
+    D = 4) against the unmodified reference; every bucket at the fp32 rule, and
+    the pure relative error of the large buckets below 1e-5 (the fixed point
+    at S = 18 for N(0,1) data)."""
+    import ctypes as C
+    from paper_2106_13062_b200 import _lib as L
+    c = configs.C4
+    n = int(np.prod(c.dims))
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    L.check(L.lib().st_device_gaussian(L.ST_F32, c.seed, n, C.c_void_p(x.data_ptr()), None))
+    got, want, rep = _c4_gpu_and_reference(x)
+    del x
     rel_close(got, want, RTOL32)
+    inf_err, rel_big = precision(got, want)
+    assert rep["fallback_ctas"] == 0 and rel_big < 1e-5, (rep, inf_err, rel_big)
+
+
+@pytest.mark.parametrize("kind", ["lognormal4", "sparse_outliers"])
+def test_dense_c4_wide_range_vs_reference(cuda, kind):
+    """Wide-dynamic-range fp32 data at config-4 geometry:
+    lognormal sigma = 4 (values e^(4 N(0,1)), up to ~1e10), and N(0,1) with
+    4096 outliers of magnitude 1e6..1e9 at random positions. Every bucket at
+    the fp32 rule and the large buckets to 1e-4 relative."""
+    import ctypes as C
+    from paper_2106_13062_b200 import _lib as L
+    c = configs.C4
+    n = int(np.prod(c.dims))
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    L.check(L.lib().st_device_gaussian(L.ST_F32, c.seed + 11, n, C.c_void_p(x.data_ptr()), None))
+    if kind == "lognormal4":
+        x.mul_(4.0).exp_()
+    else:
+        g = torch.Generator(device="cuda").manual_seed(7)
+        pos = torch.randint(0, n, (4096,), device="cuda", generator=g)
+        mag = torch.pow(10.0, 6.0 + 3.0 * torch.rand(4096, device="cuda", generator=g))
+        sgn = torch.where(torch.rand(4096, device="cuda", generator=g) < 0.5, -1.0, 1.0)
+        x[pos] = (mag * sgn).float()
+    got, want, rep = _c4_gpu_and_reference(x)
+    del x
+    rel_close(got, want, RTOL32)
+    inf_err, rel_big = precision(got, want)
+    assert rel_big < 1e-4, (rep, inf_err, rel_big)
 
 
 def test_dense_beyond_2e32_elements(cuda):
