@@ -121,11 +121,11 @@ int st_fcs_dense(int dtype, const void* tensor, size_t order, const size_t* dims
                  const uint32_t* packed, const size_t* hash_lens, double* out, int accumulate,
                  void* workspace, size_t workspace_bytes, void* stream);
 
-/* HOST, synchronous diagnostics of the last ST_F32 st_fcs_dense call that
- * used `workspace` with this shape: the fixed-point exponent S (INT_MIN when
- * that call did not take the fixed-point kernel), the number of (chunk,
+/* HOST, synchronous diagnostics of the last st_fcs_dense call of this dtype
+ * and shape that used `workspace`: the fixed-point exponent S (INT_MIN when
+ * that call did not take a fixed-point kernel), the number of (chunk,
  * family) CTAs that fell back to float atomics, and the number of CTAs. */
-int st_fcs_dense_report(size_t order, const size_t* dims, size_t last_count,
+int st_fcs_dense_report(int dtype, size_t order, const size_t* dims, size_t last_count,
                         size_t sketch_count, const size_t* hash_lens, const void* workspace,
                         size_t workspace_bytes, int* fx_exponent, size_t* fallback_ctas,
                         size_t* ctas);

@@ -34,7 +34,7 @@ SIGNATURES = {
     "st_fcs_dense_workspace": (sz, [i32, sz, p, sz, sz, p]),
     "st_fcs_dense": (i32, [i32, p, sz, p, sz, sz, sz, p, p, p, i32, p, sz, p]),
     "st_fcs_dense_host": (i32, [i32, p, sz, p, sz, sz, sz, p, p, p]),
-    "st_fcs_dense_report": (i32, [sz, p, sz, sz, p, p, sz, p, p, p]),
+    "st_fcs_dense_report": (i32, [i32, sz, p, sz, sz, p, p, sz, p, p, p]),
     "st_cs_columns": (i32, [p, sz, sz, p, sz, p, p]),
     "st_fcs_cp_workspace": (sz, [sz, p, sz, sz, p]),
     "st_fcs_cp": (i32, [p, sz, sz, p, p, sz, sz, sz, p, p, p, i32, p, sz, p]),

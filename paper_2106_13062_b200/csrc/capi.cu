@@ -171,11 +171,11 @@ size_t st_fcs_dense_workspace(int dtype, size_t order, const size_t* dims, size_
   return dense_workspace(dtype, order, dims, last_count, sketch_count, hash_lens);
 }
 
-int st_fcs_dense_report(size_t order, const size_t* dims, size_t last_count,
+int st_fcs_dense_report(int dtype, size_t order, const size_t* dims, size_t last_count,
                         size_t sketch_count, const size_t* hash_lens, const void* workspace,
                         size_t workspace_bytes, int* fx_exponent, size_t* fallback_ctas,
                         size_t* ctas) {
-  return dense_fx_report(order, dims, last_count, sketch_count, hash_lens, workspace,
+  return dense_fx_report(dtype, order, dims, last_count, sketch_count, hash_lens, workspace,
                          workspace_bytes, fx_exponent, fallback_ctas, ctas);
 }
 

@@ -76,7 +76,7 @@ inline unsigned ceil_div(size_t a, size_t b) { return static_cast<unsigned>((a +
 // out_len != 0 overrides the per-family output length (kind 0 only): the
 // row-batched sketches (codecs.cu) bake a row offset r * J~ into one mode's
 // table entries and write rows x J~ values per family.
-int dense_fx_report(size_t order, const size_t* dims, size_t last_count, size_t D,
+int dense_fx_report(int dtype, size_t order, const size_t* dims, size_t last_count, size_t D,
                     const size_t* hash_lens, const void* ws, size_t ws_bytes, int* S,
                     size_t* fallback, size_t* ctas);
 size_t dense_workspace(int dtype, size_t order, const size_t* dims, size_t last_count, size_t D,

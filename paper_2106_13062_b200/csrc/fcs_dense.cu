@@ -45,22 +45,37 @@ __device__ __forceinline__ float4 ld_stream(const float4* p) {
 
 // Sampled statistics of the input and the fixed-point exponent derived from them.
 struct FxStats {
-  unsigned maxbits;  // max |x| over the sample, float bits (non-negative floats order as ints)
+  double maxabs;     // max |x| over the kept sample
   int S;             // fixed-point fractional bits
   double sum;
   double sumsq;
   double count;
 };
-// Per-CTA partial of the sample (fx_sample_kernel), reduced in a fixed order
-// by fx_scale_kernel: no contended atomics, and the chosen scale (hence the
+// Per-fiber partial of the sample (fx_sample_warps), reduced in a fixed order
+// by fx_scale_device: no contended atomics, and the chosen scale (hence the
 // fixed-point rounding) is the same on every run.
 struct FxPart {
-  float mx;
-  float pad;
+  double mx;
   double s, s2, cnt;
 };
-constexpr int kFxSampleCtas = 1024;  // threads of fx_scale_kernel
-constexpr int kFxMaxS = 120;         // largest fixed-point exponent (2^S finite in fp32)
+// Fixed-point format limits: int32 words (fp32 input) and int64 words as two
+// int32 halves (fp64 input). elem: largest |x * 2^S| the magic-number rounding
+// keeps exact (the range check catches anything beyond); part: the largest
+// designed partial (the wrap guard trips at twice it); max_s: largest S whose
+// 2^S is finite in the input type.
+struct FxLimits {
+  double elem, part;
+  int max_s;
+};
+// What a fixed-point kernel needs to derive S itself (fx_scale_device).
+struct FxScaleArgs {
+  const FxPart* parts;
+  int nparts;
+  double n_center;  // expected elements per busiest bucket per CTA
+  FxStats* stats;   // written by CTA 0
+};
+constexpr FxLimits kFx32{4194304.0 /* 2^22 */, 1073741824.0 /* 2^30 */, 120};
+constexpr FxLimits kFx64{2251799813685248.0 /* 2^51 */, 2305843009213693952.0 /* 2^61 */, 1000};
 // A CTA whose largest |partial| stays below 2^kFxSmallBits (and is not zero)
 // saw data far smaller than the sample predicted: its fixed-point rounding
 // would be coarse relative to its own values, so it redoes its chunk with
@@ -117,159 +132,120 @@ __global__ void __launch_bounds__(1024) fcs_dense_smem_kernel(DenseArgs a,
   for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) dst[b] = sk[b];
 }
 
-// Sampled max|x|, sum and sum of squares over up to `nsample` evenly spaced
-// fibers: CTA b takes fibers b, b + gridDim.x, ... (one each at the usual
-// grid of nsample CTAs) and writes its partial.
-__global__ void fx_sample_kernel(DenseArgs a, const float* __restrict__ t, uint64_t nsample,
-                                 FxPart* __restrict__ parts) {
-  __shared__ float smx[32];
-  __shared__ double ss[32], ss2[32], scnt[32];
-  const uint32_t i0n = a.dims[0];
-  float mx = 0.f;
-  double s = 0.0, s2 = 0.0, cnt = 0.0;
-  for (uint64_t k = blockIdx.x; k < nsample; k += gridDim.x) {
-    const uint64_t f = (k * a.fibers) / nsample;
-    for (uint32_t i = threadIdx.x; i < i0n; i += blockDim.x) {
-      const float x = t[f * i0n + i];
-      mx = fmaxf(mx, fabsf(x));  // NaN is ignored here and caught by the main kernel
-      s += x;
-      s2 += static_cast<double>(x) * x;
-      cnt += 1.0;
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    s += __shfl_xor_sync(0xffffffffu, s, o);
-    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  }
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) {
-    smx[w] = mx;
-    ss[w] = s;
-    ss2[w] = s2;
-    scnt[w] = cnt;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (unsigned q = 1; q < (blockDim.x >> 5); ++q) {
-      mx = fmaxf(mx, smx[q]);
-      s += ss[q];
-      s2 += ss2[q];
-      cnt += scnt[q];
-    }
-    FxPart pt;
-    pt.mx = mx;
-    pt.pad = 0.f;
-    pt.s = s;
-    pt.s2 = s2;
-    pt.cnt = cnt;
-    parts[blockIdx.x] = pt;
-  }
-}
-
 // Fixed-point exponent: the largest S with a comfortable margin between the
 // expected largest per-CTA bucket partial and 2^31 (bias * N + 8 sigma sqrt(N)
 // + max, N = the expected count of elements a CTA adds to its busiest bucket).
-// The statistics are ROBUST to outliers: the nparts / 64 sampled fibers with
-// the largest |x| are left out, so one huge element (which its CTA handles by
+// The statistics are ROBUST to outliers: a sampled fiber whose max |x| lies
+// more than 4 standard deviations above the mean of log max|x| over the
+// sampled fibers is left out, so one huge element (which its CTA handles by
 // the exact range check + float fallback) cannot coarsen the scale for the
-// whole tensor. The excluded set comes from a bitonic sort of the per-fiber
-// maxima with ties broken by index, so S is still the same on every run.
-__global__ void __launch_bounds__(kFxSampleCtas) fx_scale_kernel(const FxPart* __restrict__ parts,
-                                                                 int nparts, FxStats* st,
-                                                                 double n_center) {
-  static_assert(kFxMaxSample == 2 * kFxSampleCtas, "two sort keys per thread");
-  __shared__ float key[kFxMaxSample];
-  __shared__ short kidx[kFxMaxSample];
-  __shared__ unsigned char kept[kFxMaxSample];
-  for (int q = threadIdx.x; q < kFxMaxSample; q += blockDim.x) {
-    key[q] = q < nparts ? parts[q].mx : -1.0f;  // NaN maxima are ignored (fmaxf), keys >= 0
-    kidx[q] = static_cast<short>(q);
-    kept[q] = 0;
+// whole tensor. Every reduction runs in a fixed order, so S is the same on
+// every run.
+// Fixed-order block reduction of K values at once: xor tree inside each warp,
+// then warp 0 reduces the per-warp values (identity-padded to 32 lanes) with
+// the same tree; every thread gets the results. op(i, x, y) combines value i.
+template <int K, typename Op>
+__device__ __forceinline__ void block_reduce(double (&v)[K], double (*red)[K], Op op) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < K; ++i) v[i] = op(i, v[i], __shfl_xor_sync(0xffffffffu, v[i], o));
+  __syncthreads();  // red is reused across calls
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int i = 0; i < K; ++i) red[threadIdx.x >> 5][i] = v[i];
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double w[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) w[i] = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x][i] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int i = 0; i < K; ++i) w[i] = op(i, w[i], __shfl_xor_sync(0xffffffffu, w[i], o));
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int i = 0; i < K; ++i) red[32][i] = w[i];
   }
   __syncthreads();
-  // descending by key, ascending index on ties
-  for (int k = 2; k <= kFxMaxSample; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < kFxMaxSample; i += blockDim.x) {
-        const int l = i ^ j;
-        if (l > i) {
-          const bool desc = (i & k) == 0;
-          const float ki = key[i], kl = key[l];
-          const bool l_first = kl > ki || (kl == ki && kidx[l] < kidx[i]);
-          if (desc == l_first) {
-            key[i] = kl;
-            key[l] = ki;
-            const short t = kidx[i];
-            kidx[i] = kidx[l];
-            kidx[l] = t;
-          }
-        }
-      }
-      __syncthreads();
+#pragma unroll
+  for (int i = 0; i < K; ++i) v[i] = red[32][i];
+}
+
+// Computed redundantly (and identically) by every CTA of a fixed-point
+// kernel from the sample partials before it scatters; CTA 0 also stores the
+// statistics for the reduction and st_fcs_dense_report. All threads of the
+// CTA must call it (it synchronises); blockDim.x == 512 (each thread holds
+// up to kFxMaxSample / 512 partials in registers: one load round).
+__device__ int fx_scale_device(const FxPart* __restrict__ parts, int nparts, double n_center,
+                               FxLimits lim, FxStats* st) {
+  constexpr int kPer = kFxMaxSample / 512;
+  __shared__ double red[33][4];
+  FxPart mine[kPer];
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int q = threadIdx.x + j * blockDim.x;
+    mine[j] = q < nparts ? parts[q] : FxPart{0.0, 0.0, 0.0, 0.0};
+  }
+  // mean and spread of log2 max|x| over the fibers with a nonzero max
+  double lv[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const double m = mine[j].mx;
+    if (m > 0.0 && m <= 1.7976931348623157e308) {
+      const double lg = log2(m);
+      lv[0] += lg;
+      lv[1] += lg * lg;
+      lv[2] += 1.0;
     }
   }
-  const int drop = nparts / 64;
-  for (int r = threadIdx.x; r < nparts; r += blockDim.x)
-    if (r >= drop) kept[kidx[r]] = 1;
-  __syncthreads();
-  // fixed-order reduction of the kept sample partials (thread t: parts t, t + 1024; xor tree)
-  __shared__ float smx[kFxSampleCtas / 32];
-  __shared__ double ss[kFxSampleCtas / 32], ss2[kFxSampleCtas / 32], scnt[kFxSampleCtas / 32];
-  float pm = 0.f;
-  double ps = 0.0, ps2 = 0.0, pc = 0.0;
-  for (int q = threadIdx.x; q < nparts; q += blockDim.x) {
-    if (!kept[q]) continue;
-    const FxPart pt = parts[q];
-    pm = fmaxf(pm, pt.mx);
-    ps += pt.s;
-    ps2 += pt.s2;
-    pc += pt.cnt;
-  }
+  block_reduce<3>(lv, reinterpret_cast<double(*)[3]>(red),
+                  [](int, double x, double y) { return x + y; });
+  const double ln = lv[2];
+  const double lmean = ln > 0.0 ? lv[0] / ln : 0.0;
+  const double lsd = ln > 0.0 ? sqrt(fmax(lv[1] / ln - lmean * lmean, 0.0)) : 0.0;
+  const double cut = exp2(lmean + 4.0 * lsd + 1.0);  // + 1: never cut a tight (sd ~ 0) sample
+  // fixed-order reduction of the kept sample partials: max, sum, sum of squares, count
+  double sv[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, o));
-    ps += __shfl_xor_sync(0xffffffffu, ps, o);
-    ps2 += __shfl_xor_sync(0xffffffffu, ps2, o);
-    pc += __shfl_xor_sync(0xffffffffu, pc, o);
+  for (int j = 0; j < kPer; ++j) {
+    if (ln >= 16.0 && mine[j].mx > cut) continue;  // small samples keep everything
+    sv[0] = fmax(sv[0], mine[j].mx);
+    sv[1] += mine[j].s;
+    sv[2] += mine[j].s2;
+    sv[3] += mine[j].cnt;
   }
-  if ((threadIdx.x & 31) == 0) {
-    smx[threadIdx.x >> 5] = pm;
-    ss[threadIdx.x >> 5] = ps;
-    ss2[threadIdx.x >> 5] = ps2;
-    scnt[threadIdx.x >> 5] = pc;
+  block_reduce<4>(sv, red, [](int i, double x, double y) { return i == 0 ? fmax(x, y) : x + y; });
+  const double pm = sv[0], ps = sv[1], ps2 = sv[2], pc = sv[3];
+  __shared__ int s_out;
+  if (threadIdx.x == 0) {
+    const double n = fmax(pc, 1.0);
+    const double mean = ps / n;
+    const double rms = sqrt(fmax(ps2 / n, 0.0));
+    const double mx = pm;
+    const double bound = fabs(mean) * n_center + 8.0 * rms * sqrt(n_center) + 2.0 * mx;
+    // An all-zero sample gives the top exponent: any element of the tensor
+    // above 2^-(max_s) * elem then trips the exact range check and its CTA
+    // redoes the chunk with float atomics, so a sample that missed the data
+    // costs time, never accuracy. Small-magnitude data gets a large S.
+    int S = lim.max_s;
+    if (bound > 0.0) S = static_cast<int>(floor(log2(lim.part / bound)));
+    // single elements must stay inside the exact-rounding range with a 1.5x
+    // margin over the sampled maximum (an element beyond it is caught exactly
+    // and its CTA falls back; N(0,1): sample max ~5, tensor max ~6.1)
+    if (mx > 0.0) S = min(S, static_cast<int>(floor(log2(lim.elem / (1.5 * mx)))));
+    S = max(-lim.max_s, min(lim.max_s, S));
+    s_out = S;
+    if (st != nullptr) {
+      st->maxabs = pm;
+      st->sum = ps;
+      st->sumsq = ps2;
+      st->count = pc;
+      st->S = S;
+    }
   }
   __syncthreads();
-  if (threadIdx.x != 0) return;
-  for (int q = 1; q < static_cast<int>(blockDim.x >> 5); ++q) {
-    pm = fmaxf(pm, smx[q]);
-    ps += ss[q];
-    ps2 += ss2[q];
-    pc += scnt[q];
-  }
-  st->maxbits = __float_as_uint(pm);
-  st->sum = ps;
-  st->sumsq = ps2;
-  st->count = pc;
-  const double n = fmax(st->count, 1.0);
-  const double mean = st->sum / n;
-  const double rms = sqrt(fmax(st->sumsq / n, 0.0));
-  const double mx = static_cast<double>(__uint_as_float(st->maxbits));
-  const double bound = fabs(mean) * n_center + 8.0 * rms * sqrt(n_center) + 2.0 * mx;
-  // An all-zero sample gives the top exponent: any element of the tensor
-  // above 2^-(kFxMaxS - 21) then trips the exact range check and its CTA
-  // redoes the chunk with float atomics, so a sample that missed the data
-  // costs time, never accuracy. Small-magnitude data gets a large S (the
-  // scale 2^S stays a finite float up to 2^127).
-  int S = kFxMaxS;
-  if (bound > 0.0) S = static_cast<int>(floor(log2(1073741824.0 / bound)));
-  // single elements must stay inside the exact-rounding range 2^22 with a
-  // 1.5x margin over the sampled maximum (an element beyond it is caught
-  // exactly and its CTA falls back; N(0,1): sample max ~5, tensor max ~6.1)
-  if (mx > 0.0) S = min(S, static_cast<int>(floor(log2(4194304.0 / (1.5 * mx)))));
-  st->S = max(-100, min(kFxMaxS, S));
+  return s_out;
 }
 
 // Bank-aware load order for the fx kernel. A warp's fiber is 4*NV 128-byte
@@ -512,7 +488,7 @@ template <int NV, int SPLIT, int THREADS, bool kFull, bool kGroup = false>
 __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
                                                               const float* __restrict__ t,
                                                               const uint32_t* __restrict__ packed,
-                                                              const FxStats* __restrict__ st,
+                                                              FxScaleArgs sc,
                                                               int32_t* __restrict__ part,
                                                               int* __restrict__ flags,
                                                               const uint8_t* __restrict__ groups) {
@@ -521,7 +497,9 @@ __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
   const int d = blockIdx.x % a.D;
   const uint64_t chunk = blockIdx.x / a.D;
   const uint32_t* tab = packed + static_cast<uint64_t>(d) * a.fam_stride;
-  const float scale = ldexpf(1.0f, st->S);
+  const float scale = ldexpf(
+      1.0f, fx_scale_device(sc.parts, sc.nparts, sc.n_center, kFx32,
+                            blockIdx.x == 0 ? sc.stats : nullptr));
   for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) sk[b] = 0;
 
   // SPLIT warps share a fiber: warp w takes part w % SPLIT (32*NV vectors) of
@@ -662,6 +640,286 @@ __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
   if (threadIdx.x == 0) flags[chunk * a.D + d] = overflowed ? 1 : 0;
 }
 
+// float64 fixed-point path (any order >= 2, I_0 <= 1024): shared-memory
+// fp64 atomics are CAS loops on sm_100a (measured 1.2 random updates/clk/SM
+// vs 9.8 for int32 ATOMS.ADD, profiles/fp64_peak.json), so each bucket holds
+// a 64-bit fixed-point partial as two int32 words (lo: unsigned, hi: signed;
+// separate arrays so both words of one instruction spread over 32 banks).
+// An element becomes q = round(x 2^S) by the fp64 magic number 1.5 * 2^52
+// (exact for |x 2^S| < 2^51); lo += q_lo returns the old word, whose carry
+// goes with q_hi into hi — every carry is exact because each add's carry is
+// a function of its own returned old value, whatever order adds arrive in.
+// The element range (exponent of the magic sum) and a guard band on hi
+// (|partial| reaching 2^61) are checked exactly; a CTA that trips either
+// redoes its chunk with fp64 CAS atomics. Partials are summed exactly in
+// 128-bit integers in the reduction, then scaled by 2^-S once.
+// Lane-owned mode-0 indices i_0 = lane + 32 k (k < NV) with their table
+// entries in registers; each lane keeps NV loads in flight per fiber.
+constexpr double kMagic64 = 6755399441055744.0;  // 1.5 * 2^52
+constexpr uint64_t kMagic64Bits = 0x4338000000000000ull;
+
+__device__ __forceinline__ double ld_stream64(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+// Output side of the fx64 kernel (kept for the report; the reduction is a
+// separate kernel).
+struct Fx64Out {
+  double* out;
+  int accumulate;
+  uint64_t nchunk;
+  uint64_t nsample;
+};
+
+// Warp-level sample statistics of fiber k * fibers / nsample into parts[k]
+// (per-fiber order fixed).
+template <typename Tin>
+__device__ void fx_sample_warps(const DenseArgs& a, const Tin* __restrict__ t, uint64_t nsample,
+                                FxPart* __restrict__ parts) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  const uint32_t i0n = a.dims[0];
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
+       k < nsample; k += nw) {
+    const uint64_t f = (k * a.fibers) / nsample;
+    double mx = 0.0, s = 0.0, s2 = 0.0, cnt = 0.0;
+    for (uint32_t i = lane; i < i0n; i += 32) {
+      const double x = static_cast<double>(t[f * i0n + i]);
+      mx = fmax(mx, fabs(x));
+      s += x;
+      s2 += x * x;
+      cnt += 1.0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    }
+    if (lane == 0) parts[k] = FxPart{mx, s, s2, cnt};
+  }
+}
+
+template <typename Tin>
+__global__ void __launch_bounds__(256) fx_sample_warps_kernel(DenseArgs a, const Tin* __restrict__ t,
+                                                              uint64_t nsample,
+                                                              FxPart* __restrict__ parts) {
+  fx_sample_warps<Tin>(a, t, nsample, parts);
+}
+
+// Sampled fibers: an eighth of the tensor's fibers, at least 256, at most 2048.
+inline uint64_t fx_nsample(uint64_t fibers) {
+  return std::min<uint64_t>(fibers, std::min<uint64_t>(kFxMaxSample,
+                                                       std::max<uint64_t>(256, fibers / 8)));
+}
+
+__device__ __forceinline__ double i128_to_double(__int128 acc);
+
+template <int NV, bool kFull>
+__global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
+                                                             const double* __restrict__ t,
+                                                             const uint32_t* __restrict__ packed,
+                                                             FxScaleArgs sc,
+                                                             uint32_t* __restrict__ part,
+                                                             int* __restrict__ flags, Fx64Out ro) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* lo = reinterpret_cast<uint32_t*>(smem_raw);
+  const int d = blockIdx.x % a.D;
+  const uint64_t chunk = blockIdx.x / a.D;
+  const uint32_t* tab = packed + static_cast<uint64_t>(d) * a.fam_stride;
+  const int S = fx_scale_device(sc.parts, sc.nparts, sc.n_center, kFx64,
+                                blockIdx.x == 0 ? sc.stats : nullptr);
+  const double scale = ldexp(1.0, S);
+  for (uint32_t b = threadIdx.x; b < 2 * a.jt; b += blockDim.x) lo[b] = 0u;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint32_t i0n = a.dims[0];
+  // mode-0 buckets two per register (bucket < jt <= 29056 < 2^16), signs and
+  // validity as bit masks (bit k: entry i_0 = lane + 32 k)
+  uint32_t bk[(NV + 1) / 2];
+  uint32_t smask = 0, vmask = 0;
+#pragma unroll
+  for (int k = 0; k < (NV + 1) / 2; ++k) bk[k] = 0u;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const uint32_t i = lane + 32u * k;
+    const uint32_t e = i < i0n ? __ldg(tab + a.i0_shift + i) : 0u;
+    bk[k / 2] |= (e & 0xffffu) << (16 * (k % 2));
+    smask |= (e >> 31) << k;
+    vmask |= (i < i0n ? 1u : 0u) << k;
+  }
+  __syncthreads();
+  const uint64_t f_begin = chunk * a.fibers_per_chunk;
+  const uint64_t f_end = min(a.fibers, f_begin + a.fibers_per_chunk);
+  const uint32_t lo_base = static_cast<uint32_t>(__cvta_generic_to_shared(lo));
+  const uint32_t hi_off = 4u * a.jt;
+  uint32_t rng_acc = 0, ovf_acc = 0;
+  // A fiber is NB batches of LB entries per lane; the next batch's loads (of
+  // this fiber or the next) are in flight while the current batch is
+  // scattered (two register buffers, ping-pong, batch index compile-time).
+  constexpr int LB = NV < 16 ? NV : 16;
+  constexpr int NB = NV / LB;
+  constexpr int G = LB < 4 ? LB : 4;
+  auto load = [&]<int KB>(uint64_t f, double* x) {
+    const double* fib = t + f * i0n;
+#pragma unroll
+    for (int k = 0; k < LB; ++k)
+      x[k] = (kFull || lane + 32u * (KB + k) < i0n) ? ld_stream64(fib + lane + 32 * (KB + k)) : 0.0;
+  };
+  uint32_t base_c = 0, fmask = 0;
+  auto scatter = [&]<int KB>(uint64_t f, const double* x) {
+    if (KB == 0) {
+      uint32_t c, sbit;
+      fiber_offset_fast(a, tab, f, c, sbit);
+      base_c = lo_base + 4u * c;
+      fmask = smask ^ (sbit ? 0xffffffffu : 0u);  // bit k: final sign of entry k
+    }
+#pragma unroll
+    for (int kg = 0; kg < LB; kg += G) {
+      uint32_t qh[G], ql[G], ad[G], old[G];
+#pragma unroll
+      for (int k = 0; k < G; ++k) {
+        constexpr int dummy = 0;
+        (void)dummy;
+        const int kk = KB + kg + k;
+        const uint32_t e = (kk % 2) ? (bk[kk / 2] >> 16) : (bk[kk / 2] & 0xffffu);
+        ad[k] = base_c + (e << 2);
+        // sign: bit kk of fmask onto the top bit of x
+        const uint64_t xb = static_cast<uint64_t>(__double_as_longlong(x[kg + k])) ^
+                            (static_cast<uint64_t>((fmask << (31 - kk)) & 0x80000000u) << 32);
+        const uint64_t bits = static_cast<uint64_t>(
+            __double_as_longlong(fma(__longlong_as_double(xb), scale, kMagic64)));
+        const uint32_t bh = static_cast<uint32_t>(bits >> 32);
+        // exponent of the magic sum must stay 52 (0x433): else out of range / non-finite
+        rng_acc |= bh ^ 0x43300000u;
+        ql[k] = static_cast<uint32_t>(bits);  // the magic's low word is 0
+        qh[k] = bh - 0x43380000u;
+      }
+      // the low-word adds first (their returned values give the carries), then the high words
+#pragma unroll
+      for (int k = 0; k < G; ++k) {
+        const int kk = KB + kg + k;
+        old[k] = 0u;
+        if (kFull)
+          asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "+r"(old[k]) : "r"(ad[k]), "r"(ql[k]));
+        else
+          asm volatile("{ .reg .pred p; setp.ne.u32 p, %3, 0; @p atom.shared.add.u32 %0, [%1], %2; }"
+                       : "+r"(old[k]) : "r"(ad[k]), "r"(ql[k]), "r"(vmask & (1u << kk)));
+      }
+#pragma unroll
+      for (int k = 0; k < G; ++k) {
+        const int kk = KB + kg + k;
+        uint32_t hv, oh = 0u;
+        // carry out of old + q_lo into q_hi
+        asm("{ .reg .u32 tmp; add.cc.u32 tmp, %1, %2; addc.u32 %0, %3, 0; }"
+            : "=r"(hv) : "r"(old[k]), "r"(ql[k]), "r"(qh[k]));
+        if (kFull)
+          asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "+r"(oh) : "r"(ad[k] + hi_off), "r"(hv));
+        else
+          asm volatile("{ .reg .pred p; setp.ne.u32 p, %3, 0; @p atom.shared.add.u32 %0, [%1], %2; }"
+                       : "+r"(oh) : "r"(ad[k] + hi_off), "r"(hv), "r"(vmask & (1u << kk)));
+        // guard band: |partial| >= 2^61 sets bit 31 of hi + 2^29 (one add moves hi < 2^20)
+        ovf_acc |= oh + 0x20000000u;
+      }
+    }
+  };
+  double cur[LB], nxt[LB];
+  uint64_t f = f_begin + warp;
+  if (f < f_end) load.template operator()<0>(f, cur);
+  if constexpr (NB == 1) {
+    for (; f < f_end; f += 2 * nwarps) {
+      if (f + nwarps < f_end) load.template operator()<0>(f + nwarps, nxt);
+      scatter.template operator()<0>(f, cur);
+      if (f + nwarps >= f_end) break;
+      if (f + 2 * nwarps < f_end) load.template operator()<0>(f + 2 * nwarps, cur);
+      scatter.template operator()<0>(f + nwarps, nxt);
+    }
+  } else {
+    static_assert(NB == 2, "NV = 32: two batches of 16");
+    for (; f < f_end; f += nwarps) {
+      load.template operator()<LB>(f, nxt);
+      scatter.template operator()<0>(f, cur);
+      if (f + nwarps < f_end) load.template operator()<0>(f + nwarps, cur);
+      scatter.template operator()<LB>(f, nxt);
+    }
+  }
+  const int ovf = (ovf_acc >> 31) | ((rng_acc >> 20) != 0);
+  const bool overflowed = __syncthreads_or(ovf);
+  if (overflowed) {  // exact fallback for this CTA: fp64 atomics over the same chunk
+    double* skd = reinterpret_cast<double*>(smem_raw);
+    for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) skd[b] = 0.0;
+    __syncthreads();
+    for (uint64_t g = f_begin + warp; g < f_end; g += nwarps) {
+      uint32_t c, sbit;
+      fiber_offset(a, tab, g, c, sbit);
+      for (uint32_t i = lane; i < i0n; i += 32) {
+        const double x = __ldcs(t + g * i0n + i);
+        const uint32_t e = __ldg(tab + a.i0_shift + i);
+        if (x != 0.0) atomicAdd(&skd[(e & 0x7fffffffu) + c], ((e ^ sbit) & 0x80000000u) ? -x : x);
+      }
+    }
+    __syncthreads();
+  }
+  // partial layout per (chunk, d): jt lo words then jt hi words (or jt doubles when flagged)
+  uint32_t* dst = part + (chunk * a.D + d) * 2ull * a.jt;
+  for (uint32_t b = threadIdx.x; b < 2 * a.jt; b += blockDim.x) dst[b] = lo[b];
+  if (threadIdx.x == 0) flags[chunk * a.D + d] = overflowed ? 1 : 0;
+  (void)ro;
+}
+
+// out[d][b] (+)= 2^-S * (exact 128-bit sum of the fixed-point partials) + the
+// fp64 partials of CTAs that fell back, both in a fixed order. 32 outputs x 32
+// chunk lanes per CTA (like reduce_partials_kernel): lane y sums chunks
+// y, y + 32, ..., then the 32 lane sums are combined in lane order.
+__device__ __forceinline__ double i128_to_double(__int128 acc) {
+  const int64_t top = static_cast<int64_t>(acc >> 64);
+  if (top == 0 || top == -1) {
+    const int64_t low = static_cast<int64_t>(acc);
+    if (static_cast<__int128>(low) == acc) return static_cast<double>(low);
+    return static_cast<double>(static_cast<int64_t>(acc >> 11)) * 2048.0;
+  }
+  return static_cast<double>(top) * 18446744073709551616.0 +
+         static_cast<double>(static_cast<uint64_t>(acc));
+}
+
+__global__ void reduce_fx64_kernel(const uint32_t* __restrict__ part, const int* __restrict__ flags,
+                                   uint64_t nchunk, int D, uint32_t jt,
+                                   const FxStats* __restrict__ st, double* __restrict__ out,
+                                   int accumulate) {
+  __shared__ __int128 ired[32][33];
+  __shared__ double dred[32][33];
+  const uint64_t per = static_cast<uint64_t>(D) * jt;
+  const uint64_t i = blockIdx.x * 32ull + threadIdx.x;
+  __int128 acc = 0;
+  double dacc = 0.0;
+  if (i < per) {
+    const int d = static_cast<int>(i / jt);
+    const uint32_t b = static_cast<uint32_t>(i - static_cast<uint64_t>(d) * jt);
+    for (uint64_t c = threadIdx.y; c < nchunk; c += 32) {
+      const uint32_t* row = part + (c * D + d) * 2ull * jt;
+      if (flags[c * D + d]) {
+        dacc += reinterpret_cast<const double*>(row)[b];
+      } else {
+        acc += static_cast<int64_t>((static_cast<uint64_t>(row[jt + b]) << 32) | row[b]);
+      }
+    }
+  }
+  ired[threadIdx.y][threadIdx.x] = acc;
+  dred[threadIdx.y][threadIdx.x] = dacc;
+  __syncthreads();
+  if (threadIdx.y == 0 && i < per) {
+    for (int y = 1; y < 32; ++y) {
+      acc += ired[y][threadIdx.x];
+      dacc += dred[y][threadIdx.x];
+    }
+    double r = ldexp(i128_to_double(acc), -st->S) + dacc;
+    if (accumulate) r += out[i];
+    out[i] = r;
+  }
+}
+
 // Fixed-order fp64 reduction of the chunk partials: out[d][b] (+)= sum_c part[c][d][b].
 // 32 outputs x 32 chunk lanes per CTA: lane y sums chunks y, y + 32, ...
 // (coalesced over the 32 outputs), then the 32 lane sums are added in lane
@@ -762,7 +1020,7 @@ int fx_group_cache(FxGroupEntry** out) {
   return ST_OK;
 }
 
-enum class Path { Global, Smem, Fx };
+enum class Path { Global, Smem, Fx, Fx64 };
 
 struct Plan {
   Path path = Path::Global;
@@ -788,7 +1046,7 @@ int fx_nv(const DenseArgs& a) {
   return a.dims[0] == (128u << (v - 1)) ? v + 4 : v;
 }
 
-using FxKernel = void (*)(DenseArgs, const float*, const uint32_t*, const FxStats*, int32_t*, int*,
+using FxKernel = void (*)(DenseArgs, const float*, const uint32_t*, FxScaleArgs, int32_t*, int*,
                           const uint8_t*);
 FxKernel fx_kernel(int v, bool group) {
   if (group) {  // full-vector kernels with the bank-aware load order
@@ -812,6 +1070,25 @@ FxKernel fx_kernel(int v, bool group) {
 }
 inline int fx_threads(int) { return 512; }
 
+// fx64 variant: NV = the smallest power of two with 32 NV >= I_0.
+int fx64_nv(uint32_t i0) {
+  int nv = 1;
+  while (32u * nv < i0) nv <<= 1;
+  return nv;
+}
+using Fx64Kernel = void (*)(DenseArgs, const double*, const uint32_t*, FxScaleArgs, uint32_t*,
+                            int*, Fx64Out);
+Fx64Kernel fx64_kernel(int nv, bool full) {
+  switch (nv) {
+    case 1: return full ? fcs_dense_fx64_kernel<1, true> : fcs_dense_fx64_kernel<1, false>;
+    case 2: return full ? fcs_dense_fx64_kernel<2, true> : fcs_dense_fx64_kernel<2, false>;
+    case 4: return full ? fcs_dense_fx64_kernel<4, true> : fcs_dense_fx64_kernel<4, false>;
+    case 8: return full ? fcs_dense_fx64_kernel<8, true> : fcs_dense_fx64_kernel<8, false>;
+    case 16: return full ? fcs_dense_fx64_kernel<16, true> : fcs_dense_fx64_kernel<16, false>;
+    default: return full ? fcs_dense_fx64_kernel<32, true> : fcs_dense_fx64_kernel<32, false>;
+  }
+}
+
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
@@ -819,7 +1096,52 @@ inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 // st_fcs_dense_workspace never under-reports; an unaligned fp32 tensor simply
 // takes the generic kernel with the same partition.
 template <typename Tin, typename Tacc>
+int make_plan_uncached(const DenseArgs& a, Plan* p);
+
+// Opt a kernel in to the largest dynamic shared memory it can ever use (its
+// static shared memory subtracted), so cached plans of any size launch.
+template <typename K>
+cudaError_t set_max_dynamic_smem(K k, const DeviceInfo& di) {
+  cudaFuncAttributes at{};
+  cudaError_t e = cudaFuncGetAttributes(&at, k);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(di.smem_optin - at.sharedSizeBytes));
+}
+
+// Plans depend only on the device, the dtype and the launch geometry; the
+// cache keeps per-call host work (function attributes, occupancy queries)
+// off the small-tensor path.
+template <typename Tin, typename Tacc>
 int make_plan(const DenseArgs& a, Plan* p) {
+  static std::mutex mu;
+  static std::map<std::vector<uint64_t>, Plan> cache;
+  int dev = 0;
+  FCS_CUDA_TRY(cudaGetDevice(&dev));
+  std::vector<uint64_t> key = {static_cast<uint64_t>(dev), sizeof(Tin), sizeof(Tacc),
+                               static_cast<uint64_t>(a.order), static_cast<uint64_t>(a.D), a.jt,
+                               a.fibers};
+  for (int n = 0; n < a.order; ++n) {
+    key.push_back(a.dims[n]);
+    key.push_back(a.mult[n]);
+  }
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *p = it->second;
+      return ST_OK;
+    }
+  }
+  if (int rc = make_plan_uncached<Tin, Tacc>(a, p)) return rc;
+  std::lock_guard<std::mutex> lock(mu);
+  if (cache.size() > 4096) cache.clear();
+  cache[key] = *p;
+  return ST_OK;
+}
+
+template <typename Tin, typename Tacc>
+int make_plan_uncached(const DenseArgs& a, Plan* p) {
   DeviceInfo di;
   if (int rc = device_info(&di)) return rc;
   p->smem_bytes = static_cast<size_t>(a.jt) * sizeof(Tacc);
@@ -830,7 +1152,30 @@ int make_plan(const DenseArgs& a, Plan* p) {
   }
   int per_sm = 0;
   p->nv = sizeof(Tin) == 4 ? fx_nv(a) : 0;
-  if (p->nv) {
+  // the fixed-point kernels also hold fx_scale_device's static scratch
+  auto fits = [&](auto k) {
+    cudaFuncAttributes at{};
+    return cudaFuncGetAttributes(&at, k) == cudaSuccess &&
+           p->smem_bytes + at.sharedSizeBytes <= di.smem_optin;
+  };
+  if (p->nv && !fits(fx_kernel(p->nv, false))) p->nv = 0;
+  static const bool no_fx64 = std::getenv("ST_FX64_OFF") != nullptr;  // A/B probe
+  // Below ~8M element-updates the call is launch/latency-bound and the CAS
+  // kernel's two launches beat the fixed point's three (c1 100^3 D=1: 27.6 vs
+  // 33.8 us; c5 operands: 37 vs 42 us); above it the fixed point wins (c3
+  // build 200^3 D=10: 200 vs 292 us; 1024^3 J=8192 D=1: 1.44 vs 3.43 ms).
+  const bool fx64_pays = static_cast<double>(a.fibers) * a.dims[0] * a.D >= 8.0e6;
+  if (sizeof(Tin) == 8 && a.order >= 2 && a.dims[0] <= 1024 && !no_fx64 && fx64_pays &&
+      fits(fx64_kernel(fx64_nv(a.dims[0]), false))) {
+    p->path = Path::Fx64;
+    p->nv = fx64_nv(a.dims[0]);
+    p->threads = 512;
+    const bool full = a.dims[0] == 32u * p->nv;
+    auto k = fx64_kernel(p->nv, full);
+    FCS_CUDA_TRY(set_max_dynamic_smem(k, di));
+    FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
+                                                               p->smem_bytes));
+  } else if (p->nv) {
     p->path = Path::Fx;
     p->threads = fx_threads(p->nv);
     // the bank-aware order pays off when atomics bind: with the searched
@@ -841,15 +1186,13 @@ int make_plan(const DenseArgs& a, Plan* p) {
     static const bool no_group = std::getenv("ST_FX_NOGROUP") != nullptr;
     p->group = p->nv >= 6 && a.D >= 2 && !no_group;
     auto k = fx_kernel(p->nv, p->group);
-    FCS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(p->smem_bytes)));
+    FCS_CUDA_TRY(set_max_dynamic_smem(k, di));
     FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
                                                                p->smem_bytes));
   } else {
     p->path = Path::Smem;
     auto k = fcs_dense_smem_kernel<Tin, Tacc>;
-    FCS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(p->smem_bytes)));
+    FCS_CUDA_TRY(set_max_dynamic_smem(k, di));
     p->threads = p->smem_bytes > di.smem_optin / 2 ? 1024 : 512;
     FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
                                                                p->smem_bytes));
@@ -857,7 +1200,9 @@ int make_plan(const DenseArgs& a, Plan* p) {
   per_sm = std::max(per_sm, 1);
   const uint64_t resident = static_cast<uint64_t>(per_sm) * di.sm_count;
   uint64_t nchunk = std::max<uint64_t>(1, resident / static_cast<uint64_t>(a.D));
-  nchunk = std::min<uint64_t>(nchunk, std::max<uint64_t>(1, a.fibers / 16));
+  // at least ~4 fibers per warp of a 512-thread CTA: per-CTA fixed costs
+  // (zeroing, the scale, writing the partial) dominate smaller shares
+  nchunk = std::min<uint64_t>(nchunk, std::max<uint64_t>(1, a.fibers / 64));
   // Small tensors: each chunk writes (and the reduction re-reads) a D x J~
   // partial, so keep the partials to at most the tensor's bytes (config 1:
   // 592 -> 333 chunks; config 4 is unaffected).
@@ -949,13 +1294,13 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
                                             align_up(p.nchunk * a.D * sizeof(int)) +
                                             align_up(sizeof(FxStats)) +
                                             align_up(static_cast<size_t>(a.D) * 32));
-    const uint64_t nsample = std::min<uint64_t>(a.fibers, kFxMaxSample);
+    const uint64_t nsample = fx_nsample(a.fibers);
     const int nparts = static_cast<int>(nsample);  // one fiber per sample CTA
-    fx_sample_kernel<<<nparts, 256, 0, st>>>(a, reinterpret_cast<const float*>(t), nsample, parts);
+    fx_sample_warps_kernel<float><<<ceil_div(nsample, 8), 256, 0, st>>>(
+        a, reinterpret_cast<const float*>(t), nsample, parts);
     FCS_CUDA_TRY(cudaGetLastError());
     const double per_cta = static_cast<double>(a.fibers_per_chunk) * a.dims[0];
-    fx_scale_kernel<<<1, kFxSampleCtas, 0, st>>>(parts, nparts, stats, 3.0 * per_cta / a.jt + 16.0);
-    FCS_CUDA_TRY(cudaGetLastError());
+    const FxScaleArgs sc{parts, nparts, 3.0 * per_cta / a.jt + 16.0, stats};
     // bank-aware load order for the full-vector kernels (I_0 = 128 NV, NV >= 2)
     uint8_t* groups = nullptr;
     const int nv_full = p.nv >= 6 ? 1 << (p.nv - 5) : 0;
@@ -972,18 +1317,46 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
       FCS_CUDA_TRY(cudaGetLastError());
     }
     fx_kernel(p.nv, p.group)<<<static_cast<unsigned>(nchunk * a.D), p.threads, p.smem_bytes, st>>>(
-        a, reinterpret_cast<const float*>(t), packed, stats, part, flags, groups);
+        a, reinterpret_cast<const float*>(t), packed, sc, part, flags, groups);
     FCS_CUDA_TRY(cudaGetLastError());
     reduce_fx_kernel<<<ceil_div(out_elems, 256), 256, 0, st>>>(part, flags, nchunk, a.D, a.jt,
                                                                stats, out, accumulate);
     FCS_CUDA_TRY(cudaGetLastError());
     return ST_OK;
   }
+  if (p.path == Path::Fx64) {
+    char* base = static_cast<char*>(ws);
+    auto* part = reinterpret_cast<uint32_t*>(base);
+    auto* flags = reinterpret_cast<int*>(base + align_up(p.part_bytes));
+    auto* stats = reinterpret_cast<FxStats*>(base + align_up(p.part_bytes) +
+                                             align_up(p.nchunk * a.D * sizeof(int)));
+    auto* parts = reinterpret_cast<FxPart*>(base + align_up(p.part_bytes) +
+                                            align_up(p.nchunk * a.D * sizeof(int)) +
+                                            align_up(sizeof(FxStats)) +
+                                            align_up(static_cast<size_t>(a.D) * 32));
+    const uint64_t nsample = fx_nsample(a.fibers);
+    const int nparts = static_cast<int>(nsample);
+    const double per_cta = static_cast<double>(a.fibers_per_chunk) * a.dims[0];
+    const FxScaleArgs sc{parts, nparts, 3.0 * per_cta / a.jt + 16.0, stats};
+    const bool full = a.dims[0] == 32u * p.nv;
+    Fx64Out ro{out, accumulate, nchunk, nsample};
+    fx_sample_warps_kernel<double><<<ceil_div(nsample, 8), 256, 0, st>>>(
+        a, reinterpret_cast<const double*>(t), nsample, parts);
+    FCS_CUDA_TRY(cudaGetLastError());
+    fx64_kernel(p.nv, full)<<<static_cast<unsigned>(nchunk * a.D), p.threads, p.smem_bytes, st>>>(
+        a, reinterpret_cast<const double*>(t), packed, sc, part, flags, ro);
+    FCS_CUDA_TRY(cudaGetLastError());
+    reduce_fx64_kernel<<<ceil_div(out_elems, 32), dim3(32, 32), 0, st>>>(part, flags, nchunk, a.D,
+                                                                        a.jt, stats, out,
+                                                                        accumulate);
+    FCS_CUDA_TRY(cudaGetLastError());
+    return ST_OK;
+  }
   int threads = p.threads;
   if (p.path == Path::Fx) {  // unaligned fp32 tensor: generic kernel, same partition
-    auto k = fcs_dense_smem_kernel<Tin, Tacc>;
-    FCS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(p.smem_bytes)));
+    DeviceInfo di;
+    if (int rc = device_info(&di)) return rc;
+    FCS_CUDA_TRY(set_max_dynamic_smem(fcs_dense_smem_kernel<Tin, Tacc>, di));
     threads = 1024;
   }
   Tacc* part = static_cast<Tacc*>(ws);
@@ -1002,7 +1375,7 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
 // the exponent S, how many (chunk, family) CTAs fell back to float atomics,
 // and how many there were. *S = INT_MIN and counts 0 when the call did not
 // take the fixed-point kernel.
-int dense_fx_report(size_t order, const size_t* dims, size_t last_count, size_t D,
+int dense_fx_report(int dtype, size_t order, const size_t* dims, size_t last_count, size_t D,
                     const size_t* hash_lens, const void* ws, size_t ws_bytes, int* S,
                     size_t* fallback, size_t* ctas) {
   DenseArgs a;
@@ -1010,8 +1383,9 @@ int dense_fx_report(size_t order, const size_t* dims, size_t last_count, size_t 
   *S = INT32_MIN;
   *fallback = *ctas = 0;
   Plan p;
-  if (int rc = make_plan<float, float>(a, &p)) return rc;
-  if (p.path != Path::Fx || a.fibers == 0) return ST_OK;
+  if (int rc = dtype == ST_F32 ? make_plan<float, float>(a, &p) : make_plan<double, double>(a, &p))
+    return rc;
+  if ((p.path != Path::Fx && p.path != Path::Fx64) || a.fibers == 0) return ST_OK;
   FCS_CHECK_ARG(ws != nullptr && ws_bytes >= p.ws, "st_fcs_dense_report: workspace too small");
   a.fibers_per_chunk = (a.fibers + p.nchunk - 1) / p.nchunk;
   const uint64_t nchunk = (a.fibers + a.fibers_per_chunk - 1) / a.fibers_per_chunk;

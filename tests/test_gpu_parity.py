@@ -222,7 +222,7 @@ def _c4_gpu_and_reference(x, report=False):
                              None))
     got = out.cpu().numpy()
     S, fb, ctas = C.c_int(0), C.c_size_t(0), C.c_size_t(0)
-    L.check(lib.st_fcs_dense_report(3, dims_a, dims[2], c.sketch_count, lens_a,
+    L.check(lib.st_fcs_dense_report(L.ST_F32, 3, dims_a, dims[2], c.sketch_count, lens_a,
                                     C.c_void_p(ws.data_ptr()), ws_bytes, C.byref(S), C.byref(fb),
                                     C.byref(ctas)))
     host = x.cpu().numpy()
@@ -800,3 +800,74 @@ def test_ts_hcs_cp_vs_oracle(cuda):
     dense = configs.densify(w, fs)
     rel_close(st.ts_sketch(cp, fam).values, st.ts_sketch(dense, fam).values.cpu().numpy(), 1e-9)
     rel_close(st.hcs_sketch(cp, fam).values, st.hcs_sketch(dense, fam).values.cpu().numpy(), 1e-9)
+
+
+# ------------------------------------------------- K1 fp64 fixed point (fx64)
+def _f64_case(x, J, D, seed=5):
+    fams = st.families_for(list(x.shape), st.EstimatorConfig(J, D, seed))
+    got = st.fcs_dense_batched(st.DenseTensor.from_array(x), fams).cpu().numpy()
+    want = []
+    for f in fams:
+        b, s, j = oracle_family(f)
+        want.append(O.fcs_dense(x, b, s, j))
+    return got, np.stack(want)
+
+
+@pytest.mark.parametrize("shape,J,D", [((1024, 64, 128), 3000, 1),  # NV = 32, full fibers
+                                       ((100, 300, 300), 1000, 1),  # NV = 4, partial
+                                       ((37, 500, 500), 800, 1),    # NV = 2, partial
+                                       ((512, 40, 40), 2048, 8),    # NV = 16, D = 8
+                                       ((300, 120, 60, 4), 500, 2)])  # order 4, NV = 16 partial
+def test_dense_f64_fixed_point_integer_bitexact(cuda, shape, J, D):
+    """fp64 fixed point (64-bit partials as two int32 words with exact carries,
+    >= 8M element-updates per call): integer data sums exactly, so the result
+    equals the reference's serial fp64 sum bit for bit."""
+    rng = np.random.default_rng(sum(shape) + J)
+    x = rng.integers(-1000, 1001, size=shape).astype(np.float64)
+    got, want = _f64_case(x, J, D)
+    assert np.array_equal(got, want)
+
+
+def test_dense_f64_fixed_point_gaussian(cuda):
+    """Gaussian fp64 data through the fixed point at the fp64 rule, and the
+    large buckets to 1e-12 relative (quantum 2^-(S+1) per element, S ~ 48)."""
+    rng = np.random.default_rng(41)
+    x = rng.standard_normal((1024, 96, 96))
+    got, want = _f64_case(x, 4096, 1)
+    rel_close(got, want, RTOL64)
+    big = np.abs(want) > 1e-3 * np.abs(want).max()
+    assert np.all(np.abs(got - want)[big] <= 1e-12 * np.abs(want)[big])
+
+
+def test_dense_f64_fixed_point_deterministic(cuda):
+    rng = np.random.default_rng(42)
+    x = rng.standard_normal((256, 200, 200))
+    fams = st.families_for([256, 200, 200], st.EstimatorConfig(2000, 2, 9))
+    t = st.DenseTensor.from_array(x)
+    first = st.fcs_dense_batched(t, fams)
+    for _ in range(2):
+        assert torch.equal(st.fcs_dense_batched(t, fams), first)
+
+
+def test_dense_f64_fixed_point_outliers_and_nan(cuda):
+    """Outliers beyond the fixed-point range (2^51 quanta) and NaN: the CTA
+    that sees one redoes its chunk with fp64 atomics; results at the rule,
+    NaN propagated to the buckets that receive it."""
+    rng = np.random.default_rng(43)
+    x = rng.standard_normal((200, 200, 200))
+    x[17, 33, 40] = 3.0e25
+    x[150, 5, 190] = -7.5e18
+    got, want = _f64_case(x, 3000, 1)
+    rel_close(got, want, RTOL64)
+    x[3, 4, 5] = np.nan
+    got, want = _f64_case(x, 3000, 1)
+    assert (np.isnan(got) == np.isnan(want)).all()
+    rel_close(np.nan_to_num(got), np.nan_to_num(want), RTOL64)
+
+
+@pytest.mark.parametrize("sigma", [1e-150, 1e150])
+def test_dense_f64_fixed_point_extreme_magnitude(cuda, sigma):
+    rng = np.random.default_rng(44)
+    x = sigma * rng.standard_normal((128, 250, 256))
+    got, want = _f64_case(x, 1500, 1)
+    rel_close(got, want, RTOL64)
