@@ -142,11 +142,26 @@ int st_fcs_dense_host(int dtype, const void* host_tensor, size_t order, const si
                       size_t last_begin, size_t last_count, size_t sketch_count,
                       const uint64_t* master_seeds, const size_t* hash_lens, double* host_out);
 
+/* st_fcs_dense_host with explicit HOST packed tables (D families in the
+ * packed layout above, e.g. hand-built pairs, hashing.cpp:24-40) instead of
+ * master seeds. Replaces D x fcs_sketch(DenseTensor(dims, data), family_d). */
+int st_fcs_dense_host_tables(int dtype, const void* host_tensor, size_t order,
+                             const size_t* dims, size_t last_begin, size_t last_count,
+                             size_t sketch_count, const uint32_t* host_packed,
+                             const size_t* hash_lens, double* host_out);
+
 /* Count sketch of R columns (cs_sketch_columns, sketch.cpp:118-133; R = 1 is
  * cs_sketch, sketch.cpp:105-116): u is I x R column-major (device), table is
  * one packed pair, out is hash_len x R column-major fp64 (overwritten). */
 int st_cs_columns(const double* u, size_t input_dim, size_t cols, const uint32_t* packed_pair,
                   size_t hash_len, double* out, void* stream);
+
+/* Read-out through one packed pair: out[l] = s(l) * src[h(l)], l < count
+ * (device). Serves the free-mode readout sign_f(i) z[bucket_f(i)] of the
+ * estimators (estimators.cpp:84-88,262-266) and the long-pair sketch's
+ * virtual tensor s(l) sk[h(l)] (estimators.cpp:290-350). */
+int st_cs_expand(const double* src, size_t src_len, const uint32_t* packed_pair, size_t count,
+                 double* out, void* stream);
 
 /* --------------------------------------------------------------- CP-form FCS */
 
@@ -175,6 +190,41 @@ int st_fcs_cp(const double* weights, size_t rank, size_t order, const size_t* di
  * two inputs, fft.cpp:75-84. */
 int st_convolve_pairs(const double* a, size_t la, const double* b, size_t lb, size_t batch,
                       double* out, void* stream);
+
+/* ---------------------------------------------- exact-length transforms */
+
+/* Forward DFT of a real device vector x (len entries) zero-padded or
+ * truncated to EXACTLY n points: out (device, 2n doubles, interleaved
+ * re/im) = sum_j x_j exp(-2 pi i jk / n), unnormalised. Bluestein chirp-z over
+ * the library's shared-memory / two-level FFTs at a smooth length >= 2n - 1.
+ * n = 0 -> ST_EINVAL "dft: zero length".
+ * Replaces dft(std::span<const double>, size_t), fft.cpp:42-51. */
+int st_dft(const double* x, size_t len, size_t n, double* out, void* stream);
+
+/* Inverse of an n-bin device spectrum (2n doubles): out (device, n) = Re of
+ * (1/n) sum_k X_k exp(+2 pi i jk / n). check != 0 makes the call synchronous
+ * and returns ST_ENUMERIC "idft_real: inverse transform is not real" when
+ * ||Im|| > 1e-9 ||Re|| + 1e-12, like the reference.
+ * Replaces idft_real(const std::vector<std::complex<double>>&), fft.cpp:53-73. */
+int st_idft_real(const double* spectrum, size_t n, double* out, int check, void* stream);
+
+/* F^-1(F(x_1, n) ... F(x_k, n)) at exactly n points (circular convolution;
+ * linear when n >= sum(len) - k + 1). inputs: HOST array of k device
+ * pointers; lens: HOST; out: device n. Synchronous (residue check).
+ * Replaces fft_convolve, fft.cpp:75-84. */
+int st_fft_convolve(const double* const* inputs, const size_t* lens, size_t k, size_t n,
+                    double* out, void* stream);
+
+/* Cross-correlation vector z (device, n) of one precomputed FCS: the exact
+ * n-point spectrum (device, 2n doubles, as st_dft returns for the sketch),
+ * the count sketches of a (la entries) and b (lb) under the two contracted
+ * modes' packed pairs (device, ja / jb buckets):
+ *   z = idft_real(S conj(F cs_a) conj(F cs_b)). Synchronous (residue check).
+ * Replaces precompute_z(const PrecomputedFcs&, a, b, free_mode),
+ * estimators.cpp:151-167 (the caller picks the pairs by free_mode). */
+int st_precompute_z(const double* spectrum, size_t n, const double* a, size_t la,
+                    const uint32_t* pair_a, size_t ja, const double* b, size_t lb,
+                    const uint32_t* pair_b, size_t jb, double* z, void* stream);
 
 /* Kronecker-product compression (BASELINE config 5): for D 4-mode families
  * (pairs p0..p3 over dims ra, ca, rb, cb) returns FCS of the outer-product
@@ -250,6 +300,15 @@ int st_engine_create(st_engine** engine, int dtype, const void* tensor, const si
 int st_engine_create_backend(st_engine** engine, int backend, int dtype, const void* tensor,
                              const size_t* dims, size_t hash_len, size_t sketch_count,
                              uint64_t seed, void* stream);
+/* An engine over GIVEN sketches instead of a tensor: D device rows of
+ * composed length 3J - 2 (ST_BACKEND_FCS: the sketches of PrecomputedFcs,
+ * estimators.cpp:140-145) or J (ST_BACKEND_TS: PrecomputedTs), the D
+ * families' device packed tables over dims (all hash lengths J). Serves
+ * estimate_uvw / estimate_iuv(std::span<const PrecomputedFcs / Ts>, ...),
+ * estimators.cpp:169-191,219-233, for callers that hold sketches. */
+int st_engine_from_sketches(st_engine** engine, int backend, const double* sketches,
+                            size_t sketch_count, const size_t* dims, size_t hash_len,
+                            const uint32_t* packed, void* stream);
 int st_engine_destroy(st_engine* engine);
 int st_engine_backend(const st_engine* engine);
 /* Sketch length (J~ FCS, J TS and CS, J^3 HCS; 0 Plain) and the current

@@ -579,3 +579,20 @@ class ResidentTensor:
             self.close()
         except Exception:
             pass
+
+
+def precompute_z(t: np.ndarray, hash_len: int, master: int, a, b, free_mode: int):
+    """precompute_fcs + precompute_z (estimators.cpp:147-167) on a cubical
+    tensor, family HashFamily({I,I,I}, J, master): (exact spectrum, z)."""
+    dim = t.shape[0]
+    n = 3 * hash_len - 2
+    data = np.ascontiguousarray(np.asarray(t, np.float64).ravel(order="F"))
+    av = np.ascontiguousarray(np.asarray(a, np.float64))
+    bv = np.ascontiguousarray(np.asarray(b, np.float64))
+    spec = np.empty(2 * n, np.float64)
+    z = np.empty(n, np.float64)
+    L = lib()
+    L.ref_precompute_z.argtypes = [_p, _sz, _sz, _u64, _p, _p, _sz, _p, _p]
+    _check(L.ref_precompute_z(_ptr(data), _sz(dim), _sz(hash_len), _u64(master), _ptr(av),
+                              _ptr(bv), _sz(free_mode), _ptr(spec), _ptr(z)))
+    return spec[0::2] + 1j * spec[1::2], z

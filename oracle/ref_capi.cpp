@@ -591,3 +591,23 @@ int ref_fcs_dense_handle(const void* t, std::size_t fam_order, const std::size_t
   });
 }
 }  // extern "C"
+
+extern "C" {
+// precompute_fcs + precompute_z (estimators.cpp:147-167) on a cubical tensor
+// with the family HashFamily({I, I, I}, J, master): the exact n-point
+// spectrum (2n doubles) and z (n doubles).
+int ref_precompute_z(const double* data, std::size_t dim, std::size_t hash_len,
+                     std::uint64_t master, const double* a, const double* b,
+                     std::size_t free_mode, double* spectrum, double* z) {
+  return guarded([&] {
+    const std::size_t dims[3] = {dim, dim, dim};
+    DenseTensor t = make_tensor(data, 3, dims);
+    const PrecomputedFcs pre = precompute_fcs(t, HashFamily(to_dims(3, dims), hash_len, master));
+    for (std::size_t k = 0; k < pre.spectrum.size(); ++k) {
+      spectrum[2 * k] = pre.spectrum[k].real();
+      spectrum[2 * k + 1] = pre.spectrum[k].imag();
+    }
+    copy_out(precompute_z(pre, vec_in(a, dim), vec_in(b, dim), free_mode), z);
+  });
+}
+}  // extern "C"

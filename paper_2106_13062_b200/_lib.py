@@ -34,12 +34,18 @@ SIGNATURES = {
     "st_fcs_dense_workspace": (sz, [i32, sz, p, sz, sz, p]),
     "st_fcs_dense": (i32, [i32, p, sz, p, sz, sz, sz, p, p, p, i32, p, sz, p]),
     "st_fcs_dense_host": (i32, [i32, p, sz, p, sz, sz, sz, p, p, p]),
+    "st_fcs_dense_host_tables": (i32, [i32, p, sz, p, sz, sz, sz, p, p, p]),
     "st_fcs_dense_report": (i32, [i32, sz, p, sz, sz, p, p, sz, p, p, p]),
     "st_cs_columns": (i32, [p, sz, sz, p, sz, p, p]),
+    "st_cs_expand": (i32, [p, sz, p, sz, p, p]),
     "st_fcs_cp_workspace": (sz, [sz, p, sz, sz, p]),
     "st_fcs_cp": (i32, [p, sz, sz, p, p, sz, sz, sz, p, p, p, i32, p, sz, p]),
     "st_convolve_pairs": (i32, [p, sz, p, sz, sz, p, p]),
     "st_fcs_kron": (i32, [p, sz, sz, p, sz, sz, sz, p, p, p, p]),
+    "st_dft": (i32, [p, sz, sz, p, p]),
+    "st_idft_real": (i32, [p, sz, p, i32, p]),
+    "st_fft_convolve": (i32, [p, p, sz, sz, p, p]),
+    "st_precompute_z": (i32, [p, sz, p, sz, p, sz, p, sz, p, sz, p, p]),
     "st_ts_dense_workspace": (sz, [i32, sz, p, sz, sz, p]),
     "st_ts_dense": (i32, [i32, p, sz, p, sz, sz, sz, p, p, p, i32, p, sz, p]),
     "st_ts_cp_workspace": (sz, [sz, p, sz, sz, p]),
@@ -50,6 +56,7 @@ SIGNATURES = {
     "st_hcs_cp": (i32, [p, sz, sz, p, p, sz, p, p, p, i32, p, sz, p]),
     "st_engine_create": (i32, [p, i32, p, p, sz, sz, u64, p]),
     "st_engine_create_backend": (i32, [p, i32, i32, p, p, sz, sz, u64, p]),
+    "st_engine_from_sketches": (i32, [p, i32, p, sz, p, sz, p, p]),
     "st_engine_destroy": (i32, [p]),
     "st_engine_backend": (i32, [p]),
     "st_engine_composed_len": (sz, [p]),

@@ -188,9 +188,13 @@ int st_fcs_dense(int dtype, const void* tensor, size_t order, const size_t* dims
                           as_stream(stream));
 }
 
-int st_fcs_dense_host(int dtype, const void* host_tensor, size_t order, const size_t* dims,
-                      size_t last_begin, size_t last_count, size_t sketch_count,
-                      const uint64_t* master_seeds, const size_t* hash_lens, double* host_out) {
+namespace {
+// st_fcs_dense_host with the families given by master seeds (K0 on the
+// device) or by explicit host packed tables (uploaded).
+int fcs_dense_host_impl(int dtype, const void* host_tensor, size_t order, const size_t* dims,
+                        size_t last_begin, size_t last_count, size_t sketch_count,
+                        const uint64_t* master_seeds, const uint32_t* host_packed,
+                        const size_t* hash_lens, double* host_out) {
   FCS_CHECK_ARG(dtype == ST_F32 || dtype == ST_F64, "st_fcs_dense_host: unknown dtype");
   FCS_CHECK_ARG(order >= 1 && order <= ST_MAX_ORDER, "fcs_sketch: unsupported tensor order");
   FCS_CHECK_ARG(sketch_count >= 1, "EstimatorConfig: hash_len and sketch_count must be >= 1");
@@ -231,9 +235,15 @@ int st_fcs_dense_host(int dtype, const void* host_tensor, size_t order, const si
       }
     }
   } drain{hc};
-  if (int rc = st_family_tables(order, dims, hash_lens, sketch_count, master_seeds,
-                                static_cast<uint32_t*>(hc->tab.p), hc->comp))
-    return rc;
+  if (master_seeds) {
+    if (int rc = st_family_tables(order, dims, hash_lens, sketch_count, master_seeds,
+                                  static_cast<uint32_t*>(hc->tab.p), hc->comp))
+      return rc;
+  } else {
+    FCS_CUDA_TRY(cudaMemcpyAsync(hc->tab.p, host_packed,
+                                 sketch_count * sum_dims * sizeof(uint32_t),
+                                 cudaMemcpyHostToDevice, hc->comp));
+  }
   if (last_count == 0)
     FCS_CUDA_TRY(cudaMemsetAsync(dout, 0, sketch_count * jt * sizeof(double), hc->comp));
   const char* src = static_cast<const char*>(host_tensor);
@@ -258,6 +268,24 @@ int st_fcs_dense_host(int dtype, const void* host_tensor, size_t order, const si
   FCS_CUDA_TRY(cudaStreamSynchronize(hc->comp));
   drain.armed = false;
   return ST_OK;
+}
+}  // namespace
+
+int st_fcs_dense_host(int dtype, const void* host_tensor, size_t order, const size_t* dims,
+                      size_t last_begin, size_t last_count, size_t sketch_count,
+                      const uint64_t* master_seeds, const size_t* hash_lens, double* host_out) {
+  FCS_CHECK_ARG(master_seeds != nullptr, "st_fcs_dense_host: null seeds");
+  return fcs_dense_host_impl(dtype, host_tensor, order, dims, last_begin, last_count,
+                             sketch_count, master_seeds, nullptr, hash_lens, host_out);
+}
+
+int st_fcs_dense_host_tables(int dtype, const void* host_tensor, size_t order,
+                             const size_t* dims, size_t last_begin, size_t last_count,
+                             size_t sketch_count, const uint32_t* host_packed,
+                             const size_t* hash_lens, double* host_out) {
+  FCS_CHECK_ARG(host_packed != nullptr, "st_fcs_dense_host_tables: null tables");
+  return fcs_dense_host_impl(dtype, host_tensor, order, dims, last_begin, last_count,
+                             sketch_count, nullptr, host_packed, hash_lens, host_out);
 }
 
 int st_host_gaussian(uint64_t seed, size_t n, double* out, int threads) {

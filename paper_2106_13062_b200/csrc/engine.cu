@@ -136,6 +136,43 @@ int st_fcs_kron(const double* a, size_t ra, size_t ca, const double* b, size_t r
   return rc;
 }
 
+int st_dft(const double* x, size_t len, size_t n, double* out, void* stream) {
+  FCS_CHECK_ARG(n > 0, "dft: zero length");
+  return exact_dft(x, nullptr, len, len, n, 1, -1.0, reinterpret_cast<double2*>(out),
+                   as_stream(stream));
+}
+
+int st_idft_real(const double* spectrum, size_t n, double* out, int check, void* stream) {
+  FCS_CHECK_ARG(n > 0, "idft_real: zero length");
+  return exact_idft_real(reinterpret_cast<const double2*>(spectrum), n, 1, out, check,
+                         as_stream(stream));
+}
+
+int st_fft_convolve(const double* const* inputs, const size_t* lens, size_t k, size_t n,
+                    double* out, void* stream) {
+  FCS_CHECK_ARG(k > 0, "fft_convolve: no inputs");
+  FCS_CHECK_ARG(n > 0, "dft: zero length");
+  return exact_fft_convolve(inputs, lens, k, n, out, as_stream(stream));
+}
+
+int st_precompute_z(const double* spectrum, size_t n, const double* a, size_t la,
+                    const uint32_t* pair_a, size_t ja, const double* b, size_t lb,
+                    const uint32_t* pair_b, size_t jb, double* z, void* stream) {
+  FCS_CHECK_ARG(n > 0, "dft: zero length");
+  FCS_CHECK_ARG(la > 0 && lb > 0 && ja > 0 && jb > 0, "HashPair: dimensions must be positive");
+  cudaStream_t st = as_stream(stream);
+  double* cs = nullptr;
+  FCS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&cs), (ja + jb) * sizeof(double), st));
+  int rc = launch_cs_columns(a, static_cast<int>(la), 1, pair_a, static_cast<int>(ja), cs, st);
+  if (!rc)
+    rc = launch_cs_columns(b, static_cast<int>(lb), 1, pair_b, static_cast<int>(jb), cs + ja, st);
+  if (!rc)
+    rc = exact_precompute_z(reinterpret_cast<const double2*>(spectrum), n, cs, ja, cs + ja, jb, z,
+                            st);
+  cudaFreeAsync(cs, st);
+  return rc;
+}
+
 int st_engine_create_backend(st_engine** engine, int backend, int dtype, const void* tensor,
                              const size_t* dims, size_t hash_len, size_t sketch_count,
                              uint64_t seed, void* stream) {
@@ -233,6 +270,105 @@ int st_engine_create_backend(st_engine** engine, int backend, int dtype, const v
                                static_cast<int>(sketch_count), e->spec, st);
   cudaFreeAsync(vals, st);
   cudaFreeAsync(ws, st);
+  if (rc) {
+    st_engine_destroy(e);
+    return rc;
+  }
+  *engine = e;
+  return ST_OK;
+}
+
+namespace {
+// out[l] = s(l) * src[h(l)] for a packed pair (bucket | sign << 31).
+__global__ void cs_expand_kernel(const double* __restrict__ src, const uint32_t* __restrict__ pair,
+                                 size_t count, double* __restrict__ out) {
+  for (size_t l = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; l < count;
+       l += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const uint32_t e = __ldg(pair + l);
+    const double v = src[e & 0x7fffffffu];
+    out[l] = (e & 0x80000000u) ? -v : v;
+  }
+}
+}  // namespace
+
+int st_cs_expand(const double* src, size_t src_len, const uint32_t* packed_pair, size_t count,
+                 double* out, void* stream) {
+  FCS_CHECK_ARG(src_len > 0, "HashPair: dimensions must be positive");
+  if (count == 0) return ST_OK;
+  cs_expand_kernel<<<static_cast<unsigned>(std::min<size_t>(ceil_div(count, 256), 65535)), 256, 0,
+                     as_stream(stream)>>>(src, packed_pair, count, out);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+namespace {
+// ext[d][k] = ts[d][k mod J], k < jt (the TS engine's periodic extension of a
+// given TS sketch; st_engine_create builds it from the FCS instead).
+__global__ void ts_periodic_kernel(const double* __restrict__ ts, int D, int J, int jt,
+                                   double* __restrict__ ext) {
+  const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<size_t>(D) * jt) return;
+  const int d = static_cast<int>(i / jt);
+  const int k = static_cast<int>(i - static_cast<size_t>(d) * jt);
+  ext[i] = ts[static_cast<size_t>(d) * J + k % J];
+}
+}  // namespace
+
+int st_engine_from_sketches(st_engine** engine, int backend, const double* sketches,
+                            size_t sketch_count, const size_t* dims, size_t hash_len,
+                            const uint32_t* packed, void* stream) {
+  FCS_CHECK_ARG(engine != nullptr, "st_engine_create: null engine pointer");
+  FCS_CHECK_ARG(backend == ST_BACKEND_FCS || backend == ST_BACKEND_TS,
+                "st_engine_from_sketches: FCS or TS backend required");
+  FCS_CHECK_ARG(hash_len > 0 && sketch_count > 0,
+                "EstimatorConfig: hash_len and sketch_count must be >= 1");
+  for (int n = 0; n < 3; ++n) FCS_CHECK_ARG(dims[n] > 0, "DenseTensor: zero dimension");
+  *engine = nullptr;
+  cudaStream_t st = as_stream(stream);
+  auto* e = new st_engine();
+  FCS_CUDA_TRY(cudaGetDevice(&e->device));
+  e->backend = backend;
+  for (int n = 0; n < 3; ++n) e->dims[n] = dims[n];
+  e->hash_len = hash_len;
+  e->D = sketch_count;
+  e->jt = 3 * hash_len - 2;
+  e->slen = backend == ST_BACKEND_TS ? hash_len : e->jt;
+  int rc = get_fft_plan(e->jt, &e->plan);
+  if (rc) {
+    delete e;
+    return rc;
+  }
+  const size_t sum_dims = dims[0] + dims[1] + dims[2];
+  const size_t vbytes = sketch_count * e->jt * sizeof(double);
+  bool ok = cudaMalloc(reinterpret_cast<void**>(&e->packed),
+                       sketch_count * sum_dims * sizeof(uint32_t)) == cudaSuccess &&
+            cudaMalloc(reinterpret_cast<void**>(&e->spec),
+                       sketch_count * e->plan.P * sizeof(double2)) == cudaSuccess;
+  if (ok && backend == ST_BACKEND_TS) {
+    const double one = 1.0;
+    ok = cudaMalloc(reinterpret_cast<void**>(&e->ext), vbytes) == cudaSuccess &&
+         cudaMalloc(reinterpret_cast<void**>(&e->one), sizeof(double)) == cudaSuccess &&
+         cudaMemcpy(e->one, &one, sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess;
+  }
+  if (!ok) {
+    st_engine_destroy(e);
+    return fail(ST_ENOMEM, "st_engine_create: device allocation failed");
+  }
+  if (cudaMemcpyAsync(e->packed, packed, sketch_count * sum_dims * sizeof(uint32_t),
+                      cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
+    st_engine_destroy(e);
+    return fail(ST_ECUDA, "st_engine_from_sketches: table copy failed");
+  }
+  const double* src = sketches;
+  if (backend == ST_BACKEND_TS) {
+    const size_t n = sketch_count * e->jt;
+    ts_periodic_kernel<<<ceil_div(n, 256), 256, 0, st>>>(
+        sketches, static_cast<int>(sketch_count), static_cast<int>(hash_len),
+        static_cast<int>(e->jt), e->ext);
+    src = e->ext;
+  }
+  rc = launch_spec_from_real(e->plan, src, e->jt, static_cast<int>(e->jt),
+                             static_cast<int>(sketch_count), e->spec, st);
   if (rc) {
     st_engine_destroy(e);
     return rc;

@@ -628,6 +628,15 @@ struct EngArgs {
 };
 
 // Two-level counterparts of the spectral launchers (spectral_large.cu).
+// Exact n-point transforms (Bluestein over the library FFTs, spectral_large.cu).
+int exact_dft(const double* xr, const double2* xc, size_t ldx, size_t len, size_t n, int items,
+              double sign, double2* out, cudaStream_t st);
+int exact_idft_real(const double2* spec, size_t n, int items, double* out, int check,
+                    cudaStream_t st);
+int exact_fft_convolve(const double* const* inputs, const size_t* lens, size_t k, size_t n,
+                       double* out, cudaStream_t st);
+int exact_precompute_z(const double2* spectrum, size_t n, const double* csa, size_t ja,
+                       const double* csb, size_t jb, double* z, cudaStream_t st);
 int large_rfft(const FftPlan& pl, const double* x, size_t ldx, int64_t len, int items,
                double2* spec, cudaStream_t st);
 int large_irfft(const FftPlan& pl, double2* spec, int items, double* out, size_t ldo,

@@ -17,6 +17,7 @@
 // Reference semantics are those of spectral.cu (fft.cpp:42-84 with padding
 // to any M >= J~, estimators.cpp:38-90 for the estimators).
 #include <algorithm>
+#include <cmath>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -498,6 +499,262 @@ int get_large_fft(const FftPlan& pl, LargeFft* out) {
   cache[{dev, pl.M}] = L;
   *out = L;
   return ST_OK;
+}
+
+
+
+// ------------------------------------------- exact-length DFT (Bluestein)
+// The reference's dft / idft_real (fft.cpp:42-73) transform at EXACTLY
+// n = J~ points (FFTW, any n, e.g. 8998 = 2 * 11 * 409). The spectral paths
+// above pad to a smooth M instead, which is exact for every value the
+// estimators read; the public dft / idft_real / fft_convolve / precompute_z
+// entries, whose callers see every bin, use the chirp-z identity
+//   jk = (j^2 + k^2 - (k - j)^2) / 2:
+//   X[k] = ch_k sum_j (x_j ch_j) conj(ch_{k-j}),  ch_m = exp(s pi i m^2 / n)
+// (s = -1 forward, +1 inverse): one circular convolution at a smooth complex
+// length P >= 2n - 1 done with the library's own FFTs (fft.cuh in shared
+// memory up to P = 6144, the two-level transform above beyond), m^2 reduced
+// modulo 2n in integers before sincospi.
+namespace {
+
+__device__ __forceinline__ double2 chirp(int64_t m, int64_t n, double sign) {
+  const int64_t r = (m % (2 * n)) * (m % (2 * n)) % (2 * n);
+  double s, c;
+  sincospi(sign * static_cast<double>(r) / static_cast<double>(n), &s, &c);
+  return make_double2(c, s);
+}
+
+// A[item][j] = x_j ch_j (j < min(len, n)), 0 up to P. Real (xr) or complex (xc) rows.
+__global__ void bs_prep_a(const double* __restrict__ xr, const double2* __restrict__ xc,
+                          size_t ldx, int64_t len, int64_t n, int64_t P, double sign,
+                          double2* __restrict__ A) {
+  const size_t item = blockIdx.y;
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < P;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double2 v = make_double2(0.0, 0.0);
+    if (j < n && j < len) {
+      const double2 x = xr ? make_double2(xr[item * ldx + j], 0.0) : xc[item * ldx + j];
+      v = cmul(x, chirp(j, n, sign));
+    }
+    A[item * P + j] = v;
+  }
+}
+
+// B[m] = conj(ch_m) for |m| < n on the circle of P points, 0 elsewhere.
+__global__ void bs_prep_b(int64_t n, int64_t P, double sign, double2* __restrict__ B) {
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < P;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double2 v = make_double2(0.0, 0.0);
+    if (j < n) v = cconj(chirp(j, n, sign));
+    else if (P - j < n) v = cconj(chirp(P - j, n, sign));
+    B[j] = v;
+  }
+}
+
+// In-place complex FFT of `items` rows of P points in global memory with a
+// one-CTA plan: forward leaves the digit-reversed slot order, inverse takes
+// it and returns natural order (unnormalised).
+template <bool kForward>
+__global__ void __launch_bounds__(kFftThreads) bs_cfft(FftPlan pl, double2* __restrict__ data) {
+  extern __shared__ __align__(16) double2 bsm[];
+  double2* tw = bsm;
+  double2* buf = bsm + table_slots(pl, false);
+  load_twiddles(tw, pl, false);
+  double2* row = data + blockIdx.x * static_cast<size_t>(pl.P);
+  for (int i = threadIdx.x; i < pl.P; i += blockDim.x) buf[swz(i)] = row[i];
+  __syncthreads();
+  if (kForward) {
+    fft_forward(buf, pl, tw);
+  } else {
+    fft_inverse(buf, pl, tw);
+  }
+  for (int i = threadIdx.x; i < pl.P; i += blockDim.x) row[i] = buf[swz(i)];
+}
+
+__global__ void bs_mul(double2* __restrict__ A, const double2* __restrict__ B, int64_t P,
+                       size_t total) {
+  for (size_t q = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; q < total;
+       q += static_cast<size_t>(gridDim.x) * blockDim.x)
+    A[q] = cmul(A[q], B[q % P]);
+}
+
+// out[item][k] = scale * ch_k conv[k], k < n.
+__global__ void bs_final(const double2* __restrict__ A, int64_t n, int64_t P, double sign,
+                         double scale, double2* __restrict__ out) {
+  const size_t item = blockIdx.y;
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[item * n + k] = cscale(cmul(A[item * P + k], chirp(k, n, sign)), scale);
+}
+
+// Real part scaled by 1/n into out, and per-row sums of re^2 and im^2 (fixed
+// order: thread strides, then a shared-memory tree) for the residue check.
+__global__ void bs_real_part(const double2* __restrict__ X, int64_t n, double* __restrict__ out,
+                             double* __restrict__ norms) {
+  __shared__ double sr[256], si[256];
+  const size_t item = blockIdx.x;
+  const double inv = 1.0 / static_cast<double>(n);
+  double r2 = 0.0, i2 = 0.0;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+    const double2 v = X[item * n + k];
+    const double re = v.x * inv, im = v.y * inv;
+    out[item * n + k] = re;
+    r2 += re * re;
+    i2 += im * im;
+  }
+  sr[threadIdx.x] = r2;
+  si[threadIdx.x] = i2;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (static_cast<int>(threadIdx.x) < s) {
+      sr[threadIdx.x] += sr[threadIdx.x + s];
+      si[threadIdx.x] += si[threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    norms[2 * item] = sr[0];
+    norms[2 * item + 1] = si[0];
+  }
+}
+
+// G = S conj(Fa) conj(Fb) over n bins (precompute_z, estimators.cpp:151-167).
+__global__ void bs_z_combine(const double2* __restrict__ S, const double2* __restrict__ Fa,
+                             const double2* __restrict__ Fb, int64_t n, double2* __restrict__ G) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    G[k] = cmul(S[k], cconj(cmul(Fa[k], Fb[k])));
+}
+
+// acc[k] *= next[k] (fft_convolve's product, fft.cpp:79-82).
+__global__ void bs_cmul_inplace(double2* __restrict__ acc, const double2* __restrict__ next,
+                                int64_t n) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    acc[k] = cmul(acc[k], next[k]);
+}
+
+unsigned grid64(int64_t n) {
+  return static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 4096));
+}
+
+}  // namespace
+
+// X = exact n-point DFT (sign -1) or unnormalised inverse (sign +1) of
+// `items` rows: real rows xr (ldx apart, len used, zero-padded / truncated
+// to n) or complex rows xc (ldx apart). out: items x n complex.
+int exact_dft(const double* xr, const double2* xc, size_t ldx, size_t len, size_t n, int items,
+              double sign, double2* out, cudaStream_t st) {
+  if (items == 0) return ST_OK;
+  FftPlan pl;
+  if (int rc = get_fft_plan(2 * (2 * n - 1), &pl)) return rc;
+  const int64_t P = pl.P;
+  DevTmp tmp(st);
+  if (int rc = tmp.alloc((static_cast<size_t>(items) + 1) * P * sizeof(double2))) return rc;
+  auto* A = static_cast<double2*>(tmp.p);
+  double2* B = A + static_cast<size_t>(items) * P;
+  bs_prep_a<<<dim3(grid64(P), items), 256, 0, st>>>(xr, xc, ldx, static_cast<int64_t>(len),
+                                                      static_cast<int64_t>(n), P, sign, A);
+  FCS_CUDA_TRY(cudaGetLastError());
+  bs_prep_b<<<grid64(P), 256, 0, st>>>(static_cast<int64_t>(n), P, sign, B);
+  FCS_CUDA_TRY(cudaGetLastError());
+  double scale = 1.0;
+  if (!pl.large_p1) {
+    const size_t sm = fft_smem_bytes(pl, false);
+    if (int rc = set_smem(bs_cfft<true>, sm)) return rc;
+    if (int rc = set_smem(bs_cfft<false>, sm)) return rc;
+    bs_cfft<true><<<items + 1, kFftThreads, sm, st>>>(pl, A);  // rows of A, then B
+    FCS_CUDA_TRY(cudaGetLastError());
+    bs_mul<<<grid64(static_cast<int64_t>(items) * P), 256, 0, st>>>(
+        A, B, P, static_cast<size_t>(items) * P);
+    FCS_CUDA_TRY(cudaGetLastError());
+    bs_cfft<false><<<items, kFftThreads, sm, st>>>(pl, A);
+    FCS_CUDA_TRY(cudaGetLastError());
+    scale = 1.0 / static_cast<double>(P);
+  } else {
+    LargeFft L;
+    if (int rc = get_large_fft(pl, &L)) return rc;
+    const size_t sa = large_smem(L.a), sb = large_smem(L.b);
+    if (int rc = set_smem(lf_cols_fwd, sa)) return rc;
+    if (int rc = set_smem(lf_rows_fwd, sb)) return rc;
+    if (int rc = set_smem(lf_rows_inv, sb)) return rc;
+    if (int rc = set_smem(lf_cols_inv, sa)) return rc;
+    // complex rows viewed as packed reals: lf_cols_fwd's z[m] = x[2m] + i x[2m+1]
+    double* Ad = reinterpret_cast<double*>(A);
+    lf_cols_fwd<<<dim3(L.P2, items + 1), kFftThreads, sa, st>>>(L, Ad, 2 * P, 2 * P, A);
+    FCS_CUDA_TRY(cudaGetLastError());
+    lf_rows_fwd<<<dim3(L.P1, items + 1), kFftThreads, sb, st>>>(L, A);
+    FCS_CUDA_TRY(cudaGetLastError());
+    bs_mul<<<grid64(static_cast<int64_t>(items) * P), 256, 0, st>>>(
+        A, B, P, static_cast<size_t>(items) * P);
+    FCS_CUDA_TRY(cudaGetLastError());
+    lf_rows_inv<<<dim3(L.P1, items), kFftThreads, sb, st>>>(L, A);
+    FCS_CUDA_TRY(cudaGetLastError());
+    lf_cols_inv<<<dim3(L.P2, items), kFftThreads, sa, st>>>(L, A, Ad, 2 * P, 2 * P, 0);
+    FCS_CUDA_TRY(cudaGetLastError());
+  }
+  bs_final<<<dim3(grid64(static_cast<int64_t>(n)), items), 256, 0, st>>>(
+      A, static_cast<int64_t>(n), P, sign, scale, out);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+// idft_real of `items` rows of n bins: out = Re(IDFT) / n, and the residue
+// check of fft.cpp:69-71 (synchronous when check != 0).
+int exact_idft_real(const double2* spec, size_t n, int items, double* out, int check,
+                    cudaStream_t st) {
+  if (items == 0) return ST_OK;
+  DevTmp tmp(st);
+  if (int rc = tmp.alloc(static_cast<size_t>(items) * n * sizeof(double2) + 16 * items + 16))
+    return rc;
+  auto* X = static_cast<double2*>(tmp.p);
+  auto* norms = reinterpret_cast<double*>(X + static_cast<size_t>(items) * n);
+  if (int rc = exact_dft(nullptr, spec, n, n, n, items, +1.0, X, st)) return rc;
+  bs_real_part<<<items, 256, 0, st>>>(X, static_cast<int64_t>(n), out, norms);
+  FCS_CUDA_TRY(cudaGetLastError());
+  if (check) {
+    std::vector<double> h(2 * static_cast<size_t>(items));
+    FCS_CUDA_TRY(cudaMemcpyAsync(h.data(), norms, h.size() * sizeof(double),
+                                 cudaMemcpyDeviceToHost, st));
+    FCS_CUDA_TRY(cudaStreamSynchronize(st));
+    for (int i = 0; i < items; ++i)
+      if (std::sqrt(h[2 * i + 1]) > 1e-9 * std::sqrt(h[2 * i]) + 1e-12)
+        return fail(ST_ENUMERIC, "idft_real: inverse transform is not real");
+  }
+  return ST_OK;
+}
+
+// fft_convolve (fft.cpp:75-84): F^-1(prod_i F(x_i, n)) at exactly n points.
+int exact_fft_convolve(const double* const* inputs, const size_t* lens, size_t k, size_t n,
+                       double* out, cudaStream_t st) {
+  DevTmp tmp(st);
+  if (int rc = tmp.alloc(2 * n * sizeof(double2))) return rc;
+  auto* acc = static_cast<double2*>(tmp.p);
+  double2* nxt = acc + n;
+  if (int rc = exact_dft(inputs[0], nullptr, 0, lens[0], n, 1, -1.0, acc, st)) return rc;
+  for (size_t i = 1; i < k; ++i) {
+    if (int rc = exact_dft(inputs[i], nullptr, 0, lens[i], n, 1, -1.0, nxt, st)) return rc;
+    bs_cmul_inplace<<<grid64(static_cast<int64_t>(n)), 256, 0, st>>>(acc, nxt,
+                                                                      static_cast<int64_t>(n));
+    FCS_CUDA_TRY(cudaGetLastError());
+  }
+  return exact_idft_real(acc, n, 1, out, 1, st);
+}
+
+// precompute_z (estimators.cpp:151-167): z = idft_real(S conj(F cs_a) conj(F cs_b)) at n.
+int exact_precompute_z(const double2* spectrum, size_t n, const double* csa, size_t ja,
+                       const double* csb, size_t jb, double* z, cudaStream_t st) {
+  DevTmp tmp(st);
+  if (int rc = tmp.alloc(3 * n * sizeof(double2))) return rc;
+  auto* fa = static_cast<double2*>(tmp.p);
+  double2* fb = fa + n;
+  double2* g = fb + n;
+  if (int rc = exact_dft(csa, nullptr, 0, ja, n, 1, -1.0, fa, st)) return rc;
+  if (int rc = exact_dft(csb, nullptr, 0, jb, n, 1, -1.0, fb, st)) return rc;
+  bs_z_combine<<<grid64(static_cast<int64_t>(n)), 256, 0, st>>>(spectrum, fa, fb,
+                                                                  static_cast<int64_t>(n), g);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return exact_idft_real(g, n, 1, z, 1, st);
 }
 
 }  // namespace fcs

@@ -534,50 +534,48 @@ def median_reduce(values):
 
 
 # ------------------------------------------------------------------ fft.hpp
+def _dvec(x) -> torch.Tensor:
+    return torch.as_tensor(x if torch.is_tensor(x) else np.asarray(x, np.float64),
+                           dtype=torch.float64).reshape(-1).to(_dev()).contiguous()
+
+
 def dft(x, n: int) -> torch.Tensor:
     """dft (fft.cpp:42-51): the n-point complex DFT of x zero-padded (or
-    truncated) to n, exact length. A utility of the reference's public API;
-    the library's spectral paths use their own padded transforms (fft.cuh), so
-    this one is a cuFFT call through torch."""
+    truncated) to EXACTLY n points, e^{-i} and unnormalised — st_dft, a
+    Bluestein chirp-z over the library's own FFTs (fft.cuh / the two-level
+    transform). Returns a complex128 device tensor of n bins."""
     if n == 0:
         raise ValueError("dft: zero length")
-    v = torch.as_tensor(x if torch.is_tensor(x) else np.asarray(x, np.float64),
-                        dtype=torch.float64).reshape(-1).to(_dev())
-    buf = torch.zeros(n, dtype=torch.float64, device=_dev())
-    m = min(n, v.numel())
-    buf[:m] = v[:m]
-    return torch.fft.fft(buf)
+    v = _dvec(x)
+    out = torch.empty(2 * n, dtype=torch.float64, device=_dev())
+    _check(L.lib().st_dft(_ptr(v), v.numel(), n, _ptr(out), _stream()))
+    return torch.view_as_complex(out.view(n, 2))
 
 
 def idft_real(spectrum) -> torch.Tensor:
-    """idft_real (fft.cpp:53-73): real part of the normalised inverse DFT;
-    RuntimeError when the imaginary residue exceeds 1e-9 of the real norm
-    (+1e-12), as the reference."""
+    """idft_real (fft.cpp:53-73): real part of the normalised inverse DFT at
+    the spectrum's length (st_idft_real); RuntimeError when the imaginary
+    residue exceeds 1e-9 of the real norm (+1e-12), as the reference."""
     s = torch.as_tensor(spectrum if torch.is_tensor(spectrum) else np.asarray(spectrum),
-                        dtype=torch.complex128).reshape(-1).to(_dev())
-    if s.numel() == 0:
+                        dtype=torch.complex128).reshape(-1).to(_dev()).contiguous()
+    n = s.numel()
+    if n == 0:
         raise ValueError("idft_real: zero length")
-    z = torch.fft.ifft(s)
-    re, im = z.real, z.imag
-    if float(torch.linalg.norm(im)) > 1e-9 * float(torch.linalg.norm(re)) + 1e-12:
-        raise RuntimeError("idft_real: inverse transform is not real")
-    return re.contiguous()
+    out = torch.empty(n, dtype=torch.float64, device=_dev())
+    _check(L.lib().st_idft_real(_ptr(torch.view_as_real(s)), n, _ptr(out), 1, _stream()))
+    return out
 
 
 def fft_convolve(inputs, n: int) -> torch.Tensor:
-    """fft_convolve (fft.cpp:75-84): circular convolution at length n of the
-    inputs truncated / zero-padded to n — computed as the linear convolution
-    (the library's shared-memory FFT, st_convolve_pairs) folded mod n."""
+    """fft_convolve (fft.cpp:75-84): F^-1(prod F(x_i, n)) at exactly n points
+    (circular; linear when n >= sum(len) - k + 1) — st_fft_convolve."""
     if len(inputs) == 0:
         raise ValueError("fft_convolve: no inputs")
     if n == 0:
         raise ValueError("dft: zero length")
-    vs = [torch.as_tensor(x if torch.is_tensor(x) else np.asarray(x, np.float64),
-                          dtype=torch.float64).reshape(-1)[:n].to(_dev()) for x in inputs]
-    acc = vs[0] if vs[0].numel() else torch.zeros(1, dtype=torch.float64, device=_dev())
-    for v in vs[1:]:
-        v = v if v.numel() else torch.zeros(1, dtype=torch.float64, device=_dev())
-        acc = convolve_pairs(acc.reshape(1, -1), v.reshape(1, -1))[0]
-    out = torch.zeros(n, dtype=torch.float64, device=_dev())
-    idx = torch.arange(acc.numel(), device=_dev()) % n
-    return out.index_add_(0, idx, acc)
+    vs = [_dvec(x) for x in inputs]
+    ptrs = (C.c_void_p * len(vs))(*[v.data_ptr() for v in vs])
+    out = torch.empty(n, dtype=torch.float64, device=_dev())
+    _check(L.lib().st_fft_convolve(ptrs, L.size_array([v.numel() for v in vs]), len(vs), n,
+                                   _ptr(out), _stream()))
+    return out
