@@ -438,6 +438,40 @@ int st_sketch_decompress(const double* sketch, size_t sketch_count, size_t len,
 int st_kron_decompress_all(const double* sketch, size_t sketch_count, size_t len,
                            const uint32_t* packed, const size_t* dims4, double* out, void* stream);
 
+/* ------------------------------------------------------------ multi-GPU */
+/* NCCL-aware entries for a C/C++ host that owns an NCCL communicator
+ * (ncclComm_t passed as void*; NCCL is resolved at run time from
+ * libnccl.so.2, so a process that already loaded NCCL shares it). One
+ * process per GPU; the partitions are SURVEY.md §8(e)'s. Failures -> ST_ENCCL. */
+size_t st_nccl_unique_id_bytes(void);                /* sizeof(ncclUniqueId) */
+int st_nccl_get_unique_id(void* id);                 /* ncclGetUniqueId on rank 0 */
+int st_nccl_comm_init_rank(void** comm, int nranks, const void* id, int rank);
+int st_nccl_comm_destroy(void* comm);
+/* HOST. The balanced contiguous share [lo, lo + count) of n items owned by
+ * `rank` of `world` (the slab / rank-range rule of every sharded entry). */
+int st_shard_range(size_t n, int rank, int world, size_t* lo, size_t* count);
+
+/* Element-sharded dense FCS: `slab` (device) holds this rank's slab
+ * i_{N-1} in st_shard_range(dims[N-1], rank, world) of the FULL tensor
+ * `dims`; K1 sketches it into out (D x J~, device) and one ncclAllReduce
+ * (sum, fp64) leaves the whole tensor's sketch on every rank. workspace as
+ * st_fcs_dense_workspace(dtype, order, dims, count, D, hash_lens).
+ * Replaces fcs_sketch(const DenseTensor&, const HashFamily&), sketch.cpp:187-201
+ * (D families) for a tensor distributed over the communicator's GPUs. */
+int st_fcs_dense_nccl(int dtype, const void* slab, size_t order, const size_t* dims,
+                      size_t sketch_count, const uint32_t* packed, const size_t* hash_lens,
+                      double* out, void* workspace, size_t workspace_bytes, void* comm,
+                      void* stream);
+
+/* Rank-sharded CP-form FCS: every rank holds the whole CP tensor (device),
+ * sketches the CP ranks st_shard_range(rank, me, world) (frequency-domain
+ * sum, st_fcs_cp) and one ncclAllReduce sums the D x J~ partials.
+ * Replaces fcs_sketch(const CpTensor&, const HashFamily&), sketch.cpp:203-207. */
+int st_fcs_cp_nccl(const double* weights, size_t rank, size_t order, const size_t* dims,
+                   const double* const* factors, size_t sketch_count, const uint32_t* packed,
+                   const size_t* hash_lens, double* out, void* workspace, size_t workspace_bytes,
+                   void* comm, void* stream);
+
 /* ---------------------------------------------------------- synthetic data */
 
 /* HOST. n draws of SplitMix64(seed).next_gaussian() (rng.cpp:8-21), host libm,

@@ -77,6 +77,13 @@ SIGNATURES = {
     "st_fcs_contraction": (i32, [i32, p, p, p, p, sz, p, p, p, p]),
     "st_sketch_decompress": (i32, [p, sz, sz, p, sz, p, sz, p, p, p]),
     "st_kron_decompress_all": (i32, [p, sz, sz, p, p, p, p]),
+    "st_nccl_unique_id_bytes": (sz, []),
+    "st_nccl_get_unique_id": (i32, [p]),
+    "st_nccl_comm_init_rank": (i32, [p, i32, p, i32]),
+    "st_nccl_comm_destroy": (i32, [p]),
+    "st_shard_range": (i32, [sz, i32, i32, p, p]),
+    "st_fcs_dense_nccl": (i32, [i32, p, sz, p, sz, p, p, p, p, sz, p, p]),
+    "st_fcs_cp_nccl": (i32, [p, sz, sz, p, p, sz, p, p, p, p, sz, p, p]),
     "st_host_gaussian": (i32, [u64, sz, p, i32]),
     "st_device_gaussian": (i32, [i32, u64, sz, p, p]),
 }

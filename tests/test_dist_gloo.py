@@ -189,3 +189,18 @@ def test_rank_sharded_cp(world):
     want = np.stack([O.fcs_cp(w, fs, *fam) for fam in fams])
     for r in range(world):
         np.testing.assert_allclose(res[r][0], want, rtol=1e-12, atol=1e-12)
+
+
+def test_c_abi_shard_range_matches_python():
+    """The C-ABI's slab / rank-range rule (st_shard_range, used by the NCCL
+    entries) is the one dist.py shards with."""
+    import ctypes as C
+    from paper_2106_13062_b200 import _lib as L
+    lib = L.lib()
+    for n in (0, 1, 7, 1024, 1000):
+        for world in (1, 2, 3, 8):
+            for rank in range(world):
+                lo, cnt = C.c_size_t(), C.c_size_t()
+                L.check(lib.st_shard_range(n, rank, world, C.byref(lo), C.byref(cnt)))
+                plo, phi = pdist.shard_range(n, rank, world)
+                assert (lo.value, lo.value + cnt.value) == (plo, phi)
