@@ -257,14 +257,14 @@ def run_gpu(args):
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_kind": peak_kind, "kernel_ms": k_ms,
                          "algorithmic_bytes_per_launch": alg,
-                         "kernel": "fcs_dense_fx_kernel<8> (+ fx_sample, fx_scale, fx_group, reduce_fx)"},
+                         "kernel": "fcs_dense_fx_kernel<8> (+ fx_sample_warps, fx_group, reduce_fx)"},
             "e2e": e2e,
-            "gpu_launches": 5 * args.steps,  # sample, scale, group, fx scatter, reduce per step
+            "gpu_launches": 4 * args.steps,  # sample, group lookup, fx scatter (+scale), reduce
             "clocks": clk.summary(),
         }
     if world == 1 and not args.no_secondary:
         try:
-            line["secondary"] = secondary(x)
+            line["secondary"] = secondary(x, cpu=not args.no_cpu)
         except Exception as e:  # never lose the headline
             line["secondary"] = {"error": repr(e)}
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -279,12 +279,53 @@ def run_gpu(args):
         print(json.dumps(line), flush=True)
 
 
-def secondary(x=None):
+def fp64_peak():
+    """Measured fp64 FMA peak (tools/microbench/peaks.cu -> profiles/fp64_peak.json)."""
+    p = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["fp64_fma_tflops"]), "measured (profiles/fp64_peak.json)"
+    except Exception:
+        return 37.0, "fallback (B200 nominal fp64)"
+
+
+def fft_flops(M: int, transforms: int) -> float:
+    """Nominal FLOPs of `transforms` real M-point FFTs (2.5 M log2 M each)."""
+    import math
+    return transforms * 2.5 * M * math.log2(M)
+
+
+def roofline_hbm(alg_bytes: float, ms: float, peak: float) -> dict:
+    ach = alg_bytes / (ms * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "algorithmic_bytes": alg_bytes}
+
+
+def roofline_fp64(flops: float, ms: float, peak: float, kind: str) -> dict:
+    ach = flops / (ms * 1e-3) / 1e12
+    return {"bound": "fp64", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+            "frac": ach / peak, "flops": flops, "peak_kind": kind,
+            "flop_model": "2.5 M log2 M per real M-point transform (5 N log2 N per complex N)"}
+
+
+def median_time(fn, reps=5):
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    return statistics.median(ts)
+
+
+def secondary(x=None, cpu=True):
     """Configs 1, 2, 3, 5 on one GPU: device-resident inputs,
-    preallocated outputs and workspaces, the C-ABI calls themselves timed with
-    CUDA events per call, median of >= 10 calls after warm-up; plus K1 on the
-    config-4 tensor `x` for D = 1, 2, 4 (the update-throughput picture behind
-    the headline's roofline fraction)."""
+    preallocated outputs and workspaces, the C-ABI calls timed with CUDA
+    events, median of >= 10 calls after warm-up. Each entry carries its
+    roofline (HBM by algorithmic bytes; fp64 FFT rate for the spectral ones,
+    against the measured DFMA peak) and the reference CPU path (oracle/_ref,
+    one host thread) on the same inputs or a stated bounded sample. Also K1
+    on the config-4 tensor for D = 1, 2, 4 and the fp64 K1 on 1024^3 (J =
+    8192, D = 1)."""
     import ctypes as C
 
     import torch
@@ -297,6 +338,10 @@ def secondary(x=None):
     stream = torch.cuda.current_stream()
     sp = C.c_void_p(stream.cuda_stream)
     peak, _ = hbm_peak()
+    fpeak, fkind = fp64_peak()
+    ref = None
+    if cpu:
+        from oracle import ref
 
     def median_ms(fn, reps=12):
         for _ in range(3):
@@ -337,14 +382,43 @@ def secondary(x=None):
                           "hbm_frac": alg / (ms * 1e-3) / 1e9 / peak,
                           "updates_per_sec": D * x.numel() / (ms * 1e-3)})
         res["c4_family_sweep"] = sweep
+        # fp64 K1 (64-bit fixed point) on the same geometry: 1024^3 fp64 (8 GiB), J = 8192, D = 1
+        try:
+            n = x.numel()
+            x64 = torch.empty(n, dtype=torch.float64, device="cuda")
+            L.check(lib.st_device_gaussian(L.ST_F64, 7, n, C.c_void_p(x64.data_ptr()), sp))
+            fams = st.families_for(list(C4_DIMS), st.EstimatorConfig(8192, 1, 7))
+            ms = median_ms(dense_call(x64, list(C4_DIMS), fams, 1, L.ST_F64), 5)
+            alg = algorithmic_bytes(n, C4_DIMS, 1, 8192, esz=8)
+            res["fp64_dense_1024^3_J8192_D1"] = {
+                "ms": ms, "elements_per_sec": n / (ms * 1e-3),
+                "roofline": roofline_hbm(alg, ms, peak),
+                "kernel": "fcs_dense_fx64_kernel<32, full> (64-bit fixed point, two int32 ATOMS)"}
+            del x64
+            torch.cuda.empty_cache()
+        except Exception as e:  # memory: 4 GiB fp32 + 8 GiB fp64 resident
+            res["fp64_dense_1024^3_J8192_D1"] = {"error": repr(e)}
+
     # c1: dense FCS of 100^3 fp64, D = 1 (the reference's CPU-runnable case)
     c = configs.C1
-    t1 = torch.from_numpy(np.ascontiguousarray(configs.c1_tensor(c).ravel(order="F"))).cuda()
+    x1 = configs.c1_tensor(c)
+    t1 = torch.from_numpy(np.ascontiguousarray(x1.ravel(order="F"))).cuda()
     fams = st.families_for(list(c.dims), st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
     ms = median_ms(dense_call(t1, list(c.dims), fams, c.sketch_count, L.ST_F64))
-    alg = configs.algorithmic_bytes("c1")
-    res["c1_dense_fcs"] = {"ms": ms, "elements_per_sec": t1.numel() / (ms * 1e-3),
-                           "hbm_gbs": alg / (ms * 1e-3) / 1e9, "seed": c.seed}
+    e = {"ms": ms, "elements_per_sec": t1.numel() / (ms * 1e-3),
+         "roofline": roofline_hbm(configs.algorithmic_bytes("c1"), ms, peak), "seed": c.seed,
+         "note": "launch/latency-bound: 8 MB moves in 1.2 us at the HBM roofline"}
+    if ref is not None:
+        rt = ref.ResidentTensor.from_array(x1)
+        b, s, _ = ref.hash_family(c.dims, c.hash_len, ref.family_seed(c.seed, 0))
+        dt = median_time(lambda: rt.fcs(b, s, [c.hash_len] * 3))
+        rt.close()
+        e["cpu_baseline"] = {"value": t1.numel() / dt, "unit": UNIT, "cores": 1,
+                             "kind": "reference",
+                             "sample": "the whole c1 tensor: fcs_sketch(DenseTensor, family 0) "
+                                       "via oracle/_ref, median of 5", "seconds": dt}
+    res["c1_dense_fcs"] = e
+
     # c2: CP-form FCS, rank 50 400^3, D = 10
     c = configs.C2
     w, fs = configs.c2_cp(c)
@@ -364,38 +438,89 @@ def secondary(x=None):
                               C.c_void_p(out2.data_ptr()), 0, C.c_void_p(wbuf2.data_ptr()), ws2,
                               sp))
     ms = median_ms(cp_call)
-    res["c2_cp_fcs"] = {"ms": ms, "sketches_per_sec": c.sketch_count / (ms * 1e-3),
-                        "hbm_gbs": configs.algorithmic_bytes("c2") / (ms * 1e-3) / 1e9,
-                        "seed": c.seed,
-                        "metric": "CP-FCS sketches/s (D=10 sketches of a rank-50 400^3 CP tensor)"}
+    M2 = 12288  # padded real length for J~ = 11998
+    fl2 = fft_flops(M2, c.sketch_count * cp.rank() * 3 + c.sketch_count)
+    e = {"ms": ms, "sketches_per_sec": c.sketch_count / (ms * 1e-3),
+         "roofline": roofline_fp64(fl2, ms, fpeak, fkind),
+         "roofline_hbm": roofline_hbm(configs.algorithmic_bytes("c2"), ms, peak),
+         "seed": c.seed, "metric": "CP-FCS sketches/s (D=10 sketches of a rank-50 400^3 CP tensor)"}
+    if ref is not None:
+        nf = 2
+        dt = median_time(lambda: [ref.fcs_cp(w, fs, c.hash_len, ref.family_seed(c.seed, d))
+                                  for d in range(nf)], reps=1)
+        e["cpu_baseline"] = {"value": nf / dt, "unit": "sketches/s", "cores": 1,
+                             "kind": "reference",
+                             "sample": f"{nf} of the 10 families: fcs_sketch(CpTensor) via "
+                                       "oracle/_ref (FFTW absent: the shim's exact-length FFT)",
+                             "seconds": dt}
+    res["c2_cp_fcs"] = e
+
     # c3: one batched T(I,u,u) step (15 restarts x 10 families) and the full RTPM
     c = configs.C3
     t, lam, V = configs.c3_tensor(c)
-    dt = st.DenseTensor.from_array(t)
+    dt3 = st.DenseTensor.from_array(t)
     est = st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed)
-    eng = st.FcsEngine(dt, est)
-    U = torch.randn(configs.C3_INITS, 200, dtype=torch.float64, device="cuda")
-    Y = torch.empty((configs.C3_INITS, 200), dtype=torch.float64, device="cuda")
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    eng = st.FcsEngine(dt3, est)  # warm-up (plans, pools)
+    del eng
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    eng = st.FcsEngine(dt3, est)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    build_ms = ev0.elapsed_time(ev1)
+    Lr = configs.C3_INITS
+    U = torch.randn(Lr, 200, dtype=torch.float64, device="cuda")
+    Y = torch.empty((Lr, 200), dtype=torch.float64, device="cuda")
+    z1 = torch.empty(Lr, dtype=torch.float64, device="cuda")
 
-    def iuv_call():
-        L.check(lib.st_engine_iuv(eng._h, configs.C3_INITS, C.c_void_p(U.data_ptr()),
+    def iuv_call(n=Lr):
+        L.check(lib.st_engine_iuv(eng._h, n, C.c_void_p(U.data_ptr()),
                                   C.c_void_p(U.data_ptr()), 0, C.c_void_p(Y.data_ptr()), 1, sp))
+
+    def uvw_call(n=Lr):
+        L.check(lib.st_engine_uvw(eng._h, n, C.c_void_p(U.data_ptr()), C.c_void_p(U.data_ptr()),
+                                  C.c_void_p(U.data_ptr()), C.c_void_p(z1.data_ptr()), 1, sp))
     ms_iuv = median_ms(iuv_call, 20)
-    rcfg = st.RtpmConfig(c.rank, configs.C3_INITS, configs.C3_ITERS, st.SketchBackend.FCS, est)
-    st.rtpm(dt, rcfg)  # warm-up: first launches of the driver's kernels, plans, pools
+    ms_iuv1 = median_ms(lambda: iuv_call(1), 20)
+    ms_uvw = median_ms(uvw_call, 20)
+    ms_uvw1 = median_ms(lambda: uvw_call(1), 20)
+    ms_defl = median_ms(lambda: L.check(lib.st_engine_deflate(
+        eng._h, C.c_double(0.0), C.c_void_p(U.data_ptr()), C.c_void_p(U.data_ptr()),
+        C.c_void_p(U.data_ptr()), sp)), 10)
+    rcfg = st.RtpmConfig(c.rank, Lr, configs.C3_ITERS, st.SketchBackend.FCS, est)
+    st.rtpm(dt3, rcfg)  # warm-up: first launches of the driver's kernels, plans, pools
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    cpd = st.rtpm(dt, rcfg)
+    cpd = st.rtpm(dt3, rcfg)
     torch.cuda.synchronize()
     t_rtpm = time.perf_counter() - t0
-    # estimates/s: one batched step gives L restarts x D sketches of T(I,u,u) (median over D
-    # gives L estimates). Weights are reported, not scored: at this size the sketch noise
-    # dominates and RTPM trajectories are chaotic.
-    res["c3_rtpm"] = {"iuv_step_ms": ms_iuv,
-                      "estimates_per_sec": configs.C3_INITS / (ms_iuv * 1e-3),
-                      "step_hbm_gbs": 1517680 / (ms_iuv * 1e-3) / 1e9,
-                      "rtpm_total_s": t_rtpm, "rtpm_timing": "second call (warm)", "seed": c.seed,
-                      "weights": [round(float(x), 6) for x in cpd.weights.cpu().numpy()]}
+    R, T = c.rank, configs.C3_ITERS
+    model = {"build_ms": build_ms, "restarts_ms": R * (T * ms_iuv + ms_uvw),
+             "refinement_ms": R * (T * ms_iuv1 + ms_uvw1), "deflation_ms": R * ms_defl}
+    model["sum_ms"] = sum(model.values())
+    M3 = 9216  # padded real length for J~ = 8998
+    fl3 = fft_flops(M3, 3 * Lr * c.sketch_count)
+    e = {"iuv_step_ms": ms_iuv, "estimates_per_sec": Lr / (ms_iuv * 1e-3),
+         "roofline": roofline_fp64(fl3, ms_iuv, fpeak, fkind),
+         "roofline_hbm": roofline_hbm(1517680, ms_iuv, peak),
+         "iuv_batch1_ms": ms_iuv1, "uvw_step_ms": ms_uvw, "uvw_batch1_ms": ms_uvw1,
+         "deflate_ms": ms_defl, "rtpm_total_s": t_rtpm, "rtpm_timing": "second call (warm), host wall",
+         "rtpm_breakdown_model": model, "seed": c.seed,
+         "weights": [round(float(v), 6) for v in cpd.weights.cpu().numpy()]}
+    if ref is not None:
+        reng = ref.Engine(t, c.hash_len, c.sketch_count, c.seed)
+        u0 = U[0].cpu().numpy()
+        ncall = 8
+        dt = median_time(lambda: [reng.iuu(u0) for _ in range(ncall)], reps=1)
+        e["cpu_baseline"] = {"value": ncall / dt, "unit": "estimates/s", "cores": 1,
+                             "kind": "reference",
+                             "sample": f"{ncall} calls of the reference FcsEngine::iuu (each the "
+                                       "median over D = 10 of T(I,u,u)) via oracle/_ref; FFTW "
+                                       "absent: the shim's exact-length FFT", "seconds": dt}
+        del reng
+    res["c3_rtpm"] = e
+
     # c5: FCS of A (x) B, 512^2 operands, D = 8 (device-resident operands)
     c = configs.C5
     A, B = configs.c5_matrices(c)
@@ -412,8 +537,22 @@ def secondary(x=None):
                                 512, 512, c.sketch_count, C.c_void_p(packed5.data_ptr()), lens5,
                                 C.c_void_p(out5.data_ptr()), sp))
     ms = median_ms(kron_call)
-    res["c5_kron"] = {"ms": ms, "hbm_gbs": configs.algorithmic_bytes("c5") / (ms * 1e-3) / 1e9,
-                      "seed": c.seed}
+    e = {"ms": ms, "sketches_per_sec": c.sketch_count / (ms * 1e-3),
+         "roofline": roofline_hbm(configs.algorithmic_bytes("c5"), ms, peak), "seed": c.seed}
+    if ref is not None:
+        def ref_kron():
+            for d in range(c.sketch_count):
+                b, sg, _ = ref.hash_family(list(c.dims), c.hash_len, ref.family_seed(c.seed, d))
+                fa = ref.fcs_dense_tables(A, [b[0], b[1]], [sg[0], sg[1]], [c.hash_len] * 2)
+                fb = ref.fcs_dense_tables(B, [b[2], b[3]], [sg[2], sg[3]], [c.hash_len] * 2)
+                ref.fft_convolve([fa, fb], len(fa) + len(fb) - 1)
+        dt = median_time(ref_kron, reps=3)
+        e["cpu_baseline"] = {"value": c.sketch_count / dt, "unit": "sketches/s", "cores": 1,
+                             "kind": "reference",
+                             "sample": "all 8 families: fcs_sketch of both operands + "
+                                       "fft_convolve via oracle/_ref, median of 3",
+                             "seconds": dt}
+    res["c5_kron"] = e
     return res
 
 

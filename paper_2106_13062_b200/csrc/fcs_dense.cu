@@ -248,6 +248,12 @@ __device__ int fx_scale_device(const FxPart* __restrict__ parts, int nparts, dou
   return s_out;
 }
 
+// One CTA: the scale of a call from its sample partials (fx_scale_device),
+// stored for the scatter, the reduction and st_fcs_dense_report.
+__global__ void __launch_bounds__(512) fx_scale_kernel(FxScaleArgs sc, FxLimits lim) {
+  fx_scale_device(sc.parts, sc.nparts, sc.n_center, lim, sc.stats);
+}
+
 // Bank-aware load order for the fx kernel. A warp's fiber is 4*NV 128-byte
 // lines; load step j brings 4 whole lines (coalesced) and issues 4 ATOMS
 // instructions, instruction k taking element k of every lane's float4. The
@@ -488,7 +494,7 @@ template <int NV, int SPLIT, int THREADS, bool kFull, bool kGroup = false>
 __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
                                                               const float* __restrict__ t,
                                                               const uint32_t* __restrict__ packed,
-                                                              FxScaleArgs sc,
+                                                              const FxStats* __restrict__ st,
                                                               int32_t* __restrict__ part,
                                                               int* __restrict__ flags,
                                                               const uint8_t* __restrict__ groups) {
@@ -497,9 +503,7 @@ __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
   const int d = blockIdx.x % a.D;
   const uint64_t chunk = blockIdx.x / a.D;
   const uint32_t* tab = packed + static_cast<uint64_t>(d) * a.fam_stride;
-  const float scale = ldexpf(
-      1.0f, fx_scale_device(sc.parts, sc.nparts, sc.n_center, kFx32,
-                            blockIdx.x == 0 ? sc.stats : nullptr));
+  const float scale = ldexpf(1.0f, st->S);
   for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) sk[b] = 0;
 
   // SPLIT warps share a fiber: warp w takes part w % SPLIT (32*NV vectors) of
@@ -664,15 +668,6 @@ __device__ __forceinline__ double ld_stream64(const double* p) {
   return v;
 }
 
-// Output side of the fx64 kernel (kept for the report; the reduction is a
-// separate kernel).
-struct Fx64Out {
-  double* out;
-  int accumulate;
-  uint64_t nchunk;
-  uint64_t nsample;
-};
-
 // Warp-level sample statistics of fiber k * fibers / nsample into parts[k]
 // (per-fiber order fixed).
 template <typename Tin>
@@ -722,17 +717,15 @@ template <int NV, bool kFull>
 __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
                                                              const double* __restrict__ t,
                                                              const uint32_t* __restrict__ packed,
-                                                             FxScaleArgs sc,
+                                                             const FxStats* __restrict__ st,
                                                              uint32_t* __restrict__ part,
-                                                             int* __restrict__ flags, Fx64Out ro) {
+                                                             int* __restrict__ flags) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* lo = reinterpret_cast<uint32_t*>(smem_raw);
   const int d = blockIdx.x % a.D;
   const uint64_t chunk = blockIdx.x / a.D;
   const uint32_t* tab = packed + static_cast<uint64_t>(d) * a.fam_stride;
-  const int S = fx_scale_device(sc.parts, sc.nparts, sc.n_center, kFx64,
-                                blockIdx.x == 0 ? sc.stats : nullptr);
-  const double scale = ldexp(1.0, S);
+  const double scale = ldexp(1.0, st->S);
   for (uint32_t b = threadIdx.x; b < 2 * a.jt; b += blockDim.x) lo[b] = 0u;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const uint32_t i0n = a.dims[0];
@@ -866,7 +859,6 @@ __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
   uint32_t* dst = part + (chunk * a.D + d) * 2ull * a.jt;
   for (uint32_t b = threadIdx.x; b < 2 * a.jt; b += blockDim.x) dst[b] = lo[b];
   if (threadIdx.x == 0) flags[chunk * a.D + d] = overflowed ? 1 : 0;
-  (void)ro;
 }
 
 // out[d][b] (+)= 2^-S * (exact 128-bit sum of the fixed-point partials) + the
@@ -1046,7 +1038,7 @@ int fx_nv(const DenseArgs& a) {
   return a.dims[0] == (128u << (v - 1)) ? v + 4 : v;
 }
 
-using FxKernel = void (*)(DenseArgs, const float*, const uint32_t*, FxScaleArgs, int32_t*, int*,
+using FxKernel = void (*)(DenseArgs, const float*, const uint32_t*, const FxStats*, int32_t*, int*,
                           const uint8_t*);
 FxKernel fx_kernel(int v, bool group) {
   if (group) {  // full-vector kernels with the bank-aware load order
@@ -1076,8 +1068,8 @@ int fx64_nv(uint32_t i0) {
   while (32u * nv < i0) nv <<= 1;
   return nv;
 }
-using Fx64Kernel = void (*)(DenseArgs, const double*, const uint32_t*, FxScaleArgs, uint32_t*,
-                            int*, Fx64Out);
+using Fx64Kernel = void (*)(DenseArgs, const double*, const uint32_t*, const FxStats*, uint32_t*,
+                            int*);
 Fx64Kernel fx64_kernel(int nv, bool full) {
   switch (nv) {
     case 1: return full ? fcs_dense_fx64_kernel<1, true> : fcs_dense_fx64_kernel<1, false>;
@@ -1301,6 +1293,8 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
     FCS_CUDA_TRY(cudaGetLastError());
     const double per_cta = static_cast<double>(a.fibers_per_chunk) * a.dims[0];
     const FxScaleArgs sc{parts, nparts, 3.0 * per_cta / a.jt + 16.0, stats};
+    fx_scale_kernel<<<1, 512, 0, st>>>(sc, kFx32);
+    FCS_CUDA_TRY(cudaGetLastError());
     // bank-aware load order for the full-vector kernels (I_0 = 128 NV, NV >= 2)
     uint8_t* groups = nullptr;
     const int nv_full = p.nv >= 6 ? 1 << (p.nv - 5) : 0;
@@ -1317,7 +1311,7 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
       FCS_CUDA_TRY(cudaGetLastError());
     }
     fx_kernel(p.nv, p.group)<<<static_cast<unsigned>(nchunk * a.D), p.threads, p.smem_bytes, st>>>(
-        a, reinterpret_cast<const float*>(t), packed, sc, part, flags, groups);
+        a, reinterpret_cast<const float*>(t), packed, stats, part, flags, groups);
     FCS_CUDA_TRY(cudaGetLastError());
     reduce_fx_kernel<<<ceil_div(out_elems, 256), 256, 0, st>>>(part, flags, nchunk, a.D, a.jt,
                                                                stats, out, accumulate);
@@ -1339,12 +1333,13 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
     const double per_cta = static_cast<double>(a.fibers_per_chunk) * a.dims[0];
     const FxScaleArgs sc{parts, nparts, 3.0 * per_cta / a.jt + 16.0, stats};
     const bool full = a.dims[0] == 32u * p.nv;
-    Fx64Out ro{out, accumulate, nchunk, nsample};
     fx_sample_warps_kernel<double><<<ceil_div(nsample, 8), 256, 0, st>>>(
         a, reinterpret_cast<const double*>(t), nsample, parts);
     FCS_CUDA_TRY(cudaGetLastError());
+    fx_scale_kernel<<<1, 512, 0, st>>>(sc, kFx64);
+    FCS_CUDA_TRY(cudaGetLastError());
     fx64_kernel(p.nv, full)<<<static_cast<unsigned>(nchunk * a.D), p.threads, p.smem_bytes, st>>>(
-        a, reinterpret_cast<const double*>(t), packed, sc, part, flags, ro);
+        a, reinterpret_cast<const double*>(t), packed, stats, part, flags);
     FCS_CUDA_TRY(cudaGetLastError());
     reduce_fx64_kernel<<<ceil_div(out_elems, 32), dim3(32, 32), 0, st>>>(part, flags, nchunk, a.D,
                                                                         a.jt, stats, out,
