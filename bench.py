@@ -399,6 +399,56 @@ def secondary(x=None, cpu=True):
         except Exception as e:  # memory: 4 GiB fp32 + 8 GiB fp64 resident
             res["fp64_dense_1024^3_J8192_D1"] = {"error": repr(e)}
 
+    # sparse (COO) FCS at config-4 geometry, 1 % density (north_star (1), O(nnz))
+    try:
+        nnz_t = (1 << 30) // 100
+        g = torch.Generator(device="cuda").manual_seed(11)
+        flat = torch.unique(torch.randint(0, 1 << 30, (nnz_t,), device="cuda", generator=g))
+        nnz = flat.numel()
+        coords = torch.stack([flat % 1024, (flat // 1024) % 1024, flat // (1 << 20)], dim=1)
+        coords = coords.to(torch.int32).contiguous()
+        vals = torch.randn(nnz, dtype=torch.float64, device="cuda", generator=g)
+        fams = st.families_for(list(C4_DIMS), st.EstimatorConfig(C4_J, C4_D, C4_SEED))
+        packed = st.packed_families(fams)
+        dims_a, lens_a = L.size_array(list(C4_DIMS)), L.size_array([C4_J] * 3)
+        outc = torch.empty((C4_D, jt_of(C4_DIMS, C4_J)), dtype=torch.float64, device="cuda")
+
+        def coo_call():
+            L.check(lib.st_fcs_coo(L.ST_F64, C.c_void_p(vals.data_ptr()),
+                                   C.c_void_p(coords.data_ptr()), nnz, 3, dims_a, C4_D,
+                                   C.c_void_p(packed.data_ptr()), lens_a,
+                                   C.c_void_p(outc.data_ptr()), 0, None, sp))
+        ms = median_ms(coo_call, 10)
+        alg = nnz * (8 + 12) + C4_D * sum(C4_DIMS) * 5 + C4_D * jt_of(C4_DIMS, C4_J) * 8
+        e = {"ms": ms, "nnz": nnz, "nnz_per_sec": nnz / (ms * 1e-3),
+             "roofline": roofline_hbm(alg, ms, peak),
+             "bound_note": "fp64 L2 reductions: nnz x D = %d RED.E.ADD.F64" % (nnz * C4_D)}
+        if ref is not None:
+            # the reference has no sparse type: a sparse tensor costs it the dense sweep
+            # with the zero test (for_each_nonzero, sketch.cpp:48-61); sample: 16 slabs
+            sample = np.zeros((1024, 1024, 16))
+            fl = flat[flat < 16 * (1 << 20)].cpu().numpy()
+            sample.reshape(-1, order="F")[fl] = vals[:fl.size].cpu().numpy()
+            rt = ref.ResidentTensor.from_array(sample)
+            tabs = [ref.hash_family(C4_DIMS, C4_J, ref.family_seed(C4_SEED, d))[:2]
+                    for d in range(C4_D)]
+
+            def ref_sparse():
+                for b, s in tabs:
+                    rt.fcs([b[0], b[1], b[2][:16]], [s[0], s[1], s[2][:16]], [C4_J] * 3)
+            dt = median_time(ref_sparse, reps=3)
+            rt.close()
+            e["cpu_baseline"] = {"value": fl.size / dt, "unit": "nnz/s", "cores": 1,
+                                 "kind": "reference",
+                                 "sample": "16 of 1024 slabs (1024x1024x16, 1 % nonzero), D = 4: "
+                                           "the reference's dense fcs_sketch with zero skipping "
+                                           "(it has no sparse input), oracle/_ref, median of 3",
+                                 "seconds": dt}
+        res["c4_sparse_coo_1pct"] = e
+        del flat, coords, vals
+    except Exception as ex:
+        res["c4_sparse_coo_1pct"] = {"error": repr(ex)}
+
     # c1: dense FCS of 100^3 fp64, D = 1 (the reference's CPU-runnable case)
     c = configs.C1
     x1 = configs.c1_tensor(c)

@@ -150,6 +150,20 @@ int st_fcs_dense_host_tables(int dtype, const void* host_tensor, size_t order,
                              size_t sketch_count, const uint32_t* host_packed,
                              const size_t* hash_lens, double* host_out);
 
+/* Sparse-input FCS (north_star (1), O(nnz)): nnz nonzeros of
+ * an order-N tensor of shape dims as COO — values[k] (ST_F32 / ST_F64) at
+ * coords[k * order + n] (uint32, device) — for D families at once, out
+ * (+)= D x J~ fp64 (device). Equal to fcs_sketch(DenseTensor) of the
+ * densified tensor (sketch.cpp:187-201; duplicate coordinates add up, zeros
+ * are skipped like for_each_nonzero, sketch.cpp:48-61). Coordinates out of
+ * range are skipped and counted into *invalid (device, may be NULL): the
+ * caller raises compose's "compose: index out of range" (hashing.cpp:90-92).
+ * fp64 global reductions: run-to-run differences at the last bit. */
+int st_fcs_coo(int dtype, const void* values, const uint32_t* coords, size_t nnz, size_t order,
+               const size_t* dims, size_t sketch_count, const uint32_t* packed,
+               const size_t* hash_lens, double* out, int accumulate,
+               unsigned long long* invalid, void* stream);
+
 /* Count sketch of R columns (cs_sketch_columns, sketch.cpp:118-133; R = 1 is
  * cs_sketch, sketch.cpp:105-116): u is I x R column-major (device), table is
  * one packed pair, out is hash_len x R column-major fp64 (overwritten). */

@@ -8,7 +8,8 @@ compute call loads the library and fails loudly if it or the GPU is missing.
 from .sketchtensor import (CpTensor, DenseTensor, EstimatorConfig, HashFamily, HashPair,  # noqa
                            SketchKind, SketchTensor, SketchVec, convolve_pairs, cs_sketch,
                            cs_sketch_columns,
-                           families_for, family_seed, fcs_cp_batched, fcs_dense_batched,
+                           families_for, family_seed, fcs_coo_batched, fcs_cp_batched,
+                           fcs_dense_batched,
                            fcs_kron, fcs_sketch, hcs_sketch, median_reduce, packed_families,
                            ts_sketch, dft, idft_real, fft_convolve)
 from .engine import (AlsConfig, ContractionEngine, CsEngine, FcsEngine, HcsEngine,  # noqa

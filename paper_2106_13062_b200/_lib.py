@@ -37,6 +37,7 @@ SIGNATURES = {
     "st_fcs_dense_host_tables": (i32, [i32, p, sz, p, sz, sz, sz, p, p, p]),
     "st_fcs_dense_report": (i32, [i32, sz, p, sz, sz, p, p, sz, p, p, p]),
     "st_cs_columns": (i32, [p, sz, sz, p, sz, p, p]),
+    "st_fcs_coo": (i32, [i32, p, p, sz, sz, p, sz, p, p, p, i32, p, p]),
     "st_cs_expand": (i32, [p, sz, p, sz, p, p]),
     "st_fcs_cp_workspace": (sz, [sz, p, sz, sz, p]),
     "st_fcs_cp": (i32, [p, sz, sz, p, p, sz, sz, sz, p, p, p, i32, p, sz, p]),

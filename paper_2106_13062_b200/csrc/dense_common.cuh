@@ -24,6 +24,14 @@ struct DenseArgs {
   uint64_t fibers_per_chunk;
 };
 
+// A sparse (COO) sketch launch (fcs_coo.cu).
+struct CooArgs {
+  uint32_t dims[ST_MAX_ORDER];
+  uint32_t tab_off[ST_MAX_ORDER];
+  uint32_t fam_stride;
+  uint32_t jt;
+};
+
 // Offset and sign bit of fiber f (slab-local) for the family at `tab`.
 __device__ __forceinline__ void fiber_offset(const DenseArgs& a, const uint32_t* __restrict__ tab,
                                              uint64_t f, uint32_t& c, uint32_t& sbit) {

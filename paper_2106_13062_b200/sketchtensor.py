@@ -346,6 +346,43 @@ def fcs_dense_batched(t: DenseTensor, families: Sequence[HashFamily],
     return out
 
 
+def fcs_coo_batched(values, coords, shape, families: Sequence[HashFamily],
+                    packed: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """D FCSs of a sparse tensor given as COO (st_fcs_coo, O(nnz)): values
+    (nnz, fp32 or fp64) at coords (nnz x order, integer), shape = the dense
+    shape. Equals fcs_sketch of the densified tensor (duplicates add up);
+    ValueError "compose: index out of range" (hashing.cpp:90-92) for a
+    coordinate outside the shape. Returns D x J~ fp64 on the device."""
+    fams = list(families)
+    shape = [int(x) for x in shape]
+    for f in fams:
+        _require_family(shape, f, "fcs_sketch")
+    lens = fams[0].hash_lens()
+    if any(f.hash_lens() != lens for f in fams):
+        raise ValueError("fcs_sketch: families differ in hash lengths")
+    v = torch.as_tensor(values if torch.is_tensor(values) else np.asarray(values)).reshape(-1)
+    if v.dtype not in (torch.float32, torch.float64):
+        v = v.to(torch.float64)
+    v = v.to(_dev()).contiguous()
+    c = torch.as_tensor(coords if torch.is_tensor(coords) else np.asarray(coords))
+    nnz = v.numel()
+    c = c.reshape(nnz, len(shape))
+    if c.numel() and (int(c.min()) < 0 or int(c.max()) >= 2 ** 32):
+        raise ValueError("compose: index out of range")
+    c = c.to(torch.int64).to(_dev()).to(torch.int32).contiguous()  # uint32 bit pattern
+    if packed is None:
+        packed = packed_families(fams)
+    out = torch.empty((len(fams), fams[0].composed_len()), dtype=torch.float64, device=_dev())
+    bad = torch.zeros(1, dtype=torch.int64, device=_dev())
+    dt = L.ST_F32 if v.dtype == torch.float32 else L.ST_F64
+    _check(L.lib().st_fcs_coo(dt, _ptr(v), _ptr(c), nnz, len(shape), L.size_array(shape),
+                              len(fams), _ptr(packed), L.size_array(lens), _ptr(out), 0,
+                              _ptr(bad), _stream()))
+    if int(bad.item()):
+        raise ValueError("compose: index out of range")
+    return out
+
+
 def fcs_cp_batched(cp: CpTensor, families: Sequence[HashFamily],
                    packed: Optional[torch.Tensor] = None) -> torch.Tensor:
     """D CP-form FCSs (K2-K5); returns a D x J~ fp64 device tensor."""

@@ -871,3 +871,68 @@ def test_dense_f64_fixed_point_extreme_magnitude(cuda, sigma):
     x = sigma * rng.standard_normal((128, 250, 256))
     got, want = _f64_case(x, 1500, 1)
     rel_close(got, want, RTOL64)
+
+
+# -------------------------------------------------------- sparse (COO) FCS
+def _coo(shape, density, seed, dtype=np.float64):
+    rng = np.random.default_rng(seed)
+    n = int(np.prod(shape))
+    nnz = max(1, int(n * density))
+    flat = rng.choice(n, size=nnz, replace=False)
+    coords = np.stack(np.unravel_index(flat, shape, order="F"), axis=1).astype(np.int64)
+    vals = rng.standard_normal(nnz).astype(dtype)
+    dense = np.zeros(shape, dtype=np.float64)
+    dense[tuple(coords.T)] = vals
+    return vals, coords, dense
+
+
+@pytest.mark.parametrize("density", [0.01, 0.001])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_sparse_coo_vs_reference(cuda, density, dtype):
+    """FCS from a COO list equals the unmodified reference's fcs_sketch of the
+    densified tensor (1 % and 0.1 % density; fp64 at the fp64 rule, fp32 values
+    widened exactly)."""
+    from oracle import ref
+    shape = (120, 90, 70)
+    vals, coords, dense = _coo(shape, density, 50 + int(1e4 * density), dtype)
+    fams = st.families_for(list(shape), st.EstimatorConfig(400, 3, 8))
+    got = st.fcs_coo_batched(vals, coords, shape, fams).cpu().numpy()
+    for d, f in enumerate(fams):
+        b, s, j = oracle_family(f)
+        rel_close(got[d], ref.fcs_dense_tables(dense, b, s, j), RTOL64)
+
+
+def test_sparse_coo_duplicates_zeros_errors(cuda):
+    shape = (7, 5, 4)
+    fams = st.families_for(list(shape), st.EstimatorConfig(9, 2, 3))
+    coords = np.array([[1, 2, 3], [1, 2, 3], [6, 4, 0], [0, 0, 0]])
+    vals = np.array([1.5, -0.25, 2.0, 0.0])
+    dense = np.zeros(shape)
+    dense[1, 2, 3] = 1.25
+    dense[6, 4, 0] = 2.0
+    got = st.fcs_coo_batched(vals, coords, shape, fams).cpu().numpy()
+    for d, f in enumerate(fams):
+        b, s, j = oracle_family(f)
+        np.testing.assert_array_equal(got[d], O.fcs_dense(dense, b, s, j))
+    empty = st.fcs_coo_batched(np.zeros(0), np.zeros((0, 3)), shape, fams)
+    assert torch.count_nonzero(empty) == 0
+    with pytest.raises(ValueError, match="compose: index out of range"):
+        st.fcs_coo_batched([1.0], [[7, 0, 0]], shape, fams)
+
+
+def test_sparse_coo_c4_geometry(cuda):
+    """Config-4 geometry (1024^3, J = 16384, D = 4) at 0.1 % density (1.07M
+    nonzeros): the COO sketch equals K1 (fp64, itself pinned to the
+    reference) on the densified tensor."""
+    shape = (1024, 1024, 1024)
+    rng = np.random.default_rng(77)
+    nnz = (1 << 30) // 1000
+    flat = np.unique(rng.integers(0, 1 << 30, size=nnz, dtype=np.int64))
+    coords = np.stack(np.unravel_index(flat, shape, order="F"), axis=1)
+    vals = rng.standard_normal(flat.size)
+    fams = st.families_for(list(shape), st.EstimatorConfig(16384, 4, 4))
+    got = st.fcs_coo_batched(vals, coords, shape, fams)
+    dense = torch.zeros(1 << 30, dtype=torch.float64, device="cuda")
+    dense[torch.from_numpy(flat).cuda()] = torch.from_numpy(vals).cuda()
+    want = st.fcs_dense_batched(st.DenseTensor(list(shape), dense), fams)
+    rel_close(got, want.cpu().numpy(), RTOL64)
