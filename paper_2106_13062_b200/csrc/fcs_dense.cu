@@ -490,19 +490,44 @@ __device__ __forceinline__ void fiber_offset_fast(const DenseArgs& a, const uint
 // warp per fiber, lane-owned mode-0 indices with their table entries in
 // registers, NV 128-bit loads per lane with the next fiber prefetched,
 // int32 fixed-point shared-memory accumulation with exact overflow detection.
-template <int NV, int SPLIT, int THREADS, bool kFull, bool kGroup = false>
+__device__ void fx_float_redo(const DenseArgs& a, const float* __restrict__ t,
+                              const uint32_t* __restrict__ tab, float scale, uint64_t chunk,
+                              bool skip_diverted, float* skf);
+
+// kRedo = false: the scatter; kRedo = true: the same loop over the chunks the
+// scatter flagged (flag 2: an element out of the fixed-point range), each
+// out-of-range element diverted to an fp64 reduction into `divert` (D x J~,
+// added by reduce_fx_kernel) so the chunk stays in fixed point; a chunk that
+// wraps (or was flagged for wrap / tiny partials, flag 4) is redone with fp32
+// shared atomics (fx_float_redo), skipping what was diverted.
+template <int NV, int SPLIT, int THREADS, bool kFull, bool kGroup = false, bool kRedo = false>
 __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
                                                               const float* __restrict__ t,
                                                               const uint32_t* __restrict__ packed,
                                                               const FxStats* __restrict__ st,
                                                               int32_t* __restrict__ part,
                                                               int* __restrict__ flags,
-                                                              const uint8_t* __restrict__ groups) {
+                                                              const uint8_t* __restrict__ groups,
+                                                              double* __restrict__ divert) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int32_t* sk = reinterpret_cast<int32_t*>(smem_raw);
   const int d = blockIdx.x % a.D;
   const uint64_t chunk = blockIdx.x / a.D;
   const uint32_t* tab = packed + static_cast<uint64_t>(d) * a.fam_stride;
+  int in_flag = 0;
+  if constexpr (kRedo) {
+    in_flag = flags[chunk * a.D + d];
+    if (!(in_flag & 2)) return;
+    if (in_flag & 4) {  // wrap or tiny partials: the fixed point cannot help
+      fx_float_redo(a, t, tab, ldexpf(1.0f, st->S), chunk, false,
+                    reinterpret_cast<float*>(smem_raw));
+      int32_t* dst = part + (chunk * a.D + d) * static_cast<uint64_t>(a.jt);
+      for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) dst[b] = sk[b];
+      if (threadIdx.x == 0) flags[chunk * a.D + d] = 1;
+      return;
+    }
+  }
+  double* dv = kRedo ? divert + static_cast<uint64_t>(d) * a.jt : nullptr;
   const float scale = ldexpf(1.0f, st->S);
   for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) sk[b] = 0;
 
@@ -586,8 +611,18 @@ __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
           // the sum's bits are 0x4B400000 + round(y), exponent 0x96; any other
           // exponent (out of range, Inf, NaN) leaves bits >= 23 in bits ^ 0x4B000000
           const uint32_t bits = __float_as_uint(fmaf(xs, scale_f, 12582912.0f));
-          rng_acc |= bits ^ 0x4B000000u;
-          const int32_t q = static_cast<int32_t>(bits - 0x4B400000u);
+          int32_t q;
+          if constexpr (kRedo) {
+            q = static_cast<int32_t>(bits - 0x4B400000u);
+            if ((bits ^ 0x4B000000u) >> 23) {  // exact fp64 reduction instead
+              atomicAdd(dv + (e & 0x7fffffffu) + c,
+                        static_cast<double>(scale_f < 0.f ? -xs : xs));
+              q = 0;
+            }
+          } else {
+            rng_acc |= bits ^ 0x4B000000u;
+            q = static_cast<int32_t>(bits - 0x4B400000u);
+          }
           int32_t old;
           asm volatile("atom.shared.add.s32 %0, [%1], %2;"
                        : "=r"(old)
@@ -607,10 +642,23 @@ __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
     if (f + 2 * nwarps < f_end) load(f + 2 * nwarps, cur);
     scatter(nxt, f + nwarps);
   }
-  ovf = (ovf_acc >> 31) | ((rng_acc >> 23) != 0);
-
-  bool overflowed = __syncthreads_or(ovf);
-  if (!overflowed) {  // precision guard (kFxSmallBits): all partials nonzero-but-tiny
+  if constexpr (kRedo) {
+    const bool wrapped = __syncthreads_or(static_cast<int>(ovf_acc >> 31));
+    if (wrapped)
+      fx_float_redo(a, t, tab, scale, chunk, true, reinterpret_cast<float*>(smem_raw));
+    int32_t* dst = part + (chunk * a.D + d) * static_cast<uint64_t>(a.jt);
+    for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) dst[b] = sk[b];
+    if (threadIdx.x == 0) flags[chunk * a.D + d] = wrapped ? 1 : 8;  // 8: fixed point, redone
+    return;
+  }
+  // A CTA that saw an out-of-range or non-finite element (range), a partial
+  // reaching 2^30 (wrap), or only nonzero-but-tiny partials (precision guard,
+  // kFxSmallBits) leaves its chunk to the kRedo instantiation: flag 2 (+4 when
+  // the fixed point cannot help: wrap or tiny partials).
+  const bool wrapped = __syncthreads_or(static_cast<int>(ovf_acc >> 31));
+  const bool ranged = __syncthreads_or(static_cast<int>((rng_acc >> 23) != 0));
+  bool tiny = false;
+  if (!wrapped && !ranged) {  // precision guard: all partials nonzero-but-tiny
     int nz = 0, big = 0;
     for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) {
       const int32_t v = sk[b];
@@ -619,29 +667,47 @@ __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
       big |= (m >> kFxSmallBits) != 0u;
     }
     const bool any_big = __syncthreads_or(big);
-    overflowed = __syncthreads_or(nz) && !any_big;
+    tiny = __syncthreads_or(nz) && !any_big;
   }
-  if (overflowed) {
-    // Exact fallback for this CTA: float atomics over the same chunk.
-    float* skf = reinterpret_cast<float*>(smem_raw);
-    for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) skf[b] = 0.f;
-    __syncthreads();
-    const int wall = threadIdx.x >> 5, nwall = blockDim.x >> 5;
-    for (uint64_t g = f_begin + wall; g < f_end; g += nwall) {
-      uint32_t c, sbit;
-      fiber_offset(a, tab, g, c, sbit);
-      for (uint32_t i = lane; i < i0n; i += 32) {
-        const float x = __ldcs(t + g * i0n + i);
-        const uint32_t e = __ldg(tab + a.i0_shift + i);
-        atomicAdd(&skf[(e & 0x7fffffffu) + c],
-                  __uint_as_float(__float_as_uint(x) ^ ((e ^ sbit) & 0x80000000u)));
-      }
-    }
-    __syncthreads();
-  }
+  // (an out-of-range element also adds a garbage word, which can fake a wrap:
+  // with `ranged` the redo decides about wrapping itself)
+  if (threadIdx.x == 0)
+    flags[chunk * a.D + d] =
+        (wrapped || ranged || tiny) ? (2 | ((!ranged && (wrapped || tiny)) ? 4 : 0)) : 0;
+  if (wrapped || ranged || tiny) return;
   int32_t* dst = part + (chunk * a.D + d) * static_cast<uint64_t>(a.jt);
   for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) dst[b] = sk[b];
-  if (threadIdx.x == 0) flags[chunk * a.D + d] = overflowed ? 1 : 0;
+}
+
+// fp32 shared-atomic redo of one chunk into skf (the CTA's sketch memory);
+// skip_diverted: leave out the elements the fixed-point redo diverted (out of
+// range at this scale) — they are already in `divert`.
+__device__ void fx_float_redo(const DenseArgs& a, const float* __restrict__ t,
+                              const uint32_t* __restrict__ tab, float scale, uint64_t chunk,
+                              bool skip_diverted, float* skf) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint64_t f_begin = chunk * a.fibers_per_chunk;
+  const uint64_t f_end = min(a.fibers, f_begin + a.fibers_per_chunk);
+  const uint32_t i0n = a.dims[0];
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) skf[b] = 0.f;
+  __syncthreads();
+  for (uint64_t g = f_begin + warp; g < f_end; g += nwarps) {
+    uint32_t c, sbit;
+    fiber_offset(a, tab, g, c, sbit);
+    const float scale_f = sbit ? -scale : scale;
+    for (uint32_t i = lane; i < i0n; i += 32) {
+      const float x = __ldcs(t + g * i0n + i);
+      const uint32_t e = __ldg(tab + a.i0_shift + i);
+      if (skip_diverted) {
+        const float xs = __uint_as_float(__float_as_uint(x) ^ (e & 0x80000000u));
+        if ((__float_as_uint(fmaf(xs, scale_f, 12582912.0f)) ^ 0x4B000000u) >> 23) continue;
+      }
+      atomicAdd(&skf[(e & 0x7fffffffu) + c],
+                __uint_as_float(__float_as_uint(x) ^ ((e ^ sbit) & 0x80000000u)));
+    }
+  }
+  __syncthreads();
 }
 
 // float64 fixed-point path (any order >= 2, I_0 <= 1024): shared-memory
@@ -939,8 +1005,8 @@ __global__ void reduce_partials_kernel(const Tacc* __restrict__ part, uint64_t n
 // Same for fixed-point partials (flag 0: int32 * 2^-S, flag 1: float bits).
 __global__ void reduce_fx_kernel(const int32_t* __restrict__ part, const int* __restrict__ flags,
                                  uint64_t nchunk, int D, uint32_t jt,
-                                 const FxStats* __restrict__ st, double* __restrict__ out,
-                                 int accumulate) {
+                                 const FxStats* __restrict__ st, const double* __restrict__ divert,
+                                 double* __restrict__ out, int accumulate) {
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   const uint64_t per = static_cast<uint64_t>(D) * jt;
   if (i >= per) return;
@@ -948,7 +1014,7 @@ __global__ void reduce_fx_kernel(const int32_t* __restrict__ part, const int* __
   const double inv = ldexp(1.0, -st->S);
   double acc = accumulate ? out[i] : 0.0;
   auto term = [&](int32_t w, int fl) {
-    return fl ? static_cast<double>(__int_as_float(w)) : static_cast<double>(w) * inv;
+    return fl == 1 ? static_cast<double>(__int_as_float(w)) : static_cast<double>(w) * inv;
   };
   uint64_t c = 0;
   for (; c + 4 <= nchunk; c += 4) {  // four partials in flight, summed in chunk order
@@ -963,7 +1029,7 @@ __global__ void reduce_fx_kernel(const int32_t* __restrict__ part, const int* __
     for (int u = 0; u < 4; ++u) acc += term(w[u], fl[u]);
   }
   for (; c < nchunk; ++c) acc += term(part[c * per + i], flags[c * D + d]);
-  out[i] = acc;
+  out[i] = acc + divert[i];
 }
 
 // Fallback when one family's sketch does not fit in shared memory: fp64
@@ -1039,26 +1105,30 @@ int fx_nv(const DenseArgs& a) {
 }
 
 using FxKernel = void (*)(DenseArgs, const float*, const uint32_t*, const FxStats*, int32_t*, int*,
-                          const uint8_t*);
-FxKernel fx_kernel(int v, bool group) {
+                          const uint8_t*, double*);
+template <bool kRedo>
+FxKernel fx_kernel_t(int v, bool group) {
   if (group) {  // full-vector kernels with the bank-aware load order
     switch (v) {
-      case 6: return fcs_dense_fx_kernel<2, 1, 512, true, true>;
-      case 7: return fcs_dense_fx_kernel<4, 1, 512, true, true>;
-      case 8: return fcs_dense_fx_kernel<8, 1, 512, true, true>;
+      case 6: return fcs_dense_fx_kernel<2, 1, 512, true, true, kRedo>;
+      case 7: return fcs_dense_fx_kernel<4, 1, 512, true, true, kRedo>;
+      case 8: return fcs_dense_fx_kernel<8, 1, 512, true, true, kRedo>;
       default: break;
     }
   }
   switch (v) {
-    case 1: return fcs_dense_fx_kernel<1, 1, 512, false>;
-    case 2: return fcs_dense_fx_kernel<2, 1, 512, false>;
-    case 3: return fcs_dense_fx_kernel<4, 1, 512, false>;
-    case 4: return fcs_dense_fx_kernel<8, 1, 512, false>;
-    case 5: return fcs_dense_fx_kernel<1, 1, 512, true>;
-    case 6: return fcs_dense_fx_kernel<2, 1, 512, true>;
-    case 7: return fcs_dense_fx_kernel<4, 1, 512, true>;
-    default: return fcs_dense_fx_kernel<8, 1, 512, true>;
+    case 1: return fcs_dense_fx_kernel<1, 1, 512, false, false, kRedo>;
+    case 2: return fcs_dense_fx_kernel<2, 1, 512, false, false, kRedo>;
+    case 3: return fcs_dense_fx_kernel<4, 1, 512, false, false, kRedo>;
+    case 4: return fcs_dense_fx_kernel<8, 1, 512, false, false, kRedo>;
+    case 5: return fcs_dense_fx_kernel<1, 1, 512, true, false, kRedo>;
+    case 6: return fcs_dense_fx_kernel<2, 1, 512, true, false, kRedo>;
+    case 7: return fcs_dense_fx_kernel<4, 1, 512, true, false, kRedo>;
+    default: return fcs_dense_fx_kernel<8, 1, 512, true, false, kRedo>;
   }
+}
+FxKernel fx_kernel(int v, bool group, bool redo = false) {
+  return redo ? fx_kernel_t<true>(v, group) : fx_kernel_t<false>(v, group);
 }
 inline int fx_threads(int) { return 512; }
 
@@ -1179,6 +1249,7 @@ int make_plan_uncached(const DenseArgs& a, Plan* p) {
     p->group = p->nv >= 6 && a.D >= 2 && !no_group;
     auto k = fx_kernel(p->nv, p->group);
     FCS_CUDA_TRY(set_max_dynamic_smem(k, di));
+    FCS_CUDA_TRY(set_max_dynamic_smem(fx_kernel(p->nv, p->group, true), di));
     FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
                                                                p->smem_bytes));
   } else {
@@ -1205,7 +1276,8 @@ int make_plan_uncached(const DenseArgs& a, Plan* p) {
   p->part_bytes = nchunk * a.D * static_cast<size_t>(a.jt) * sizeof(Tacc);
   p->ws = align_up(p->part_bytes) + align_up(nchunk * a.D * sizeof(int)) +
           align_up(sizeof(FxStats)) + align_up(static_cast<size_t>(a.D) * 32) +
-          align_up(kFxMaxSample * sizeof(FxPart));
+          align_up(kFxMaxSample * sizeof(FxPart)) +
+          align_up(static_cast<size_t>(a.D) * a.jt * sizeof(double));  // fp32: divert
   return ST_OK;
 }
 
@@ -1310,11 +1382,21 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
                                             groups, cache);
       FCS_CUDA_TRY(cudaGetLastError());
     }
+    auto* divert = reinterpret_cast<double*>(
+        base + align_up(p.part_bytes) + align_up(p.nchunk * a.D * sizeof(int)) +
+        align_up(sizeof(FxStats)) + align_up(static_cast<size_t>(a.D) * 32) +
+        align_up(kFxMaxSample * sizeof(FxPart)));
+    FCS_CUDA_TRY(cudaMemsetAsync(divert, 0, out_elems * sizeof(double), st));
     fx_kernel(p.nv, p.group)<<<static_cast<unsigned>(nchunk * a.D), p.threads, p.smem_bytes, st>>>(
-        a, reinterpret_cast<const float*>(t), packed, stats, part, flags, groups);
+        a, reinterpret_cast<const float*>(t), packed, stats, part, flags, groups, divert);
+    FCS_CUDA_TRY(cudaGetLastError());
+    // redo of the flagged chunks (unflagged CTAs exit at once)
+    fx_kernel(p.nv, p.group, true)<<<static_cast<unsigned>(nchunk * a.D), p.threads, p.smem_bytes,
+                                     st>>>(a, reinterpret_cast<const float*>(t), packed, stats,
+                                           part, flags, groups, divert);
     FCS_CUDA_TRY(cudaGetLastError());
     reduce_fx_kernel<<<ceil_div(out_elems, 256), 256, 0, st>>>(part, flags, nchunk, a.D, a.jt,
-                                                               stats, out, accumulate);
+                                                               stats, divert, out, accumulate);
     FCS_CUDA_TRY(cudaGetLastError());
     return ST_OK;
   }
