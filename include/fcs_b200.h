@@ -108,12 +108,16 @@ size_t st_fcs_dense_workspace(int dtype, size_t order, const size_t* dims, size_
  * 16-byte aligned tensor accumulates each CTA's partial sketch in int32 fixed
  * point, value * 2^S rounded to nearest, with S chosen per call from a
  * sampled bound on the partials (error <= 2^-(S+1) per element; the same S
- * and result on every run); an element out of range, a non-finite element,
- * a partial reaching 2^30, or a CTA whose partials all stay below 2^16 makes
- * that CTA redo its chunk with fp32 shared-memory atomics (order-dependent
- * rounding). Other fp32 shapes accumulate in fp32 atomics. ST_F64 accumulates
- * in fp64. Partials are reduced in fp64 in a fixed order. accumulate != 0
- * adds to out instead of overwriting it.
+ * and result on every run). A CTA that meets an element out of range or
+ * non-finite redoes its chunk in fixed point with those elements diverted to
+ * an exact fp64 reduction; a partial reaching 2^30, or partials that all stay
+ * below 2^16, make it redo the chunk with fp32 shared-memory atomics
+ * (order-dependent rounding). Other fp32 shapes accumulate in fp32 atomics.
+ * ST_F64 with I_0 <= 1024 and >= 8M element-updates accumulates in 64-bit
+ * fixed point (two int32 atomics per element, exact carries; partials summed
+ * exactly in 128-bit integers; deterministic), smaller calls in fp64 atomics.
+ * Partials are reduced in a fixed order. accumulate != 0 adds to out instead
+ * of overwriting it.
  * Replaces fcs_sketch(const DenseTensor&, const HashFamily&), sketch.cpp:187-201
  * (D calls, one per family). */
 int st_fcs_dense(int dtype, const void* tensor, size_t order, const size_t* dims,
