@@ -1263,9 +1263,11 @@ int make_plan_uncached(const DenseArgs& a, Plan* p) {
   per_sm = std::max(per_sm, 1);
   const uint64_t resident = static_cast<uint64_t>(per_sm) * di.sm_count;
   uint64_t nchunk = std::max<uint64_t>(1, resident / static_cast<uint64_t>(a.D));
-  // at least ~4 fibers per warp of a 512-thread CTA: per-CTA fixed costs
-  // (zeroing, the scale, writing the partial) dominate smaller shares
-  nchunk = std::min<uint64_t>(nchunk, std::max<uint64_t>(1, a.fibers / 64));
+  // fixed point: at least ~4 fibers per warp of a 512-thread CTA (per-CTA
+  // fixed costs — zeroing, writing the partial — dominate smaller shares);
+  // the atomic kernel keeps 16 fibers per chunk (c1: 333 chunks, 22 us)
+  const bool fixed = p->path == Path::Fx || p->path == Path::Fx64;
+  nchunk = std::min<uint64_t>(nchunk, std::max<uint64_t>(1, a.fibers / (fixed ? 64 : 16)));
   // Small tensors: each chunk writes (and the reduction re-reads) a D x J~
   // partial, so keep the partials to at most the tensor's bytes (config 1:
   // 592 -> 333 chunks; config 4 is unaffected).

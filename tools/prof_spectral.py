@@ -53,6 +53,23 @@ def main():
             eng.iuv_batch(U, U, 0)
         torch.cuda.synchronize()
         res["c3_iuv_ms"] = (time.perf_counter() - t0) * 50
+    if "c5" in which:
+        c = configs.C5
+        A, B = configs.c5_matrices(c)
+        fams = st.families_for(list(c.dims), st.EstimatorConfig(c.hash_len, c.sketch_count, c.seed))
+        for _ in range(args.reps):
+            st.fcs_kron(A, B, fams)
+        torch.cuda.synchronize()
+    if "coo" in which:  # sparse FCS at config-4 geometry, 1 % density
+        g = torch.Generator(device="cuda").manual_seed(11)
+        flat = torch.unique(torch.randint(0, 1 << 30, ((1 << 30) // 100,), device="cuda",
+                                          generator=g))
+        coords = torch.stack([flat % 1024, (flat // 1024) % 1024, flat // (1 << 20)], 1)
+        vals = torch.randn(flat.numel(), dtype=torch.float64, device="cuda", generator=g)
+        fams = st.families_for([1024] * 3, st.EstimatorConfig(16384, 4, 4))
+        for _ in range(args.reps):
+            st.fcs_coo_batched(vals, coords, [1024] * 3, fams)
+        torch.cuda.synchronize()
     print(res)
 
 
