@@ -733,6 +733,13 @@ __device__ __forceinline__ double ld_stream64(const double* p) {
   asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
+// fp32 input to the 64-bit fixed point (fp32 tensors the int32 kernel does not
+// take: I_0 % 4 != 0); widened exactly.
+__device__ __forceinline__ double ld_stream64(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return static_cast<double>(v);
+}
 
 // Warp-level sample statistics of fiber k * fibers / nsample into parts[k]
 // (per-fiber order fixed).
@@ -779,9 +786,9 @@ inline uint64_t fx_nsample(uint64_t fibers) {
 
 __device__ __forceinline__ double i128_to_double(__int128 acc);
 
-template <int NV, bool kFull>
+template <typename Tin, int NV, bool kFull>
 __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
-                                                             const double* __restrict__ t,
+                                                             const Tin* __restrict__ t,
                                                              const uint32_t* __restrict__ packed,
                                                              const FxStats* __restrict__ st,
                                                              uint32_t* __restrict__ part,
@@ -795,19 +802,20 @@ __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
   for (uint32_t b = threadIdx.x; b < 2 * a.jt; b += blockDim.x) lo[b] = 0u;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const uint32_t i0n = a.dims[0];
-  // mode-0 buckets two per register (bucket < jt <= 29056 < 2^16), signs and
-  // validity as bit masks (bit k: entry i_0 = lane + 32 k)
+  // mode-0 buckets two per register (bucket < jt <= 29056 < 2^16) and signs
+  // as a bit mask (bit k: entry i_0 = lane + 32 k). Entries past I_0 load no
+  // data (x = 0 adds q = 0) and point at bucket `lane`: distinct banks, so the
+  // padding lanes of a partial fiber cost no conflicts and need no predicate.
   uint32_t bk[(NV + 1) / 2];
-  uint32_t smask = 0, vmask = 0;
+  uint32_t smask = 0;
 #pragma unroll
   for (int k = 0; k < (NV + 1) / 2; ++k) bk[k] = 0u;
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     const uint32_t i = lane + 32u * k;
-    const uint32_t e = i < i0n ? __ldg(tab + a.i0_shift + i) : 0u;
+    const uint32_t e = i < i0n ? __ldg(tab + a.i0_shift + i) : static_cast<uint32_t>(lane);
     bk[k / 2] |= (e & 0xffffu) << (16 * (k % 2));
     smask |= (e >> 31) << k;
-    vmask |= (i < i0n ? 1u : 0u) << k;
   }
   __syncthreads();
   const uint64_t f_begin = chunk * a.fibers_per_chunk;
@@ -822,7 +830,7 @@ __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
   constexpr int NB = NV / LB;
   constexpr int G = LB < 4 ? LB : 4;
   auto load = [&]<int KB>(uint64_t f, double* x) {
-    const double* fib = t + f * i0n;
+    const Tin* fib = t + f * i0n;
 #pragma unroll
     for (int k = 0; k < LB; ++k)
       x[k] = (kFull || lane + 32u * (KB + k) < i0n) ? ld_stream64(fib + lane + 32 * (KB + k)) : 0.0;
@@ -858,27 +866,15 @@ __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
       }
       // the low-word adds first (their returned values give the carries), then the high words
 #pragma unroll
-      for (int k = 0; k < G; ++k) {
-        const int kk = KB + kg + k;
-        old[k] = 0u;
-        if (kFull)
-          asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "+r"(old[k]) : "r"(ad[k]), "r"(ql[k]));
-        else
-          asm volatile("{ .reg .pred p; setp.ne.u32 p, %3, 0; @p atom.shared.add.u32 %0, [%1], %2; }"
-                       : "+r"(old[k]) : "r"(ad[k]), "r"(ql[k]), "r"(vmask & (1u << kk)));
-      }
+      for (int k = 0; k < G; ++k)
+        asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old[k]) : "r"(ad[k]), "r"(ql[k]));
 #pragma unroll
       for (int k = 0; k < G; ++k) {
-        const int kk = KB + kg + k;
-        uint32_t hv, oh = 0u;
+        uint32_t hv, oh;
         // carry out of old + q_lo into q_hi
         asm("{ .reg .u32 tmp; add.cc.u32 tmp, %1, %2; addc.u32 %0, %3, 0; }"
             : "=r"(hv) : "r"(old[k]), "r"(ql[k]), "r"(qh[k]));
-        if (kFull)
-          asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "+r"(oh) : "r"(ad[k] + hi_off), "r"(hv));
-        else
-          asm volatile("{ .reg .pred p; setp.ne.u32 p, %3, 0; @p atom.shared.add.u32 %0, [%1], %2; }"
-                       : "+r"(oh) : "r"(ad[k] + hi_off), "r"(hv), "r"(vmask & (1u << kk)));
+        asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(oh) : "r"(ad[k] + hi_off), "r"(hv));
         // guard band: |partial| >= 2^61 sets bit 31 of hi + 2^29 (one add moves hi < 2^20)
         ovf_acc |= oh + 0x20000000u;
       }
@@ -914,7 +910,7 @@ __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
       uint32_t c, sbit;
       fiber_offset(a, tab, g, c, sbit);
       for (uint32_t i = lane; i < i0n; i += 32) {
-        const double x = __ldcs(t + g * i0n + i);
+        const double x = static_cast<double>(__ldcs(t + g * i0n + i));
         const uint32_t e = __ldg(tab + a.i0_shift + i);
         if (x != 0.0) atomicAdd(&skd[(e & 0x7fffffffu) + c], ((e ^ sbit) & 0x80000000u) ? -x : x);
       }
@@ -925,6 +921,124 @@ __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
   uint32_t* dst = part + (chunk * a.D + d) * 2ull * a.jt;
   for (uint32_t b = threadIdx.x; b < 2 * a.jt; b += blockDim.x) dst[b] = lo[b];
   if (threadIdx.x == 0) flags[chunk * a.D + d] = overflowed ? 1 : 0;
+}
+
+// float32 fixed point with scalar loads (fp32 tensors off the float4 path:
+// I_0 % 4 != 0 or a tensor not 16-byte aligned, I_0 <= 1024): the int32
+// fixed point of fcs_dense_fx_kernel (same scale, range check, wrap guard and
+// partial format) on the fx64 kernel's lane layout — i_0 = lane + 32 k,
+// k < NV, buckets packed two per register, signs as a bit mask, padding lanes
+// of a partial fiber adding 0 to bucket `lane`, batches of LB loads in flight.
+// A flagged chunk (range, wrap or tiny partials) is redone with fp32 shared
+// atomics. One LDG.32 per element moves the same 128-byte lines as the float4
+// loads, so the LSU wavefronts per element are unchanged.
+template <int NV, bool kFull>
+__global__ void __launch_bounds__(512) fcs_dense_fx32s_kernel(DenseArgs a,
+                                                              const float* __restrict__ t,
+                                                              const uint32_t* __restrict__ packed,
+                                                              const FxStats* __restrict__ st,
+                                                              int32_t* __restrict__ part,
+                                                              int* __restrict__ flags) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int32_t* sk = reinterpret_cast<int32_t*>(smem_raw);
+  const int d = blockIdx.x % a.D;
+  const uint64_t chunk = blockIdx.x / a.D;
+  const uint32_t* tab = packed + static_cast<uint64_t>(d) * a.fam_stride;
+  const float scale = ldexpf(1.0f, st->S);
+  for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) sk[b] = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint32_t i0n = a.dims[0];
+  uint32_t bk[(NV + 1) / 2];
+  uint32_t smask = 0;
+#pragma unroll
+  for (int k = 0; k < (NV + 1) / 2; ++k) bk[k] = 0u;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const uint32_t i = lane + 32u * k;
+    const uint32_t e = i < i0n ? __ldg(tab + a.i0_shift + i) : static_cast<uint32_t>(lane);
+    bk[k / 2] |= (e & 0xffffu) << (16 * (k % 2));
+    smask |= (e >> 31) << k;
+  }
+  __syncthreads();
+  const uint64_t f_begin = chunk * a.fibers_per_chunk;
+  const uint64_t f_end = min(a.fibers, f_begin + a.fibers_per_chunk);
+  const uint32_t sk_base = static_cast<uint32_t>(__cvta_generic_to_shared(sk));
+  uint32_t rng_acc = 0, ovf_acc = 0;
+  constexpr int LB = NV < 16 ? NV : 16;
+  constexpr int NB = NV / LB;
+  auto load = [&]<int KB>(uint64_t f, float* x) {
+    const float* fib = t + f * i0n;
+#pragma unroll
+    for (int k = 0; k < LB; ++k) {
+      const uint32_t i = lane + 32u * (KB + k);
+      if (kFull || i < i0n) {
+        asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(x[k]) : "l"(fib + i));
+      } else {
+        x[k] = 0.f;
+      }
+    }
+  };
+  uint32_t base_c = 0;
+  float scale_f = scale;
+  auto scatter = [&]<int KB>(uint64_t f, const float* x) {
+    if (KB == 0) {
+      uint32_t c, sbit;
+      fiber_offset_fast(a, tab, f, c, sbit);
+      base_c = sk_base + 4u * c;
+      scale_f = sbit ? -scale : scale;
+    }
+#pragma unroll
+    for (int k = 0; k < LB; ++k) {
+      const int kk = KB + k;
+      const uint32_t e = (kk % 2) ? (bk[kk / 2] >> 16) : (bk[kk / 2] & 0xffffu);
+      const float xs = __uint_as_float(__float_as_uint(x[k]) ^
+                                       ((smask >> kk) << 31));
+      const uint32_t bits = __float_as_uint(fmaf(xs, scale_f, 12582912.0f));
+      rng_acc |= bits ^ 0x4B000000u;
+      int32_t old;
+      asm volatile("atom.shared.add.s32 %0, [%1], %2;"
+                   : "=r"(old)
+                   : "r"(base_c + (e << 2)), "r"(static_cast<int32_t>(bits - 0x4B400000u)));
+      ovf_acc |= static_cast<uint32_t>(old) + 0x40000000u;
+    }
+  };
+  float cur[LB], nxt[LB];
+  uint64_t f = f_begin + warp;
+  if (f < f_end) load.template operator()<0>(f, cur);
+  if constexpr (NB == 1) {
+    for (; f < f_end; f += 2 * nwarps) {
+      if (f + nwarps < f_end) load.template operator()<0>(f + nwarps, nxt);
+      scatter.template operator()<0>(f, cur);
+      if (f + nwarps >= f_end) break;
+      if (f + 2 * nwarps < f_end) load.template operator()<0>(f + 2 * nwarps, cur);
+      scatter.template operator()<0>(f + nwarps, nxt);
+    }
+  } else {
+    static_assert(NB == 2, "NV <= 32: at most two batches of 16");
+    for (; f < f_end; f += nwarps) {
+      load.template operator()<LB>(f, nxt);
+      scatter.template operator()<0>(f, cur);
+      if (f + nwarps < f_end) load.template operator()<0>(f + nwarps, cur);
+      scatter.template operator()<LB>(f, nxt);
+    }
+  }
+  const bool bad = __syncthreads_or(static_cast<int>((ovf_acc >> 31) | ((rng_acc >> 23) != 0)));
+  bool tiny = false;
+  if (!bad) {  // precision guard (kFxSmallBits), as in fcs_dense_fx_kernel
+    int nz = 0, big = 0;
+    for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) {
+      const int32_t v = sk[b];
+      const uint32_t m = static_cast<uint32_t>(v < 0 ? -v : v);
+      nz |= m != 0u;
+      big |= (m >> kFxSmallBits) != 0u;
+    }
+    const bool any_big = __syncthreads_or(big);
+    tiny = __syncthreads_or(nz) && !any_big;
+  }
+  if (bad || tiny) fx_float_redo(a, t, tab, scale, chunk, false, reinterpret_cast<float*>(smem_raw));
+  int32_t* dst = part + (chunk * a.D + d) * static_cast<uint64_t>(a.jt);
+  for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) dst[b] = sk[b];
+  if (threadIdx.x == 0) flags[chunk * a.D + d] = (bad || tiny) ? 1 : 0;
 }
 
 // out[d][b] (+)= 2^-S * (exact 128-bit sum of the fixed-point partials) + the
@@ -1078,7 +1192,7 @@ int fx_group_cache(FxGroupEntry** out) {
   return ST_OK;
 }
 
-enum class Path { Global, Smem, Fx, Fx64 };
+enum class Path { Global, Smem, Fx, Fx32S, Fx64 };
 
 struct Plan {
   Path path = Path::Global;
@@ -1138,16 +1252,34 @@ int fx64_nv(uint32_t i0) {
   while (32u * nv < i0) nv <<= 1;
   return nv;
 }
-using Fx64Kernel = void (*)(DenseArgs, const double*, const uint32_t*, const FxStats*, uint32_t*,
-                            int*);
-Fx64Kernel fx64_kernel(int nv, bool full) {
+using Fx32sKernel = void (*)(DenseArgs, const float*, const uint32_t*, const FxStats*, int32_t*,
+                             int*);
+// fx32s variant: NV = the smallest power of two with 32 NV >= I_0 (I_0 <= 1024).
+Fx32sKernel fx32s_kernel(int nv, bool full) {
   switch (nv) {
-    case 1: return full ? fcs_dense_fx64_kernel<1, true> : fcs_dense_fx64_kernel<1, false>;
-    case 2: return full ? fcs_dense_fx64_kernel<2, true> : fcs_dense_fx64_kernel<2, false>;
-    case 4: return full ? fcs_dense_fx64_kernel<4, true> : fcs_dense_fx64_kernel<4, false>;
-    case 8: return full ? fcs_dense_fx64_kernel<8, true> : fcs_dense_fx64_kernel<8, false>;
-    case 16: return full ? fcs_dense_fx64_kernel<16, true> : fcs_dense_fx64_kernel<16, false>;
-    default: return full ? fcs_dense_fx64_kernel<32, true> : fcs_dense_fx64_kernel<32, false>;
+    case 1: return full ? fcs_dense_fx32s_kernel<1, true> : fcs_dense_fx32s_kernel<1, false>;
+    case 2: return full ? fcs_dense_fx32s_kernel<2, true> : fcs_dense_fx32s_kernel<2, false>;
+    case 4: return full ? fcs_dense_fx32s_kernel<4, true> : fcs_dense_fx32s_kernel<4, false>;
+    case 8: return full ? fcs_dense_fx32s_kernel<8, true> : fcs_dense_fx32s_kernel<8, false>;
+    case 16: return full ? fcs_dense_fx32s_kernel<16, true> : fcs_dense_fx32s_kernel<16, false>;
+    default: return full ? fcs_dense_fx32s_kernel<32, true> : fcs_dense_fx32s_kernel<32, false>;
+  }
+}
+
+template <typename Tin>
+using Fx64Kernel = void (*)(DenseArgs, const Tin*, const uint32_t*, const FxStats*, uint32_t*,
+                            int*);
+template <typename Tin>
+Fx64Kernel<Tin> fx64_kernel(int nv, bool full) {
+  switch (nv) {
+    case 1: return full ? fcs_dense_fx64_kernel<Tin, 1, true> : fcs_dense_fx64_kernel<Tin, 1, false>;
+    case 2: return full ? fcs_dense_fx64_kernel<Tin, 2, true> : fcs_dense_fx64_kernel<Tin, 2, false>;
+    case 4: return full ? fcs_dense_fx64_kernel<Tin, 4, true> : fcs_dense_fx64_kernel<Tin, 4, false>;
+    case 8: return full ? fcs_dense_fx64_kernel<Tin, 8, true> : fcs_dense_fx64_kernel<Tin, 8, false>;
+    case 16:
+      return full ? fcs_dense_fx64_kernel<Tin, 16, true> : fcs_dense_fx64_kernel<Tin, 16, false>;
+    default:
+      return full ? fcs_dense_fx64_kernel<Tin, 32, true> : fcs_dense_fx64_kernel<Tin, 32, false>;
   }
 }
 
@@ -1227,13 +1359,26 @@ int make_plan_uncached(const DenseArgs& a, Plan* p) {
   // 33.8 us; c5 operands: 37 vs 42 us); above it the fixed point wins (c3
   // build 200^3 D=10: 200 vs 292 us; 1024^3 J=8192 D=1: 1.44 vs 3.43 ms).
   const bool fx64_pays = static_cast<double>(a.fibers) * a.dims[0] * a.D >= 8.0e6;
-  if (sizeof(Tin) == 8 && a.order >= 2 && a.dims[0] <= 1024 && !no_fx64 && fx64_pays &&
-      fits(fx64_kernel(fx64_nv(a.dims[0]), false))) {
+  // fp32 shapes the float4 kernel does not take (I_0 % 4 != 0), I_0 <= 1024:
+  // the same int32 fixed point with scalar loads
+  const bool fx32s_ok = sizeof(Tin) == 4 && a.order >= 2 && a.dims[0] <= 1024 &&
+                        fits(fx32s_kernel(fx64_nv(a.dims[0]), false));
+  if (sizeof(Tin) == 4 && !p->nv && fx32s_ok && fx64_pays) {
+    p->path = Path::Fx32S;
+    p->nv = fx64_nv(a.dims[0]);
+    p->threads = 512;
+    auto k = fx32s_kernel(p->nv, a.dims[0] == 32u * p->nv);
+    FCS_CUDA_TRY(set_max_dynamic_smem(k, di));
+    FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
+                                                               p->smem_bytes));
+  } else if (sizeof(Tin) == 8 && a.order >= 2 && a.dims[0] <= 1024 && !no_fx64 && fx64_pays &&
+             fits(fx64_kernel<Tin>(fx64_nv(a.dims[0]), false))) {
+    // fp64: 64-bit fixed point, 8 bytes per bucket
     p->path = Path::Fx64;
     p->nv = fx64_nv(a.dims[0]);
     p->threads = 512;
     const bool full = a.dims[0] == 32u * p->nv;
-    auto k = fx64_kernel(p->nv, full);
+    auto k = fx64_kernel<Tin>(p->nv, full);
     FCS_CUDA_TRY(set_max_dynamic_smem(k, di));
     FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
                                                                p->smem_bytes));
@@ -1250,6 +1395,9 @@ int make_plan_uncached(const DenseArgs& a, Plan* p) {
     auto k = fx_kernel(p->nv, p->group);
     FCS_CUDA_TRY(set_max_dynamic_smem(k, di));
     FCS_CUDA_TRY(set_max_dynamic_smem(fx_kernel(p->nv, p->group, true), di));
+    if (fx32s_ok)  // an unaligned tensor on this plan takes the scalar-load kernel
+      FCS_CUDA_TRY(set_max_dynamic_smem(
+          fx32s_kernel(fx64_nv(a.dims[0]), a.dims[0] == 32u * fx64_nv(a.dims[0])), di));
     FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
                                                                p->smem_bytes));
   } else {
@@ -1266,7 +1414,7 @@ int make_plan_uncached(const DenseArgs& a, Plan* p) {
   // fixed point: at least ~4 fibers per warp of a 512-thread CTA (per-CTA
   // fixed costs — zeroing, writing the partial — dominate smaller shares);
   // the atomic kernel keeps 16 fibers per chunk (c1: 333 chunks, 22 us)
-  const bool fixed = p->path == Path::Fx || p->path == Path::Fx64;
+  const bool fixed = p->path == Path::Fx || p->path == Path::Fx32S || p->path == Path::Fx64;
   nchunk = std::min<uint64_t>(nchunk, std::max<uint64_t>(1, a.fibers / (fixed ? 64 : 16)));
   // Small tensors: each chunk writes (and the reduction re-reads) a D x J~
   // partial, so keep the partials to at most the tensor's bytes (config 1:
@@ -1275,7 +1423,8 @@ int make_plan_uncached(const DenseArgs& a, Plan* p) {
   const uint64_t part_per_chunk = static_cast<uint64_t>(a.D) * a.jt * sizeof(Tacc);
   nchunk = std::min<uint64_t>(nchunk, std::max<uint64_t>(1, elems * sizeof(Tin) / part_per_chunk));
   p->nchunk = nchunk;
-  p->part_bytes = nchunk * a.D * static_cast<size_t>(a.jt) * sizeof(Tacc);
+  p->part_bytes = nchunk * a.D * static_cast<size_t>(a.jt) *
+                  (p->path == Path::Fx64 ? 8 : sizeof(Tacc));  // Fx32S: int32 like Fx
   p->ws = align_up(p->part_bytes) + align_up(nchunk * a.D * sizeof(int)) +
           align_up(sizeof(FxStats)) + align_up(static_cast<size_t>(a.D) * 32) +
           align_up(kFxMaxSample * sizeof(FxPart)) +
@@ -1350,6 +1499,40 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
   a.fibers_per_chunk = (a.fibers + p.nchunk - 1) / p.nchunk;
   const uint64_t nchunk = (a.fibers + a.fibers_per_chunk - 1) / a.fibers_per_chunk;
   const bool aligned = (reinterpret_cast<uintptr_t>(t) & 15u) == 0;
+  if (p.path == Path::Fx32S || (p.path == Path::Fx && !aligned && a.order >= 2 &&
+                                 a.dims[0] <= 1024)) {
+    char* base = static_cast<char*>(ws);
+    auto* part = reinterpret_cast<int32_t*>(base);
+    auto* flags = reinterpret_cast<int*>(base + align_up(p.part_bytes));
+    auto* stats = reinterpret_cast<FxStats*>(base + align_up(p.part_bytes) +
+                                             align_up(p.nchunk * a.D * sizeof(int)));
+    auto* parts = reinterpret_cast<FxPart*>(base + align_up(p.part_bytes) +
+                                            align_up(p.nchunk * a.D * sizeof(int)) +
+                                            align_up(sizeof(FxStats)) +
+                                            align_up(static_cast<size_t>(a.D) * 32));
+    auto* divert = reinterpret_cast<double*>(
+        base + align_up(p.part_bytes) + align_up(p.nchunk * a.D * sizeof(int)) +
+        align_up(sizeof(FxStats)) + align_up(static_cast<size_t>(a.D) * 32) +
+        align_up(kFxMaxSample * sizeof(FxPart)));
+    const uint64_t nsample = fx_nsample(a.fibers);
+    const double per_cta = static_cast<double>(a.fibers_per_chunk) * a.dims[0];
+    const FxScaleArgs sc{parts, static_cast<int>(nsample), 3.0 * per_cta / a.jt + 16.0, stats};
+    const float* tf = reinterpret_cast<const float*>(t);
+    fx_sample_warps_kernel<float><<<ceil_div(nsample, 8), 256, 0, st>>>(a, tf, nsample, parts);
+    FCS_CUDA_TRY(cudaGetLastError());
+    fx_scale_kernel<<<1, 512, 0, st>>>(sc, kFx32);
+    FCS_CUDA_TRY(cudaGetLastError());
+    FCS_CUDA_TRY(cudaMemsetAsync(divert, 0, out_elems * sizeof(double), st));
+    const int nv = fx64_nv(a.dims[0]);
+    fx32s_kernel(nv, a.dims[0] == 32u * nv)<<<static_cast<unsigned>(nchunk * a.D), 512,
+                                              p.smem_bytes, st>>>(a, tf, packed, stats, part,
+                                                                  flags);
+    FCS_CUDA_TRY(cudaGetLastError());
+    reduce_fx_kernel<<<ceil_div(out_elems, 256), 256, 0, st>>>(part, flags, nchunk, a.D, a.jt,
+                                                               stats, divert, out, accumulate);
+    FCS_CUDA_TRY(cudaGetLastError());
+    return ST_OK;
+  }
   if (p.path == Path::Fx && aligned) {
     char* base = static_cast<char*>(ws);
     auto* part = reinterpret_cast<int32_t*>(base);
@@ -1417,13 +1600,12 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
     const double per_cta = static_cast<double>(a.fibers_per_chunk) * a.dims[0];
     const FxScaleArgs sc{parts, nparts, 3.0 * per_cta / a.jt + 16.0, stats};
     const bool full = a.dims[0] == 32u * p.nv;
-    fx_sample_warps_kernel<double><<<ceil_div(nsample, 8), 256, 0, st>>>(
-        a, reinterpret_cast<const double*>(t), nsample, parts);
+    fx_sample_warps_kernel<Tin><<<ceil_div(nsample, 8), 256, 0, st>>>(a, t, nsample, parts);
     FCS_CUDA_TRY(cudaGetLastError());
     fx_scale_kernel<<<1, 512, 0, st>>>(sc, kFx64);
     FCS_CUDA_TRY(cudaGetLastError());
-    fx64_kernel(p.nv, full)<<<static_cast<unsigned>(nchunk * a.D), p.threads, p.smem_bytes, st>>>(
-        a, reinterpret_cast<const double*>(t), packed, stats, part, flags);
+    fx64_kernel<Tin>(p.nv, full)<<<static_cast<unsigned>(nchunk * a.D), p.threads, p.smem_bytes,
+                                   st>>>(a, t, packed, stats, part, flags);
     FCS_CUDA_TRY(cudaGetLastError());
     reduce_fx64_kernel<<<ceil_div(out_elems, 32), dim3(32, 32), 0, st>>>(part, flags, nchunk, a.D,
                                                                         a.jt, stats, out,
@@ -1464,7 +1646,8 @@ int dense_fx_report(int dtype, size_t order, const size_t* dims, size_t last_cou
   Plan p;
   if (int rc = dtype == ST_F32 ? make_plan<float, float>(a, &p) : make_plan<double, double>(a, &p))
     return rc;
-  if ((p.path != Path::Fx && p.path != Path::Fx64) || a.fibers == 0) return ST_OK;
+  if ((p.path != Path::Fx && p.path != Path::Fx32S && p.path != Path::Fx64) || a.fibers == 0)
+    return ST_OK;
   FCS_CHECK_ARG(ws != nullptr && ws_bytes >= p.ws, "st_fcs_dense_report: workspace too small");
   a.fibers_per_chunk = (a.fibers + p.nchunk - 1) / p.nchunk;
   const uint64_t nchunk = (a.fibers + a.fibers_per_chunk - 1) / a.fibers_per_chunk;

@@ -938,3 +938,22 @@ def test_sparse_coo_c4_geometry(cuda):
     dense[torch.from_numpy(flat).cuda()] = torch.from_numpy(vals).cuda()
     want = st.fcs_dense_batched(st.DenseTensor(list(shape), dense), fams)
     rel_close(got, want.cpu().numpy(), RTOL64)
+
+
+@pytest.mark.parametrize("shape,J,D", [((1022, 96, 90), 2000, 1), ((333, 200, 130), 1500, 1)])
+def test_dense_f32_odd_fiber_fixed_point(cuda, shape, J, D):
+    """fp32 tensors whose fibers the float4 kernel cannot take (I_0 % 4 != 0)
+    go through the same int32 fixed point with scalar loads: integer data
+    bit-exact, Gaussian data at the fp32 rule."""
+    rng = np.random.default_rng(sum(shape))
+    xi = rng.integers(-50, 51, size=shape).astype(np.float32)
+    fams = st.families_for(list(shape), st.EstimatorConfig(J, D, 6))
+    got = st.fcs_dense_batched(st.DenseTensor.from_array(xi), fams).cpu().numpy()
+    for d, f in enumerate(fams):
+        b, s_, j = oracle_family(f)
+        assert np.array_equal(got[d], O.fcs_dense(xi.astype(np.float64), b, s_, j))
+    xg = rng.standard_normal(shape).astype(np.float32)
+    got = st.fcs_dense_batched(st.DenseTensor.from_array(xg), fams).cpu().numpy()
+    for d, f in enumerate(fams):
+        b, s_, j = oracle_family(f)
+        rel_close(got[d], O.fcs_dense(xg.astype(np.float64), b, s_, j), RTOL32)
