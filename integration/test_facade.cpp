@@ -14,6 +14,7 @@
 //   test_facade fft <x.bin> <len> <n> <out.bin>
 //   test_facade z <t.bin> <I> <J> <seed> <a.bin> <b.bin> <free> <out.bin>
 //   test_facade sketches <t.bin> <I0> <I1> <I2> <J> <seed> <out.bin>   (cs/ts/hcs, TS/HCS CP)
+//   test_facade mixed <t.bin> <I0> <I1> <I2> <J0> <J1> <J2> <D> <seed> <v.bin> <free> <out.bin>
 //   test_facade errors
 #include <sketchtensor/cpd.hpp>
 #include <sketchtensor/estimators.hpp>
@@ -234,6 +235,29 @@ int run(int argc, char** argv) {
     const Eigen::MatrixXd cols = cs_sketch_columns(fs[0], fam.pair(0));
     o.add(cols.data(), static_cast<size_t>(cols.size()));
     o.write(S(8));
+  } else if (cmd == "mixed") {
+    // estimators over PrecomputedFcs of families with unequal hash lengths
+    // (the facade's per-family exact path)
+    const std::vector<size_t> dims = {U(3), U(4), U(5)}, lens = {U(6), U(7), U(8)};
+    DenseTensor t(dims, read_bin(S(2), prod(dims)));
+    const size_t D = U(9), free_mode = U(12);
+    std::vector<PrecomputedFcs> pres;
+    for (size_t d = 0; d < D; ++d)
+      pres.push_back(precompute_fcs(t, HashFamily(dims, lens, family_seed(U(10), d))));
+    const size_t per = dims[0] + dims[1] + dims[2];
+    std::vector<double> all = read_bin(S(11), per);
+    Eigen::VectorXd v[3];
+    size_t off = 0;
+    for (int n = 0; n < 3; ++n) {
+      v[n] = Eigen::VectorXd(static_cast<Eigen::Index>(dims[n]));
+      for (size_t i = 0; i < dims[n]; ++i) v[n][static_cast<Eigen::Index>(i)] = all[off + i];
+      off += dims[n];
+    }
+    Out o;
+    o.add(estimate_uvw(std::span<const PrecomputedFcs>(pres), v[0], v[1], v[2]));
+    const size_t c1 = free_mode == 0 ? 1 : 0, c2 = free_mode == 2 ? 1 : 2;
+    o.add(estimate_iuv(std::span<const PrecomputedFcs>(pres), v[c1], v[c2], free_mode));
+    o.write(S(13));
   } else if (cmd == "errors") {
     auto expect = [](const char* what, const std::function<void()>& fn, bool runtime) {
       try {

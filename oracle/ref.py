@@ -596,3 +596,20 @@ def precompute_z(t: np.ndarray, hash_len: int, master: int, a, b, free_mode: int
     _check(L.ref_precompute_z(_ptr(data), _sz(dim), _sz(hash_len), _u64(master), _ptr(av),
                               _ptr(bv), _sz(free_mode), _ptr(spec), _ptr(z)))
     return spec[0::2] + 1j * spec[1::2], z
+
+
+def estimate_mixed(t: np.ndarray, lens, count: int, seed: int, u, v, w, free_mode: int):
+    """estimate_uvw / estimate_iuv over precompute_fcs of families with
+    unequal hash lengths (estimators.cpp:169-186): (uvw, iuv)."""
+    dims = _dims(t.shape)
+    data = np.ascontiguousarray(np.asarray(t, np.float64).ravel(order="F"))
+    ln = _dims(lens)
+    u, v, w = (np.ascontiguousarray(np.asarray(x, np.float64)) for x in (u, v, w))
+    out = np.empty(int(dims[free_mode]), np.float64)
+    uvw = _d(0)
+    L = lib()
+    L.ref_estimate_mixed.argtypes = [_p, _p, _p, _sz, _u64, _p, _p, _p, _sz, _p, _p]
+    _check(L.ref_estimate_mixed(_ptr(data), _ptr(dims), _ptr(ln), _sz(count), _u64(seed),
+                                _ptr(u), _ptr(v), _ptr(w), _sz(free_mode), C.byref(uvw),
+                                _ptr(out)))
+    return uvw.value, out

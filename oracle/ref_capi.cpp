@@ -611,3 +611,26 @@ int ref_precompute_z(const double* data, std::size_t dim, std::size_t hash_len,
   });
 }
 }  // extern "C"
+
+extern "C" {
+// estimate_uvw / estimate_iuv over PrecomputedFcs built with families of
+// UNEQUAL hash lengths (HashFamily(dims, lens, family_seed(seed, d))): the
+// span estimators of estimators.cpp:169-186 outside families_for.
+int ref_estimate_mixed(const double* data, const std::size_t* dims, const std::size_t* lens,
+                       std::size_t count, std::uint64_t seed, const double* u, const double* v,
+                       const double* w, std::size_t free_mode, double* uvw_out, double* iuv_out) {
+  return guarded([&] {
+    DenseTensor t = make_tensor(data, 3, dims);
+    std::vector<PrecomputedFcs> pres;
+    for (std::size_t d = 0; d < count; ++d)
+      pres.push_back(precompute_fcs(t, HashFamily(to_dims(3, dims), to_dims(3, lens),
+                                                  family_seed(seed, d))));
+    const Eigen::VectorXd vu = vec_in(u, dims[0]), vv = vec_in(v, dims[1]), vw = vec_in(w, dims[2]);
+    *uvw_out = estimate_uvw(std::span<const PrecomputedFcs>(pres), vu, vv, vw);
+    const Eigen::VectorXd* in[3] = {&vu, &vv, &vw};
+    const std::size_t c1 = free_mode == 0 ? 1 : 0, c2 = free_mode == 2 ? 1 : 2;
+    copy_out(estimate_iuv(std::span<const PrecomputedFcs>(pres), *in[c1], *in[c2], free_mode),
+             iuv_out);
+  });
+}
+}  // extern "C"

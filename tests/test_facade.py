@@ -230,3 +230,22 @@ def test_facade_errors(cuda, tmp_path):
                 "median_reduce: empty input", "PrecomputedFcs: FCS sketch required",
                 "estimator: no sketches"):
         assert msg in out, msg
+
+
+@pytest.mark.parametrize("free_mode", [0, 2])
+def test_facade_estimators_unequal_hash_lengths(cuda, tmp_path, free_mode):
+    """estimate_uvw / estimate_iuv over PrecomputedFcs whose families have
+    unequal hash lengths per mode (outside families_for): the facade's
+    per-family exact path (st_fft_convolve / st_precompute_z + read-out)
+    against the reference."""
+    rng = np.random.default_rng(60 + free_mode)
+    dims, lens = (18, 14, 11), (37, 29, 23)
+    t = rng.standard_normal(dims)
+    v = rng.standard_normal(sum(dims))
+    run(tmp_path, "mixed", put(tmp_path, "t.bin", t.ravel(order="F")), *dims, *lens, 3, 9,
+        put(tmp_path, "v.bin", v), free_mode, os.path.join(tmp_path, "o.bin"))
+    got = get(tmp_path, "o.bin")
+    u0, u1, u2 = v[:dims[0]], v[dims[0]:dims[0] + dims[1]], v[dims[0] + dims[1]:]
+    uvw, iuv = ref.estimate_mixed(t, lens, 3, 9, u0, u1, u2, free_mode)
+    rel_close(got[:1], [uvw], 1e-10)
+    rel_close(got[1:], iuv, 1e-10)
