@@ -321,8 +321,16 @@ int rtpm_on(st_engine* e, size_t dim, size_t rank, size_t L, size_t num_iters, u
     // L restarts advance in lockstep; a row whose norm underflows stays zero,
     // exactly like the reference's early break (iuu(0) = 0).
     for (size_t it = 0; it < num_iters; ++it) {
-      if (int rc = st_engine_iuv(e, L, U, U, 0, Y, 1, st)) return rc;
-      if (int rc = launch_normalize_rows(Y, static_cast<int>(L), static_cast<int>(dim), st)) return rc;
+      // small batches: one cluster kernel with the median and the row
+      // normalisation fused in; else estimator, median and normalisation kernels
+      const int rc = engine_iuv_fused(e, L, U, 0, 2, Y, nullptr, nullptr, st);
+      if (rc == 1) {
+        if (int rc2 = st_engine_iuv(e, L, U, U, 0, Y, 1, st)) return rc2;
+        if (int rc2 = launch_normalize_rows(Y, static_cast<int>(L), static_cast<int>(dim), st))
+          return rc2;
+      } else if (rc) {
+        return rc;
+      }
       std::swap(U, Y);
     }
     if (int rc = st_engine_uvw(e, L, U, U, U, vals, 1, st)) return rc;
@@ -340,8 +348,14 @@ int rtpm_on(st_engine* e, size_t dim, size_t rank, size_t L, size_t num_iters, u
     FCS_CUDA_TRY(cudaMemcpyAsync(best, U + arg * dim, dim * sizeof(double), cudaMemcpyDeviceToDevice, st));
     FCS_CUDA_TRY(cudaMemsetAsync(stopped, 0, sizeof(int), st));
     for (size_t it = 0; it < num_iters; ++it) {  // refinement (cpd.cpp:266-270)
-      if (int rc = st_engine_iuv(e, 1, best, best, 0, next, 1, st)) return rc;
-      if (int rc = launch_refine_update(best, next, static_cast<int>(dim), stopped, st)) return rc;
+      const int rc = engine_iuv_fused(e, 1, best, 0, 3, next, best, stopped, st);
+      if (rc == 1) {
+        if (int rc2 = st_engine_iuv(e, 1, best, best, 0, next, 1, st)) return rc2;
+        if (int rc2 = launch_refine_update(best, next, static_cast<int>(dim), stopped, st))
+          return rc2;
+      } else if (rc) {
+        return rc;
+      }
     }
     if (int rc = st_engine_uvw(e, 1, best, best, best, vals, 1, st)) return rc;
     double weight = 0.0;

@@ -38,6 +38,33 @@ int launch_ts_extend(const double* in, int D, int jt, int J, double* ext, double
 
 using namespace fcs;
 
+namespace fcs {
+static int iuv_fused_ab(st_engine* e, size_t batch, const double* a, const double* b, size_t free_mode,
+                 int mode, double* out, double* best, int* stopped, cudaStream_t st) {
+  if (is_exact(e) || e->plan.large_p1 || batch == 0) return 1;
+  int c1, c2;
+  contracted(free_mode, &c1, &c2);
+  const size_t nf = e->dims[free_mode];
+  const size_t had = e->cnt.bytes;
+  if (int rc = e->cnt.ensure(std::max<size_t>(batch, 64) * sizeof(int), st)) return rc;
+  if (e->cnt.bytes != had) FCS_CUDA_TRY(cudaMemsetAsync(e->cnt.p, 0, e->cnt.bytes, st));
+  if (int rc = e->est.ensure(batch * e->D * nf * sizeof(double), st)) return rc;
+  IuvTail t;
+  t.mode = mode;
+  t.cnt = static_cast<int*>(e->cnt.p);
+  t.out = out;
+  t.best = best;
+  t.stopped = stopped;
+  return launch_iuv_cluster(e->plan, e->args(), static_cast<int>(batch), a, b, c1, c2,
+                            static_cast<int>(free_mode), static_cast<double*>(e->est.p), t, st);
+}
+
+int engine_iuv_fused(st_engine* e, size_t batch, const double* a, size_t free_mode, int mode,
+                     double* out, double* best, int* stopped, cudaStream_t st) {
+  return iuv_fused_ab(e, batch, a, a, free_mode, mode, out, best, stopped, st);
+}
+}  // namespace fcs
+
 extern "C" {
 
 int st_cs_columns(const double* u, size_t input_dim, size_t cols, const uint32_t* packed_pair,
@@ -396,6 +423,7 @@ int st_engine_destroy(st_engine* e) {
   e->est.release(nullptr);
   e->vec.release(nullptr);
   e->vec2.release(nullptr);
+  e->cnt.release(nullptr);
   cudaDeviceSynchronize();
   delete e;
   return ST_OK;
@@ -423,6 +451,7 @@ int st_engine_sketches(st_engine* e, double* out, void* stream) {
                                static_cast<int>(e->jt), 0, as_stream(stream));
 }
 
+
 int st_engine_iuv(st_engine* e, size_t batch, const double* a, const double* b, size_t free_mode,
                   double* out, int median, void* stream) {
   FCS_CHECK_ARG(e != nullptr, "st_engine_iuv: null engine");
@@ -443,6 +472,10 @@ int st_engine_iuv(st_engine* e, size_t batch, const double* a, const double* b, 
     return med ? launch_median(est, static_cast<int>(batch), static_cast<int>(e->D),
                                static_cast<int>(nf), out, st)
                : ST_OK;
+  }
+  if (median) {  // small batches: cluster estimator with the median fused in
+    const int rc = iuv_fused_ab(e, batch, a, b, free_mode, 1, out, nullptr, nullptr, st);
+    if (rc != 1) return rc;
   }
   if (int rc = e->scratch.ensure(batch * e->D * e->plan.P * sizeof(double2), st)) return rc;
   double* est = out;

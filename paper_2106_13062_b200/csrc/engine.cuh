@@ -155,6 +155,7 @@ struct st_engine {
   double* dense = nullptr;     // Plain: the tensor; HCS: D x J^3 sketches; CS: D x J sketches
   uint64_t* seeds = nullptr;   // CS: the D long pairs' seeds
   fcs::Scratch scratch, est, vec, vec2;
+  fcs::Scratch cnt;  // per-vector arrival counters of the fused cluster tail (kept zero)
   fcs::EngArgs args() const {
     fcs::EngArgs e{};
     size_t off = 0;
@@ -173,6 +174,11 @@ struct st_engine {
 };
 
 namespace fcs {
+// The cluster estimator with its fused tail (IuvTail modes 1-3) over `batch`
+// vectors a (= b) with free mode 0; returns 1 when the cluster path does not
+// apply (the caller runs the separate kernels).
+int engine_iuv_fused(st_engine* e, size_t batch, const double* a, size_t free_mode, int mode,
+                     double* out, double* best, int* stopped, cudaStream_t st);
 inline bool is_exact(const st_engine* e) {
   return e->backend == ST_BACKEND_PLAIN || e->backend == ST_BACKEND_HCS ||
          e->backend == ST_BACKEND_CS;

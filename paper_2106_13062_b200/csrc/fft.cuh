@@ -627,6 +627,25 @@ struct EngArgs {
   const double2* spec;     // D x P cached spectra S_d (slot order)
 };
 
+// Fused epilogue of the cluster estimator: the last cluster of vector b to
+// finish (per-vector arrival counter) takes the median over the D families
+// and, by mode, normalises the row (the rtpm restart step) or applies the
+// refinement update (cpd.cpp:266-270).
+struct IuvTail {
+  int mode = 0;             // 0: estimates only; 1: median -> out; 2: median, row / ||row|| -> out;
+                            // 3: median -> out (scratch), best = out / ||out|| unless stopped
+  int* cnt = nullptr;       // batch arrival counters, zero between launches
+  double* out = nullptr;    // batch x nf
+  double* best = nullptr;   // mode 3
+  int* stopped = nullptr;   // mode 3: sticky underflow flag
+};
+// Cluster (8-CTA, DSMEM) form of the iuv estimator for M in {8192, 9216} and
+// batches that fit one wave of clusters (spectral_cluster.cu); returns 1
+// without launching otherwise.
+int launch_iuv_cluster(const FftPlan& pl, const EngArgs& e, int batch, const double* A,
+                       const double* B, int c1, int c2, int f, double* est, const IuvTail& tail,
+                       cudaStream_t st);
+
 // Two-level counterparts of the spectral launchers (spectral_large.cu).
 // Exact n-point transforms (Bluestein over the library FFTs, spectral_large.cu).
 int exact_dft(const double* xr, const double2* xc, size_t ldx, size_t len, size_t n, int items,

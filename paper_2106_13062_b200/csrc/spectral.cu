@@ -12,6 +12,7 @@
 #include <math_constants.h>
 
 #include "fft.cuh"
+#include "median.cuh"
 
 namespace fcs {
 
@@ -438,81 +439,15 @@ __global__ void __launch_bounds__(kFftThreads) deflate_kernel(FftPlan pl, EngArg
 }
 
 // K8: elementwise median over D (median_reduce, estimators.cpp:117-138):
-// est[b][d][i] -> out[b][i]; even D averages the two middle order statistics.
-// Finite values, D <= N: all D values in registers (fully unrolled, padded
-// with +inf) and the order statistics by rank counting — the same value a
-// sort yields. Returns false (caller falls back) on a non-finite input.
-template <int N>
-__device__ __forceinline__ bool median_regs(const double* col, int D, int len, double* res) {
-  double v[N];
-  bool finite = true;
-#pragma unroll
-  for (int k = 0; k < N; ++k) {
-    v[k] = k < D ? col[static_cast<size_t>(k) * len] : CUDART_INF;
-    if (k < D) finite &= isfinite(v[k]);
-  }
-  if (!finite) return false;
-  const int m1 = (D - 1) / 2, m2 = D / 2;  // equal for odd D
-  double lo = 0.0, hi = 0.0;
-#pragma unroll
-  for (int k = 0; k < N; ++k) {
-    int less = 0, eq = 0;
-#pragma unroll
-    for (int j = 0; j < N; ++j) {
-      less += v[j] < v[k];
-      eq += v[j] == v[k];
-    }
-    if (k < D) {
-      if (less <= m1 && m1 < less + eq) lo = v[k];
-      if (less <= m2 && m2 < less + eq) hi = v[k];
-    }
-  }
-  *res = (D & 1) ? hi : 0.5 * (lo + hi);
-  return true;
-}
-
+// est[b][d][i] -> out[b][i]; median_col (median.cuh) is shared with the fused
+// tail of the cluster estimator.
 __global__ void median_kernel(const double* __restrict__ est, int batch, int D, int len,
                               double* __restrict__ out) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= batch * len) return;
   const int b = idx / len, i = idx - b * len;
   const double* col = est + static_cast<size_t>(b) * D * len + i;  // stride len
-  double r;
-  if ((D <= 8 && median_regs<8>(col, D, len, &r)) ||
-      (D > 8 && D <= 16 && median_regs<16>(col, D, len, &r))) {
-    out[idx] = r;
-    return;
-  }
-  if (D > 64) {
-    // rank selection without storage (O(D^2)): x_k is the m-th order
-    // statistic iff #less <= m < #less + #equal (std::sort order for finite values)
-    auto order_stat = [&](int m) {
-      for (int k = 0; k < D; ++k) {
-        const double x = col[static_cast<size_t>(k) * len];
-        int less = 0, eq = 0;
-        for (int j = 0; j < D; ++j) {
-          const double y = col[static_cast<size_t>(j) * len];
-          less += y < x;
-          eq += y == x;
-        }
-        if (less <= m && m < less + eq) return x;
-      }
-      return col[0];  // non-finite input: no consistent order
-    };
-    out[idx] = (D & 1) ? order_stat(D / 2) : 0.5 * (order_stat(D / 2 - 1) + order_stat(D / 2));
-    return;
-  }
-  double v[64];
-  for (int d = 0; d < D; ++d) {
-    const double x = est[(static_cast<size_t>(b) * D + d) * len + i];
-    int k = d;
-    while (k > 0 && v[k - 1] > x) {
-      v[k] = v[k - 1];
-      --k;
-    }
-    v[k] = x;
-  }
-  out[idx] = (D & 1) ? v[D / 2] : 0.5 * (v[D / 2 - 1] + v[D / 2]);
+  out[idx] = median_col(col, D, len, [](const double* p) { return *p; });
 }
 
 // Per-column count sketch into global memory (cs_sketch_columns, sketch.cpp:118-133).
@@ -648,6 +583,10 @@ int launch_conv(const FftPlan& pl, const double* a, int la, size_t lda, const do
 int launch_iuv(const FftPlan& pl, const EngArgs& e, int batch, const double* A, const double* B,
                int c1, int c2, int f, double2* scratch, double* est, cudaStream_t st) {
   if (pl.large_p1) return large_iuv(pl, e, batch, A, B, c1, c2, f, e.hash_len, est, st);
+  {  // small batches: one 8-CTA cluster per item (spectral_cluster.cu)
+    const int rc = launch_iuv_cluster(pl, e, batch, A, B, c1, c2, f, est, IuvTail{}, st);
+    if (rc != 1) return rc;
+  }
   size_t sm2, sm1;
   if (int rc = prep(iuv_kernel, pl, &sm2, 2)) return rc;
   if (int rc = prep(iuv1_kernel, pl, &sm1, 1)) return rc;

@@ -1,0 +1,490 @@
+// K6 over a thread-block cluster: the sketched contraction T(I, a, b) of one
+// (vector, family) item spread over 8 CTAs that exchange their transposes
+// through distributed shared memory (iuv_spectral, estimators.cpp:66-90).
+//
+// The one-CTA kernel (spectral.cu, iuv1_kernel) runs one item per CTA at 8
+// warps: each P = 4608-point pass is fp64-issue and latency bound, and a
+// batch of 10-150 items leaves most SMs idle (config 3: 12.6 % warps active,
+// the batch-1 refinement step on 10 SMs). Here an item is a cluster of 8 CTAs
+// and the length-M transforms are four-step transforms whose transposes go
+// over DSMEM:
+//
+//   forward, complex M = 64 * N2 points of w = cs_a + i cs_b (n = n1 + 64 n2):
+//     F1  CTA r: columns n1 in [8r, 8r+8): N2-point DFTs over n2 (two radix
+//         passes), twiddle w_M^{n1 k2}, store to the owner of k2 (remote);
+//     F3  CTA r: its k2 rows (mirror-closed: k2 and N2 - k2 together):
+//         64-point DFTs over n1 -> X[k2 + N2 k1];
+//   product: A = (X[k] + conj X[-k]) / 2, B = (X[k] - conj X[-k]) / 2i
+//         (both real sketches from one complex transform; -k stays in the
+//         CTA), G = S_d conj(A B), then the c2r pre map over (k, k + M/2)
+//         (same row) -> U[k], k < P = M/2;
+//   inverse, P = 32 * N2 points (k = k2 + N2 k1):
+//     I1  per k2 row: 32-point inverse DFT over k1, twiddle w_P^{-m1 k2},
+//         store to the owner of m1 (CTA r: m1 in [4r, 4r+4));
+//     I3  per m1: N2-point inverse DFT over k2 -> u[m1 + 32 m2] =
+//         P (z[2m] + i z[2m+1]);
+//   gather est[i] = s_f(i) z[h_f(i)] by the CTA that holds z[h_f(i)].
+//
+// The cached spectrum S_d is read in frequency order through the plan's
+// frequency -> slot table. Same arithmetic as the one-CTA path up to fp64
+// round-off (different factorisation of the same transform length).
+#include <cooperative_groups.h>
+#include <cstdlib>
+
+#include "fft.cuh"
+#include "median.cuh"
+
+namespace fcs {
+
+namespace cg = cooperative_groups;
+
+namespace {
+
+constexpr int kClC = 8;          // CTAs per item
+constexpr int kN1 = 64;          // forward: M = 64 N2
+
+template <int RA, int RB>
+struct ClGeom {
+  static constexpr int N2 = RA * RB;
+  static constexpr int M = kN1 * N2;
+  static constexpr int P = M / 2;
+  static constexpr int Q = N2 / (2 * kClC);  // mirror classes of k2 per CTA
+  static constexpr int ROWS = 2 * Q;         // k2 rows per CTA
+  static constexpr int COLS = kN1 / kClC;    // n1 columns per CTA
+  static constexpr int M1 = 32 / kClC;       // inverse m1 per CTA
+  static_assert(N2 % (2 * kClC) == 0, "N2 must be a multiple of 16");
+  static constexpr int kTw = (1 << kTwLoBits) + (M >> kTwLoBits);
+  static constexpr size_t smem_bytes() {
+    return static_cast<size_t>(kTw + COLS * N2 + ROWS * kN1 + M1 * N2) * sizeof(double2);
+  }
+};
+
+// Slot swizzle of the DSMEM-exchanged buffers: bits 0-2 (16-byte slot in a
+// 128-byte wavefront) XOR bits 3-5 and 4-6, so the stride-1, -4, -8 and -16
+// slot patterns of the passes fall on distinct bank groups.
+__device__ __forceinline__ int sw(int s) { return s ^ (((s >> 3) ^ (s >> 4)) & 7); }
+__device__ __forceinline__ int pick3(const int* v, int i) { return i == 0 ? v[0] : i == 1 ? v[1] : v[2]; }
+
+// k2 -> (owning CTA, local row); row -> k2. Class c = min(k2, N2 - k2) except
+// that k2 = N2/2 joins class 0 (with k2 = 0) as its second member.
+template <int N2, int Q>
+__device__ __forceinline__ void k2_owner(int k2, int& owner, int& row) {
+  const int h = N2 / 2;
+  const int cls = k2 == h ? 0 : min(k2, N2 - k2);
+  const int member = (k2 == 0 || k2 < h) ? 0 : 1;
+  owner = cls / Q;
+  row = 2 * (cls % Q) + member;
+}
+template <int N2, int Q>
+__device__ __forceinline__ int row_k2(int r, int row) {
+  const int cls = r * Q + (row >> 1);
+  if ((row & 1) == 0) return cls;
+  return cls == 0 ? N2 / 2 : N2 - cls;
+}
+
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int RA, int RB, int kClThreads>
+__global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads)
+    iuv_cluster_kernel(FftPlan pl, EngArgs e, const double* __restrict__ A,
+                       const double* __restrict__ B, int c1, int c2, int f,
+                       double* __restrict__ est, IuvTail tail) {
+  using Gm = ClGeom<RA, RB>;
+  constexpr int N2 = Gm::N2, M = Gm::M, P = Gm::P, Q = Gm::Q, ROWS = Gm::ROWS,
+                COLS = Gm::COLS, M1 = Gm::M1;
+  constexpr int hi = 1 << kTwLoBits;
+  constexpr int kGU = (ROWS * 32 + kClThreads - 1) / kClThreads;  // product units per thread
+  constexpr int kGather = 2;                                       // gather entries per thread
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* tw = reinterpret_cast<double2*>(smem_raw);
+  double2* colbuf = tw + Gm::kTw;          // F1 columns [COLS][N2]; later U rows [ROWS][32]
+  double2* rowbuf = colbuf + COLS * N2;    // F3 rows [ROWS][64] (written by every CTA)
+  double2* ibuf = rowbuf + ROWS * kN1;     // I3 rows [M1][N2] (written by every CTA)
+  cg::cluster_group cl = cg::this_cluster();
+  const int r = static_cast<int>(cl.block_rank());
+  const int item = blockIdx.x / kClC;
+  const int bvec = item / e.D, d = item % e.D;
+  const int t0 = threadIdx.x;
+  // every CTA of the cluster has started before anyone writes remote memory
+  cluster_arrive();
+  const uint32_t* tab = e.packed + static_cast<size_t>(d) * e.fam_stride;
+  const int na = pick3(e.dims, c1), nb = pick3(e.dims, c2), nf = pick3(e.dims, f);
+  const uint32_t* ta = tab + pick3(e.tab_off, c1);
+  const uint32_t* tb = tab + pick3(e.tab_off, c2);
+  const uint32_t* tf = tab + pick3(e.tab_off, f);
+  const double* av = A + static_cast<size_t>(bvec) * na;
+  const double* bv = B + static_cast<size_t>(bvec) * nb;
+  // Early loads, all in flight together: twiddles, the count-sketch inputs,
+  // the gather table entries and the slots of this thread's spectrum values.
+  constexpr int kTwPer = (Gm::kTw + kClThreads - 1) / kClThreads;
+  double2 twr[kTwPer];  // stored after the scatter, so both load streams overlap
+#pragma unroll
+  for (int q = 0; q < kTwPer; ++q) {
+    const int i = t0 + q * kClThreads;
+    if (i < Gm::kTw) twr[q] = __ldg(pl.tw + i);
+  }
+  constexpr int kSc = 4;  // scatter inputs per thread per round
+  for (int i = t0; i < COLS * N2; i += kClThreads) colbuf[i] = make_double2(0.0, 0.0);
+  uint32_t gt[kGather];
+#pragma unroll
+  for (int g = 0; g < kGather; ++g) {
+    const int i = t0 + g * kClThreads;
+    gt[g] = i < nf ? __ldg(tf + i) : 0u;
+  }
+  const double2* sp = e.spec + static_cast<size_t>(d) * P;
+  int sslot[kGU][2];
+#pragma unroll
+  for (int g = 0; g < kGU; ++g) {
+    const int u = t0 + g * kClThreads;
+    const int row = u >> 5, k1 = u & 31;
+    const int k2 = row_k2<N2, Q>(r, row < ROWS ? row : 0);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = k2 + N2 * (k1 + 32 * h);
+      // frequency of the half spectrum and whether it is conjugated / a real bin
+      const int kh = k <= P ? k : M - k;
+      sslot[g][h] = (u < ROWS * 32 && kh != 0 && kh != P) ? __ldg(pl.f2p + kh) : 0;
+    }
+  }
+  __syncthreads();
+  for (int i0 = t0; i0 < na + nb; i0 += kSc * kClThreads) {
+    double v[kSc];
+    uint32_t t[kSc];
+#pragma unroll
+    for (int q = 0; q < kSc; ++q) {
+      const int i = i0 + q * kClThreads;
+      v[q] = 0.0;
+      t[q] = 0u;
+      if (i < na) {
+        v[q] = av[i];
+        t[q] = __ldg(ta + i);
+      } else if (i < na + nb) {
+        v[q] = bv[i - na];
+        t[q] = __ldg(tb + i - na);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kSc; ++q) {
+      const int i = i0 + q * kClThreads;
+      const uint32_t h = t[q] & 0x7fffffffu;
+      const int n1 = static_cast<int>(h & 63u);
+      if (v[q] == 0.0 || n1 / COLS != r) continue;
+      double2& s = colbuf[sw((n1 % COLS) * N2 + static_cast<int>(h >> 6))];
+      atomicAdd(i < na ? &s.x : &s.y, (t[q] >> 31) ? -v[q] : v[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kTwPer; ++q) {
+    const int i = t0 + q * kClThreads;
+    if (i < Gm::kTw) tw[i] = twr[q];
+  }
+  __syncthreads();
+  // F1 pass A: DFT_RB over b of x[a + RA b], twiddle w_N2^{a kb}
+  for (int u = t0; u < COLS * RA; u += kClThreads) {
+    const int j = u / RA, a = u % RA;
+    const int c = j * N2 + a;
+    double2 x[RB];
+#pragma unroll
+    for (int q = 0; q < RB; ++q) x[q] = colbuf[sw(c + RA * q)];
+    RegDft<RB>::run(x, -1.0);
+#pragma unroll
+    for (int kb = 1; kb < RB; ++kb)
+      if (a) x[kb] = cmul(x[kb], twiddle(tw, hi, static_cast<uint32_t>((kN1 * a * kb) % M)));
+#pragma unroll
+    for (int q = 0; q < RB; ++q) colbuf[sw(c + RA * q)] = x[q];
+  }
+  // spectrum values for the product phase (in flight through the passes below)
+  double2 sv[kGU][2];
+#pragma unroll
+  for (int g = 0; g < kGU; ++g) {
+    const int u = t0 + g * kClThreads;
+    const int row = u >> 5, k1 = u & 31;
+    const int k2 = row_k2<N2, Q>(r, row < ROWS ? row : 0);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = k2 + N2 * (k1 + 32 * h);
+      const int kh = k <= P ? k : M - k;
+      double2 x = make_double2(0.0, 0.0);
+      if (u < ROWS * 32) {
+        if (kh == 0) x = make_double2(__ldg(&sp[__ldg(pl.f2p)].x), 0.0);
+        else if (kh == P) x = make_double2(__ldg(&sp[__ldg(pl.f2p)].y), 0.0);
+        else x = __ldg(sp + sslot[g][h]);
+        if (k > P) x = cconj(x);
+      }
+      sv[g][h] = x;
+    }
+  }
+  __syncthreads();
+  cluster_wait();
+  // F1 pass B: DFT_RA over a -> t[kb + RB ka]; twiddle w_M^{n1 k2}; to the owner of k2
+  for (int u = t0; u < COLS * RB; u += kClThreads) {
+    const int j = u / RB, kb = u % RB;
+    const int n1 = COLS * r + j;
+    const int c = j * N2 + RA * kb;
+    double2 y[RA];
+#pragma unroll
+    for (int q = 0; q < RA; ++q) y[q] = colbuf[sw(c + q)];
+    RegDft<RA>::run(y, -1.0);
+#pragma unroll
+    for (int ka = 0; ka < RA; ++ka) {
+      const int k2 = kb + RB * ka;
+      const double2 v = (n1 * k2) ? cmul(y[ka], twiddle(tw, hi, static_cast<uint32_t>(n1 * k2)))
+                                  : y[ka];
+      int owner, row;
+      k2_owner<N2, Q>(k2, owner, row);
+      double2* dst = cl.map_shared_rank(rowbuf, owner);
+      dst[sw(row * kN1 + n1)] = v;
+    }
+  }
+  cl.sync();
+  // F3: 64-point DFTs over n1 (8 x 8), in place: slot ka + 8 kb <- X[k2 + N2 (kb + 8 ka)]
+  for (int u = t0; u < ROWS * 8; u += kClThreads) {
+    const int row = u >> 3, a = u & 7;
+    const int c = row * kN1 + a;
+    double2 x[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = rowbuf[sw(c + 8 * q)];
+    RegDft<8>::run(x, -1.0);
+#pragma unroll
+    for (int kb = 1; kb < 8; ++kb)
+      if (a) x[kb] = cmul(x[kb], twiddle(tw, hi, static_cast<uint32_t>(N2 * a * kb)));
+#pragma unroll
+    for (int q = 0; q < 8; ++q) rowbuf[sw(c + 8 * q)] = x[q];
+  }
+  __syncthreads();
+  for (int u = t0; u < ROWS * 8; u += kClThreads) {
+    const int row = u >> 3, kb = u & 7;
+    const int c = row * kN1 + 8 * kb;
+    double2 y[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) y[q] = rowbuf[sw(c + q)];
+    RegDft<8>::run(y, -1.0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) rowbuf[sw(c + q)] = y[q];
+  }
+  __syncthreads();
+  // product with S_d and the c2r pre map: U[k2 + N2 k1], k1 < 32, into colbuf rows of 32
+  double2* ubuf = colbuf;
+#pragma unroll
+  for (int g = 0; g < kGU; ++g) {
+    const int u = t0 + g * kClThreads;
+    if (u >= ROWS * 32) break;
+    const int row = u >> 5, k1 = u & 31;
+    const int k2 = row_k2<N2, Q>(r, row);
+    const int mrow = (k2 == 0 || k2 == N2 / 2) ? row : (row ^ 1);
+    double2 gg[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int kk = k1 + 32 * h;
+      const int km = k2 == 0 ? ((kN1 - kk) & (kN1 - 1)) : (kN1 - 1 - kk);
+      const double2 X = rowbuf[sw(row * kN1 + (kk >> 3) + 8 * (kk & 7))];
+      const double2 Xm = rowbuf[sw(mrow * kN1 + (km >> 3) + 8 * (km & 7))];
+      // A = (X + conj Xm) / 2, B = (X - conj Xm) / 2i
+      const double2 a2 = make_double2(0.5 * (X.x + Xm.x), 0.5 * (X.y - Xm.y));
+      const double2 b2 = make_double2(0.5 * (X.y + Xm.y), -0.5 * (X.x - Xm.x));
+      gg[h] = cmul(sv[g][h], cconj(cmul(a2, b2)));
+    }
+    // E = (G0 + G1) / 2, O = (G0 - G1) w_M^{-k} / 2, U = E + i O
+    const int k = k2 + N2 * k1;
+    const double2 ev = make_double2(0.5 * (gg[0].x + gg[1].x), 0.5 * (gg[0].y + gg[1].y));
+    double2 ov = make_double2(0.5 * (gg[0].x - gg[1].x), 0.5 * (gg[0].y - gg[1].y));
+    if (k) ov = cmul(ov, cconj(twiddle(tw, hi, static_cast<uint32_t>(k))));
+    ubuf[sw(row * 32 + k1)] = make_double2(ev.x - ov.y, ev.y + ov.x);
+  }
+  __syncthreads();
+  // I1: 32-point inverse DFTs over k1 = a + 4 b (4 x 8)
+  for (int u = t0; u < ROWS * 4; u += kClThreads) {
+    const int row = u >> 2, a = u & 3;
+    const int c = row * 32 + a;
+    double2 x[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = ubuf[sw(c + 4 * q)];
+    RegDft<8>::run(x, +1.0);
+#pragma unroll
+    for (int mb = 1; mb < 8; ++mb)
+      if (a) x[mb] = cmul(x[mb], cconj(twiddle(tw, hi, static_cast<uint32_t>((M / 32) * a * mb))));
+#pragma unroll
+    for (int q = 0; q < 8; ++q) ubuf[sw(c + 4 * q)] = x[q];
+  }
+  __syncthreads();
+  for (int u = t0; u < ROWS * 8; u += kClThreads) {
+    const int row = u >> 3, mb = u & 7;
+    const int k2 = row_k2<N2, Q>(r, row);
+    const int c = row * 32 + 4 * mb;
+    double2 y[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) y[q] = ubuf[sw(c + q)];
+    RegDft<4>::run(y, +1.0);
+#pragma unroll
+    for (int ma = 0; ma < 4; ++ma) {
+      const int m1 = mb + 8 * ma;
+      const int e2 = (2 * m1 * k2) % M;  // w_P^{m1 k2} = w_M^{2 m1 k2}
+      const double2 v = e2 ? cmul(y[ma], cconj(twiddle(tw, hi, static_cast<uint32_t>(e2)))) : y[ma];
+      double2* dst = cl.map_shared_rank(ibuf, m1 / M1);
+      dst[sw((m1 % M1) * N2 + k2)] = v;
+    }
+  }
+  cl.sync();
+  // I3: N2-point inverse DFTs over k2 = a + RA b; slot ma + RA mb <- u[m1 + 32 (mb + RB ma)]
+  for (int u = t0; u < M1 * RA; u += kClThreads) {
+    const int ml = u / RA, a = u % RA;
+    const int c = ml * N2 + a;
+    double2 x[RB];
+#pragma unroll
+    for (int q = 0; q < RB; ++q) x[q] = ibuf[sw(c + RA * q)];
+    RegDft<RB>::run(x, +1.0);
+#pragma unroll
+    for (int mb = 1; mb < RB; ++mb)
+      if (a) x[mb] = cmul(x[mb], cconj(twiddle(tw, hi, static_cast<uint32_t>((kN1 * a * mb) % M))));
+#pragma unroll
+    for (int q = 0; q < RB; ++q) ibuf[sw(c + RA * q)] = x[q];
+  }
+  __syncthreads();
+  for (int u = t0; u < M1 * RB; u += kClThreads) {
+    const int ml = u / RB, mb = u % RB;
+    const int c = ml * N2 + RA * mb;
+    double2 y[RA];
+#pragma unroll
+    for (int q = 0; q < RA; ++q) y[q] = ibuf[sw(c + q)];
+    RegDft<RA>::run(y, +1.0);
+#pragma unroll
+    for (int q = 0; q < RA; ++q) ibuf[sw(c + q)] = y[q];
+  }
+  __syncthreads();
+  // gather: z[h] = u[h / 2] component h % 2, scaled 1 / P
+  double* o = est + static_cast<size_t>(item) * nf;
+  const double inv = 1.0 / P;
+#pragma unroll
+  for (int g = 0; g < kGather; ++g) {
+    const int i = t0 + g * kClThreads;
+    if (i >= nf) break;
+    const uint32_t t = gt[g];
+    const uint32_t h = t & 0x7fffffffu;
+    const int m = static_cast<int>(h >> 1);
+    const int m1 = m & 31, m2 = m >> 5;
+    if (m1 / M1 != r) continue;
+    const double2 v = ibuf[sw((m1 % M1) * N2 + (m2 / RB) + RA * (m2 % RB))];
+    const double z = ((h & 1u) ? v.y : v.x) * inv;
+    o[i] = (t >> 31) ? -z : z;
+  }
+  for (int i = t0 + kGather * kClThreads; i < nf; i += kClThreads) {  // nf > 256
+    const uint32_t t = __ldg(tf + i);
+    const uint32_t h = t & 0x7fffffffu;
+    const int m = static_cast<int>(h >> 1);
+    const int m1 = m & 31, m2 = m >> 5;
+    if (m1 / M1 != r) continue;
+    const double2 v = ibuf[sw((m1 % M1) * N2 + (m2 / RB) + RA * (m2 % RB))];
+    const double z = ((h & 1u) ? v.y : v.x) * inv;
+    o[i] = (t >> 31) ? -z : z;
+  }
+  if (tail.mode != 0) {
+    // The last of the D clusters of vector bvec (per-vector arrival counter)
+    // takes the median over the families with all 8 CTAs, then (modes 2, 3)
+    // the row norm from per-CTA partials exchanged over DSMEM.
+    __shared__ int last;
+    __shared__ double part[kClC];
+    __shared__ double red[kClThreads / 32];
+    __threadfence();
+    cl.sync();
+    if (r == 0 && t0 == 0) {
+      const int old = atomicAdd(tail.cnt + bvec, 1);
+      const int is_last = old == e.D - 1;
+      if (is_last) tail.cnt[bvec] = 0;  // every cluster of bvec has arrived: ready for the next launch
+      for (int q = 0; q < kClC; ++q) *cl.map_shared_rank(&last, q) = is_last;
+    }
+    cl.sync();
+    if (!last) return;
+    __threadfence();
+    if (tail.mode == 3 && *reinterpret_cast<volatile int*>(tail.stopped)) return;
+    const double* col0 = est + static_cast<size_t>(bvec) * e.D * nf;
+    double* ob = tail.out + static_cast<size_t>(bvec) * nf;
+    double acc = 0.0;
+    for (int i = r * kClThreads + t0; i < nf; i += kClC * kClThreads) {
+      const double m = median_col(col0 + i, e.D, nf, [](const double* p) { return __ldcg(p); });
+      ob[i] = m;
+      acc += m * m;
+    }
+    if (tail.mode == 1) return;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((t0 & 31) == 0) red[t0 >> 5] = acc;
+    __syncthreads();
+    if (t0 < kClC) {  // this CTA's partial to every CTA of the cluster (slot r)
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kClThreads / 32; ++w) s += red[w];
+      *cl.map_shared_rank(&part[r], t0) = s;
+    }
+    cl.sync();
+    double tot = 0.0;
+#pragma unroll
+    for (int q = 0; q < kClC; ++q) tot += part[q];
+    const double nv = sqrt(tot);
+    if (tail.mode == 2) {
+      for (int i = r * kClThreads + t0; i < nf; i += kClC * kClThreads)
+        ob[i] = nv < 1e-150 ? 0.0 : ob[i] / nv;
+    } else {
+      if (nv < 1e-150) {
+        if (r == 0 && t0 == 0) *tail.stopped = 1;
+        return;
+      }
+      for (int i = r * kClThreads + t0; i < nf; i += kClC * kClThreads) tail.best[i] = ob[i] / nv;
+    }
+  }
+}
+
+template <int RA, int RB>
+int launch_cl(const FftPlan& pl, const EngArgs& e, int batch, const double* A, const double* B,
+              int c1, int c2, int f, double* est, const IuvTail& tail, cudaStream_t st) {
+  using Gm = ClGeom<RA, RB>;
+  constexpr int kThreads = 128;
+  auto k = iuv_cluster_kernel<RA, RB, kThreads>;
+  const size_t smem = Gm::smem_bytes();
+  // once per process: the shared-memory opt-in (per function) and the number
+  // of clusters that fit the device at once
+  static int max_clusters_dev[64];
+  static bool init_dev[64];
+  int dev = 0;
+  FCS_CUDA_TRY(cudaGetDevice(&dev));
+  int& max_clusters = max_clusters_dev[dev & 63];
+  if (!init_dev[dev & 63]) {
+    init_dev[dev & 63] = true;
+    FCS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(kClC);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    int n = 0;
+    FCS_CUDA_TRY(cudaOccupancyMaxActiveClusters(&n, k, &cfg));
+    max_clusters = n;
+  }
+  // one wave only: beyond it the one-CTA kernel's throughput wins (config 3,
+  // 150 items: 47 vs 65 us per step)
+  if (static_cast<long>(batch) * e.D > max_clusters) return 1;
+  const unsigned grid = static_cast<unsigned>(batch) * e.D * kClC;
+  k<<<grid, kThreads, smem, st>>>(pl, e, A, B, c1, c2, f, est, tail);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+}  // namespace
+
+int launch_iuv_cluster(const FftPlan& pl, const EngArgs& e, int batch, const double* A,
+                       const double* B, int c1, int c2, int f, double* est, const IuvTail& tail,
+                       cudaStream_t st) {
+  static const bool off = std::getenv("ST_IUV_CLUSTER_OFF") != nullptr;  // A/B probe
+  if (off || pl.large_p1 || batch <= 0) return 1;
+  switch (pl.M) {
+    case 9216: return launch_cl<16, 9>(pl, e, batch, A, B, c1, c2, f, est, tail, st);
+    case 8192: return launch_cl<16, 8>(pl, e, batch, A, B, c1, c2, f, est, tail, st);
+    default: return 1;
+  }
+}
+
+}  // namespace fcs

@@ -55,3 +55,50 @@ st.rtpm(dt, rcfg)
 torch.cuda.synchronize()
 res["rtpm_s"] = time.perf_counter() - t0
 print(json.dumps(res))
+
+
+def pipelined(n, calls=200):
+    for _ in range(5):
+        iuv(n)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(calls):
+        iuv(n)
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / calls
+
+
+print(json.dumps({"pipelined_step15_ms": pipelined(15), "pipelined_step1_ms": pipelined(1)}))
+
+import time as _t
+for n in (1, 15):
+    torch.cuda.synchronize()
+    t0 = _t.perf_counter()
+    for _ in range(200):
+        iuv(n)
+    t1 = _t.perf_counter()
+    torch.cuda.synchronize()
+    t2 = _t.perf_counter()
+    print(json.dumps({"batch": n, "host_enqueue_us_per_call": (t1 - t0) / 200 * 1e6,
+                      "wall_us_per_call": (t2 - t0) / 200 * 1e6}))
+
+
+def iuv_nomed(n):
+    L.check(lib.st_engine_iuv(eng._h, n, C.c_void_p(U.data_ptr()), C.c_void_p(U.data_ptr()), 0,
+                              C.c_void_p(Yd.data_ptr()), 0, None))
+
+
+Yd = torch.empty((15 * 10, 200), dtype=torch.float64, device="cuda")
+for n in (1, 15):
+    for _ in range(5):
+        iuv_nomed(n)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(200):
+        iuv_nomed(n)
+    b.record()
+    torch.cuda.synchronize()
+    print(json.dumps({"batch": n, "pipelined_kernel_only_us": a.elapsed_time(b) / 200 * 1e3}))
