@@ -53,9 +53,11 @@ struct ClGeom {
   static constexpr int COLS = kN1 / kClC;    // n1 columns per CTA
   static constexpr int M1 = 32 / kClC;       // inverse m1 per CTA
   static_assert(N2 % (2 * kClC) == 0, "N2 must be a multiple of 16");
+  // U rows (ROWS x 32) and the I3 rows (M1 x N2) share the F1 column buffer
+  static_assert(ROWS * 32 + M1 * N2 <= COLS * N2, "column buffer too small");
   static constexpr int kTw = (1 << kTwLoBits) + (M >> kTwLoBits);
   static constexpr size_t smem_bytes() {
-    return static_cast<size_t>(kTw + COLS * N2 + ROWS * kN1 + M1 * N2) * sizeof(double2);
+    return static_cast<size_t>(kTw + COLS * N2 + ROWS * kN1) * sizeof(double2);
   }
 };
 
@@ -89,8 +91,13 @@ __device__ __forceinline__ void cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// For batches that fit one wave of clusters: the spectrum values are fetched
+// at the start and held in registers through the forward passes. (A
+// throughput form for larger batches — fetched before the product, 96
+// registers, 5 CTAs/SM — measured 47.8 us at config 3's 150 items against
+// 46.7 us for the one-CTA kernel, so larger batches stay there.)
 template <int RA, int RB, int kClThreads>
-__global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads)
+__global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
     iuv_cluster_kernel(FftPlan pl, EngArgs e, const double* __restrict__ A,
                        const double* __restrict__ B, int c1, int c2, int f,
                        double* __restrict__ est, IuvTail tail) {
@@ -104,7 +111,9 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads)
   double2* tw = reinterpret_cast<double2*>(smem_raw);
   double2* colbuf = tw + Gm::kTw;          // F1 columns [COLS][N2]; later U rows [ROWS][32]
   double2* rowbuf = colbuf + COLS * N2;    // F3 rows [ROWS][64] (written by every CTA)
-  double2* ibuf = rowbuf + ROWS * kN1;     // I3 rows [M1][N2] (written by every CTA)
+  // I3 rows [M1][N2] (written by every CTA): the F1 columns are dead once the
+  // first cluster barrier has passed, and the U rows take only the first part
+  double2* ibuf = colbuf + ROWS * 32;
   cg::cluster_group cl = cg::this_cluster();
   const int r = static_cast<int>(cl.block_rank());
   const int item = blockIdx.x / kClC;
@@ -138,6 +147,7 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads)
   }
   const double2* sp = e.spec + static_cast<size_t>(d) * P;
   int sslot[kGU][2];
+  auto load_slots = [&]() {
 #pragma unroll
   for (int g = 0; g < kGU; ++g) {
     const int u = t0 + g * kClThreads;
@@ -151,6 +161,8 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads)
       sslot[g][h] = (u < ROWS * 32 && kh != 0 && kh != P) ? __ldg(pl.f2p + kh) : 0;
     }
   }
+  };
+  load_slots();
   __syncthreads();
   for (int i0 = t0; i0 < na + nb; i0 += kSc * kClThreads) {
     double v[kSc];
@@ -198,8 +210,9 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads)
 #pragma unroll
     for (int q = 0; q < RB; ++q) colbuf[sw(c + RA * q)] = x[q];
   }
-  // spectrum values for the product phase (in flight through the passes below)
+  // spectrum values for the product phase
   double2 sv[kGU][2];
+  auto load_sv = [&]() {
 #pragma unroll
   for (int g = 0; g < kGU; ++g) {
     const int u = t0 + g * kClThreads;
@@ -219,6 +232,8 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads)
       sv[g][h] = x;
     }
   }
+  };
+  load_sv();  // in flight through the forward passes
   __syncthreads();
   cluster_wait();
   // F1 pass B: DFT_RA over a -> t[kb + RB ka]; twiddle w_M^{n1 k2}; to the owner of k2
@@ -445,7 +460,7 @@ int launch_cl(const FftPlan& pl, const EngArgs& e, int batch, const double* A, c
   constexpr int kThreads = 128;
   auto k = iuv_cluster_kernel<RA, RB, kThreads>;
   const size_t smem = Gm::smem_bytes();
-  // once per process: the shared-memory opt-in (per function) and the number
+  // once per device: the shared-memory opt-in (per function) and the number
   // of clusters that fit the device at once
   static int max_clusters_dev[64];
   static bool init_dev[64];
@@ -464,8 +479,7 @@ int launch_cl(const FftPlan& pl, const EngArgs& e, int batch, const double* A, c
     FCS_CUDA_TRY(cudaOccupancyMaxActiveClusters(&n, k, &cfg));
     max_clusters = n;
   }
-  // one wave only: beyond it the one-CTA kernel's throughput wins (config 3,
-  // 150 items: 47 vs 65 us per step)
+  // one wave only: beyond it the one-CTA kernel's throughput wins
   if (static_cast<long>(batch) * e.D > max_clusters) return 1;
   const unsigned grid = static_cast<unsigned>(batch) * e.D * kClC;
   k<<<grid, kThreads, smem, st>>>(pl, e, A, B, c1, c2, f, est, tail);
