@@ -957,3 +957,54 @@ def test_dense_f32_odd_fiber_fixed_point(cuda, shape, J, D):
     for d, f in enumerate(fams):
         b, s_, j = oracle_family(f)
         rel_close(got[d], O.fcs_dense(xg.astype(np.float64), b, s_, j), RTOL32)
+
+
+# ------------------------------------------- cluster (8-CTA, DSMEM) estimator
+@pytest.mark.parametrize("dims,J,D,seed", [((30, 24, 18), 2500, 5, 7),   # M = 8192 instantiation
+                                           ((20, 26, 31), 3000, 4, 8)])  # M = 9216 (config-3 J)
+def test_cluster_estimator_vs_oracle(cuda, dims, J, D, seed):
+    """The cluster estimator (spectral_cluster.cu) on both of its transform
+    lengths, every free mode (non-cubic, so the contracted-mode tables differ),
+    with the median fused in (batch 1 and 3: one wave of clusters) and without
+    it (per-family estimates), against the oracle engine; a batch beyond one
+    wave takes the one-CTA kernel and must agree too."""
+    rng = np.random.default_rng(seed)
+    t = rng.standard_normal(dims)
+    eng = st.FcsEngine(st.DenseTensor.from_array(t), st.EstimatorConfig(J, D, seed))
+    oeng = O.FcsEngine(t, J, D, seed)
+    for f in range(3):
+        c1 = 1 if f == 0 else 0
+        c2 = 1 if f == 2 else 2
+        for n in (1, 3, 16):
+            A = rng.standard_normal((n, dims[c1]))
+            B = rng.standard_normal((n, dims[c2]))
+            got = eng.iuv_batch(A, B, f).cpu().numpy()
+            per = eng.iuv_batch(A, B, f, median=False).cpu().numpy()
+            for b in (0, n - 1):
+                rel_close(got[b], oeng.iuv(A[b], B[b], f), RTOL64)
+                for d in (0, D - 1):
+                    want = O.iuv_spectral(oeng.pres[d], A[b], B[b], f)
+                    rel_close(per[b, d], want, RTOL64)
+
+
+def test_rtpm_cluster_tail_vs_oracle(cuda):
+    """rtpm where both phases take the fused cluster tail (J = 2500 -> M = 8192;
+    5 restarts x 5 families and the batch-1 refinement fit one wave): the
+    median + row normalisation (restarts) and the refinement update with its
+    sticky underflow stop equal the oracle's rtpm; a zero tensor exercises the
+    underflow branches (rows become 0, the refinement stops at once)."""
+    rng = np.random.default_rng(37)
+    q, _ = np.linalg.qr(rng.standard_normal((36, 3)))
+    t = configs.densify([3.0, 2.0, 1.5], [q, q, q]) + 1e-4 * rng.standard_normal((36, 36, 36))
+    est = st.EstimatorConfig(2500, 5, 19)
+    cp = st.rtpm(st.DenseTensor.from_array(t), st.RtpmConfig(3, 5, 8, st.SketchBackend.FCS, est))
+    w, f = O.rtpm(O.FcsEngine(t, 2500, 5, 19), 36, 3, 5, 8, 19)
+    rel_close(cp.weights, w, 1e-8)
+    rel_close(cp._factors_cm[0].t(), f, 1e-8)
+    assert np.allclose(np.sort(w)[::-1], [3.0, 2.0, 1.5], atol=0.15)
+    z = np.zeros((12, 12, 12))
+    cpz = st.rtpm(st.DenseTensor.from_array(z), st.RtpmConfig(2, 3, 4, st.SketchBackend.FCS,
+                                                             st.EstimatorConfig(2500, 3, 5)))
+    wz, fz = O.rtpm(O.FcsEngine(z, 2500, 3, 5), 12, 2, 3, 4, 5)
+    np.testing.assert_array_equal(cpz.weights.cpu().numpy(), wz)
+    np.testing.assert_array_equal(cpz._factors_cm[0].t().cpu().numpy(), fz)
