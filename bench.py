@@ -533,6 +533,18 @@ def secondary(x=None, cpu=True):
                                   C.c_void_p(U.data_ptr()), C.c_void_p(z1.data_ptr()), 1, sp))
     ms_iuv = median_ms(iuv_call, 20)
     ms_iuv1 = median_ms(lambda: iuv_call(1), 20)
+    def pipelined_ms(fn, calls=100):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(calls):
+            fn()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        return ev0.elapsed_time(ev1) / calls
+    pipe_iuv = pipelined_ms(iuv_call)
+    pipe_iuv1 = pipelined_ms(lambda: iuv_call(1))
     ms_uvw = median_ms(uvw_call, 20)
     ms_uvw1 = median_ms(lambda: uvw_call(1), 20)
     ms_defl = median_ms(lambda: L.check(lib.st_engine_deflate(
@@ -554,7 +566,13 @@ def secondary(x=None, cpu=True):
     e = {"iuv_step_ms": ms_iuv, "estimates_per_sec": Lr / (ms_iuv * 1e-3),
          "roofline": roofline_fp64(fl3, ms_iuv, fpeak, fkind),
          "roofline_hbm": roofline_hbm(1517680, ms_iuv, peak),
-         "iuv_batch1_ms": ms_iuv1, "uvw_step_ms": ms_uvw, "uvw_batch1_ms": ms_uvw1,
+         "iuv_batch1_ms": ms_iuv1,
+         "iuv_batch1_path": "8-CTA cluster per (vector, family) item, transposes over DSMEM, "
+                            "median fused into the last cluster (spectral_cluster.cu)",
+         "roofline_batch1": roofline_fp64(fft_flops(M3, 3 * c.sketch_count), ms_iuv1, fpeak, fkind),
+         "pipelined_ms": {"iuv_step": pipe_iuv, "iuv_batch1": pipe_iuv1,
+                          "note": "100 back-to-back calls on one stream (as inside rtpm)"},
+         "uvw_step_ms": ms_uvw, "uvw_batch1_ms": ms_uvw1,
          "deflate_ms": ms_defl, "rtpm_total_s": t_rtpm, "rtpm_timing": "second call (warm), host wall",
          "rtpm_breakdown_model": model, "seed": c.seed,
          "weights": [round(float(v), 6) for v in cpd.weights.cpu().numpy()]}

@@ -45,6 +45,36 @@ int device_info(DeviceInfo* out) {
   return ST_OK;
 }
 
+cudaError_t malloc_async_raw(void** p, size_t bytes, cudaStream_t st) {
+  static std::once_flag once[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::call_once(once[dev & 63], [dev]() {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  });
+  return cudaMallocAsync(p, bytes, st);
+}
+
+cudaError_t side_stream(cudaStream_t* out) {
+  static std::mutex mu;
+  static cudaStream_t per_dev[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (per_dev[dev & 63] == nullptr) {
+    e = cudaStreamCreateWithFlags(&per_dev[dev & 63], cudaStreamNonBlocking);
+    if (e != cudaSuccess) return e;
+  }
+  *out = per_dev[dev & 63];
+  return cudaSuccess;
+}
+
 // kernels (hash.cu, fcs_dense.cu)
 int launch_hash_tabulate(uint64_t, size_t, size_t, uint32_t*, int8_t*, cudaStream_t);
 int launch_family_tables(size_t, const size_t*, const size_t*, size_t, const uint64_t*,

@@ -175,7 +175,7 @@ struct DevMem {
   int alloc(T** p, size_t n) {
     *p = nullptr;
     void* q = nullptr;
-    FCS_CUDA_TRY(cudaMallocAsync(&q, std::max<size_t>(1, n * sizeof(T)), st));
+    FCS_CUDA_TRY(malloc_async(&q, std::max<size_t>(1, n * sizeof(T)), st));
     ptrs.push_back(q);
     *p = static_cast<T*>(q);
     return ST_OK;

@@ -70,6 +70,19 @@ struct DeviceInfo {
 };
 int device_info(DeviceInfo* out);
 
+// Stream-ordered allocation from the device's default pool. The first call
+// per device raises the pool's release threshold so freed blocks stay
+// reserved across stream synchronisations (otherwise every call after a
+// sync maps fresh memory: config 5's kron call 0.29 ms instead of 0.08 ms).
+cudaError_t malloc_async_raw(void** p, size_t bytes, cudaStream_t st);
+// A per-device non-blocking side stream for fork/join inside one API call
+// (independent launches that each fill only part of the device).
+cudaError_t side_stream(cudaStream_t* out);
+template <typename T>
+inline cudaError_t malloc_async(T** p, size_t bytes, cudaStream_t st) {
+  return malloc_async_raw(reinterpret_cast<void**>(p), bytes, st);
+}
+
 inline unsigned ceil_div(size_t a, size_t b) { return static_cast<unsigned>((a + b - 1) / b); }
 
 // K1 launch (fcs_dense.cu). kind 0: FCS bucket sum, 1: HCS mixed radix.

@@ -512,7 +512,7 @@ int st_psnr(int dtype, const void* reference, const void* estimate, size_t n, do
   cudaStream_t st = as_stream(stream);
   const int nblk = residual_blocks();
   double* part = nullptr;
-  FCS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), 2 * nblk * sizeof(double), st));
+  FCS_CUDA_TRY(malloc_async(reinterpret_cast<void**>(&part), 2 * nblk * sizeof(double), st));
   if (dtype == ST_F64)
     psnr_kernel<double><<<nblk, 256, 0, st>>>(static_cast<const double*>(reference),
                                               static_cast<const double*>(estimate), n, part);
@@ -546,7 +546,7 @@ int st_residual_norm(int dtype, const void* tensor, const size_t* dims, const do
   cudaStream_t st = as_stream(stream);
   const int nblk = residual_blocks();
   double* part = nullptr;
-  FCS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), (2 * nblk + 2) * sizeof(double), st));
+  FCS_CUDA_TRY(malloc_async(reinterpret_cast<void**>(&part), (2 * nblk + 2) * sizeof(double), st));
   double sums[2];
   const double* A0 = factors;
   const double* A1 = A0 + dims[0] * rank;

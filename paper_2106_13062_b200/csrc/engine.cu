@@ -127,7 +127,7 @@ int st_convolve_pairs(const double* a, size_t la, const double* b, size_t lb, si
   if (int rc = get_fft_plan(la + lb - 1, &pl)) return rc;
   cudaStream_t st = as_stream(stream);
   double2* scr = nullptr;
-  FCS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&scr), batch * pl.P * sizeof(double2), st));
+  FCS_CUDA_TRY(malloc_async(reinterpret_cast<void**>(&scr), batch * pl.P * sizeof(double2), st));
   const int rc = launch_conv(pl, a, static_cast<int>(la), la, b, static_cast<int>(lb), lb,
                              static_cast<int>(batch), scr, out, la + lb - 1, st);
   cudaFreeAsync(scr, st);
@@ -148,14 +148,34 @@ int st_fcs_kron(const double* a, size_t ra, size_t ca, const double* b, size_t r
   const size_t wsb = dense_workspace(ST_F64, 2, db, cb, D, hash_lens + 2);
   void* ws = nullptr;
   double *fa = nullptr, *fb = nullptr;
-  FCS_CUDA_TRY(cudaMallocAsync(&ws, std::max<size_t>(1, std::max(wsa, wsb)), st));
-  FCS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&fa), D * la * sizeof(double), st));
-  FCS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&fb), D * lb * sizeof(double), st));
+  const size_t wa = (std::max<size_t>(1, wsa) + 255) / 256 * 256;
+  FCS_CUDA_TRY(malloc_async(&ws, wa + std::max<size_t>(1, wsb), st));
+  FCS_CUDA_TRY(malloc_async(reinterpret_cast<void**>(&fa), D * la * sizeof(double), st));
+  FCS_CUDA_TRY(malloc_async(reinterpret_cast<void**>(&fb), D * lb * sizeof(double), st));
+  // the two operand sketches are independent and each fills ~one wave: B's
+  // runs on a side stream (fork / join by events) concurrently with A's
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  const bool forked = side_stream(&st2) == cudaSuccess &&
+                      cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) == cudaSuccess &&
+                      cudaEventCreateWithFlags(&join, cudaEventDisableTiming) == cudaSuccess &&
+                      cudaEventRecord(fork, st) == cudaSuccess &&
+                      cudaStreamWaitEvent(st2, fork, 0) == cudaSuccess;
+  if (!forked) {
+    cudaGetLastError();
+    st2 = st;
+  }
   int rc = launch_fcs_dense(ST_F64, a, 2, da, 0, ca, D, packed, hash_lens, fa, 0, ws, wsa, st,
                             stride);
-  if (!rc)
-    rc = launch_fcs_dense(ST_F64, b, 2, db, 0, cb, D, packed + ra + ca, hash_lens + 2, fb, 0, ws,
-                          wsb, st, stride);
+  const int rcb = launch_fcs_dense(ST_F64, b, 2, db, 0, cb, D, packed + ra + ca, hash_lens + 2, fb,
+                                   0, static_cast<char*>(ws) + wa, wsb, st2, stride);
+  if (forked) {  // join before anything else on st, whatever the launches returned
+    if (cudaEventRecord(join, st2) != cudaSuccess || cudaStreamWaitEvent(st, join, 0) != cudaSuccess)
+      FCS_CUDA_TRY(cudaStreamSynchronize(st2));
+  }
+  if (fork) cudaEventDestroy(fork);
+  if (join) cudaEventDestroy(join);
+  if (!rc) rc = rcb;
   if (!rc) rc = st_convolve_pairs(fa, la, fb, lb, D, out, st);
   cudaFreeAsync(ws, st);
   cudaFreeAsync(fa, st);
@@ -189,7 +209,7 @@ int st_precompute_z(const double* spectrum, size_t n, const double* a, size_t la
   FCS_CHECK_ARG(la > 0 && lb > 0 && ja > 0 && jb > 0, "HashPair: dimensions must be positive");
   cudaStream_t st = as_stream(stream);
   double* cs = nullptr;
-  FCS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&cs), (ja + jb) * sizeof(double), st));
+  FCS_CUDA_TRY(malloc_async(reinterpret_cast<void**>(&cs), (ja + jb) * sizeof(double), st));
   int rc = launch_cs_columns(a, static_cast<int>(la), 1, pair_a, static_cast<int>(ja), cs, st);
   if (!rc)
     rc = launch_cs_columns(b, static_cast<int>(lb), 1, pair_b, static_cast<int>(jb), cs + ja, st);
@@ -264,12 +284,12 @@ int st_engine_create_backend(st_engine** engine, int backend, int dtype, const v
   void* ws = nullptr;
   const size_t wsb = dense_workspace(dtype, 3, dims, dims[2], sketch_count, hl);
   const size_t vbytes = sketch_count * e->jt * sizeof(double);
-  bool ok = cudaMallocAsync(reinterpret_cast<void**>(&e->packed),
+  bool ok = malloc_async(reinterpret_cast<void**>(&e->packed),
                             sketch_count * sum_dims * sizeof(uint32_t), st) == cudaSuccess &&
-            cudaMallocAsync(reinterpret_cast<void**>(&e->spec),
+            malloc_async(reinterpret_cast<void**>(&e->spec),
                             sketch_count * e->plan.P * sizeof(double2), st) == cudaSuccess &&
-            cudaMallocAsync(reinterpret_cast<void**>(&vals), vbytes, st) == cudaSuccess &&
-            cudaMallocAsync(&ws, std::max<size_t>(1, wsb), st) == cudaSuccess;
+            malloc_async(reinterpret_cast<void**>(&vals), vbytes, st) == cudaSuccess &&
+            malloc_async(&ws, std::max<size_t>(1, wsb), st) == cudaSuccess;
   if (ok && backend == ST_BACKEND_TS) {
     const double one = 1.0;
     ok = cudaMalloc(reinterpret_cast<void**>(&e->ext), vbytes) == cudaSuccess &&

@@ -65,7 +65,7 @@ struct Scratch {
     if (p) FCS_CUDA_TRY(cudaFreeAsync(p, st));
     p = nullptr;
     bytes = 0;
-    FCS_CUDA_TRY(cudaMallocAsync(&p, need, st));
+    FCS_CUDA_TRY(malloc_async(&p, need, st));
     bytes = need;
     return ST_OK;
   }

@@ -390,7 +390,7 @@ int exact_create(st_engine* e, int dtype, const void* tensor, cudaStream_t st) {
     const size_t hl[3] = {J, J, J};
     const size_t wsb = dense_workspace(dtype, 3, e->dims, e->dims[2], D, hl, 1);
     void* ws = nullptr;
-    FCS_CUDA_TRY(cudaMallocAsync(&ws, std::max<size_t>(wsb, 1), st));
+    FCS_CUDA_TRY(malloc_async(&ws, std::max<size_t>(wsb, 1), st));
     const int rc = launch_fcs_dense(dtype, tensor, 3, e->dims, 0, e->dims[2], D, e->packed, hl,
                                     e->dense, 0, ws, wsb, st, 0, 1);
     cudaFreeAsync(ws, st);

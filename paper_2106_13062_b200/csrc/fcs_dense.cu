@@ -1421,7 +1421,11 @@ int make_plan_uncached(const DenseArgs& a, Plan* p) {
   // 592 -> 333 chunks; config 4 is unaffected).
   const uint64_t elems = a.fibers * a.dims[0];
   const uint64_t part_per_chunk = static_cast<uint64_t>(a.D) * a.jt * sizeof(Tacc);
-  nchunk = std::min<uint64_t>(nchunk, std::max<uint64_t>(1, elems * sizeof(Tin) / part_per_chunk));
+  // ... but never below one CTA per SM (config 5's 512^2 operands, D = 8: 8 -> 19 chunks,
+  // 103 -> 78 us per kron call)
+  const uint64_t by_bytes = std::max<uint64_t>(1, elems * sizeof(Tin) / part_per_chunk);
+  const uint64_t one_wave = (static_cast<uint64_t>(di.sm_count) + a.D - 1) / a.D;
+  nchunk = std::min<uint64_t>(nchunk, std::max(by_bytes, one_wave));
   p->nchunk = nchunk;
   p->part_bytes = nchunk * a.D * static_cast<size_t>(a.jt) *
                   (p->path == Path::Fx64 ? 8 : sizeof(Tacc));  // Fx32S: int32 like Fx

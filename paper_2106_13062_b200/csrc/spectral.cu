@@ -573,6 +573,10 @@ int launch_cp(const FftPlan& pl, const CpArgs& a, int D, const uint32_t* packed,
 int launch_conv(const FftPlan& pl, const double* a, int la, size_t lda, const double* b, int lb,
                 size_t ldb, int items, double2* scratch, double* out, size_t ldo, cudaStream_t st) {
   if (pl.large_p1) return large_conv(pl, a, la, lda, b, lb, ldb, items, out, ldo, st);
+  {  // one wave of items: an 8-CTA cluster per item (spectral_cluster.cu)
+    const int rc = launch_conv_cluster(pl, a, la, lda, b, lb, ldb, items, out, ldo, st);
+    if (rc != 1) return rc;
+  }
   size_t sm;
   if (int rc = prep(conv_kernel, pl, &sm)) return rc;
   conv_kernel<<<items, kFftThreads, sm, st>>>(pl, a, la, lda, b, lb, ldb, scratch, out, ldo);

@@ -91,6 +91,205 @@ __device__ __forceinline__ void cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// The distributed transform shared by the cluster kernels. Buffers (slot
+// indices swizzled by sw): colbuf [COLS][N2] F1 columns, later U rows
+// [ROWS][32] and the I3 rows [M1][N2] behind them; rowbuf [ROWS][64] F3 rows.
+template <int RA, int RB, int kThreads>
+struct ClFft {
+  using Gm = ClGeom<RA, RB>;
+  static constexpr int N2 = Gm::N2, M = Gm::M, P = Gm::P, Q = Gm::Q, ROWS = Gm::ROWS,
+                       COLS = Gm::COLS, M1 = Gm::M1;
+  static constexpr int hi = 1 << kTwLoBits;
+  const double2* tw;
+  double2* colbuf;
+  double2* rowbuf;
+  double2* ubuf;
+  double2* ibuf;
+  int r, t0;
+
+  __device__ ClFft(unsigned char* smem, int rank)
+      : tw(reinterpret_cast<double2*>(smem)), r(rank), t0(threadIdx.x) {
+    colbuf = reinterpret_cast<double2*>(smem) + Gm::kTw;
+    rowbuf = colbuf + COLS * N2;
+    ubuf = colbuf;
+    ibuf = colbuf + ROWS * 32;  // F1 columns are dead after the first cluster barrier
+  }
+
+  // F1 pass A: DFT_RB over b of x[a + RA b], twiddle w_N2^{a kb}
+  __device__ void f1a() const {
+    for (int u = t0; u < COLS * RA; u += kThreads) {
+      const int j = u / RA, a = u % RA;
+      const int c = j * N2 + a;
+      double2 x[RB];
+#pragma unroll
+      for (int q = 0; q < RB; ++q) x[q] = colbuf[sw(c + RA * q)];
+      RegDft<RB>::run(x, -1.0);
+#pragma unroll
+      for (int kb = 1; kb < RB; ++kb)
+        if (a) x[kb] = cmul(x[kb], twiddle(tw, hi, static_cast<uint32_t>((kN1 * a * kb) % M)));
+#pragma unroll
+      for (int q = 0; q < RB; ++q) colbuf[sw(c + RA * q)] = x[q];
+    }
+  }
+  // F1 pass B: DFT_RA over a -> t[kb + RB ka]; twiddle w_M^{n1 k2}; to the owner of k2;
+  // then the cluster barrier and F3 (64-point DFTs over n1, 8 x 8, in place:
+  // slot ka + 8 kb <- X[k2 + N2 (kb + 8 ka)])
+  __device__ void f1b_f3(cg::cluster_group& cl) const {
+    for (int u = t0; u < COLS * RB; u += kThreads) {
+      const int j = u / RB, kb = u % RB;
+      const int n1 = COLS * r + j;
+      const int c = j * N2 + RA * kb;
+      double2 y[RA];
+#pragma unroll
+      for (int q = 0; q < RA; ++q) y[q] = colbuf[sw(c + q)];
+      RegDft<RA>::run(y, -1.0);
+#pragma unroll
+      for (int ka = 0; ka < RA; ++ka) {
+        const int k2 = kb + RB * ka;
+        const double2 v =
+            (n1 * k2) ? cmul(y[ka], twiddle(tw, hi, static_cast<uint32_t>(n1 * k2))) : y[ka];
+        int owner, row;
+        k2_owner<N2, Q>(k2, owner, row);
+        double2* dst = cl.map_shared_rank(rowbuf, owner);
+        dst[sw(row * kN1 + n1)] = v;
+      }
+    }
+    cl.sync();
+    for (int u = t0; u < ROWS * 8; u += kThreads) {
+      const int row = u >> 3, a = u & 7;
+      const int c = row * kN1 + a;
+      double2 x[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) x[q] = rowbuf[sw(c + 8 * q)];
+      RegDft<8>::run(x, -1.0);
+#pragma unroll
+      for (int kb = 1; kb < 8; ++kb)
+        if (a) x[kb] = cmul(x[kb], twiddle(tw, hi, static_cast<uint32_t>(N2 * a * kb)));
+#pragma unroll
+      for (int q = 0; q < 8; ++q) rowbuf[sw(c + 8 * q)] = x[q];
+    }
+    __syncthreads();
+    for (int u = t0; u < ROWS * 8; u += kThreads) {
+      const int row = u >> 3, kb = u & 7;
+      const int c = row * kN1 + 8 * kb;
+      double2 y[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) y[q] = rowbuf[sw(c + q)];
+      RegDft<8>::run(y, -1.0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) rowbuf[sw(c + q)] = y[q];
+    }
+    __syncthreads();
+  }
+  // Spectra of both real inputs at k = k2 + N2 kk (w = a + i b): A = (X[k] + conj X[-k]) / 2,
+  // B = (X[k] - conj X[-k]) / 2i; -k stays in this CTA.
+  __device__ void spectra(int row, int k2, int kk, double2& a2, double2& b2) const {
+    const int mrow = (k2 == 0 || k2 == N2 / 2) ? row : (row ^ 1);
+    const int km = k2 == 0 ? ((kN1 - kk) & (kN1 - 1)) : (kN1 - 1 - kk);
+    const double2 X = rowbuf[sw(row * kN1 + (kk >> 3) + 8 * (kk & 7))];
+    const double2 Xm = rowbuf[sw(mrow * kN1 + (km >> 3) + 8 * (km & 7))];
+    a2 = make_double2(0.5 * (X.x + Xm.x), 0.5 * (X.y - Xm.y));
+    b2 = make_double2(0.5 * (X.y + Xm.y), -0.5 * (X.x - Xm.x));
+  }
+  // The c2r pre map of G at k and k + P (k = k2 + N2 k1, k1 < 32) into U.
+  __device__ void put_u(int row, int k2, int k1, double2 g0, double2 g1) const {
+    const int k = k2 + N2 * k1;
+    const double2 ev = make_double2(0.5 * (g0.x + g1.x), 0.5 * (g0.y + g1.y));
+    double2 ov = make_double2(0.5 * (g0.x - g1.x), 0.5 * (g0.y - g1.y));
+    if (k) ov = cmul(ov, cconj(twiddle(tw, hi, static_cast<uint32_t>(k))));
+    ubuf[sw(row * 32 + k1)] = make_double2(ev.x - ov.y, ev.y + ov.x);
+  }
+  // I1 (32-point inverse DFTs over k1 = a + 4 b), twiddle w_P^{-m1 k2}, to the
+  // owner of m1; the cluster barrier; I3 (N2-point inverse DFTs over k2):
+  // ibuf slot ma + RA mb of local row m1 % M1 <- P u[m1 + 32 (mb + RB ma)].
+  __device__ void inverse(cg::cluster_group& cl) const {
+    for (int u = t0; u < ROWS * 4; u += kThreads) {
+      const int row = u >> 2, a = u & 3;
+      const int c = row * 32 + a;
+      double2 x[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) x[q] = ubuf[sw(c + 4 * q)];
+      RegDft<8>::run(x, +1.0);
+#pragma unroll
+      for (int mb = 1; mb < 8; ++mb)
+        if (a)
+          x[mb] = cmul(x[mb], cconj(twiddle(tw, hi, static_cast<uint32_t>((M / 32) * a * mb))));
+#pragma unroll
+      for (int q = 0; q < 8; ++q) ubuf[sw(c + 4 * q)] = x[q];
+    }
+    __syncthreads();
+    for (int u = t0; u < ROWS * 8; u += kThreads) {
+      const int row = u >> 3, mb = u & 7;
+      const int k2 = row_k2<N2, Q>(r, row);
+      const int c = row * 32 + 4 * mb;
+      double2 y[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) y[q] = ubuf[sw(c + q)];
+      RegDft<4>::run(y, +1.0);
+#pragma unroll
+      for (int ma = 0; ma < 4; ++ma) {
+        const int m1 = mb + 8 * ma;
+        const int e2 = (2 * m1 * k2) % M;  // w_P^{m1 k2} = w_M^{2 m1 k2}
+        const double2 v =
+            e2 ? cmul(y[ma], cconj(twiddle(tw, hi, static_cast<uint32_t>(e2)))) : y[ma];
+        double2* dst = cl.map_shared_rank(ibuf, m1 / M1);
+        dst[sw((m1 % M1) * N2 + k2)] = v;
+      }
+    }
+    cl.sync();
+    for (int u = t0; u < M1 * RA; u += kThreads) {
+      const int ml = u / RA, a = u % RA;
+      const int c = ml * N2 + a;
+      double2 x[RB];
+#pragma unroll
+      for (int q = 0; q < RB; ++q) x[q] = ibuf[sw(c + RA * q)];
+      RegDft<RB>::run(x, +1.0);
+#pragma unroll
+      for (int mb = 1; mb < RB; ++mb)
+        if (a)
+          x[mb] = cmul(x[mb], cconj(twiddle(tw, hi, static_cast<uint32_t>((kN1 * a * mb) % M))));
+#pragma unroll
+      for (int q = 0; q < RB; ++q) ibuf[sw(c + RA * q)] = x[q];
+    }
+    __syncthreads();
+    for (int u = t0; u < M1 * RB; u += kThreads) {
+      const int ml = u / RB, mb = u % RB;
+      const int c = ml * N2 + RA * mb;
+      double2 y[RA];
+#pragma unroll
+      for (int q = 0; q < RA; ++q) y[q] = ibuf[sw(c + q)];
+      RegDft<RA>::run(y, +1.0);
+#pragma unroll
+      for (int q = 0; q < RA; ++q) ibuf[sw(c + q)] = y[q];
+    }
+    __syncthreads();
+  }
+  // z[h] (times P) if this CTA holds it: u[h / 2], component h % 2
+  __device__ bool owns(int h) const { return ((h >> 1) & 31) / M1 == r; }
+  __device__ double zval(int h) const {
+    const int m = h >> 1;
+    const int m1 = m & 31, m2 = m >> 5;
+    const double2 v = ibuf[sw((m1 % M1) * N2 + (m2 / RB) + RA * (m2 % RB))];
+    return (h & 1) ? v.y : v.x;
+  }
+  // twiddle table: loads issued into registers (stored by store_tw)
+  static constexpr int kTwPer = (Gm::kTw + kThreads - 1) / kThreads;
+  __device__ void load_tw(const FftPlan& pl, double2 (&twr)[kTwPer]) const {
+#pragma unroll
+    for (int q = 0; q < kTwPer; ++q) {
+      const int i = t0 + q * kThreads;
+      if (i < Gm::kTw) twr[q] = __ldg(pl.tw + i);
+    }
+  }
+  __device__ void store_tw(const double2 (&twr)[kTwPer]) const {
+#pragma unroll
+    for (int q = 0; q < kTwPer; ++q) {
+      const int i = t0 + q * kThreads;
+      if (i < Gm::kTw) const_cast<double2*>(tw)[i] = twr[q];
+    }
+  }
+};
+
 // For batches that fit one wave of clusters: the spectrum values are fetched
 // at the start and held in registers through the forward passes. (A
 // throughput form for larger batches — fetched before the product, 96
@@ -101,24 +300,16 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
     iuv_cluster_kernel(FftPlan pl, EngArgs e, const double* __restrict__ A,
                        const double* __restrict__ B, int c1, int c2, int f,
                        double* __restrict__ est, IuvTail tail) {
-  using Gm = ClGeom<RA, RB>;
-  constexpr int N2 = Gm::N2, M = Gm::M, P = Gm::P, Q = Gm::Q, ROWS = Gm::ROWS,
-                COLS = Gm::COLS, M1 = Gm::M1;
-  constexpr int hi = 1 << kTwLoBits;
+  using F = ClFft<RA, RB, kClThreads>;
+  constexpr int N2 = F::N2, M = F::M, P = F::P, Q = F::Q, ROWS = F::ROWS, COLS = F::COLS;
   constexpr int kGU = (ROWS * 32 + kClThreads - 1) / kClThreads;  // product units per thread
   constexpr int kGather = 2;                                       // gather entries per thread
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double2* tw = reinterpret_cast<double2*>(smem_raw);
-  double2* colbuf = tw + Gm::kTw;          // F1 columns [COLS][N2]; later U rows [ROWS][32]
-  double2* rowbuf = colbuf + COLS * N2;    // F3 rows [ROWS][64] (written by every CTA)
-  // I3 rows [M1][N2] (written by every CTA): the F1 columns are dead once the
-  // first cluster barrier has passed, and the U rows take only the first part
-  double2* ibuf = colbuf + ROWS * 32;
   cg::cluster_group cl = cg::this_cluster();
-  const int r = static_cast<int>(cl.block_rank());
+  const F fx(smem_raw, static_cast<int>(cl.block_rank()));
+  const int r = fx.r, t0 = fx.t0;
   const int item = blockIdx.x / kClC;
   const int bvec = item / e.D, d = item % e.D;
-  const int t0 = threadIdx.x;
   // every CTA of the cluster has started before anyone writes remote memory
   cluster_arrive();
   const uint32_t* tab = e.packed + static_cast<size_t>(d) * e.fam_stride;
@@ -130,15 +321,10 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
   const double* bv = B + static_cast<size_t>(bvec) * nb;
   // Early loads, all in flight together: twiddles, the count-sketch inputs,
   // the gather table entries and the slots of this thread's spectrum values.
-  constexpr int kTwPer = (Gm::kTw + kClThreads - 1) / kClThreads;
-  double2 twr[kTwPer];  // stored after the scatter, so both load streams overlap
-#pragma unroll
-  for (int q = 0; q < kTwPer; ++q) {
-    const int i = t0 + q * kClThreads;
-    if (i < Gm::kTw) twr[q] = __ldg(pl.tw + i);
-  }
+  double2 twr[F::kTwPer];  // stored after the scatter, so both load streams overlap
+  fx.load_tw(pl, twr);
   constexpr int kSc = 4;  // scatter inputs per thread per round
-  for (int i = t0; i < COLS * N2; i += kClThreads) colbuf[i] = make_double2(0.0, 0.0);
+  for (int i = t0; i < COLS * N2; i += kClThreads) fx.colbuf[i] = make_double2(0.0, 0.0);
   uint32_t gt[kGather];
 #pragma unroll
   for (int g = 0; g < kGather; ++g) {
@@ -147,7 +333,6 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
   }
   const double2* sp = e.spec + static_cast<size_t>(d) * P;
   int sslot[kGU][2];
-  auto load_slots = [&]() {
 #pragma unroll
   for (int g = 0; g < kGU; ++g) {
     const int u = t0 + g * kClThreads;
@@ -156,13 +341,10 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int k = k2 + N2 * (k1 + 32 * h);
-      // frequency of the half spectrum and whether it is conjugated / a real bin
-      const int kh = k <= P ? k : M - k;
+      const int kh = k <= P ? k : M - k;  // half-spectrum frequency
       sslot[g][h] = (u < ROWS * 32 && kh != 0 && kh != P) ? __ldg(pl.f2p + kh) : 0;
     }
   }
-  };
-  load_slots();
   __syncthreads();
   for (int i0 = t0; i0 < na + nb; i0 += kSc * kClThreads) {
     double v[kSc];
@@ -186,33 +368,15 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
       const uint32_t h = t[q] & 0x7fffffffu;
       const int n1 = static_cast<int>(h & 63u);
       if (v[q] == 0.0 || n1 / COLS != r) continue;
-      double2& s = colbuf[sw((n1 % COLS) * N2 + static_cast<int>(h >> 6))];
+      double2& s = fx.colbuf[sw((n1 % COLS) * N2 + static_cast<int>(h >> 6))];
       atomicAdd(i < na ? &s.x : &s.y, (t[q] >> 31) ? -v[q] : v[q]);
     }
   }
-#pragma unroll
-  for (int q = 0; q < kTwPer; ++q) {
-    const int i = t0 + q * kClThreads;
-    if (i < Gm::kTw) tw[i] = twr[q];
-  }
+  fx.store_tw(twr);
   __syncthreads();
-  // F1 pass A: DFT_RB over b of x[a + RA b], twiddle w_N2^{a kb}
-  for (int u = t0; u < COLS * RA; u += kClThreads) {
-    const int j = u / RA, a = u % RA;
-    const int c = j * N2 + a;
-    double2 x[RB];
-#pragma unroll
-    for (int q = 0; q < RB; ++q) x[q] = colbuf[sw(c + RA * q)];
-    RegDft<RB>::run(x, -1.0);
-#pragma unroll
-    for (int kb = 1; kb < RB; ++kb)
-      if (a) x[kb] = cmul(x[kb], twiddle(tw, hi, static_cast<uint32_t>((kN1 * a * kb) % M)));
-#pragma unroll
-    for (int q = 0; q < RB; ++q) colbuf[sw(c + RA * q)] = x[q];
-  }
-  // spectrum values for the product phase
+  fx.f1a();
+  // spectrum values for the product phase, in flight through the forward passes
   double2 sv[kGU][2];
-  auto load_sv = [&]() {
 #pragma unroll
   for (int g = 0; g < kGU; ++g) {
     const int u = t0 + g * kClThreads;
@@ -232,145 +396,27 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
       sv[g][h] = x;
     }
   }
-  };
-  load_sv();  // in flight through the forward passes
   __syncthreads();
   cluster_wait();
-  // F1 pass B: DFT_RA over a -> t[kb + RB ka]; twiddle w_M^{n1 k2}; to the owner of k2
-  for (int u = t0; u < COLS * RB; u += kClThreads) {
-    const int j = u / RB, kb = u % RB;
-    const int n1 = COLS * r + j;
-    const int c = j * N2 + RA * kb;
-    double2 y[RA];
-#pragma unroll
-    for (int q = 0; q < RA; ++q) y[q] = colbuf[sw(c + q)];
-    RegDft<RA>::run(y, -1.0);
-#pragma unroll
-    for (int ka = 0; ka < RA; ++ka) {
-      const int k2 = kb + RB * ka;
-      const double2 v = (n1 * k2) ? cmul(y[ka], twiddle(tw, hi, static_cast<uint32_t>(n1 * k2)))
-                                  : y[ka];
-      int owner, row;
-      k2_owner<N2, Q>(k2, owner, row);
-      double2* dst = cl.map_shared_rank(rowbuf, owner);
-      dst[sw(row * kN1 + n1)] = v;
-    }
-  }
-  cl.sync();
-  // F3: 64-point DFTs over n1 (8 x 8), in place: slot ka + 8 kb <- X[k2 + N2 (kb + 8 ka)]
-  for (int u = t0; u < ROWS * 8; u += kClThreads) {
-    const int row = u >> 3, a = u & 7;
-    const int c = row * kN1 + a;
-    double2 x[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) x[q] = rowbuf[sw(c + 8 * q)];
-    RegDft<8>::run(x, -1.0);
-#pragma unroll
-    for (int kb = 1; kb < 8; ++kb)
-      if (a) x[kb] = cmul(x[kb], twiddle(tw, hi, static_cast<uint32_t>(N2 * a * kb)));
-#pragma unroll
-    for (int q = 0; q < 8; ++q) rowbuf[sw(c + 8 * q)] = x[q];
-  }
-  __syncthreads();
-  for (int u = t0; u < ROWS * 8; u += kClThreads) {
-    const int row = u >> 3, kb = u & 7;
-    const int c = row * kN1 + 8 * kb;
-    double2 y[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) y[q] = rowbuf[sw(c + q)];
-    RegDft<8>::run(y, -1.0);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) rowbuf[sw(c + q)] = y[q];
-  }
-  __syncthreads();
-  // product with S_d and the c2r pre map: U[k2 + N2 k1], k1 < 32, into colbuf rows of 32
-  double2* ubuf = colbuf;
+  fx.f1b_f3(cl);
+  // G = S_d conj(A B) and the c2r pre map
 #pragma unroll
   for (int g = 0; g < kGU; ++g) {
     const int u = t0 + g * kClThreads;
     if (u >= ROWS * 32) break;
     const int row = u >> 5, k1 = u & 31;
     const int k2 = row_k2<N2, Q>(r, row);
-    const int mrow = (k2 == 0 || k2 == N2 / 2) ? row : (row ^ 1);
     double2 gg[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int kk = k1 + 32 * h;
-      const int km = k2 == 0 ? ((kN1 - kk) & (kN1 - 1)) : (kN1 - 1 - kk);
-      const double2 X = rowbuf[sw(row * kN1 + (kk >> 3) + 8 * (kk & 7))];
-      const double2 Xm = rowbuf[sw(mrow * kN1 + (km >> 3) + 8 * (km & 7))];
-      // A = (X + conj Xm) / 2, B = (X - conj Xm) / 2i
-      const double2 a2 = make_double2(0.5 * (X.x + Xm.x), 0.5 * (X.y - Xm.y));
-      const double2 b2 = make_double2(0.5 * (X.y + Xm.y), -0.5 * (X.x - Xm.x));
+      double2 a2, b2;
+      fx.spectra(row, k2, k1 + 32 * h, a2, b2);
       gg[h] = cmul(sv[g][h], cconj(cmul(a2, b2)));
     }
-    // E = (G0 + G1) / 2, O = (G0 - G1) w_M^{-k} / 2, U = E + i O
-    const int k = k2 + N2 * k1;
-    const double2 ev = make_double2(0.5 * (gg[0].x + gg[1].x), 0.5 * (gg[0].y + gg[1].y));
-    double2 ov = make_double2(0.5 * (gg[0].x - gg[1].x), 0.5 * (gg[0].y - gg[1].y));
-    if (k) ov = cmul(ov, cconj(twiddle(tw, hi, static_cast<uint32_t>(k))));
-    ubuf[sw(row * 32 + k1)] = make_double2(ev.x - ov.y, ev.y + ov.x);
+    fx.put_u(row, k2, k1, gg[0], gg[1]);
   }
   __syncthreads();
-  // I1: 32-point inverse DFTs over k1 = a + 4 b (4 x 8)
-  for (int u = t0; u < ROWS * 4; u += kClThreads) {
-    const int row = u >> 2, a = u & 3;
-    const int c = row * 32 + a;
-    double2 x[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) x[q] = ubuf[sw(c + 4 * q)];
-    RegDft<8>::run(x, +1.0);
-#pragma unroll
-    for (int mb = 1; mb < 8; ++mb)
-      if (a) x[mb] = cmul(x[mb], cconj(twiddle(tw, hi, static_cast<uint32_t>((M / 32) * a * mb))));
-#pragma unroll
-    for (int q = 0; q < 8; ++q) ubuf[sw(c + 4 * q)] = x[q];
-  }
-  __syncthreads();
-  for (int u = t0; u < ROWS * 8; u += kClThreads) {
-    const int row = u >> 3, mb = u & 7;
-    const int k2 = row_k2<N2, Q>(r, row);
-    const int c = row * 32 + 4 * mb;
-    double2 y[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) y[q] = ubuf[sw(c + q)];
-    RegDft<4>::run(y, +1.0);
-#pragma unroll
-    for (int ma = 0; ma < 4; ++ma) {
-      const int m1 = mb + 8 * ma;
-      const int e2 = (2 * m1 * k2) % M;  // w_P^{m1 k2} = w_M^{2 m1 k2}
-      const double2 v = e2 ? cmul(y[ma], cconj(twiddle(tw, hi, static_cast<uint32_t>(e2)))) : y[ma];
-      double2* dst = cl.map_shared_rank(ibuf, m1 / M1);
-      dst[sw((m1 % M1) * N2 + k2)] = v;
-    }
-  }
-  cl.sync();
-  // I3: N2-point inverse DFTs over k2 = a + RA b; slot ma + RA mb <- u[m1 + 32 (mb + RB ma)]
-  for (int u = t0; u < M1 * RA; u += kClThreads) {
-    const int ml = u / RA, a = u % RA;
-    const int c = ml * N2 + a;
-    double2 x[RB];
-#pragma unroll
-    for (int q = 0; q < RB; ++q) x[q] = ibuf[sw(c + RA * q)];
-    RegDft<RB>::run(x, +1.0);
-#pragma unroll
-    for (int mb = 1; mb < RB; ++mb)
-      if (a) x[mb] = cmul(x[mb], cconj(twiddle(tw, hi, static_cast<uint32_t>((kN1 * a * mb) % M))));
-#pragma unroll
-    for (int q = 0; q < RB; ++q) ibuf[sw(c + RA * q)] = x[q];
-  }
-  __syncthreads();
-  for (int u = t0; u < M1 * RB; u += kClThreads) {
-    const int ml = u / RB, mb = u % RB;
-    const int c = ml * N2 + RA * mb;
-    double2 y[RA];
-#pragma unroll
-    for (int q = 0; q < RA; ++q) y[q] = ibuf[sw(c + q)];
-    RegDft<RA>::run(y, +1.0);
-#pragma unroll
-    for (int q = 0; q < RA; ++q) ibuf[sw(c + q)] = y[q];
-  }
-  __syncthreads();
+  fx.inverse(cl);
   // gather: z[h] = u[h / 2] component h % 2, scaled 1 / P
   double* o = est + static_cast<size_t>(item) * nf;
   const double inv = 1.0 / P;
@@ -379,22 +425,16 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
     const int i = t0 + g * kClThreads;
     if (i >= nf) break;
     const uint32_t t = gt[g];
-    const uint32_t h = t & 0x7fffffffu;
-    const int m = static_cast<int>(h >> 1);
-    const int m1 = m & 31, m2 = m >> 5;
-    if (m1 / M1 != r) continue;
-    const double2 v = ibuf[sw((m1 % M1) * N2 + (m2 / RB) + RA * (m2 % RB))];
-    const double z = ((h & 1u) ? v.y : v.x) * inv;
+    const int h = static_cast<int>(t & 0x7fffffffu);
+    if (!fx.owns(h)) continue;
+    const double z = fx.zval(h) * inv;
     o[i] = (t >> 31) ? -z : z;
   }
   for (int i = t0 + kGather * kClThreads; i < nf; i += kClThreads) {  // nf > 256
     const uint32_t t = __ldg(tf + i);
-    const uint32_t h = t & 0x7fffffffu;
-    const int m = static_cast<int>(h >> 1);
-    const int m1 = m & 31, m2 = m >> 5;
-    if (m1 / M1 != r) continue;
-    const double2 v = ibuf[sw((m1 % M1) * N2 + (m2 / RB) + RA * (m2 % RB))];
-    const double z = ((h & 1u) ? v.y : v.x) * inv;
+    const int h = static_cast<int>(t & 0x7fffffffu);
+    if (!fx.owns(h)) continue;
+    const double z = fx.zval(h) * inv;
     o[i] = (t >> 31) ? -z : z;
   }
   if (tail.mode != 0) {
@@ -453,36 +493,113 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
   }
 }
 
-template <int RA, int RB>
-int launch_cl(const FftPlan& pl, const EngArgs& e, int batch, const double* A, const double* B,
-              int c1, int c2, int f, double* est, const IuvTail& tail, cudaStream_t st) {
+// Linear convolution of row pairs (fft_convolve of two sequences,
+// fft.cpp:75-84; config 5's Kronecker composition): one cluster per item,
+// w = a + i b transformed once, G = A B, out[t] = z[t] for t < la + lb - 1.
+template <int RA, int RB, int kClThreads>
+__global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
+    conv_cluster_kernel(FftPlan pl, const double* __restrict__ a, int la, size_t lda,
+                        const double* __restrict__ b, int lb, size_t ldb,
+                        double* __restrict__ out, size_t ldo) {
+  using F = ClFft<RA, RB, kClThreads>;
+  constexpr int N2 = F::N2, P = F::P, ROWS = F::ROWS, COLS = F::COLS;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  cg::cluster_group cl = cg::this_cluster();
+  const F fx(smem_raw, static_cast<int>(cl.block_rank()));
+  const int r = fx.r, t0 = fx.t0;
+  const int item = blockIdx.x / kClC;
+  cluster_arrive();
+  double2 twr[F::kTwPer];
+  fx.load_tw(pl, twr);
+  const double* ar = a + static_cast<size_t>(item) * lda;
+  const double* br = b + static_cast<size_t>(item) * ldb;
+  // this CTA's columns n1 = 8 r + j: w[n1 + 64 n2] for every n2 (zero past the rows)
+  for (int i = t0; i < COLS * N2; i += kClThreads) {
+    const int j = i / N2, n2 = i % N2;
+    const int n = COLS * r + j + kN1 * n2;
+    fx.colbuf[sw(i)] = make_double2(n < la ? __ldg(ar + n) : 0.0, n < lb ? __ldg(br + n) : 0.0);
+  }
+  fx.store_tw(twr);
+  __syncthreads();
+  fx.f1a();
+  __syncthreads();
+  cluster_wait();
+  fx.f1b_f3(cl);
+  for (int u = t0; u < ROWS * 32; u += kClThreads) {
+    const int row = u >> 5, k1 = u & 31;
+    const int k2 = row_k2<N2, F::Q>(r, row);
+    double2 gg[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double2 a2, b2;
+      fx.spectra(row, k2, k1 + 32 * h, a2, b2);
+      gg[h] = cmul(a2, b2);
+    }
+    fx.put_u(row, k2, k1, gg[0], gg[1]);
+  }
+  __syncthreads();
+  fx.inverse(cl);
+  // out[t] = z[t] / P for the t this CTA holds: t = 2m + c, m1 = m % 32 in [4r, 4r + 4)
+  const int lo = la + lb - 1;
+  double* o = out + static_cast<size_t>(item) * ldo;
+  const double inv = 1.0 / P;
+  for (int i = t0; i < F::M1 * N2 * 2; i += kClThreads) {
+    const int ml = i / (2 * N2), rest = i % (2 * N2);
+    const int m2 = rest >> 1, c = rest & 1;
+    const int t = 2 * (F::M1 * r + ml + 32 * m2) + c;
+    if (t < lo) o[t] = fx.zval(t) * inv;
+  }
+}
+
+template <int RA, int RB, typename K>
+int cluster_prep(K k, int* max_clusters_out) {
   using Gm = ClGeom<RA, RB>;
-  constexpr int kThreads = 128;
-  auto k = iuv_cluster_kernel<RA, RB, kThreads>;
   const size_t smem = Gm::smem_bytes();
-  // once per device: the shared-memory opt-in (per function) and the number
-  // of clusters that fit the device at once
+  // once per device and kernel: the shared-memory opt-in and the number of
+  // clusters that fit the device at once
   static int max_clusters_dev[64];
   static bool init_dev[64];
   int dev = 0;
   FCS_CUDA_TRY(cudaGetDevice(&dev));
-  int& max_clusters = max_clusters_dev[dev & 63];
   if (!init_dev[dev & 63]) {
-    init_dev[dev & 63] = true;
     FCS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(kClC);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(128);
     cfg.dynamicSmemBytes = smem;
     int n = 0;
     FCS_CUDA_TRY(cudaOccupancyMaxActiveClusters(&n, k, &cfg));
-    max_clusters = n;
+    max_clusters_dev[dev & 63] = n;
+    init_dev[dev & 63] = true;
   }
+  *max_clusters_out = max_clusters_dev[dev & 63];
+  return ST_OK;
+}
+
+template <int RA, int RB>
+int launch_cl(const FftPlan& pl, const EngArgs& e, int batch, const double* A, const double* B,
+              int c1, int c2, int f, double* est, const IuvTail& tail, cudaStream_t st) {
+  auto k = iuv_cluster_kernel<RA, RB, 128>;
+  int max_clusters = 0;
+  if (int rc = cluster_prep<RA, RB>(k, &max_clusters)) return rc;
   // one wave only: beyond it the one-CTA kernel's throughput wins
   if (static_cast<long>(batch) * e.D > max_clusters) return 1;
   const unsigned grid = static_cast<unsigned>(batch) * e.D * kClC;
-  k<<<grid, kThreads, smem, st>>>(pl, e, A, B, c1, c2, f, est, tail);
+  k<<<grid, 128, ClGeom<RA, RB>::smem_bytes(), st>>>(pl, e, A, B, c1, c2, f, est, tail);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+template <int RA, int RB>
+int launch_conv_cl(const FftPlan& pl, const double* a, int la, size_t lda, const double* b, int lb,
+                   size_t ldb, int items, double* out, size_t ldo, cudaStream_t st) {
+  auto k = conv_cluster_kernel<RA, RB, 128>;
+  int max_clusters = 0;
+  if (int rc = cluster_prep<RA, RB>(k, &max_clusters)) return rc;
+  if (items > max_clusters) return 1;
+  k<<<static_cast<unsigned>(items) * kClC, 128, ClGeom<RA, RB>::smem_bytes(), st>>>(
+      pl, a, la, lda, b, lb, ldb, out, ldo);
   FCS_CUDA_TRY(cudaGetLastError());
   return ST_OK;
 }
@@ -497,6 +614,17 @@ int launch_iuv_cluster(const FftPlan& pl, const EngArgs& e, int batch, const dou
   switch (pl.M) {
     case 9216: return launch_cl<16, 9>(pl, e, batch, A, B, c1, c2, f, est, tail, st);
     case 8192: return launch_cl<16, 8>(pl, e, batch, A, B, c1, c2, f, est, tail, st);
+    default: return 1;
+  }
+}
+
+int launch_conv_cluster(const FftPlan& pl, const double* a, int la, size_t lda, const double* b,
+                        int lb, size_t ldb, int items, double* out, size_t ldo, cudaStream_t st) {
+  static const bool off = std::getenv("ST_IUV_CLUSTER_OFF") != nullptr;  // A/B probe
+  if (off || pl.large_p1 || items <= 0) return 1;
+  switch (pl.M) {
+    case 9216: return launch_conv_cl<16, 9>(pl, a, la, lda, b, lb, ldb, items, out, ldo, st);
+    case 8192: return launch_conv_cl<16, 8>(pl, a, la, lda, b, lb, ldb, items, out, ldo, st);
     default: return 1;
   }
 }

@@ -279,7 +279,7 @@ struct DevTmp {
     if (p) cudaFreeAsync(p, st);
   }
   int alloc(size_t bytes) {
-    FCS_CUDA_TRY(cudaMallocAsync(&p, std::max<size_t>(bytes, 1), st));
+    FCS_CUDA_TRY(malloc_async(&p, std::max<size_t>(bytes, 1), st));
     return ST_OK;
   }
 };
