@@ -60,19 +60,46 @@ cudaError_t malloc_async_raw(void** p, size_t bytes, cudaStream_t st) {
   return cudaMallocAsync(p, bytes, st);
 }
 
-cudaError_t side_stream(cudaStream_t* out) {
-  static std::mutex mu;
-  static cudaStream_t per_dev[64];
+namespace {
+struct SideStream {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+std::mutex g_side_mu;
+SideStream g_side[64];
+cudaError_t side_of(SideStream** out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  std::lock_guard<std::mutex> lock(mu);
-  if (per_dev[dev & 63] == nullptr) {
-    e = cudaStreamCreateWithFlags(&per_dev[dev & 63], cudaStreamNonBlocking);
-    if (e != cudaSuccess) return e;
+  SideStream& s = g_side[dev & 63];
+  if (s.side == nullptr) {
+    if ((e = cudaStreamCreateWithFlags(&s.side, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming)) != cudaSuccess)
+      return e;
   }
-  *out = per_dev[dev & 63];
+  *out = &s;
   return cudaSuccess;
+}
+}  // namespace
+
+cudaError_t fork_side(cudaStream_t st, cudaStream_t* side) {
+  std::lock_guard<std::mutex> lock(g_side_mu);
+  SideStream* s = nullptr;
+  cudaError_t e = side_of(&s);
+  if (e == cudaSuccess) e = cudaEventRecord(s->fork, st);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s->side, s->fork, 0);
+  if (e == cudaSuccess) *side = s->side;
+  return e;
+}
+
+cudaError_t join_side(cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(g_side_mu);
+  SideStream* s = nullptr;
+  cudaError_t e = side_of(&s);
+  if (e == cudaSuccess) e = cudaEventRecord(s->join, s->side);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, s->join, 0);
+  return e;
 }
 
 // kernels (hash.cu, fcs_dense.cu)

@@ -75,9 +75,14 @@ int device_info(DeviceInfo* out);
 // reserved across stream synchronisations (otherwise every call after a
 // sync maps fresh memory: config 5's kron call 0.29 ms instead of 0.08 ms).
 cudaError_t malloc_async_raw(void** p, size_t bytes, cudaStream_t st);
-// A per-device non-blocking side stream for fork/join inside one API call
-// (independent launches that each fill only part of the device).
-cudaError_t side_stream(cudaStream_t* out);
+// Fork / join with a per-device non-blocking side stream inside one API call
+// (independent launches that each fill only part of the device): fork_side
+// orders the side stream after everything already on st and returns it;
+// join_side orders st after everything enqueued on the side stream. The
+// events are per device and reused (a wait binds to the latest record at
+// enqueue time), so a call costs two record/wait pairs and no allocation.
+cudaError_t fork_side(cudaStream_t st, cudaStream_t* side);
+cudaError_t join_side(cudaStream_t st);
 template <typename T>
 inline cudaError_t malloc_async(T** p, size_t bytes, cudaStream_t st) {
   return malloc_async_raw(reinterpret_cast<void**>(p), bytes, st);

@@ -325,9 +325,18 @@ int rtpm_on(st_engine* e, size_t dim, size_t rank, size_t L, size_t num_iters, u
       // normalisation fused in; else estimator, median and normalisation kernels
       const int rc = engine_iuv_fused(e, L, U, 0, 2, Y, nullptr, nullptr, st);
       if (rc == 1) {
-        if (int rc2 = st_engine_iuv(e, L, U, U, 0, Y, 1, st)) return rc2;
-        if (int rc2 = launch_normalize_rows(Y, static_cast<int>(L), static_cast<int>(dim), st))
-          return rc2;
+        if (is_exact(e)) {
+          if (int rc2 = st_engine_iuv(e, L, U, U, 0, Y, 1, st)) return rc2;
+          if (int rc2 = launch_normalize_rows(Y, static_cast<int>(L), static_cast<int>(dim), st))
+            return rc2;
+        } else {  // per-family estimates, then one median + normalisation kernel
+          if (int rc2 = e->est2.ensure(L * e->D * dim * sizeof(double), st)) return rc2;
+          double* est = static_cast<double*>(e->est2.p);
+          if (int rc2 = st_engine_iuv(e, L, U, U, 0, est, 0, st)) return rc2;
+          if (int rc2 = launch_median_normalize(est, static_cast<int>(L), static_cast<int>(e->D),
+                                                static_cast<int>(dim), Y, st))
+            return rc2;
+        }
       } else if (rc) {
         return rc;
       }

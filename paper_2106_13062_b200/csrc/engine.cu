@@ -153,28 +153,14 @@ int st_fcs_kron(const double* a, size_t ra, size_t ca, const double* b, size_t r
   FCS_CUDA_TRY(malloc_async(reinterpret_cast<void**>(&fa), D * la * sizeof(double), st));
   FCS_CUDA_TRY(malloc_async(reinterpret_cast<void**>(&fb), D * lb * sizeof(double), st));
   // the two operand sketches are independent and each fills ~one wave: B's
-  // runs on a side stream (fork / join by events) concurrently with A's
+  // runs on the side stream (fork / join) concurrently with A's
   cudaStream_t st2 = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
-  const bool forked = side_stream(&st2) == cudaSuccess &&
-                      cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) == cudaSuccess &&
-                      cudaEventCreateWithFlags(&join, cudaEventDisableTiming) == cudaSuccess &&
-                      cudaEventRecord(fork, st) == cudaSuccess &&
-                      cudaStreamWaitEvent(st2, fork, 0) == cudaSuccess;
-  if (!forked) {
-    cudaGetLastError();
-    st2 = st;
-  }
+  FCS_CUDA_TRY(fork_side(st, &st2));
   int rc = launch_fcs_dense(ST_F64, a, 2, da, 0, ca, D, packed, hash_lens, fa, 0, ws, wsa, st,
                             stride);
   const int rcb = launch_fcs_dense(ST_F64, b, 2, db, 0, cb, D, packed + ra + ca, hash_lens + 2, fb,
                                    0, static_cast<char*>(ws) + wa, wsb, st2, stride);
-  if (forked) {  // join before anything else on st, whatever the launches returned
-    if (cudaEventRecord(join, st2) != cudaSuccess || cudaStreamWaitEvent(st, join, 0) != cudaSuccess)
-      FCS_CUDA_TRY(cudaStreamSynchronize(st2));
-  }
-  if (fork) cudaEventDestroy(fork);
-  if (join) cudaEventDestroy(join);
+  FCS_CUDA_TRY(join_side(st));  // before anything else on st, whatever the launches returned
   if (!rc) rc = rcb;
   if (!rc) rc = st_convolve_pairs(fa, la, fb, lb, D, out, st);
   cudaFreeAsync(ws, st);
@@ -444,6 +430,7 @@ int st_engine_destroy(st_engine* e) {
   e->vec.release(nullptr);
   e->vec2.release(nullptr);
   e->cnt.release(nullptr);
+  e->est2.release(nullptr);
   cudaDeviceSynchronize();
   delete e;
   return ST_OK;

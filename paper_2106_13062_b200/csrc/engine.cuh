@@ -28,6 +28,7 @@ int launch_deflate(const FftPlan&, const EngArgs&, double, const double*, const 
 int launch_median(const double*, int, int, int, double*, cudaStream_t);
 int launch_cs_columns(const double*, int, int, const uint32_t*, int, double*, cudaStream_t);
 int launch_normalize_rows(double*, int, int, cudaStream_t);
+int launch_median_normalize(const double*, int, int, int, double*, cudaStream_t);
 int launch_refine_update(double*, const double*, int, int*, cudaStream_t);
 int launch_family_tables(size_t, const size_t*, const size_t*, size_t, const uint64_t*,
                          uint32_t*, cudaStream_t);
@@ -156,6 +157,7 @@ struct st_engine {
   uint64_t* seeds = nullptr;   // CS: the D long pairs' seeds
   fcs::Scratch scratch, est, vec, vec2;
   fcs::Scratch cnt;  // per-vector arrival counters of the fused cluster tail (kept zero)
+  fcs::Scratch est2;  // per-family estimates of the rtpm restart step
   fcs::EngArgs args() const {
     fcs::EngArgs e{};
     size_t off = 0;
