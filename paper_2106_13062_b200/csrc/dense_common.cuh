@@ -22,6 +22,10 @@ struct DenseArgs {
   uint32_t inv_d1;                 // floor(2^32 / dims[1]) for fast division (order 3)
   uint64_t fibers;                 // mode-0 fibers in this slab
   uint64_t fibers_per_chunk;
+  // fixed-point kernels with lane-owned entries (fx64 / fx32s): a fiber is
+  // 2^lseg segments of seg_len entries (the last one shorter), one warp each
+  uint32_t seg_len;
+  uint32_t lseg;
 };
 
 // A sparse (COO) sketch launch (fcs_coo.cu).

@@ -802,10 +802,15 @@ __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
   for (uint32_t b = threadIdx.x; b < 2 * a.jt; b += blockDim.x) lo[b] = 0u;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const uint32_t i0n = a.dims[0];
+  // I_0 > 1024: warp w takes segment w % 2^lseg of the fibers (entries
+  // s0 .. s0 + slen of every fiber), 16 / 2^lseg fibers at a time
+  const uint32_t s0 = (static_cast<uint32_t>(warp) & ((1u << a.lseg) - 1u)) * a.seg_len;
+  const uint32_t slen = min(a.seg_len, i0n - s0);
+  const int fstride = nwarps >> a.lseg;
   // mode-0 buckets two per register (bucket < jt <= 29056 < 2^16) and signs
-  // as a bit mask (bit k: entry i_0 = lane + 32 k). Entries past I_0 load no
-  // data (x = 0 adds q = 0) and point at bucket `lane`: distinct banks, so the
-  // padding lanes of a partial fiber cost no conflicts and need no predicate.
+  // as a bit mask (bit k: entry i_0 = s0 + lane + 32 k). Entries past the
+  // segment load no data (x = 0 adds q = 0) and point at bucket `lane`:
+  // distinct banks, so the padding lanes cost no conflicts and need no predicate.
   uint32_t bk[(NV + 1) / 2];
   uint32_t smask = 0;
 #pragma unroll
@@ -813,7 +818,7 @@ __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     const uint32_t i = lane + 32u * k;
-    const uint32_t e = i < i0n ? __ldg(tab + a.i0_shift + i) : static_cast<uint32_t>(lane);
+    const uint32_t e = i < slen ? __ldg(tab + a.i0_shift + s0 + i) : static_cast<uint32_t>(lane);
     bk[k / 2] |= (e & 0xffffu) << (16 * (k % 2));
     smask |= (e >> 31) << k;
   }
@@ -830,10 +835,10 @@ __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
   constexpr int NB = NV / LB;
   constexpr int G = LB < 4 ? LB : 4;
   auto load = [&]<int KB>(uint64_t f, double* x) {
-    const Tin* fib = t + f * i0n;
+    const Tin* fib = t + f * i0n + s0;
 #pragma unroll
     for (int k = 0; k < LB; ++k)
-      x[k] = (kFull || lane + 32u * (KB + k) < i0n) ? ld_stream64(fib + lane + 32 * (KB + k)) : 0.0;
+      x[k] = (kFull || lane + 32u * (KB + k) < slen) ? ld_stream64(fib + lane + 32 * (KB + k)) : 0.0;
   };
   uint32_t base_c = 0, fmask = 0;
   auto scatter = [&]<int KB>(uint64_t f, const double* x) {
@@ -881,22 +886,22 @@ __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
     }
   };
   double cur[LB], nxt[LB];
-  uint64_t f = f_begin + warp;
+  uint64_t f = f_begin + (warp >> a.lseg);
   if (f < f_end) load.template operator()<0>(f, cur);
   if constexpr (NB == 1) {
-    for (; f < f_end; f += 2 * nwarps) {
-      if (f + nwarps < f_end) load.template operator()<0>(f + nwarps, nxt);
+    for (; f < f_end; f += 2 * fstride) {
+      if (f + fstride < f_end) load.template operator()<0>(f + fstride, nxt);
       scatter.template operator()<0>(f, cur);
-      if (f + nwarps >= f_end) break;
-      if (f + 2 * nwarps < f_end) load.template operator()<0>(f + 2 * nwarps, cur);
-      scatter.template operator()<0>(f + nwarps, nxt);
+      if (f + fstride >= f_end) break;
+      if (f + 2 * fstride < f_end) load.template operator()<0>(f + 2 * fstride, cur);
+      scatter.template operator()<0>(f + fstride, nxt);
     }
   } else {
     static_assert(NB == 2, "NV = 32: two batches of 16");
-    for (; f < f_end; f += nwarps) {
+    for (; f < f_end; f += fstride) {
       load.template operator()<LB>(f, nxt);
       scatter.template operator()<0>(f, cur);
-      if (f + nwarps < f_end) load.template operator()<0>(f + nwarps, cur);
+      if (f + fstride < f_end) load.template operator()<0>(f + fstride, cur);
       scatter.template operator()<LB>(f, nxt);
     }
   }
@@ -948,6 +953,10 @@ __global__ void __launch_bounds__(512) fcs_dense_fx32s_kernel(DenseArgs a,
   for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) sk[b] = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const uint32_t i0n = a.dims[0];
+  // I_0 > 1024: segments of the fibers per warp, as fcs_dense_fx64_kernel
+  const uint32_t s0 = (static_cast<uint32_t>(warp) & ((1u << a.lseg) - 1u)) * a.seg_len;
+  const uint32_t slen = min(a.seg_len, i0n - s0);
+  const int fstride = nwarps >> a.lseg;
   uint32_t bk[(NV + 1) / 2];
   uint32_t smask = 0;
 #pragma unroll
@@ -955,7 +964,7 @@ __global__ void __launch_bounds__(512) fcs_dense_fx32s_kernel(DenseArgs a,
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     const uint32_t i = lane + 32u * k;
-    const uint32_t e = i < i0n ? __ldg(tab + a.i0_shift + i) : static_cast<uint32_t>(lane);
+    const uint32_t e = i < slen ? __ldg(tab + a.i0_shift + s0 + i) : static_cast<uint32_t>(lane);
     bk[k / 2] |= (e & 0xffffu) << (16 * (k % 2));
     smask |= (e >> 31) << k;
   }
@@ -967,11 +976,11 @@ __global__ void __launch_bounds__(512) fcs_dense_fx32s_kernel(DenseArgs a,
   constexpr int LB = NV < 16 ? NV : 16;
   constexpr int NB = NV / LB;
   auto load = [&]<int KB>(uint64_t f, float* x) {
-    const float* fib = t + f * i0n;
+    const float* fib = t + f * i0n + s0;
 #pragma unroll
     for (int k = 0; k < LB; ++k) {
       const uint32_t i = lane + 32u * (KB + k);
-      if (kFull || i < i0n) {
+      if (kFull || i < slen) {
         asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(x[k]) : "l"(fib + i));
       } else {
         x[k] = 0.f;
@@ -1003,22 +1012,22 @@ __global__ void __launch_bounds__(512) fcs_dense_fx32s_kernel(DenseArgs a,
     }
   };
   float cur[LB], nxt[LB];
-  uint64_t f = f_begin + warp;
+  uint64_t f = f_begin + (warp >> a.lseg);
   if (f < f_end) load.template operator()<0>(f, cur);
   if constexpr (NB == 1) {
-    for (; f < f_end; f += 2 * nwarps) {
-      if (f + nwarps < f_end) load.template operator()<0>(f + nwarps, nxt);
+    for (; f < f_end; f += 2 * fstride) {
+      if (f + fstride < f_end) load.template operator()<0>(f + fstride, nxt);
       scatter.template operator()<0>(f, cur);
-      if (f + nwarps >= f_end) break;
-      if (f + 2 * nwarps < f_end) load.template operator()<0>(f + 2 * nwarps, cur);
-      scatter.template operator()<0>(f + nwarps, nxt);
+      if (f + fstride >= f_end) break;
+      if (f + 2 * fstride < f_end) load.template operator()<0>(f + 2 * fstride, cur);
+      scatter.template operator()<0>(f + fstride, nxt);
     }
   } else {
     static_assert(NB == 2, "NV <= 32: at most two batches of 16");
-    for (; f < f_end; f += nwarps) {
+    for (; f < f_end; f += fstride) {
       load.template operator()<LB>(f, nxt);
       scatter.template operator()<0>(f, cur);
-      if (f + nwarps < f_end) load.template operator()<0>(f + nwarps, cur);
+      if (f + fstride < f_end) load.template operator()<0>(f + fstride, cur);
       scatter.template operator()<LB>(f, nxt);
     }
   }
@@ -1252,6 +1261,28 @@ int fx64_nv(uint32_t i0) {
   while (32u * nv < i0) nv <<= 1;
   return nv;
 }
+
+// Lane-owned fixed-point kernels (fx64, fx32s) take I_0 <= 16384: 2^lseg
+// segments (one warp each, 16 warps per CTA) of seg_len <= 1024 entries, a
+// multiple of 32 (the last segment shorter); NV from seg_len.
+constexpr uint32_t kFxSegMaxI0 = 16384;
+inline void fx_segments(uint32_t i0, uint32_t* seg_len, uint32_t* lseg) {
+  uint32_t l = 0;
+  while (((i0 + (1u << l) - 1) >> l) > 1024u) ++l;
+  *lseg = l;
+  *seg_len = (((i0 + (1u << l) - 1) >> l) + 31u) / 32u * 32u;
+}
+inline int fx_seg_nv(uint32_t i0) {
+  uint32_t len, l;
+  fx_segments(i0, &len, &l);
+  return fx64_nv(len);
+}
+// every segment holds exactly 32 NV entries (no per-entry guard)
+inline bool fx_seg_full(uint32_t i0) {
+  uint32_t len, l;
+  fx_segments(i0, &len, &l);
+  return i0 == (32u * fx64_nv(len)) << l;
+}
 using Fx32sKernel = void (*)(DenseArgs, const float*, const uint32_t*, const FxStats*, int32_t*,
                              int*);
 // fx32s variant: NV = the smallest power of two with 32 NV >= I_0 (I_0 <= 1024).
@@ -1361,23 +1392,23 @@ int make_plan_uncached(const DenseArgs& a, Plan* p) {
   const bool fx64_pays = static_cast<double>(a.fibers) * a.dims[0] * a.D >= 8.0e6;
   // fp32 shapes the float4 kernel does not take (I_0 % 4 != 0), I_0 <= 1024:
   // the same int32 fixed point with scalar loads
-  const bool fx32s_ok = sizeof(Tin) == 4 && a.order >= 2 && a.dims[0] <= 1024 &&
-                        fits(fx32s_kernel(fx64_nv(a.dims[0]), false));
+  const bool fx32s_ok = sizeof(Tin) == 4 && a.order >= 2 && a.dims[0] <= kFxSegMaxI0 &&
+                        fits(fx32s_kernel(fx_seg_nv(a.dims[0]), false));
   if (sizeof(Tin) == 4 && !p->nv && fx32s_ok && fx64_pays) {
     p->path = Path::Fx32S;
-    p->nv = fx64_nv(a.dims[0]);
+    p->nv = fx_seg_nv(a.dims[0]);
     p->threads = 512;
-    auto k = fx32s_kernel(p->nv, a.dims[0] == 32u * p->nv);
+    auto k = fx32s_kernel(p->nv, fx_seg_full(a.dims[0]));
     FCS_CUDA_TRY(set_max_dynamic_smem(k, di));
     FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
                                                                p->smem_bytes));
-  } else if (sizeof(Tin) == 8 && a.order >= 2 && a.dims[0] <= 1024 && !no_fx64 && fx64_pays &&
-             fits(fx64_kernel<Tin>(fx64_nv(a.dims[0]), false))) {
+  } else if (sizeof(Tin) == 8 && a.order >= 2 && a.dims[0] <= kFxSegMaxI0 && !no_fx64 &&
+             fx64_pays && fits(fx64_kernel<Tin>(fx_seg_nv(a.dims[0]), false))) {
     // fp64: 64-bit fixed point, 8 bytes per bucket
     p->path = Path::Fx64;
-    p->nv = fx64_nv(a.dims[0]);
+    p->nv = fx_seg_nv(a.dims[0]);
     p->threads = 512;
-    const bool full = a.dims[0] == 32u * p->nv;
+    const bool full = fx_seg_full(a.dims[0]);
     auto k = fx64_kernel<Tin>(p->nv, full);
     FCS_CUDA_TRY(set_max_dynamic_smem(k, di));
     FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
@@ -1397,7 +1428,7 @@ int make_plan_uncached(const DenseArgs& a, Plan* p) {
     FCS_CUDA_TRY(set_max_dynamic_smem(fx_kernel(p->nv, p->group, true), di));
     if (fx32s_ok)  // an unaligned tensor on this plan takes the scalar-load kernel
       FCS_CUDA_TRY(set_max_dynamic_smem(
-          fx32s_kernel(fx64_nv(a.dims[0]), a.dims[0] == 32u * fx64_nv(a.dims[0])), di));
+          fx32s_kernel(fx_seg_nv(a.dims[0]), fx_seg_full(a.dims[0])), di));
     FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
                                                                p->smem_bytes));
   } else {
@@ -1503,6 +1534,7 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
   a.fibers_per_chunk = (a.fibers + p.nchunk - 1) / p.nchunk;
   const uint64_t nchunk = (a.fibers + a.fibers_per_chunk - 1) / a.fibers_per_chunk;
   const bool aligned = (reinterpret_cast<uintptr_t>(t) & 15u) == 0;
+  fx_segments(a.dims[0], &a.seg_len, &a.lseg);
   if (p.path == Path::Fx32S || (p.path == Path::Fx && !aligned && a.order >= 2 &&
                                  a.dims[0] <= 1024)) {
     char* base = static_cast<char*>(ws);
@@ -1527,8 +1559,8 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
     fx_scale_kernel<<<1, 512, 0, st>>>(sc, kFx32);
     FCS_CUDA_TRY(cudaGetLastError());
     FCS_CUDA_TRY(cudaMemsetAsync(divert, 0, out_elems * sizeof(double), st));
-    const int nv = fx64_nv(a.dims[0]);
-    fx32s_kernel(nv, a.dims[0] == 32u * nv)<<<static_cast<unsigned>(nchunk * a.D), 512,
+    const int nv = fx_seg_nv(a.dims[0]);
+    fx32s_kernel(nv, fx_seg_full(a.dims[0]))<<<static_cast<unsigned>(nchunk * a.D), 512,
                                               p.smem_bytes, st>>>(a, tf, packed, stats, part,
                                                                   flags);
     FCS_CUDA_TRY(cudaGetLastError());
@@ -1603,7 +1635,7 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
     const int nparts = static_cast<int>(nsample);
     const double per_cta = static_cast<double>(a.fibers_per_chunk) * a.dims[0];
     const FxScaleArgs sc{parts, nparts, 3.0 * per_cta / a.jt + 16.0, stats};
-    const bool full = a.dims[0] == 32u * p.nv;
+    const bool full = fx_seg_full(a.dims[0]);
     fx_sample_warps_kernel<Tin><<<ceil_div(nsample, 8), 256, 0, st>>>(a, t, nsample, parts);
     FCS_CUDA_TRY(cudaGetLastError());
     fx_scale_kernel<<<1, 512, 0, st>>>(sc, kFx64);

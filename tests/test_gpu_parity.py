@@ -830,6 +830,39 @@ def test_dense_f64_fixed_point_integer_bitexact(cuda, shape, J, D):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("shape,J,D", [((2048, 70, 60), 3000, 1),   # 2 full segments of 1024
+                                       ((3000, 50, 60), 2000, 1),   # 4 segments of 768, last 696
+                                       ((1100, 90, 90), 1500, 1),   # 2 segments of 576 / 524
+                                       ((16384, 24, 24), 4096, 1)])  # 16 segments (the limit)
+def test_dense_f64_fixed_point_long_fibers(cuda, shape, J, D):
+    """I_0 > 1024: each fiber split into 2^l segments, one warp per segment
+    (fx_segments): integer data bit-exact against the reference's serial sum,
+    Gaussian data at the fp64 rule."""
+    rng = np.random.default_rng(sum(shape))
+    x = rng.integers(-1000, 1001, size=shape).astype(np.float64)
+    got, want = _f64_case(x, J, D)
+    assert np.array_equal(got, want)
+    x = rng.standard_normal(shape)
+    got, want = _f64_case(x, J, D)
+    rel_close(got, want, RTOL64)
+
+
+@pytest.mark.parametrize("shape", [(2048, 64, 66), (1100, 90, 90), (3001, 50, 60)])
+def test_dense_f32_fixed_point_long_fibers(cuda, shape):
+    """fp32 with I_0 > 1024 (formerly fp32 shared atomics): the scalar-load
+    int32 fixed point over fiber segments, at the fp32 rule against the oracle
+    and bit-identical across runs."""
+    rng = np.random.default_rng(sum(shape) + 1)
+    x = rng.standard_normal(shape).astype(np.float32)
+    fams = st.families_for(list(shape), st.EstimatorConfig(2500, 2, 3))
+    t = st.DenseTensor.from_array(x)
+    got = st.fcs_dense_batched(t, fams)
+    assert torch.equal(st.fcs_dense_batched(t, fams), got)
+    for d, f in enumerate(fams):
+        b, s, j = oracle_family(f)
+        rel_close(got[d], O.fcs_dense(x.astype(np.float64), b, s, j), RTOL32)
+
+
 def test_dense_f64_fixed_point_gaussian(cuda):
     """Gaussian fp64 data through the fixed point at the fp64 rule, and the
     large buckets to 1e-12 relative (quantum 2^-(S+1) per element, S ~ 48)."""

@@ -40,7 +40,7 @@ if __name__ == "__main__":
     res = {}
     for dims, J, note in [((1024, 1024, 1024), 16384, "fast path (int32 fixed point)"),
                           ((1022, 1024, 1026), 16384, "I0 % 4 != 0 (int32 fixed point, scalar loads)"),
-                          ((2048, 1024, 512), 16384, "I0 > 1024 (fp32 atomics)"),
+                          ((2048, 1024, 512), 16384, "I0 > 1024 (int32 fixed point, scalar loads, 2 segments per fiber)"),
                           ((1024, 1024, 1024), 4096, "fast path, J = 4096"),
                           ((1022, 1024, 1026), 4096, "I0 % 4 != 0, J = 4096 (scalar loads)"),
                           ((1000, 1024, 1049), 16384, "I0 = 1000 (scalar loads, partial fibers)")]:
