@@ -26,6 +26,10 @@ struct DenseArgs {
   // 2^lseg segments of seg_len entries (the last one shorter), one warp each
   uint32_t seg_len;
   uint32_t lseg;
+  // fx64 with J~ beyond shared memory: the buckets in rparts ranges of rspan,
+  // one CTA per (chunk, family, range)
+  uint32_t rparts;
+  uint32_t rspan;
 };
 
 // A sparse (COO) sketch launch (fcs_coo.cu).

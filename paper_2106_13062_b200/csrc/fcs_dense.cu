@@ -786,7 +786,7 @@ inline uint64_t fx_nsample(uint64_t fibers) {
 
 __device__ __forceinline__ double i128_to_double(__int128 acc);
 
-template <typename Tin, int NV, bool kFull>
+template <typename Tin, int NV, bool kFull, bool kRange>
 __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
                                                              const Tin* __restrict__ t,
                                                              const uint32_t* __restrict__ packed,
@@ -796,10 +796,19 @@ __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* lo = reinterpret_cast<uint32_t*>(smem_raw);
   const int d = blockIdx.x % a.D;
-  const uint64_t chunk = blockIdx.x / a.D;
+  // kRange: this CTA holds buckets [r_lo, r_lo + r_cnt) of its family (plus
+  // 32 dummy buckets: an element of another range adds 0 to bucket `lane`
+  // past the range, so no predicate and no bank conflict)
+  const uint32_t rp = kRange ? (blockIdx.x / a.D) % a.rparts : 0u;
+  const uint64_t chunk = kRange ? blockIdx.x / (a.D * a.rparts) : blockIdx.x / a.D;
+  const uint32_t span = kRange ? a.rspan : a.jt;
+  const uint32_t r_lo = rp * span;
+  const uint32_t r_cnt = kRange ? min(span, a.jt - r_lo) : a.jt;
+  const uint32_t words = kRange ? span + 32u : a.jt;  // per word array
+  const uint64_t prow = kRange ? (chunk * a.D + d) * a.rparts + rp : chunk * a.D + d;
   const uint32_t* tab = packed + static_cast<uint64_t>(d) * a.fam_stride;
   const double scale = ldexp(1.0, st->S);
-  for (uint32_t b = threadIdx.x; b < 2 * a.jt; b += blockDim.x) lo[b] = 0u;
+  for (uint32_t b = threadIdx.x; b < 2 * words; b += blockDim.x) lo[b] = 0u;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const uint32_t i0n = a.dims[0];
   // I_0 > 1024: warp w takes segment w % 2^lseg of the fibers (entries
@@ -826,7 +835,7 @@ __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
   const uint64_t f_begin = chunk * a.fibers_per_chunk;
   const uint64_t f_end = min(a.fibers, f_begin + a.fibers_per_chunk);
   const uint32_t lo_base = static_cast<uint32_t>(__cvta_generic_to_shared(lo));
-  const uint32_t hi_off = 4u * a.jt;
+  const uint32_t hi_off = 4u * words;
   uint32_t rng_acc = 0, ovf_acc = 0;
   // A fiber is NB batches of LB entries per lane; the next batch's loads (of
   // this fiber or the next) are in flight while the current batch is
@@ -845,7 +854,7 @@ __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
     if (KB == 0) {
       uint32_t c, sbit;
       fiber_offset_fast(a, tab, f, c, sbit);
-      base_c = lo_base + 4u * c;
+      base_c = kRange ? c - r_lo : lo_base + 4u * c;  // kRange: range-relative offset
       fmask = smask ^ (sbit ? 0xffffffffu : 0u);  // bit k: final sign of entry k
     }
 #pragma unroll
@@ -857,7 +866,14 @@ __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
         (void)dummy;
         const int kk = KB + kg + k;
         const uint32_t e = (kk % 2) ? (bk[kk / 2] >> 16) : (bk[kk / 2] & 0xffffu);
-        ad[k] = base_c + (e << 2);
+        bool in_range = true;
+        if constexpr (kRange) {
+          const uint32_t lb = base_c + e;
+          in_range = lb < r_cnt;
+          ad[k] = lo_base + 4u * (in_range ? lb : span + static_cast<uint32_t>(lane));
+        } else {
+          ad[k] = base_c + (e << 2);
+        }
         // sign: bit kk of fmask onto the top bit of x
         const uint64_t xb = static_cast<uint64_t>(__double_as_longlong(x[kg + k])) ^
                             (static_cast<uint64_t>((fmask << (31 - kk)) & 0x80000000u) << 32);
@@ -866,8 +882,8 @@ __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
         const uint32_t bh = static_cast<uint32_t>(bits >> 32);
         // exponent of the magic sum must stay 52 (0x433): else out of range / non-finite
         rng_acc |= bh ^ 0x43300000u;
-        ql[k] = static_cast<uint32_t>(bits);  // the magic's low word is 0
-        qh[k] = bh - 0x43380000u;
+        ql[k] = in_range ? static_cast<uint32_t>(bits) : 0u;  // the magic's low word is 0
+        qh[k] = in_range ? bh - 0x43380000u : 0u;
       }
       // the low-word adds first (their returned values give the carries), then the high words
 #pragma unroll
@@ -909,7 +925,7 @@ __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
   const bool overflowed = __syncthreads_or(ovf);
   if (overflowed) {  // exact fallback for this CTA: fp64 atomics over the same chunk
     double* skd = reinterpret_cast<double*>(smem_raw);
-    for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) skd[b] = 0.0;
+    for (uint32_t b = threadIdx.x; b < r_cnt; b += blockDim.x) skd[b] = 0.0;
     __syncthreads();
     for (uint64_t g = f_begin + warp; g < f_end; g += nwarps) {
       uint32_t c, sbit;
@@ -917,15 +933,24 @@ __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
       for (uint32_t i = lane; i < i0n; i += 32) {
         const double x = static_cast<double>(__ldcs(t + g * i0n + i));
         const uint32_t e = __ldg(tab + a.i0_shift + i);
-        if (x != 0.0) atomicAdd(&skd[(e & 0x7fffffffu) + c], ((e ^ sbit) & 0x80000000u) ? -x : x);
+        const uint32_t lb = (e & 0x7fffffffu) + c - r_lo;
+        if (x != 0.0 && lb < r_cnt) atomicAdd(&skd[lb], ((e ^ sbit) & 0x80000000u) ? -x : x);
       }
     }
     __syncthreads();
   }
-  // partial layout per (chunk, d): jt lo words then jt hi words (or jt doubles when flagged)
-  uint32_t* dst = part + (chunk * a.D + d) * 2ull * a.jt;
-  for (uint32_t b = threadIdx.x; b < 2 * a.jt; b += blockDim.x) dst[b] = lo[b];
-  if (threadIdx.x == 0) flags[chunk * a.D + d] = overflowed ? 1 : 0;
+  // partial layout per (chunk, d[, range]): span lo words then span hi words
+  // (or span doubles when flagged); kRange = false: span = J~
+  uint32_t* dst = part + prow * 2ull * span;
+  if (overflowed) {
+    for (uint32_t b = threadIdx.x; b < 2 * r_cnt; b += blockDim.x) dst[b] = lo[b];
+  } else {
+    for (uint32_t b = threadIdx.x; b < r_cnt; b += blockDim.x) {
+      dst[b] = lo[b];
+      dst[span + b] = lo[words + b];
+    }
+  }
+  if (threadIdx.x == 0) flags[prow] = overflowed ? 1 : 0;
 }
 
 // float32 fixed point with scalar loads (fp32 tensors off the float4 path:
@@ -1066,9 +1091,9 @@ __device__ __forceinline__ double i128_to_double(__int128 acc) {
 }
 
 __global__ void reduce_fx64_kernel(const uint32_t* __restrict__ part, const int* __restrict__ flags,
-                                   uint64_t nchunk, int D, uint32_t jt,
-                                   const FxStats* __restrict__ st, double* __restrict__ out,
-                                   int accumulate) {
+                                   uint64_t nchunk, int D, uint32_t jt, uint32_t rparts,
+                                   uint32_t span, const FxStats* __restrict__ st,
+                                   double* __restrict__ out, int accumulate) {
   __shared__ __int128 ired[32][33];
   __shared__ double dred[32][33];
   const uint64_t per = static_cast<uint64_t>(D) * jt;
@@ -1077,13 +1102,15 @@ __global__ void reduce_fx64_kernel(const uint32_t* __restrict__ part, const int*
   double dacc = 0.0;
   if (i < per) {
     const int d = static_cast<int>(i / jt);
-    const uint32_t b = static_cast<uint32_t>(i - static_cast<uint64_t>(d) * jt);
+    const uint32_t bb = static_cast<uint32_t>(i - static_cast<uint64_t>(d) * jt);
+    const uint32_t rp = bb / span, b = bb - rp * span;  // range part, bucket within it
     for (uint64_t c = threadIdx.y; c < nchunk; c += 32) {
-      const uint32_t* row = part + (c * D + d) * 2ull * jt;
-      if (flags[c * D + d]) {
+      const uint64_t prow = (c * D + d) * rparts + rp;
+      const uint32_t* row = part + prow * 2ull * span;
+      if (flags[prow]) {
         dacc += reinterpret_cast<const double*>(row)[b];
       } else {
-        acc += static_cast<int64_t>((static_cast<uint64_t>(row[jt + b]) << 32) | row[b]);
+        acc += static_cast<int64_t>((static_cast<uint64_t>(row[span + b]) << 32) | row[b]);
       }
     }
   }
@@ -1205,6 +1232,8 @@ enum class Path { Global, Smem, Fx, Fx32S, Fx64 };
 
 struct Plan {
   Path path = Path::Global;
+  uint32_t rparts = 1;  // fx64: bucket ranges per family (J~ beyond shared memory)
+  uint32_t rspan = 0;
   bool group = false;  // fx: bank-aware load order
   size_t smem_bytes = 0;
   int threads = 0;
@@ -1300,18 +1329,25 @@ Fx32sKernel fx32s_kernel(int nv, bool full) {
 template <typename Tin>
 using Fx64Kernel = void (*)(DenseArgs, const Tin*, const uint32_t*, const FxStats*, uint32_t*,
                             int*);
-template <typename Tin>
-Fx64Kernel<Tin> fx64_kernel(int nv, bool full) {
+template <typename Tin, bool kRange>
+Fx64Kernel<Tin> fx64_kernel_r(int nv, bool full) {
   switch (nv) {
-    case 1: return full ? fcs_dense_fx64_kernel<Tin, 1, true> : fcs_dense_fx64_kernel<Tin, 1, false>;
-    case 2: return full ? fcs_dense_fx64_kernel<Tin, 2, true> : fcs_dense_fx64_kernel<Tin, 2, false>;
-    case 4: return full ? fcs_dense_fx64_kernel<Tin, 4, true> : fcs_dense_fx64_kernel<Tin, 4, false>;
-    case 8: return full ? fcs_dense_fx64_kernel<Tin, 8, true> : fcs_dense_fx64_kernel<Tin, 8, false>;
+    case 1: return full ? fcs_dense_fx64_kernel<Tin, 1, true, kRange> : fcs_dense_fx64_kernel<Tin, 1, false, kRange>;
+    case 2: return full ? fcs_dense_fx64_kernel<Tin, 2, true, kRange> : fcs_dense_fx64_kernel<Tin, 2, false, kRange>;
+    case 4: return full ? fcs_dense_fx64_kernel<Tin, 4, true, kRange> : fcs_dense_fx64_kernel<Tin, 4, false, kRange>;
+    case 8: return full ? fcs_dense_fx64_kernel<Tin, 8, true, kRange> : fcs_dense_fx64_kernel<Tin, 8, false, kRange>;
     case 16:
-      return full ? fcs_dense_fx64_kernel<Tin, 16, true> : fcs_dense_fx64_kernel<Tin, 16, false>;
+      return full ? fcs_dense_fx64_kernel<Tin, 16, true, kRange>
+                  : fcs_dense_fx64_kernel<Tin, 16, false, kRange>;
     default:
-      return full ? fcs_dense_fx64_kernel<Tin, 32, true> : fcs_dense_fx64_kernel<Tin, 32, false>;
+      return full ? fcs_dense_fx64_kernel<Tin, 32, true, kRange>
+                  : fcs_dense_fx64_kernel<Tin, 32, false, kRange>;
   }
+}
+// range = true: the bucket-range split for J~ beyond shared memory
+template <typename Tin>
+Fx64Kernel<Tin> fx64_kernel(int nv, bool full, bool range = false) {
+  return range ? fx64_kernel_r<Tin, true>(nv, full) : fx64_kernel_r<Tin, false>(nv, full);
 }
 
 constexpr size_t kAlign = 256;
@@ -1370,78 +1406,102 @@ int make_plan_uncached(const DenseArgs& a, Plan* p) {
   DeviceInfo di;
   if (int rc = device_info(&di)) return rc;
   p->smem_bytes = static_cast<size_t>(a.jt) * sizeof(Tacc);
-  if (p->smem_bytes > di.smem_optin) {
-    p->path = Path::Global;
-    p->ws = 0;
-    return ST_OK;
-  }
+  static const bool no_fx64_env = std::getenv("ST_FX64_OFF") != nullptr;  // A/B probe
+  const bool fx64_shape = sizeof(Tin) == 8 && a.order >= 2 && a.dims[0] <= kFxSegMaxI0 &&
+                          !no_fx64_env &&
+                          static_cast<double>(a.fibers) * a.dims[0] * a.D >= 8.0e6;
   int per_sm = 0;
-  p->nv = sizeof(Tin) == 4 ? fx_nv(a) : 0;
-  // the fixed-point kernels also hold fx_scale_device's static scratch
-  auto fits = [&](auto k) {
-    cudaFuncAttributes at{};
-    return cudaFuncGetAttributes(&at, k) == cudaSuccess &&
-           p->smem_bytes + at.sharedSizeBytes <= di.smem_optin;
-  };
-  if (p->nv && !fits(fx_kernel(p->nv, false))) p->nv = 0;
-  static const bool no_fx64 = std::getenv("ST_FX64_OFF") != nullptr;  // A/B probe
-  // Below ~8M element-updates the call is launch/latency-bound and the CAS
-  // kernel's two launches beat the fixed point's three (c1 100^3 D=1: 27.6 vs
-  // 33.8 us; c5 operands: 37 vs 42 us); above it the fixed point wins (c3
-  // build 200^3 D=10: 200 vs 292 us; 1024^3 J=8192 D=1: 1.44 vs 3.43 ms).
-  const bool fx64_pays = static_cast<double>(a.fibers) * a.dims[0] * a.D >= 8.0e6;
-  // fp32 shapes the float4 kernel does not take (I_0 % 4 != 0), I_0 <= 1024:
-  // the same int32 fixed point with scalar loads
-  const bool fx32s_ok = sizeof(Tin) == 4 && a.order >= 2 && a.dims[0] <= kFxSegMaxI0 &&
-                        fits(fx32s_kernel(fx_seg_nv(a.dims[0]), false));
-  if (sizeof(Tin) == 4 && !p->nv && fx32s_ok && fx64_pays) {
-    p->path = Path::Fx32S;
-    p->nv = fx_seg_nv(a.dims[0]);
-    p->threads = 512;
-    auto k = fx32s_kernel(p->nv, fx_seg_full(a.dims[0]));
-    FCS_CUDA_TRY(set_max_dynamic_smem(k, di));
-    FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
-                                                               p->smem_bytes));
-  } else if (sizeof(Tin) == 8 && a.order >= 2 && a.dims[0] <= kFxSegMaxI0 && !no_fx64 &&
-             fx64_pays && fits(fx64_kernel<Tin>(fx_seg_nv(a.dims[0]), false))) {
-    // fp64: 64-bit fixed point, 8 bytes per bucket
+  if (fx64_shape ? p->smem_bytes + 4096 > di.smem_optin : p->smem_bytes > di.smem_optin) {
+    // fp64 with J~ beyond shared memory: the 64-bit fixed point over R bucket
+    // ranges (one CTA per chunk, family and range; each element read R times
+    // through L2) instead of fp64 global atomics (1024 x 1024 x 512,
+    // J~ = 49,150, D = 1: 4.45 ms with global atomics)
+    const size_t avail = di.smem_optin - 4096;  // static shared memory + the 32 dummy buckets
+    const uint32_t R = static_cast<uint32_t>((static_cast<size_t>(a.jt) * 8 + avail - 1) / avail);
+    if (!fx64_shape || R > 8) {
+      p->path = Path::Global;
+      p->ws = 0;
+      return ST_OK;
+    }
     p->path = Path::Fx64;
+    p->rparts = R;
+    p->rspan = (a.jt + R - 1) / R;
     p->nv = fx_seg_nv(a.dims[0]);
     p->threads = 512;
-    const bool full = fx_seg_full(a.dims[0]);
-    auto k = fx64_kernel<Tin>(p->nv, full);
+    p->smem_bytes = (static_cast<size_t>(p->rspan) + 32) * 8;
+    auto k = fx64_kernel<Tin>(p->nv, fx_seg_full(a.dims[0]), true);
     FCS_CUDA_TRY(set_max_dynamic_smem(k, di));
-    FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
-                                                               p->smem_bytes));
-  } else if (p->nv) {
-    p->path = Path::Fx;
-    p->threads = fx_threads(p->nv);
-    // the bank-aware order pays off when atomics bind: with the searched
-    // groups, config-4 geometry D = 2: 1.333 -> 1.155 ms, D = 4: -4 %; with one
-    // family the kernel is load-bound (D = 1: 0.722 vs 0.725 ms) and keeps
-    // the immediate-offset loads.
-    // ST_FX_NOGROUP=1 keeps the identity order (A/B probe).
-    static const bool no_group = std::getenv("ST_FX_NOGROUP") != nullptr;
-    p->group = p->nv >= 6 && a.D >= 2 && !no_group;
-    auto k = fx_kernel(p->nv, p->group);
-    FCS_CUDA_TRY(set_max_dynamic_smem(k, di));
-    FCS_CUDA_TRY(set_max_dynamic_smem(fx_kernel(p->nv, p->group, true), di));
-    if (fx32s_ok)  // an unaligned tensor on this plan takes the scalar-load kernel
-      FCS_CUDA_TRY(set_max_dynamic_smem(
-          fx32s_kernel(fx_seg_nv(a.dims[0]), fx_seg_full(a.dims[0])), di));
-    FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
-                                                               p->smem_bytes));
-  } else {
-    p->path = Path::Smem;
-    auto k = fcs_dense_smem_kernel<Tin, Tacc>;
-    FCS_CUDA_TRY(set_max_dynamic_smem(k, di));
-    p->threads = p->smem_bytes > di.smem_optin / 2 ? 1024 : 512;
     FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
                                                                p->smem_bytes));
   }
+  if (p->rparts == 1) {
+    p->nv = sizeof(Tin) == 4 ? fx_nv(a) : 0;
+    // the fixed-point kernels also hold fx_scale_device's static scratch
+    auto fits = [&](auto k) {
+      cudaFuncAttributes at{};
+      return cudaFuncGetAttributes(&at, k) == cudaSuccess &&
+             p->smem_bytes + at.sharedSizeBytes <= di.smem_optin;
+    };
+    if (p->nv && !fits(fx_kernel(p->nv, false))) p->nv = 0;
+    static const bool no_fx64 = std::getenv("ST_FX64_OFF") != nullptr;  // A/B probe
+    // Below ~8M element-updates the call is launch/latency-bound and the CAS
+    // kernel's two launches beat the fixed point's three (c1 100^3 D=1: 27.6 vs
+    // 33.8 us; c5 operands: 37 vs 42 us); above it the fixed point wins (c3
+    // build 200^3 D=10: 200 vs 292 us; 1024^3 J=8192 D=1: 1.44 vs 3.43 ms).
+    const bool fx64_pays = static_cast<double>(a.fibers) * a.dims[0] * a.D >= 8.0e6;
+    // fp32 shapes the float4 kernel does not take (I_0 % 4 != 0), I_0 <= 1024:
+    // the same int32 fixed point with scalar loads
+    const bool fx32s_ok = sizeof(Tin) == 4 && a.order >= 2 && a.dims[0] <= kFxSegMaxI0 &&
+                          fits(fx32s_kernel(fx_seg_nv(a.dims[0]), false));
+    if (sizeof(Tin) == 4 && !p->nv && fx32s_ok && fx64_pays) {
+      p->path = Path::Fx32S;
+      p->nv = fx_seg_nv(a.dims[0]);
+      p->threads = 512;
+      auto k = fx32s_kernel(p->nv, fx_seg_full(a.dims[0]));
+      FCS_CUDA_TRY(set_max_dynamic_smem(k, di));
+      FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
+                                                                 p->smem_bytes));
+    } else if (sizeof(Tin) == 8 && a.order >= 2 && a.dims[0] <= kFxSegMaxI0 && !no_fx64 &&
+               fx64_pays && fits(fx64_kernel<Tin>(fx_seg_nv(a.dims[0]), false))) {
+      // fp64: 64-bit fixed point, 8 bytes per bucket
+      p->path = Path::Fx64;
+      p->nv = fx_seg_nv(a.dims[0]);
+      p->threads = 512;
+      const bool full = fx_seg_full(a.dims[0]);
+      auto k = fx64_kernel<Tin>(p->nv, full);
+      FCS_CUDA_TRY(set_max_dynamic_smem(k, di));
+      FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
+                                                                 p->smem_bytes));
+    } else if (p->nv) {
+      p->path = Path::Fx;
+      p->threads = fx_threads(p->nv);
+      // the bank-aware order pays off when atomics bind: with the searched
+      // groups, config-4 geometry D = 2: 1.333 -> 1.155 ms, D = 4: -4 %; with one
+      // family the kernel is load-bound (D = 1: 0.722 vs 0.725 ms) and keeps
+      // the immediate-offset loads.
+      // ST_FX_NOGROUP=1 keeps the identity order (A/B probe).
+      static const bool no_group = std::getenv("ST_FX_NOGROUP") != nullptr;
+      p->group = p->nv >= 6 && a.D >= 2 && !no_group;
+      auto k = fx_kernel(p->nv, p->group);
+      FCS_CUDA_TRY(set_max_dynamic_smem(k, di));
+      FCS_CUDA_TRY(set_max_dynamic_smem(fx_kernel(p->nv, p->group, true), di));
+      if (fx32s_ok)  // an unaligned tensor on this plan takes the scalar-load kernel
+        FCS_CUDA_TRY(set_max_dynamic_smem(
+            fx32s_kernel(fx_seg_nv(a.dims[0]), fx_seg_full(a.dims[0])), di));
+      FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
+                                                                 p->smem_bytes));
+    } else {
+      p->path = Path::Smem;
+      auto k = fcs_dense_smem_kernel<Tin, Tacc>;
+      FCS_CUDA_TRY(set_max_dynamic_smem(k, di));
+      p->threads = p->smem_bytes > di.smem_optin / 2 ? 1024 : 512;
+      FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
+                                                                 p->smem_bytes));
+    }
+  }  // rparts == 1
   per_sm = std::max(per_sm, 1);
   const uint64_t resident = static_cast<uint64_t>(per_sm) * di.sm_count;
-  uint64_t nchunk = std::max<uint64_t>(1, resident / static_cast<uint64_t>(a.D));
+  uint64_t nchunk = std::max<uint64_t>(1, resident / (static_cast<uint64_t>(a.D) * p->rparts));
   // fixed point: at least ~4 fibers per warp of a 512-thread CTA (per-CTA
   // fixed costs — zeroing, writing the partial — dominate smaller shares);
   // the atomic kernel keeps 16 fibers per chunk (c1: 333 chunks, 22 us)
@@ -1458,9 +1518,11 @@ int make_plan_uncached(const DenseArgs& a, Plan* p) {
   const uint64_t one_wave = (static_cast<uint64_t>(di.sm_count) + a.D - 1) / a.D;
   nchunk = std::min<uint64_t>(nchunk, std::max(by_bytes, one_wave));
   p->nchunk = nchunk;
-  p->part_bytes = nchunk * a.D * static_cast<size_t>(a.jt) *
-                  (p->path == Path::Fx64 ? 8 : sizeof(Tacc));  // Fx32S: int32 like Fx
-  p->ws = align_up(p->part_bytes) + align_up(nchunk * a.D * sizeof(int)) +
+  p->part_bytes = p->rparts > 1
+                      ? nchunk * a.D * p->rparts * static_cast<size_t>(p->rspan) * 8
+                      : nchunk * a.D * static_cast<size_t>(a.jt) *
+                            (p->path == Path::Fx64 ? 8 : sizeof(Tacc));  // Fx32S: int32 like Fx
+  p->ws = align_up(p->part_bytes) + align_up(nchunk * a.D * p->rparts * sizeof(int)) +
           align_up(sizeof(FxStats)) + align_up(static_cast<size_t>(a.D) * 32) +
           align_up(kFxMaxSample * sizeof(FxPart)) +
           align_up(static_cast<size_t>(a.D) * a.jt * sizeof(double));  // fp32: divert
@@ -1541,13 +1603,13 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
     auto* part = reinterpret_cast<int32_t*>(base);
     auto* flags = reinterpret_cast<int*>(base + align_up(p.part_bytes));
     auto* stats = reinterpret_cast<FxStats*>(base + align_up(p.part_bytes) +
-                                             align_up(p.nchunk * a.D * sizeof(int)));
+                                             align_up(p.nchunk * a.D * p.rparts * sizeof(int)));
     auto* parts = reinterpret_cast<FxPart*>(base + align_up(p.part_bytes) +
-                                            align_up(p.nchunk * a.D * sizeof(int)) +
+                                            align_up(p.nchunk * a.D * p.rparts * sizeof(int)) +
                                             align_up(sizeof(FxStats)) +
                                             align_up(static_cast<size_t>(a.D) * 32));
     auto* divert = reinterpret_cast<double*>(
-        base + align_up(p.part_bytes) + align_up(p.nchunk * a.D * sizeof(int)) +
+        base + align_up(p.part_bytes) + align_up(p.nchunk * a.D * p.rparts * sizeof(int)) +
         align_up(sizeof(FxStats)) + align_up(static_cast<size_t>(a.D) * 32) +
         align_up(kFxMaxSample * sizeof(FxPart)));
     const uint64_t nsample = fx_nsample(a.fibers);
@@ -1574,9 +1636,9 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
     auto* part = reinterpret_cast<int32_t*>(base);
     auto* flags = reinterpret_cast<int*>(base + align_up(p.part_bytes));
     auto* stats = reinterpret_cast<FxStats*>(base + align_up(p.part_bytes) +
-                                             align_up(p.nchunk * a.D * sizeof(int)));
+                                             align_up(p.nchunk * a.D * p.rparts * sizeof(int)));
     auto* parts = reinterpret_cast<FxPart*>(base + align_up(p.part_bytes) +
-                                            align_up(p.nchunk * a.D * sizeof(int)) +
+                                            align_up(p.nchunk * a.D * p.rparts * sizeof(int)) +
                                             align_up(sizeof(FxStats)) +
                                             align_up(static_cast<size_t>(a.D) * 32));
     const uint64_t nsample = fx_nsample(a.fibers);
@@ -1593,7 +1655,7 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
     const int nv_full = p.nv >= 6 ? 1 << (p.nv - 5) : 0;
     if (p.group) {
       groups = reinterpret_cast<uint8_t*>(base + align_up(p.part_bytes) +
-                                          align_up(p.nchunk * a.D * sizeof(int)) +
+                                          align_up(p.nchunk * a.D * p.rparts * sizeof(int)) +
                                           align_up(sizeof(FxStats)));
       FxGroupEntry* cache = nullptr;
       if (int rc = fx_group_cache(&cache)) return rc;
@@ -1604,7 +1666,7 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
       FCS_CUDA_TRY(cudaGetLastError());
     }
     auto* divert = reinterpret_cast<double*>(
-        base + align_up(p.part_bytes) + align_up(p.nchunk * a.D * sizeof(int)) +
+        base + align_up(p.part_bytes) + align_up(p.nchunk * a.D * p.rparts * sizeof(int)) +
         align_up(sizeof(FxStats)) + align_up(static_cast<size_t>(a.D) * 32) +
         align_up(kFxMaxSample * sizeof(FxPart)));
     FCS_CUDA_TRY(cudaMemsetAsync(divert, 0, out_elems * sizeof(double), st));
@@ -1626,9 +1688,9 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
     auto* part = reinterpret_cast<uint32_t*>(base);
     auto* flags = reinterpret_cast<int*>(base + align_up(p.part_bytes));
     auto* stats = reinterpret_cast<FxStats*>(base + align_up(p.part_bytes) +
-                                             align_up(p.nchunk * a.D * sizeof(int)));
+                                             align_up(p.nchunk * a.D * p.rparts * sizeof(int)));
     auto* parts = reinterpret_cast<FxPart*>(base + align_up(p.part_bytes) +
-                                            align_up(p.nchunk * a.D * sizeof(int)) +
+                                            align_up(p.nchunk * a.D * p.rparts * sizeof(int)) +
                                             align_up(sizeof(FxStats)) +
                                             align_up(static_cast<size_t>(a.D) * 32));
     const uint64_t nsample = fx_nsample(a.fibers);
@@ -1640,12 +1702,14 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
     FCS_CUDA_TRY(cudaGetLastError());
     fx_scale_kernel<<<1, 512, 0, st>>>(sc, kFx64);
     FCS_CUDA_TRY(cudaGetLastError());
-    fx64_kernel<Tin>(p.nv, full)<<<static_cast<unsigned>(nchunk * a.D), p.threads, p.smem_bytes,
-                                   st>>>(a, t, packed, stats, part, flags);
+    a.rparts = p.rparts;
+    a.rspan = p.rparts > 1 ? p.rspan : a.jt;
+    fx64_kernel<Tin>(p.nv, full, p.rparts > 1)<<<static_cast<unsigned>(nchunk * a.D * p.rparts),
+                                                 p.threads, p.smem_bytes, st>>>(a, t, packed,
+                                                                                stats, part, flags);
     FCS_CUDA_TRY(cudaGetLastError());
-    reduce_fx64_kernel<<<ceil_div(out_elems, 32), dim3(32, 32), 0, st>>>(part, flags, nchunk, a.D,
-                                                                        a.jt, stats, out,
-                                                                        accumulate);
+    reduce_fx64_kernel<<<ceil_div(out_elems, 32), dim3(32, 32), 0, st>>>(
+        part, flags, nchunk, a.D, a.jt, a.rparts, a.rspan, stats, out, accumulate);
     FCS_CUDA_TRY(cudaGetLastError());
     return ST_OK;
   }
@@ -1688,11 +1752,11 @@ int dense_fx_report(int dtype, size_t order, const size_t* dims, size_t last_cou
   a.fibers_per_chunk = (a.fibers + p.nchunk - 1) / p.nchunk;
   const uint64_t nchunk = (a.fibers + a.fibers_per_chunk - 1) / a.fibers_per_chunk;
   const char* base = static_cast<const char*>(ws);
-  std::vector<int> flags(nchunk * a.D);
+  std::vector<int> flags(nchunk * a.D * p.rparts);
   FCS_CUDA_TRY(cudaMemcpy(flags.data(), base + align_up(p.part_bytes), flags.size() * sizeof(int),
                           cudaMemcpyDeviceToHost));
   FxStats stats;
-  FCS_CUDA_TRY(cudaMemcpy(&stats, base + align_up(p.part_bytes) + align_up(p.nchunk * a.D * sizeof(int)),
+  FCS_CUDA_TRY(cudaMemcpy(&stats, base + align_up(p.part_bytes) + align_up(p.nchunk * a.D * p.rparts * sizeof(int)),
                           sizeof(FxStats), cudaMemcpyDeviceToHost));
   *S = stats.S;
   *ctas = flags.size();

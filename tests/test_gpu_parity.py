@@ -847,6 +847,24 @@ def test_dense_f64_fixed_point_long_fibers(cuda, shape, J, D):
     rel_close(got, want, RTOL64)
 
 
+@pytest.mark.parametrize("shape,J,D", [((256, 200, 200), 10000, 1),   # J~ = 29,998: 2 ranges
+                                       ((300, 150, 190), 20000, 2),   # J~ = 59,998: 3 ranges
+                                       ((2048, 80, 64), 12000, 1)])   # ranges x segments
+def test_dense_f64_fixed_point_bucket_ranges(cuda, shape, J, D):
+    """fp64 with J~ beyond shared memory: the fixed point over R bucket
+    ranges, one CTA per (chunk, family, range) (formerly fp64 global
+    atomics). Integer data bit-exact, Gaussian data at the fp64 rule, and an
+    outlier that sends one range's CTA to its fp64-atomic redo."""
+    rng = np.random.default_rng(sum(shape) + J)
+    x = rng.integers(-1000, 1001, size=shape).astype(np.float64)
+    got, want = _f64_case(x, J, D)
+    assert np.array_equal(got, want)
+    x = rng.standard_normal(shape)
+    x[5, 7, 9] = 4.0e22
+    got, want = _f64_case(x, J, D)
+    rel_close(got, want, RTOL64)
+
+
 @pytest.mark.parametrize("shape", [(2048, 64, 66), (1100, 90, 90), (3001, 50, 60)])
 def test_dense_f32_fixed_point_long_fibers(cuda, shape):
     """fp32 with I_0 > 1024 (formerly fp32 shared atomics): the scalar-load

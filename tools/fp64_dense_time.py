@@ -63,6 +63,11 @@ def run(dims, J, D, seed=1, reps=10):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "wide":  # J~ beyond shared memory (8-byte buckets)
+        print(json.dumps({"wide_J16384_D1": run((1024, 1024, 512), 16384, 1, seed=9, reps=5),
+                          "wide_J16384_D4": run((1024, 1024, 512), 16384, 4, seed=9, reps=3),
+                          "wide_J12000_D1": run((1024, 1024, 512), 12000, 1, seed=9, reps=5)}))
+        sys.exit(0)
     res = {"fx64": os.environ.get("ST_FX64_OFF") is None,
            "c1": run((100, 100, 100), 1000, 1),
            "c3_build": run((200, 200, 200), 3000, 10, seed=3),
