@@ -158,6 +158,14 @@ int host_ctx(HostCtx** out) {
   if (dev < 0 || dev >= 64) return fail(ST_ECUDA, "device index out of range");
   std::lock_guard<std::mutex> lock(mu);
   if (!ctx[dev]) {
+    // The side stream of fork_side is created before these two: created
+    // after them it measured slower concurrency (config 3's split step 41 ->
+    // 54 us after one host-buffer call), created first it does not.
+    {
+      std::lock_guard<std::mutex> side_lock(g_side_mu);
+      SideStream* side = nullptr;
+      FCS_CUDA_TRY(side_of(&side));
+    }
     auto* c = new HostCtx();
     FCS_CUDA_TRY(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
     FCS_CUDA_TRY(cudaStreamCreateWithFlags(&c->comp, cudaStreamNonBlocking));

@@ -18,3 +18,13 @@ for med in (0, 1, 0):
     for _ in range(100): call(med)
     b.record(); torch.cuda.synchronize()
     print("median", med, "us per call", a.elapsed_time(b) * 10)
+z = torch.zeros(1, device="cuda")
+for _ in range(5): call(0); z.add_(1)
+torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
+for _ in range(100):
+    call(0)
+    z.add_(1)
+b.record(); torch.cuda.synchronize()
+print("median 0 + tiny kernel: us per call", a.elapsed_time(b) * 10)
