@@ -112,10 +112,16 @@ size_t st_fcs_dense_workspace(int dtype, size_t order, const size_t* dims, size_
  * non-finite redoes its chunk in fixed point with those elements diverted to
  * an exact fp64 reduction; a partial reaching 2^30, or partials that all stay
  * below 2^16, make it redo the chunk with fp32 shared-memory atomics
- * (order-dependent rounding). Other fp32 shapes accumulate in fp32 atomics.
- * ST_F64 with I_0 <= 1024 and >= 8M element-updates accumulates in 64-bit
+ * (order-dependent rounding). Other fp32 shapes with I_0 <= 16384 and >= 8M
+ * element-updates take the same int32 fixed point with scalar loads (fibers
+ * longer than 1024 split into warp segments; a flagged CTA redoes its chunk
+ * with fp32 atomics); the rest accumulate in atomics.
+ * ST_F64 with I_0 <= 16384 and >= 8M element-updates accumulates in 64-bit
  * fixed point (two int32 atomics per element, exact carries; partials summed
- * exactly in 128-bit integers; deterministic), smaller calls in fp64 atomics.
+ * exactly in 128-bit integers; deterministic; a sketch wider than shared
+ * memory is split into bucket ranges, one CTA each; a CTA that meets an
+ * element out of range redoes its chunk with fp64 atomics), smaller calls in
+ * fp64 atomics.
  * Partials are reduced in a fixed order. accumulate != 0 adds to out instead
  * of overwriting it.
  * Replaces fcs_sketch(const DenseTensor&, const HashFamily&), sketch.cpp:187-201
