@@ -1059,3 +1059,35 @@ def test_rtpm_cluster_tail_vs_oracle(cuda):
     wz, fz = O.rtpm(O.FcsEngine(z, 2500, 3, 5), 12, 2, 3, 4, 5)
     np.testing.assert_array_equal(cpz.weights.cpu().numpy(), wz)
     np.testing.assert_array_equal(cpz._factors_cm[0].t().cpu().numpy(), fz)
+
+
+def test_cluster_estimator_edges_vs_oracle(cuda):
+    """Cluster estimator edges: a free mode longer than the early-gather
+    registers (nf = 300 > 256), D = 17 (the fused median's general branch),
+    the TS engine (the FCS kernels on the J-periodic extension, J = 2500 ->
+    M = 8192), a NaN in a vector (non-finite median branch) and zero vectors."""
+    rng = np.random.default_rng(53)
+    dims = (300, 22, 18)
+    t = rng.standard_normal(dims)
+    J = 2500
+    eng = st.FcsEngine(st.DenseTensor.from_array(t), st.EstimatorConfig(J, 17, 4))
+    oeng = O.FcsEngine(t, J, 17, 4)
+    A = rng.standard_normal((2, dims[1]))
+    B = rng.standard_normal((2, dims[2]))
+    got = eng.iuv_batch(A, B, 0).cpu().numpy()
+    for b in range(2):
+        rel_close(got[b], oeng.iuv(A[b], B[b], 0), RTOL64)
+    A[1, 3] = np.nan
+    got = eng.iuv_batch(A, B, 0).cpu().numpy()
+    want = oeng.iuv(A[1], B[1], 0)
+    assert (np.isnan(got[1]) == np.isnan(want)).all()
+    rel_close(got[0], oeng.iuv(A[0], B[0], 0), RTOL64)
+    z = eng.iuv_batch(np.zeros((1, dims[1])), np.zeros((1, dims[2])), 0).cpu().numpy()
+    assert np.array_equal(z, np.zeros((1, dims[0])))
+    ts = st.TsEngine(st.DenseTensor.from_array(t), st.EstimatorConfig(J, 5, 6))
+    ots = O.TsEngine(t, J, 5, 6)
+    for f in range(3):
+        c1 = 1 if f == 0 else 0
+        c2 = 1 if f == 2 else 2
+        a, b = rng.standard_normal(dims[c1]), rng.standard_normal(dims[c2])
+        rel_close(ts.iuv(a, b, f), ots.iuv(a, b, f), 1e-9)
