@@ -1418,7 +1418,8 @@ int make_plan_uncached(const DenseArgs& a, Plan* p) {
     // J~ = 49,150, D = 1: 4.45 ms with global atomics)
     const size_t avail = di.smem_optin - 4096;  // static shared memory + the 32 dummy buckets
     const uint32_t R = static_cast<uint32_t>((static_cast<size_t>(a.jt) * 8 + avail - 1) / avail);
-    if (!fx64_shape || R > 8) {
+    // (the lane-owned mode-0 buckets are packed in 16 bits: J~ < 2^16 bounds them)
+    if (!fx64_shape || R > 8 || a.jt >= 65536u) {
       p->path = Path::Global;
       p->ws = 0;
       return ST_OK;

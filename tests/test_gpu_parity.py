@@ -849,7 +849,8 @@ def test_dense_f64_fixed_point_long_fibers(cuda, shape, J, D):
 
 @pytest.mark.parametrize("shape,J,D", [((256, 200, 200), 10000, 1),   # J~ = 29,998: 2 ranges
                                        ((300, 150, 190), 20000, 2),   # J~ = 59,998: 3 ranges
-                                       ((2048, 80, 64), 12000, 1)])   # ranges x segments
+                                       ((2048, 80, 64), 12000, 1),    # ranges x segments
+                                       ((64, 200, 700), 22000, 1)])   # J~ = 65,998 >= 2^16: global
 def test_dense_f64_fixed_point_bucket_ranges(cuda, shape, J, D):
     """fp64 with J~ beyond shared memory: the fixed point over R bucket
     ranges, one CTA per (chunk, family, range) (formerly fp64 global
