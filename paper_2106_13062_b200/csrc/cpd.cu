@@ -7,6 +7,7 @@
 // Restarts (rtpm, rtpm_asym) and MTTKRP columns (als) are batched into one
 // engine call each; the control flow, the initial-vector stream and the argmax
 // rule follow the reference so that the same estimates yield the same result.
+#include <math_constants.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -303,21 +304,74 @@ struct EngineGuard {
 };
 
 // rtpm (cpd.cpp:234-277) on an engine.
+// Device-side steps of rtpm between the engine calls, so a whole run needs
+// one host synchronisation (the reference's control flow, cpd.cpp:234-277):
+// the restart argmax with strict > (first wins, NaN never wins) copying the
+// winner to best, and the component's bookkeeping.
+__global__ void rtpm_argmax_kernel(const double* __restrict__ vals, int L,
+                                   const double* __restrict__ U, int dim,
+                                   double* __restrict__ best, int* __restrict__ bad) {
+  __shared__ int arg;
+  if (threadIdx.x == 0) {
+    double bv = -CUDART_INF;
+    int a = -1;
+    for (int l = 0; l < L; ++l)
+      if (vals[l] > bv) {
+        bv = vals[l];
+        a = l;
+      }
+    if (a < 0) *bad = 1;  // no finite candidate: reported after the run
+    arg = a < 0 ? 0 : a;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < dim; i += blockDim.x) best[i] = U[static_cast<size_t>(arg) * dim + i];
+}
+
+// weight = the refined contraction value: weights[r], factor column r, and
+// the weighted vector the deflation subtracts (weight u o u o u =
+// u o u o (weight u): linear in the last factor).
+__global__ void rtpm_component_kernel(const double* __restrict__ val,
+                                      const double* __restrict__ best, int dim,
+                                      double* __restrict__ weight_out,
+                                      double* __restrict__ factor_out,
+                                      double* __restrict__ wbest) {
+  const double w = *val;
+  if (threadIdx.x == 0) *weight_out = w;
+  for (int i = threadIdx.x; i < dim; i += blockDim.x) {
+    factor_out[i] = best[i];
+    wbest[i] = w * best[i];
+  }
+}
+
 int rtpm_on(st_engine* e, size_t dim, size_t rank, size_t L, size_t num_iters, uint64_t seed,
             double* weights, double* factor, cudaStream_t st) {
-  if (int rc = e->vec.ensure((2 * L + 2) * dim * sizeof(double) + (L + 1) * sizeof(double) + 16, st))
-    return rc;
-  double* U = static_cast<double*>(e->vec.p);
-  double* Y = U + L * dim;
-  double* best = Y + L * dim;
+  // device: the R x L initial vectors, two L x dim iterate buffers, best /
+  // next / weighted best, values, R weights, R x dim factors, flags
+  const size_t need = (rank * L + 2 * L + 3) * dim * sizeof(double) +
+                      (L + 1 + rank) * sizeof(double) + rank * dim * sizeof(double) + 16;
+  if (int rc = e->vec.ensure(need, st)) return rc;
+  double* U0 = static_cast<double*>(e->vec.p);
+  double* Ubuf = U0 + rank * L * dim;
+  double* Ybuf = Ubuf + L * dim;
+  double* best = Ybuf + L * dim;
   double* next = best + dim;
-  double* vals = next + dim;
-  int* stopped = reinterpret_cast<int*>(vals + L + 1);
-  std::vector<double> hU(L * dim), hvals(L);
+  double* wbest = next + dim;
+  double* vals = wbest + dim;
+  double* wdev = vals + L + 1;
+  double* fdev = wdev + rank;
+  int* flags = reinterpret_cast<int*>(fdev + rank * dim);  // [0] stopped, [1] no finite candidate
+  // every component's initial vectors up front, in the reference's draw order
+  std::vector<double> hU(rank * L * dim);
   HostRng rng(splitmix_draw(seed ^ 0x7274706dULL, 1));  // init_rng (cpd.cpp:245)
+  for (size_t i = 0; i < rank * L; ++i) rng.unit(hU.data() + i * dim, dim);
+  FCS_CUDA_TRY(cudaMemcpyAsync(U0, hU.data(), hU.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  FCS_CUDA_TRY(cudaMemsetAsync(flags, 0, 2 * sizeof(int), st));
+  const int tpb = 256;
   for (size_t r = 0; r < rank; ++r) {
-    for (size_t l = 0; l < L; ++l) rng.unit(hU.data() + l * dim, dim);
-    FCS_CUDA_TRY(cudaMemcpyAsync(U, hU.data(), L * dim * sizeof(double), cudaMemcpyHostToDevice, st));
+    double* U = Ubuf;
+    double* Y = Ybuf;
+    FCS_CUDA_TRY(cudaMemcpyAsync(U, U0 + r * L * dim, L * dim * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, st));
     // L restarts advance in lockstep; a row whose norm underflows stays zero,
     // exactly like the reference's early break (iuu(0) = 0).
     for (size_t it = 0; it < num_iters; ++it) {
@@ -343,38 +397,32 @@ int rtpm_on(st_engine* e, size_t dim, size_t rank, size_t L, size_t num_iters, u
       std::swap(U, Y);
     }
     if (int rc = st_engine_uvw(e, L, U, U, U, vals, 1, st)) return rc;
-    FCS_CUDA_TRY(cudaMemcpyAsync(hvals.data(), vals, L * sizeof(double), cudaMemcpyDeviceToHost, st));
-    FCS_CUDA_TRY(cudaStreamSynchronize(st));
-    double best_value = -std::numeric_limits<double>::infinity();
-    long arg = -1;
-    for (size_t l = 0; l < L; ++l) {
-      if (hvals[l] > best_value) {  // strict >, first wins (cpd.cpp:260)
-        best_value = hvals[l];
-        arg = static_cast<long>(l);
-      }
-    }
-    if (arg < 0) return fail(ST_ENUMERIC, "rtpm: no candidate with a finite contraction value");
-    FCS_CUDA_TRY(cudaMemcpyAsync(best, U + arg * dim, dim * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    FCS_CUDA_TRY(cudaMemsetAsync(stopped, 0, sizeof(int), st));
+    rtpm_argmax_kernel<<<1, tpb, 0, st>>>(vals, static_cast<int>(L), U, static_cast<int>(dim), best,
+                                          flags + 1);
+    FCS_CUDA_TRY(cudaGetLastError());
+    FCS_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int), st));
     for (size_t it = 0; it < num_iters; ++it) {  // refinement (cpd.cpp:266-270)
-      const int rc = engine_iuv_fused(e, 1, best, 0, 3, next, best, stopped, st);
+      const int rc = engine_iuv_fused(e, 1, best, 0, 3, next, best, flags, st);
       if (rc == 1) {
         if (int rc2 = st_engine_iuv(e, 1, best, best, 0, next, 1, st)) return rc2;
-        if (int rc2 = launch_refine_update(best, next, static_cast<int>(dim), stopped, st))
+        if (int rc2 = launch_refine_update(best, next, static_cast<int>(dim), flags, st))
           return rc2;
       } else if (rc) {
         return rc;
       }
     }
     if (int rc = st_engine_uvw(e, 1, best, best, best, vals, 1, st)) return rc;
-    double weight = 0.0;
-    FCS_CUDA_TRY(cudaMemcpyAsync(&weight, vals, sizeof(double), cudaMemcpyDeviceToHost, st));
-    FCS_CUDA_TRY(cudaMemcpyAsync(factor + r * dim, best, dim * sizeof(double), cudaMemcpyDeviceToHost, st));
-    FCS_CUDA_TRY(cudaStreamSynchronize(st));
-    weights[r] = weight;
-    if (int rc = st_engine_deflate(e, weight, best, best, best, st)) return rc;
+    rtpm_component_kernel<<<1, tpb, 0, st>>>(vals, best, static_cast<int>(dim), wdev + r,
+                                             fdev + r * dim, wbest);
+    FCS_CUDA_TRY(cudaGetLastError());
+    if (int rc = st_engine_deflate(e, 1.0, best, best, wbest, st)) return rc;
   }
+  int bad = 0;
+  FCS_CUDA_TRY(cudaMemcpyAsync(weights, wdev, rank * sizeof(double), cudaMemcpyDeviceToHost, st));
+  FCS_CUDA_TRY(cudaMemcpyAsync(factor, fdev, rank * dim * sizeof(double), cudaMemcpyDeviceToHost, st));
+  FCS_CUDA_TRY(cudaMemcpyAsync(&bad, flags + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
   FCS_CUDA_TRY(cudaStreamSynchronize(st));
+  if (bad) return fail(ST_ENUMERIC, "rtpm: no candidate with a finite contraction value");
   return ST_OK;
 }
 
