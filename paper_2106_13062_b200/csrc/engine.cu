@@ -40,7 +40,8 @@ using namespace fcs;
 
 namespace fcs {
 static int iuv_fused_ab(st_engine* e, size_t batch, const double* a, const double* b, size_t free_mode,
-                 int mode, double* out, double* best, int* stopped, cudaStream_t st) {
+                 int mode, double* out, double* best, int* stopped, cudaStream_t st,
+                 const double* wvec = nullptr) {
   if (is_exact(e) || e->plan.large_p1 || batch == 0) return 1;
   int c1, c2;
   contracted(free_mode, &c1, &c2);
@@ -55,6 +56,7 @@ static int iuv_fused_ab(st_engine* e, size_t batch, const double* a, const doubl
   t.out = out;
   t.best = best;
   t.stopped = stopped;
+  t.wvec = wvec;
   return launch_iuv_cluster(e->plan, e->args(), static_cast<int>(batch), a, b, c1, c2,
                             static_cast<int>(free_mode), static_cast<double*>(e->est.p), t, st);
 }
@@ -515,6 +517,10 @@ int st_engine_uvw(st_engine* e, size_t batch, const double* u, const double* v, 
     if (int rc = exact_uvw(e, batch, u, v, w, est, st)) return rc;
     return med ? launch_median(est, static_cast<int>(batch), static_cast<int>(e->D), 1, out, st)
                : ST_OK;
+  }
+  if (median) {  // small batches: <w, T(u, v, I)> per family on the cluster estimator, median fused
+    const int rc = iuv_fused_ab(e, batch, u, v, 2, 4, out, nullptr, nullptr, st, w);
+    if (rc != 1) return rc;
   }
   if (int rc = e->scratch.ensure(batch * e->D * e->plan.P * sizeof(double2), st)) return rc;
   double* est = out;

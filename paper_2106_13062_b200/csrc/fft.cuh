@@ -633,11 +633,13 @@ struct EngArgs {
 // refinement update (cpd.cpp:266-270).
 struct IuvTail {
   int mode = 0;             // 0: estimates only; 1: median -> out; 2: median, row / ||row|| -> out;
-                            // 3: median -> out (scratch), best = out / ||out|| unless stopped
+                            // 3: median -> out (scratch), best = out / ||out|| unless stopped;
+                            // 4: T(u, v, w) = <w, T(u, v, I)> per family, median -> out[b]
   int* cnt = nullptr;       // batch arrival counters, zero between launches
   double* out = nullptr;    // batch x nf
   double* best = nullptr;   // mode 3
   int* stopped = nullptr;   // mode 3: sticky underflow flag
+  const double* wvec = nullptr;  // mode 4: batch x dims[2] third vectors
 };
 // Cluster (8-CTA, DSMEM) form of the iuv estimator for M in {8192, 9216} and
 // batches that fit one wave of clusters (spectral_cluster.cu); returns 1

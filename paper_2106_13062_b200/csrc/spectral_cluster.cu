@@ -417,9 +417,14 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
   }
   __syncthreads();
   fx.inverse(cl);
-  // gather: z[h] = u[h / 2] component h % 2, scaled 1 / P
+  // gather: z[h] = u[h / 2] component h % 2, scaled 1 / P. Tail mode 4
+  // (T(u, v, w)): instead of the estimates, their dot product with w — the
+  // family's T(u, v, w) by linearity — summed over the CTAs in a fixed order.
+  const bool dotw = tail.mode == 4;
   double* o = est + static_cast<size_t>(item) * nf;
+  const double* wv = dotw ? tail.wvec + static_cast<size_t>(bvec) * nf : nullptr;
   const double inv = 1.0 / P;
+  double dacc = 0.0;
 #pragma unroll
   for (int g = 0; g < kGather; ++g) {
     const int i = t0 + g * kClThreads;
@@ -428,14 +433,37 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
     const int h = static_cast<int>(t & 0x7fffffffu);
     if (!fx.owns(h)) continue;
     const double z = fx.zval(h) * inv;
-    o[i] = (t >> 31) ? -z : z;
+    if (dotw) dacc += wv[i] * ((t >> 31) ? -z : z);
+    else o[i] = (t >> 31) ? -z : z;
   }
   for (int i = t0 + kGather * kClThreads; i < nf; i += kClThreads) {  // nf > 256
     const uint32_t t = __ldg(tf + i);
     const int h = static_cast<int>(t & 0x7fffffffu);
     if (!fx.owns(h)) continue;
     const double z = fx.zval(h) * inv;
-    o[i] = (t >> 31) ? -z : z;
+    if (dotw) dacc += wv[i] * ((t >> 31) ? -z : z);
+    else o[i] = (t >> 31) ? -z : z;
+  }
+  if (dotw) {  // est[item] = sum over the CTAs (rank order) of the block sums
+    __shared__ double wred[kClThreads / 32];
+    __shared__ double wpart[kClC];
+#pragma unroll
+    for (int q = 16; q > 0; q >>= 1) dacc += __shfl_xor_sync(0xffffffffu, dacc, q);
+    if ((t0 & 31) == 0) wred[t0 >> 5] = dacc;
+    __syncthreads();
+    if (t0 == 0) {
+      double sblk = 0.0;
+#pragma unroll
+      for (int q = 0; q < kClThreads / 32; ++q) sblk += wred[q];
+      *cl.map_shared_rank(&wpart[r], 0) = sblk;
+    }
+    cl.sync();
+    if (r == 0 && t0 == 0) {
+      double sum = 0.0;
+#pragma unroll
+      for (int q = 0; q < kClC; ++q) sum += wpart[q];
+      est[item] = sum;
+    }
   }
   if (tail.mode != 0) {
     // The last of the D clusters of vector bvec (per-vector arrival counter)
@@ -456,15 +484,16 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
     if (!last) return;
     __threadfence();
     if (tail.mode == 3 && *reinterpret_cast<volatile int*>(tail.stopped)) return;
-    const double* col0 = est + static_cast<size_t>(bvec) * e.D * nf;
-    double* ob = tail.out + static_cast<size_t>(bvec) * nf;
+    const int nt = dotw ? 1 : nf;  // values per family: one contraction value, or the row
+    const double* col0 = est + static_cast<size_t>(bvec) * e.D * nt;
+    double* ob = tail.out + static_cast<size_t>(bvec) * nt;
     double acc = 0.0;
-    for (int i = r * kClThreads + t0; i < nf; i += kClC * kClThreads) {
-      const double m = median_col(col0 + i, e.D, nf, [](const double* p) { return __ldcg(p); });
+    for (int i = r * kClThreads + t0; i < nt; i += kClC * kClThreads) {
+      const double m = median_col(col0 + i, e.D, nt, [](const double* p) { return __ldcg(p); });
       ob[i] = m;
       acc += m * m;
     }
-    if (tail.mode == 1) return;
+    if (tail.mode == 1 || tail.mode == 4) return;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if ((t0 & 31) == 0) red[t0 >> 5] = acc;

@@ -1037,6 +1037,13 @@ def test_cluster_estimator_vs_oracle(cuda, dims, J, D, seed):
                 for d in (0, D - 1):
                     want = O.iuv_spectral(oeng.pres[d], A[b], B[b], f)
                     rel_close(per[b, d], want, RTOL64)
+    # T(u, v, w) as <w, T(u, v, I)> per family on the cluster estimator (median fused)
+    for n in (1, 4):
+        U, V, W = (rng.standard_normal((n, dims[m])) for m in range(3))
+        got = eng.uvw_batch(U, V, W).cpu().numpy()
+        for b in range(n):
+            want = oeng.uvw(U[b], V[b], W[b])
+            assert abs(got[b] - want) <= RTOL64 * 2 * abs(want) + 1e-300, (got[b], want)
 
 
 def test_rtpm_cluster_tail_vs_oracle(cuda):
