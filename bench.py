@@ -544,8 +544,8 @@ def secondary(x=None, cpu=True):
         torch.cuda.synchronize()
         return ev0.elapsed_time(ev1) / calls
     with ClockSampler(torch.cuda.current_device()) as clk3:
-        pipe_iuv = pipelined_ms(iuv_call, 400)
-        pipe_iuv1 = pipelined_ms(lambda: iuv_call(1), 1000)
+        pipe_iuv = pipelined_ms(iuv_call, 3000)  # >= 100 ms each: clock samples land inside
+        pipe_iuv1 = pipelined_ms(lambda: iuv_call(1), 6000)
     ms_uvw = median_ms(uvw_call, 20)
     ms_uvw1 = median_ms(lambda: uvw_call(1), 20)
     ms_defl = median_ms(lambda: L.check(lib.st_engine_deflate(
@@ -572,7 +572,7 @@ def secondary(x=None, cpu=True):
                             "median fused into the last cluster (spectral_cluster.cu)",
          "roofline_batch1": roofline_fp64(fft_flops(M3, 3 * c.sketch_count), ms_iuv1, fpeak, fkind),
          "pipelined_ms": {"iuv_step": pipe_iuv, "iuv_batch1": pipe_iuv1,
-                          "note": "400 / 1000 back-to-back calls on one stream (as inside rtpm)",
+                          "note": "3000 / 6000 back-to-back calls on one stream (as inside rtpm)",
                           "clocks": clk3.summary()},
          "uvw_step_ms": ms_uvw, "uvw_batch1_ms": ms_uvw1,
          "deflate_ms": ms_defl, "rtpm_total_s": t_rtpm, "rtpm_timing": "second call (warm), host wall",
