@@ -774,8 +774,14 @@ __device__ void fx_sample_warps(const DenseArgs& a, const Tin* __restrict__ t, u
 template <typename Tin>
 __global__ void __launch_bounds__(256) fx_sample_warps_kernel(DenseArgs a, const Tin* __restrict__ t,
                                                               uint64_t nsample,
-                                                              FxPart* __restrict__ parts) {
+                                                              FxPart* __restrict__ parts,
+                                                              double* __restrict__ zero = nullptr,
+                                                              uint64_t nzero = 0) {
   fx_sample_warps<Tin>(a, t, nsample, parts);
+  // the fp64 diversion buffer of the fp32 path, cleared here instead of by a memset
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < nzero;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    zero[i] = 0.0;
 }
 
 // Sampled fibers: an eighth of the tensor's fibers, at least 256, at most 2048.
@@ -1167,16 +1173,18 @@ __global__ void reduce_fx_kernel(const int32_t* __restrict__ part, const int* __
     return fl == 1 ? static_cast<double>(__int_as_float(w)) : static_cast<double>(w) * inv;
   };
   uint64_t c = 0;
-  for (; c + 4 <= nchunk; c += 4) {  // four partials in flight, summed in chunk order
-    int32_t w[4];
-    int fl[4];
+  constexpr int kU = 8;  // partials in flight, summed in chunk order (config 4: 37 chunks;
+                         // 12.3 -> 11.3 us vs 4; a 32 x 8 chunk-lane layout: 28 us)
+  for (; c + kU <= nchunk; c += kU) {
+    int32_t w[kU];
+    int fl[kU];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      w[u] = part[(c + u) * per + i];
-      fl[u] = flags[(c + u) * D + d];
+    for (int u = 0; u < kU; ++u) {
+      w[u] = __ldcs(part + (c + u) * per + i);
+      fl[u] = __ldg(flags + (c + u) * D + d);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) acc += term(w[u], fl[u]);
+    for (int u = 0; u < kU; ++u) acc += term(w[u], fl[u]);
   }
   for (; c < nchunk; ++c) acc += term(part[c * per + i], flags[c * D + d]);
   out[i] = acc + divert[i];
@@ -1644,8 +1652,14 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
                                             align_up(static_cast<size_t>(a.D) * 32));
     const uint64_t nsample = fx_nsample(a.fibers);
     const int nparts = static_cast<int>(nsample);  // one fiber per sample CTA
+    auto* divert = reinterpret_cast<double*>(
+        base + align_up(p.part_bytes) + align_up(p.nchunk * a.D * p.rparts * sizeof(int)) +
+        align_up(sizeof(FxStats)) + align_up(static_cast<size_t>(a.D) * 32) +
+        align_up(kFxMaxSample * sizeof(FxPart)));
+    // (programmatic dependent launch of the chain measured no gain: 2.29-2.36 vs
+    // 2.28-2.32 ms at config 4, tools/experiments/k1_pdl.txt)
     fx_sample_warps_kernel<float><<<ceil_div(nsample, 8), 256, 0, st>>>(
-        a, reinterpret_cast<const float*>(t), nsample, parts);
+        a, reinterpret_cast<const float*>(t), nsample, parts, divert, out_elems);
     FCS_CUDA_TRY(cudaGetLastError());
     const double per_cta = static_cast<double>(a.fibers_per_chunk) * a.dims[0];
     const FxScaleArgs sc{parts, nparts, 3.0 * per_cta / a.jt + 16.0, stats};
@@ -1666,18 +1680,13 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
                                             groups, cache);
       FCS_CUDA_TRY(cudaGetLastError());
     }
-    auto* divert = reinterpret_cast<double*>(
-        base + align_up(p.part_bytes) + align_up(p.nchunk * a.D * p.rparts * sizeof(int)) +
-        align_up(sizeof(FxStats)) + align_up(static_cast<size_t>(a.D) * 32) +
-        align_up(kFxMaxSample * sizeof(FxPart)));
-    FCS_CUDA_TRY(cudaMemsetAsync(divert, 0, out_elems * sizeof(double), st));
+    const float* tf = reinterpret_cast<const float*>(t);
     fx_kernel(p.nv, p.group)<<<static_cast<unsigned>(nchunk * a.D), p.threads, p.smem_bytes, st>>>(
-        a, reinterpret_cast<const float*>(t), packed, stats, part, flags, groups, divert);
+        a, tf, packed, stats, part, flags, groups, divert);
     FCS_CUDA_TRY(cudaGetLastError());
     // redo of the flagged chunks (unflagged CTAs exit at once)
     fx_kernel(p.nv, p.group, true)<<<static_cast<unsigned>(nchunk * a.D), p.threads, p.smem_bytes,
-                                     st>>>(a, reinterpret_cast<const float*>(t), packed, stats,
-                                           part, flags, groups, divert);
+                                     st>>>(a, tf, packed, stats, part, flags, groups, divert);
     FCS_CUDA_TRY(cudaGetLastError());
     reduce_fx_kernel<<<ceil_div(out_elems, 256), 256, 0, st>>>(part, flags, nchunk, a.D, a.jt,
                                                                stats, divert, out, accumulate);
