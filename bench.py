@@ -259,7 +259,9 @@ def run_gpu(args):
                          "algorithmic_bytes_per_launch": alg,
                          "kernel": "fcs_dense_fx_kernel<8> (+ fx_sample_warps, fx_group, reduce_fx)"},
             "e2e": e2e,
-            "gpu_launches": 4 * args.steps,  # sample, group lookup, fx scatter (+scale), reduce
+            # per step: fx_sample_warps, fx_scale, fx_group (cached lookup), the scatter
+            # fcs_dense_fx_kernel, its redo instantiation (exits unless flagged), reduce_fx
+            "gpu_launches": 6 * args.steps,
             "clocks": clk.summary(),
         }
     if world == 1 and not args.no_secondary:
