@@ -114,8 +114,9 @@ size_t st_fcs_dense_workspace(int dtype, size_t order, const size_t* dims, size_
  * below 2^16, make it redo the chunk with fp32 shared-memory atomics
  * (order-dependent rounding). Other fp32 shapes with I_0 <= 16384 and >= 8M
  * element-updates take the same int32 fixed point with scalar loads (fibers
- * longer than 1024 split into warp segments; a flagged CTA redoes its chunk
- * with fp32 atomics); the rest accumulate in atomics.
+ * longer than 1024 split into warp segments, sketches wider than shared
+ * memory into bucket ranges; a flagged CTA redoes its chunk or range with
+ * fp32 atomics); the rest accumulate in atomics.
  * ST_F64 with I_0 <= 16384 and >= 8M element-updates accumulates in 64-bit
  * fixed point (two int32 atomics per element, exact carries; partials summed
  * exactly in 128-bit integers; deterministic; a sketch wider than shared

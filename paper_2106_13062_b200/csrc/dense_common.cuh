@@ -30,6 +30,7 @@ struct DenseArgs {
   // one CTA per (chunk, family, range)
   uint32_t rparts;
   uint32_t rspan;
+  uint32_t j0;  // mode-0 hash length (the lane-owned kernels pack mode-0 buckets in 16 bits)
 };
 
 // A sparse (COO) sketch launch (fcs_coo.cu).

@@ -492,7 +492,8 @@ __device__ __forceinline__ void fiber_offset_fast(const DenseArgs& a, const uint
 // int32 fixed-point shared-memory accumulation with exact overflow detection.
 __device__ void fx_float_redo(const DenseArgs& a, const float* __restrict__ t,
                               const uint32_t* __restrict__ tab, float scale, uint64_t chunk,
-                              bool skip_diverted, float* skf);
+                              bool skip_diverted, float* skf, uint32_t r_lo = 0,
+                              uint32_t r_cnt = 0xffffffffu);
 
 // kRedo = false: the scatter; kRedo = true: the same loop over the chunks the
 // scatter flagged (flag 2: an element out of the fixed-point range), each
@@ -682,15 +683,18 @@ __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
 // fp32 shared-atomic redo of one chunk into skf (the CTA's sketch memory);
 // skip_diverted: leave out the elements the fixed-point redo diverted (out of
 // range at this scale) — they are already in `divert`.
+// r_lo / r_cnt: only buckets [r_lo, r_lo + r_cnt) (a bucket-range CTA; skf
+// holds that range); the defaults take every bucket.
 __device__ void fx_float_redo(const DenseArgs& a, const float* __restrict__ t,
                               const uint32_t* __restrict__ tab, float scale, uint64_t chunk,
-                              bool skip_diverted, float* skf) {
+                              bool skip_diverted, float* skf, uint32_t r_lo, uint32_t r_cnt) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const uint64_t f_begin = chunk * a.fibers_per_chunk;
   const uint64_t f_end = min(a.fibers, f_begin + a.fibers_per_chunk);
   const uint32_t i0n = a.dims[0];
+  r_cnt = min(r_cnt, a.jt);
   __syncthreads();
-  for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) skf[b] = 0.f;
+  for (uint32_t b = threadIdx.x; b < r_cnt; b += blockDim.x) skf[b] = 0.f;
   __syncthreads();
   for (uint64_t g = f_begin + warp; g < f_end; g += nwarps) {
     uint32_t c, sbit;
@@ -703,8 +707,9 @@ __device__ void fx_float_redo(const DenseArgs& a, const float* __restrict__ t,
         const float xs = __uint_as_float(__float_as_uint(x) ^ (e & 0x80000000u));
         if ((__float_as_uint(fmaf(xs, scale_f, 12582912.0f)) ^ 0x4B000000u) >> 23) continue;
       }
-      atomicAdd(&skf[(e & 0x7fffffffu) + c],
-                __uint_as_float(__float_as_uint(x) ^ ((e ^ sbit) & 0x80000000u)));
+      const uint32_t lb = (e & 0x7fffffffu) + c - r_lo;
+      if (lb < r_cnt)
+        atomicAdd(&skf[lb], __uint_as_float(__float_as_uint(x) ^ ((e ^ sbit) & 0x80000000u)));
     }
   }
   __syncthreads();
@@ -968,7 +973,9 @@ __global__ void __launch_bounds__(512) fcs_dense_fx64_kernel(DenseArgs a,
 // A flagged chunk (range, wrap or tiny partials) is redone with fp32 shared
 // atomics. One LDG.32 per element moves the same 128-byte lines as the float4
 // loads, so the LSU wavefronts per element are unchanged.
-template <int NV, bool kFull>
+// kRange: J~ beyond shared memory — this CTA holds buckets [r_lo, r_lo +
+// r_cnt) of its family (+ 32 dummy buckets), as fcs_dense_fx64_kernel.
+template <int NV, bool kFull, bool kRange>
 __global__ void __launch_bounds__(512) fcs_dense_fx32s_kernel(DenseArgs a,
                                                               const float* __restrict__ t,
                                                               const uint32_t* __restrict__ packed,
@@ -978,10 +985,15 @@ __global__ void __launch_bounds__(512) fcs_dense_fx32s_kernel(DenseArgs a,
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int32_t* sk = reinterpret_cast<int32_t*>(smem_raw);
   const int d = blockIdx.x % a.D;
-  const uint64_t chunk = blockIdx.x / a.D;
+  const uint32_t rp = kRange ? (blockIdx.x / a.D) % a.rparts : 0u;
+  const uint64_t chunk = kRange ? blockIdx.x / (a.D * a.rparts) : blockIdx.x / a.D;
+  const uint32_t span = kRange ? a.rspan : a.jt;
+  const uint32_t r_lo = rp * span;
+  const uint32_t r_cnt = kRange ? min(span, a.jt - r_lo) : a.jt;
+  const uint64_t prow = kRange ? (chunk * a.D + d) * a.rparts + rp : chunk * a.D + d;
   const uint32_t* tab = packed + static_cast<uint64_t>(d) * a.fam_stride;
   const float scale = ldexpf(1.0f, st->S);
-  for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) sk[b] = 0;
+  for (uint32_t b = threadIdx.x; b < (kRange ? span + 32u : a.jt); b += blockDim.x) sk[b] = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const uint32_t i0n = a.dims[0];
   // I_0 > 1024: segments of the fibers per warp, as fcs_dense_fx64_kernel
@@ -1024,7 +1036,7 @@ __global__ void __launch_bounds__(512) fcs_dense_fx32s_kernel(DenseArgs a,
     if (KB == 0) {
       uint32_t c, sbit;
       fiber_offset_fast(a, tab, f, c, sbit);
-      base_c = sk_base + 4u * c;
+      base_c = kRange ? c - r_lo : sk_base + 4u * c;  // kRange: range-relative offset
       scale_f = sbit ? -scale : scale;
     }
 #pragma unroll
@@ -1035,10 +1047,18 @@ __global__ void __launch_bounds__(512) fcs_dense_fx32s_kernel(DenseArgs a,
                                        ((smask >> kk) << 31));
       const uint32_t bits = __float_as_uint(fmaf(xs, scale_f, 12582912.0f));
       rng_acc |= bits ^ 0x4B000000u;
+      int32_t q = static_cast<int32_t>(bits - 0x4B400000u);
+      uint32_t addr;
+      if constexpr (kRange) {  // another range's element adds 0 to dummy bucket `lane`
+        const uint32_t lb = base_c + e;
+        const bool in = lb < r_cnt;
+        addr = sk_base + 4u * (in ? lb : span + static_cast<uint32_t>(lane));
+        q = in ? q : 0;
+      } else {
+        addr = base_c + (e << 2);
+      }
       int32_t old;
-      asm volatile("atom.shared.add.s32 %0, [%1], %2;"
-                   : "=r"(old)
-                   : "r"(base_c + (e << 2)), "r"(static_cast<int32_t>(bits - 0x4B400000u)));
+      asm volatile("atom.shared.add.s32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(q));
       ovf_acc |= static_cast<uint32_t>(old) + 0x40000000u;
     }
   };
@@ -1066,7 +1086,7 @@ __global__ void __launch_bounds__(512) fcs_dense_fx32s_kernel(DenseArgs a,
   bool tiny = false;
   if (!bad) {  // precision guard (kFxSmallBits), as in fcs_dense_fx_kernel
     int nz = 0, big = 0;
-    for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) {
+    for (uint32_t b = threadIdx.x; b < r_cnt; b += blockDim.x) {
       const int32_t v = sk[b];
       const uint32_t m = static_cast<uint32_t>(v < 0 ? -v : v);
       nz |= m != 0u;
@@ -1075,10 +1095,12 @@ __global__ void __launch_bounds__(512) fcs_dense_fx32s_kernel(DenseArgs a,
     const bool any_big = __syncthreads_or(big);
     tiny = __syncthreads_or(nz) && !any_big;
   }
-  if (bad || tiny) fx_float_redo(a, t, tab, scale, chunk, false, reinterpret_cast<float*>(smem_raw));
-  int32_t* dst = part + (chunk * a.D + d) * static_cast<uint64_t>(a.jt);
-  for (uint32_t b = threadIdx.x; b < a.jt; b += blockDim.x) dst[b] = sk[b];
-  if (threadIdx.x == 0) flags[chunk * a.D + d] = (bad || tiny) ? 1 : 0;
+  if (bad || tiny)
+    fx_float_redo(a, t, tab, scale, chunk, false, reinterpret_cast<float*>(smem_raw), r_lo, r_cnt);
+  // partial row per (chunk, d[, range]) of span words (kRange = false: span = J~)
+  int32_t* dst = part + prow * static_cast<uint64_t>(span);
+  for (uint32_t b = threadIdx.x; b < r_cnt; b += blockDim.x) dst[b] = sk[b];
+  if (threadIdx.x == 0) flags[prow] = (bad || tiny) ? 1 : 0;
 }
 
 // out[d][b] (+)= 2^-S * (exact 128-bit sum of the fixed-point partials) + the
@@ -1159,14 +1181,34 @@ __global__ void reduce_partials_kernel(const Tacc* __restrict__ part, uint64_t n
 }
 
 // Same for fixed-point partials (flag 0: int32 * 2^-S, flag 1: float bits).
+// rparts > 1: per-(chunk, family, range) partial rows of span words (the
+// bucket-range split of fcs_dense_fx32s_kernel); rparts = 1, span = J~ is the
+// plain (chunk, family) layout.
 __global__ void reduce_fx_kernel(const int32_t* __restrict__ part, const int* __restrict__ flags,
                                  uint64_t nchunk, int D, uint32_t jt,
                                  const FxStats* __restrict__ st, const double* __restrict__ divert,
-                                 double* __restrict__ out, int accumulate) {
+                                 double* __restrict__ out, int accumulate, uint32_t rparts = 1,
+                                 uint32_t span = 0) {
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  const uint64_t per = static_cast<uint64_t>(D) * jt;
-  if (i >= per) return;
-  const int d = static_cast<int>(i / jt);
+  const uint64_t per0 = static_cast<uint64_t>(D) * jt;
+  if (i >= per0) return;
+  const int d0 = static_cast<int>(i / jt);
+  if (rparts > 1) {  // ranged layout: one partial row per (chunk, family, range)
+    const uint32_t b = static_cast<uint32_t>(i - static_cast<uint64_t>(d0) * jt);
+    const uint32_t rp = b / span, lb = b - rp * span;
+    const double inv = ldexp(1.0, -st->S);
+    double acc = accumulate ? out[i] : 0.0;
+    for (uint64_t c = 0; c < nchunk; ++c) {
+      const uint64_t prow = (c * D + d0) * rparts + rp;
+      const int32_t w = __ldcs(part + prow * span + lb);
+      acc += __ldg(flags + prow) == 1 ? static_cast<double>(__int_as_float(w))
+                                      : static_cast<double>(w) * inv;
+    }
+    out[i] = acc + divert[i];
+    return;
+  }
+  const uint64_t per = per0;
+  const int d = d0;
   const double inv = ldexp(1.0, -st->S);
   double acc = accumulate ? out[i] : 0.0;
   auto term = [&](int32_t w, int fl) {
@@ -1322,16 +1364,25 @@ inline bool fx_seg_full(uint32_t i0) {
 }
 using Fx32sKernel = void (*)(DenseArgs, const float*, const uint32_t*, const FxStats*, int32_t*,
                              int*);
-// fx32s variant: NV = the smallest power of two with 32 NV >= I_0 (I_0 <= 1024).
-Fx32sKernel fx32s_kernel(int nv, bool full) {
+// fx32s variant: NV = the smallest power of two with 32 NV >= the segment length.
+template <bool kRange>
+Fx32sKernel fx32s_kernel_r(int nv, bool full) {
   switch (nv) {
-    case 1: return full ? fcs_dense_fx32s_kernel<1, true> : fcs_dense_fx32s_kernel<1, false>;
-    case 2: return full ? fcs_dense_fx32s_kernel<2, true> : fcs_dense_fx32s_kernel<2, false>;
-    case 4: return full ? fcs_dense_fx32s_kernel<4, true> : fcs_dense_fx32s_kernel<4, false>;
-    case 8: return full ? fcs_dense_fx32s_kernel<8, true> : fcs_dense_fx32s_kernel<8, false>;
-    case 16: return full ? fcs_dense_fx32s_kernel<16, true> : fcs_dense_fx32s_kernel<16, false>;
-    default: return full ? fcs_dense_fx32s_kernel<32, true> : fcs_dense_fx32s_kernel<32, false>;
+    case 1: return full ? fcs_dense_fx32s_kernel<1, true, kRange> : fcs_dense_fx32s_kernel<1, false, kRange>;
+    case 2: return full ? fcs_dense_fx32s_kernel<2, true, kRange> : fcs_dense_fx32s_kernel<2, false, kRange>;
+    case 4: return full ? fcs_dense_fx32s_kernel<4, true, kRange> : fcs_dense_fx32s_kernel<4, false, kRange>;
+    case 8: return full ? fcs_dense_fx32s_kernel<8, true, kRange> : fcs_dense_fx32s_kernel<8, false, kRange>;
+    case 16:
+      return full ? fcs_dense_fx32s_kernel<16, true, kRange>
+                  : fcs_dense_fx32s_kernel<16, false, kRange>;
+    default:
+      return full ? fcs_dense_fx32s_kernel<32, true, kRange>
+                  : fcs_dense_fx32s_kernel<32, false, kRange>;
   }
+}
+// range = true: the bucket-range split for J~ beyond shared memory
+Fx32sKernel fx32s_kernel(int nv, bool full, bool range = false) {
+  return range ? fx32s_kernel_r<true>(nv, full) : fx32s_kernel_r<false>(nv, full);
 }
 
 template <typename Tin>
@@ -1415,33 +1466,45 @@ int make_plan_uncached(const DenseArgs& a, Plan* p) {
   if (int rc = device_info(&di)) return rc;
   p->smem_bytes = static_cast<size_t>(a.jt) * sizeof(Tacc);
   static const bool no_fx64_env = std::getenv("ST_FX64_OFF") != nullptr;  // A/B probe
-  const bool fx64_shape = sizeof(Tin) == 8 && a.order >= 2 && a.dims[0] <= kFxSegMaxI0 &&
-                          !no_fx64_env &&
-                          static_cast<double>(a.fibers) * a.dims[0] * a.D >= 8.0e6;
+  // lane-owned fixed-point kernels (64-bit for fp64 input, int32 for fp32 input
+  // with scalar loads): their mode-0 buckets are packed in 16 bits
+  const bool lane_fx_shape = a.order >= 2 && a.dims[0] <= kFxSegMaxI0 && a.j0 < 65536u &&
+                             static_cast<double>(a.fibers) * a.dims[0] * a.D >= 8.0e6;
+  const bool fx64_shape = sizeof(Tin) == 8 && lane_fx_shape && !no_fx64_env;
+  const bool fx32_shape = sizeof(Tin) == 4 && lane_fx_shape;
   int per_sm = 0;
-  if (fx64_shape ? p->smem_bytes + 4096 > di.smem_optin : p->smem_bytes > di.smem_optin) {
+  if ((fx64_shape || fx32_shape) ? p->smem_bytes + 4096 > di.smem_optin
+                                 : p->smem_bytes > di.smem_optin) {
     // fp64 with J~ beyond shared memory: the 64-bit fixed point over R bucket
     // ranges (one CTA per chunk, family and range; each element read R times
     // through L2) instead of fp64 global atomics (1024 x 1024 x 512,
     // J~ = 49,150, D = 1: 4.45 ms with global atomics)
     const size_t avail = di.smem_optin - 4096;  // static shared memory + the 32 dummy buckets
-    const uint32_t R = static_cast<uint32_t>((static_cast<size_t>(a.jt) * 8 + avail - 1) / avail);
-    // (the lane-owned mode-0 buckets are packed in 16 bits: J~ < 2^16 bounds them)
-    if (!fx64_shape || R > 8 || a.jt >= 65536u) {
+    const size_t wb = sizeof(Tin) == 8 ? 8 : 4;   // bytes per bucket
+    const uint32_t R = static_cast<uint32_t>((static_cast<size_t>(a.jt) * wb + avail - 1) / avail);
+    if (!(fx64_shape || fx32_shape) || R > 8) {
       p->path = Path::Global;
       p->ws = 0;
       return ST_OK;
     }
-    p->path = Path::Fx64;
     p->rparts = R;
     p->rspan = (a.jt + R - 1) / R;
     p->nv = fx_seg_nv(a.dims[0]);
     p->threads = 512;
-    p->smem_bytes = (static_cast<size_t>(p->rspan) + 32) * 8;
-    auto k = fx64_kernel<Tin>(p->nv, fx_seg_full(a.dims[0]), true);
-    FCS_CUDA_TRY(set_max_dynamic_smem(k, di));
-    FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
-                                                               p->smem_bytes));
+    p->smem_bytes = (static_cast<size_t>(p->rspan) + 32) * wb;
+    if constexpr (sizeof(Tin) == 8) {
+      p->path = Path::Fx64;
+      auto k = fx64_kernel<Tin>(p->nv, fx_seg_full(a.dims[0]), true);
+      FCS_CUDA_TRY(set_max_dynamic_smem(k, di));
+      FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
+                                                                 p->smem_bytes));
+    } else {  // fp32 (1024^3, J = 32768, D = 4: 23.8 ms with fp64 global atomics)
+      p->path = Path::Fx32S;
+      auto k = fx32s_kernel(p->nv, fx_seg_full(a.dims[0]), true);
+      FCS_CUDA_TRY(set_max_dynamic_smem(k, di));
+      FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p->threads,
+                                                                 p->smem_bytes));
+    }
   }
   if (p->rparts == 1) {
     p->nv = sizeof(Tin) == 4 ? fx_nv(a) : 0;
@@ -1528,7 +1591,8 @@ int make_plan_uncached(const DenseArgs& a, Plan* p) {
   nchunk = std::min<uint64_t>(nchunk, std::max(by_bytes, one_wave));
   p->nchunk = nchunk;
   p->part_bytes = p->rparts > 1
-                      ? nchunk * a.D * p->rparts * static_cast<size_t>(p->rspan) * 8
+                      ? nchunk * a.D * p->rparts * static_cast<size_t>(p->rspan) *
+                            (p->path == Path::Fx64 ? 8 : 4)
                       : nchunk * a.D * static_cast<size_t>(a.jt) *
                             (p->path == Path::Fx64 ? 8 : sizeof(Tacc));  // Fx32S: int32 like Fx
   p->ws = align_up(p->part_bytes) + align_up(nchunk * a.D * p->rparts * sizeof(int)) +
@@ -1563,6 +1627,7 @@ int fill_args(size_t order, const size_t* dims, size_t last_begin, size_t last_c
                 "fcs_sketch: family too large");
   FCS_CHECK_ARG(last_begin + last_count <= dims[order - 1], "fcs_sketch: slab out of range");
   a->fam_stride = static_cast<uint32_t>(sum_dims);
+  a->j0 = static_cast<uint32_t>(hash_lens[0]);
   a->jt = static_cast<uint32_t>(kind == 1 ? prod_j : sum_j - order + 1);
   if (out_len) {
     FCS_CHECK_ARG(kind == 0 && out_len < (1ull << 31), "fcs_sketch: batched output too large");
@@ -1631,12 +1696,15 @@ int run_dense(DenseArgs a, const Tin* t, const uint32_t* packed, double* out, in
     FCS_CUDA_TRY(cudaGetLastError());
     FCS_CUDA_TRY(cudaMemsetAsync(divert, 0, out_elems * sizeof(double), st));
     const int nv = fx_seg_nv(a.dims[0]);
-    fx32s_kernel(nv, fx_seg_full(a.dims[0]))<<<static_cast<unsigned>(nchunk * a.D), 512,
-                                              p.smem_bytes, st>>>(a, tf, packed, stats, part,
-                                                                  flags);
+    a.rparts = p.rparts;
+    a.rspan = p.rparts > 1 ? p.rspan : a.jt;
+    fx32s_kernel(nv, fx_seg_full(a.dims[0]), p.rparts > 1)<<<
+        static_cast<unsigned>(nchunk * a.D * p.rparts), 512, p.smem_bytes, st>>>(a, tf, packed,
+                                                                                stats, part, flags);
     FCS_CUDA_TRY(cudaGetLastError());
     reduce_fx_kernel<<<ceil_div(out_elems, 256), 256, 0, st>>>(part, flags, nchunk, a.D, a.jt,
-                                                               stats, divert, out, accumulate);
+                                                               stats, divert, out, accumulate,
+                                                               a.rparts, a.rspan);
     FCS_CUDA_TRY(cudaGetLastError());
     return ST_OK;
   }

@@ -866,6 +866,30 @@ def test_dense_f64_fixed_point_bucket_ranges(cuda, shape, J, D):
     rel_close(got, want, RTOL64)
 
 
+@pytest.mark.parametrize("shape,J,D", [((512, 128, 128), 25000, 1),   # J~ = 74,998: 2 ranges
+                                       ((1024, 96, 96), 40000, 2)])   # J~ = 119,998: 3 ranges
+def test_dense_f32_fixed_point_bucket_ranges(cuda, shape, J, D):
+    """fp32 with J~ beyond shared memory (int32 buckets): the scalar-load
+    fixed point over bucket ranges (formerly fp64 global atomics). Integer
+    data bit-exact; Gaussian data at the fp32 rule; an outlier sends its
+    range CTA to the float redo."""
+    rng = np.random.default_rng(sum(shape) + J)
+    fams = st.families_for(list(shape), st.EstimatorConfig(J, D, 8))
+    for kind in ("int", "gauss"):
+        x = (rng.integers(-8, 9, size=shape) if kind == "int"
+             else rng.standard_normal(shape)).astype(np.float32)
+        if kind == "gauss":
+            x[3, 5, 7] = 2.0e9
+        got = st.fcs_dense_batched(st.DenseTensor.from_array(x), fams).cpu().numpy()
+        for d, f in enumerate(fams):
+            b, s_, j = oracle_family(f)
+            want = O.fcs_dense(x.astype(np.float64), b, s_, j)
+            if kind == "int":
+                assert np.array_equal(got[d], want), d
+            else:
+                rel_close(got[d], want, RTOL32)
+
+
 @pytest.mark.parametrize("shape", [(2048, 64, 66), (1100, 90, 90), (3001, 50, 60)])
 def test_dense_f32_fixed_point_long_fibers(cuda, shape):
     """fp32 with I_0 > 1024 (formerly fp32 shared atomics): the scalar-load
