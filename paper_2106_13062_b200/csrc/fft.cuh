@@ -641,9 +641,9 @@ struct IuvTail {
   int* stopped = nullptr;   // mode 3: sticky underflow flag
   const double* wvec = nullptr;  // mode 4: batch x dims[2] third vectors
 };
-// Cluster (8-CTA, DSMEM) form of the iuv estimator for M in {8192, 9216} and
-// batches that fit one wave of clusters (spectral_cluster.cu); returns 1
-// without launching otherwise.
+// Cluster (8-CTA, DSMEM) form of the iuv estimator for M in {2048, 3072, 4096,
+// 8192, 9216} and batches that fit one wave of clusters (spectral_cluster.cu);
+// returns 1 without launching otherwise.
 int launch_iuv_cluster(const FftPlan& pl, const EngArgs& e, int batch, const double* A,
                        const double* B, int c1, int c2, int f, double* est, const IuvTail& tail,
                        cudaStream_t st);
