@@ -250,6 +250,50 @@ struct RegDft<9> {
   }
 };
 
+// R = P Q with n = Q n1 + n2, k = k1 + P k2: DFT_P over n1 for each n2,
+// twiddle w_R^{n2 k1}, DFT_Q over n2 for each k1; output y[k1 + P k2] in
+// natural order (as RegDft<9>). Twiddles from exact cos/sin of 2 pi m / R.
+template <int P, int Q>
+__device__ __forceinline__ void reg_dft_pq(double2* x, double sign) {
+  constexpr int R = P * Q;
+  constexpr double kTwoPi = 6.283185307179586476925286766559;
+  double2 a[Q][P];  // a[n2][k1]
+#pragma unroll
+  for (int n2 = 0; n2 < Q; ++n2) {
+    double2 t[P];
+#pragma unroll
+    for (int n1 = 0; n1 < P; ++n1) t[n1] = x[Q * n1 + n2];
+    RegDft<P>::run(t, sign);
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1) {
+      const int m = (n2 * k1) % R;
+      if (m == 0) {
+        a[n2][k1] = t[k1];
+      } else {
+        const double2 w = make_double2(cos(kTwoPi * m / R), sign * sin(kTwoPi * m / R));
+        a[n2][k1] = cmul(t[k1], w);
+      }
+    }
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < P; ++k1) {
+    double2 t[Q];
+#pragma unroll
+    for (int n2 = 0; n2 < Q; ++n2) t[n2] = a[n2][k1];
+    RegDft<Q>::run(t, sign);
+#pragma unroll
+    for (int k2 = 0; k2 < Q; ++k2) x[k1 + P * k2] = t[k2];
+  }
+}
+template <>
+struct RegDft<6> {
+  static __device__ __forceinline__ void run(double2* x, double sign) { reg_dft_pq<3, 2>(x, sign); }
+};
+template <>
+struct RegDft<12> {
+  static __device__ __forceinline__ void run(double2* x, double sign) { reg_dft_pq<4, 3>(x, sign); }
+};
+
 // ----------------------------------------------------- block-wide passes
 // One radix-R pass over all butterflies of sub-transforms of length L.
 // Forward (DIF): DFT then twiddle w_L^{j r'}; inverse (DIT): conj twiddle then DFT.

@@ -645,6 +645,8 @@ int launch_iuv_cluster(const FftPlan& pl, const EngArgs& e, int batch, const dou
     case 8192: return launch_cl<16, 8>(pl, e, batch, A, B, c1, c2, f, est, tail, st);
     // small transforms too (batch-1 step with the median, D = 10, 100-long
     // vectors: M = 3072 20.5 -> 13.8 us, M = 2048 18.5 -> 12.3 us)
+    case 12288: return launch_cl<16, 12>(pl, e, batch, A, B, c1, c2, f, est, tail, st);
+    case 6144: return launch_cl<16, 6>(pl, e, batch, A, B, c1, c2, f, est, tail, st);
     case 4096: return launch_cl<16, 4>(pl, e, batch, A, B, c1, c2, f, est, tail, st);
     case 3072: return launch_cl<16, 3>(pl, e, batch, A, B, c1, c2, f, est, tail, st);
     case 2048: return launch_cl<16, 2>(pl, e, batch, A, B, c1, c2, f, est, tail, st);
@@ -659,6 +661,8 @@ int launch_conv_cluster(const FftPlan& pl, const double* a, int la, size_t lda, 
   switch (pl.M) {
     case 9216: return launch_conv_cl<16, 9>(pl, a, la, lda, b, lb, ldb, items, out, ldo, st);
     case 8192: return launch_conv_cl<16, 8>(pl, a, la, lda, b, lb, ldb, items, out, ldo, st);
+    case 12288: return launch_conv_cl<16, 12>(pl, a, la, lda, b, lb, ldb, items, out, ldo, st);
+    case 6144: return launch_conv_cl<16, 6>(pl, a, la, lda, b, lb, ldb, items, out, ldo, st);
     case 4096: return launch_conv_cl<16, 4>(pl, a, la, lda, b, lb, ldb, items, out, ldo, st);
     case 3072: return launch_conv_cl<16, 3>(pl, a, la, lda, b, lb, ldb, items, out, ldo, st);
     case 2048: return launch_conv_cl<16, 2>(pl, a, la, lda, b, lb, ldb, items, out, ldo, st);

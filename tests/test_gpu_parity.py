@@ -1037,7 +1037,11 @@ def test_dense_f32_odd_fiber_fixed_point(cuda, shape, J, D):
 
 # ------------------------------------------- cluster (8-CTA, DSMEM) estimator
 @pytest.mark.parametrize("dims,J,D,seed", [((30, 24, 18), 2500, 5, 7),   # M = 8192 instantiation
-                                           ((20, 26, 31), 3000, 4, 8)])  # M = 9216 (config-3 J)
+                                           ((20, 26, 31), 3000, 4, 8),   # M = 9216 (config-3 J)
+                                           ((22, 19, 27), 1800, 3, 9),   # M = 6144 (radix-6 pass)
+                                           ((17, 23, 21), 4000, 3, 10),  # M = 12288 (radix 12)
+                                           ((25, 20, 16), 1000, 4, 11),  # M = 3072
+                                           ((16, 18, 20), 650, 3, 12)])  # M = 2048
 def test_cluster_estimator_vs_oracle(cuda, dims, J, D, seed):
     """The cluster estimator (spectral_cluster.cu) on both of its transform
     lengths, every free mode (non-cubic, so the contracted-mode tables differ),
