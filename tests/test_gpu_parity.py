@@ -1127,3 +1127,26 @@ def test_cluster_estimator_edges_vs_oracle(cuda):
         c2 = 1 if f == 2 else 2
         a, b = rng.standard_normal(dims[c1]), rng.standard_normal(dims[c2])
         rel_close(ts.iuv(a, b, f), ots.iuv(a, b, f), 1e-9)
+
+
+def test_cluster_estimator_repeatable(cuda):
+    """Race check for the DSMEM exchanges, cluster barriers and the fused tail:
+    100 rounds of back-to-back calls (T(I,u,v) at batch 1 and 4 with the fused
+    median, and T(u,v,w)) must all agree with the first result to fp64
+    round-off (compute-sanitizer is unavailable on this pool)."""
+    rng = np.random.default_rng(61)
+    t = rng.standard_normal((20, 18, 16))
+    eng = st.FcsEngine(st.DenseTensor.from_array(t), st.EstimatorConfig(2500, 5, 13))
+    A = torch.as_tensor(rng.standard_normal((4, 18)), device="cuda")
+    B = torch.as_tensor(rng.standard_normal((4, 16)), device="cuda")
+    V = torch.as_tensor(rng.standard_normal((4, 18)), device="cuda")
+    U = torch.as_tensor(rng.standard_normal((4, 20)), device="cuda")
+    first = [x.cpu().numpy() for x in
+             [eng.iuv_batch(A[:n], B[:n], 0) for n in (1, 4)] + [eng.uvw_batch(U, V, B)]]
+    outs = []
+    for _ in range(100):
+        outs.append([eng.iuv_batch(A[:n], B[:n], 0) for n in (1, 4)] + [eng.uvw_batch(U, V, B)])
+    torch.cuda.synchronize()
+    for o in outs:
+        for g, f in zip(o, first):
+            rel_close(g, f, 1e-12)
