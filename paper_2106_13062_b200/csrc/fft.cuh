@@ -691,6 +691,10 @@ struct IuvTail {
 int launch_iuv_cluster(const FftPlan& pl, const EngArgs& e, int batch, const double* A,
                        const double* B, int c1, int c2, int f, double* est, const IuvTail& tail,
                        cudaStream_t st);
+// Cluster form of the per-family inverse of a half spectrum in slot order
+// (cp_sum_kernel: out[d][t] (+)= z[t], t < jt).
+int launch_spec_inverse_cluster(const FftPlan& pl, const double2* acc, int D, double* out, int jt,
+                                int accumulate, cudaStream_t st);
 // Cluster form of the row-pair linear convolution (same lengths; one wave).
 int launch_conv_cluster(const FftPlan& pl, const double* a, int la, size_t lda, const double* b,
                         int lb, size_t ldb, int items, double* out, size_t ldo, cudaStream_t st);

@@ -587,6 +587,10 @@ int launch_cp(const FftPlan& pl, const CpArgs& a, int D, const uint32_t* packed,
   cp_rank_sum_kernel<<<dim3(ceil_div(pl.P, 32), D), dim3(32, 8), 0, st>>>(Q, a.weights, a.r_begin,
                                                                           a.r_count, pl.P, acc);
   FCS_CUDA_TRY(cudaGetLastError());
+  {  // D families: one 8-CTA cluster each (spectral_cluster.cu)
+    const int rc = launch_spec_inverse_cluster(pl, acc, D, out, jt, accumulate, st);
+    if (rc != 1) return rc;
+  }
   if (int rc = prep(cp_sum_kernel, pl, &sm)) return rc;
   // D CTAs only: twice the threads per CTA shortens the one-transform latency
   cp_sum_kernel<<<D, 2 * kFftThreads, sm, st>>>(pl, acc, out, jt, accumulate);

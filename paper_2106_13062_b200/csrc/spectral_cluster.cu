@@ -580,6 +580,56 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
   }
 }
 
+// K5 over a cluster: the inverse of the summed CP spectrum of family d
+// (cp_sum_kernel: the one-CTA plan's half spectrum in slot order, read in
+// frequency order through the frequency -> slot table), out[d][t] (+)= z[t]
+// for t < jt. D clusters instead of D CTAs.
+template <int RA, int RB, int kClThreads>
+__global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
+    spec_inverse_cluster_kernel(FftPlan pl, const double2* __restrict__ acc,
+                                double* __restrict__ out, int jt, int accumulate) {
+  using F = ClFft<RA, RB, kClThreads>;
+  constexpr int N2 = F::N2, M = F::M, P = F::P, ROWS = F::ROWS;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  cg::cluster_group cl = cg::this_cluster();
+  const F fx(smem_raw, static_cast<int>(cl.block_rank()));
+  const int r = fx.r, t0 = fx.t0;
+  const int d = blockIdx.x / kClC;
+  cluster_arrive();
+  double2 twr[F::kTwPer];
+  fx.load_tw(pl, twr);
+  const double2* sp = acc + static_cast<size_t>(d) * P;
+  // the full spectrum G[k] from the half spectrum (slot f2p[0] holds X0, XP)
+  auto G = [&](int k) {
+    const int kh = k <= P ? k : M - k;
+    if (kh == 0) return make_double2(__ldg(&sp[__ldg(pl.f2p)].x), 0.0);
+    if (kh == P) return make_double2(__ldg(&sp[__ldg(pl.f2p)].y), 0.0);
+    const double2 v = __ldg(sp + __ldg(pl.f2p + kh));
+    return k > P ? cconj(v) : v;
+  };
+  fx.store_tw(twr);
+  __syncthreads();
+  for (int u = t0; u < ROWS * 32; u += kClThreads) {
+    const int row = u >> 5, k1 = u & 31;
+    const int k2 = row_k2<N2, F::Q>(r, row);
+    fx.put_u(row, k2, k1, G(k2 + N2 * k1), G(k2 + N2 * (k1 + 32)));
+  }
+  __syncthreads();
+  cluster_wait();
+  fx.inverse(cl);
+  double* o = out + static_cast<size_t>(d) * jt;
+  const double inv = 1.0 / P;
+  for (int i = t0; i < F::M1 * N2 * 2; i += kClThreads) {
+    const int ml = i / (2 * N2), rest = i % (2 * N2);
+    const int m2 = rest >> 1, c = rest & 1;
+    const int t = 2 * (F::M1 * r + ml + 32 * m2) + c;
+    if (t < jt) {
+      const double v = fx.zval(t) * inv;
+      o[t] = accumulate ? o[t] + v : v;
+    }
+  }
+}
+
 template <int RA, int RB, typename K>
 int cluster_prep(K k, int* max_clusters_out) {
   using Gm = ClGeom<RA, RB>;
@@ -633,7 +683,36 @@ int launch_conv_cl(const FftPlan& pl, const double* a, int la, size_t lda, const
   return ST_OK;
 }
 
+template <int RA, int RB>
+int launch_inv_cl(const FftPlan& pl, const double2* acc, int D, double* out, int jt, int accumulate,
+                  cudaStream_t st) {
+  auto k = spec_inverse_cluster_kernel<RA, RB, 128>;
+  int max_clusters = 0;
+  if (int rc = cluster_prep<RA, RB>(k, &max_clusters)) return rc;
+  if (D > max_clusters) return 1;
+  k<<<static_cast<unsigned>(D) * kClC, 128, ClGeom<RA, RB>::smem_bytes(), st>>>(pl, acc, out, jt,
+                                                                               accumulate);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
 }  // namespace
+
+int launch_spec_inverse_cluster(const FftPlan& pl, const double2* acc, int D, double* out, int jt,
+                                int accumulate, cudaStream_t st) {
+  static const bool off = std::getenv("ST_IUV_CLUSTER_OFF") != nullptr;  // A/B probe
+  if (off || pl.large_p1 || D <= 0) return 1;
+  switch (pl.M) {
+    case 12288: return launch_inv_cl<16, 12>(pl, acc, D, out, jt, accumulate, st);
+    case 9216: return launch_inv_cl<16, 9>(pl, acc, D, out, jt, accumulate, st);
+    case 8192: return launch_inv_cl<16, 8>(pl, acc, D, out, jt, accumulate, st);
+    case 6144: return launch_inv_cl<16, 6>(pl, acc, D, out, jt, accumulate, st);
+    case 4096: return launch_inv_cl<16, 4>(pl, acc, D, out, jt, accumulate, st);
+    case 3072: return launch_inv_cl<16, 3>(pl, acc, D, out, jt, accumulate, st);
+    case 2048: return launch_inv_cl<16, 2>(pl, acc, D, out, jt, accumulate, st);
+    default: return 1;
+  }
+}
 
 int launch_iuv_cluster(const FftPlan& pl, const EngArgs& e, int batch, const double* A,
                        const double* B, int c1, int c2, int f, double* est, const IuvTail& tail,
