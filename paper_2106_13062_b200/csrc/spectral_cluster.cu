@@ -28,6 +28,13 @@
 // The cached spectrum S_d is read in frequency order through the plan's
 // frequency -> slot table. Same arithmetic as the one-CTA path up to fp64
 // round-off (different factorisation of the same transform length).
+//
+// Users of the same distributed transform (ClFft): the estimator with its
+// fused tails (IuvTail: median over the D families by the last cluster to
+// finish, the rtpm row normalisation / refinement update, and T(u,v,w) as
+// <w, T(u,v,I)> per family), the row-pair linear convolution (config 5) and
+// the per-family inverse of a half spectrum (the CP sketch's last step).
+// M = 64 N2 with N2 in {32, 48, 64, 96, 128, 144, 192}.
 #include <cooperative_groups.h>
 #include <cstdlib>
 
