@@ -633,7 +633,9 @@ int launch_iuv(const FftPlan& pl, const EngArgs& e, int batch, const double* A, 
   // cluster kernel on the side stream, concurrently (config 3's 15 x 10
   // items: 140 one-CTA items + 10 clusters, 51 -> 41 us per step with the
   // median, instead of two CTAs sharing an SM setting the span).
-  const int nb1 = di.sm_count / e.D;  // (nb1 - 1 .. - 4: 43.8-51.2 us, measured)
+  // (nb1 - 1 .. - 4: 43.8-51.2 us; the two-buffer kernel for the one-CTA part:
+  // 52 us pipelined — measured)
+  const int nb1 = di.sm_count / e.D;
   if (nb1 > 0 && batch > nb1 && scratch != nullptr) {
     cudaStream_t st2 = nullptr;
     FCS_CUDA_TRY(fork_side(st, &st2));
