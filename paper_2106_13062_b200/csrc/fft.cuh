@@ -691,6 +691,9 @@ struct IuvTail {
 int launch_iuv_cluster(const FftPlan& pl, const EngArgs& e, int batch, const double* A,
                        const double* B, int c1, int c2, int f, double* est, const IuvTail& tail,
                        cudaStream_t st);
+// Cluster form of the deflation S_d -= weight F(cs_u) F(cs_v) F(cs_w) (D <= 32).
+int launch_deflate_cluster(const FftPlan& pl, const EngArgs& e, double weight, const double* U,
+                           const double* V, const double* W, double2* spec, cudaStream_t st);
 // Cluster form of the per-family inverse of a half spectrum in slot order
 // (cp_sum_kernel: out[d][t] (+)= z[t], t < jt).
 int launch_spec_inverse_cluster(const FftPlan& pl, const double2* acc, int D, double* out, int jt,

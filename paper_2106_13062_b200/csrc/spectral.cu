@@ -675,6 +675,10 @@ int launch_deflate(const FftPlan& pl, const EngArgs& e, double weight, const dou
                    const double* V, const double* W, double2* scratch, double2* spec,
                    cudaStream_t st) {
   if (pl.large_p1) return large_deflate(pl, e, weight, U, V, W, e.hash_len, spec, st);
+  {  // one 8-CTA cluster per family (spectral_cluster.cu)
+    const int rc = launch_deflate_cluster(pl, e, weight, U, V, W, spec, st);
+    if (rc != 1) return rc;
+  }
   size_t sm;
   if (int rc = prep(deflate_kernel, pl, &sm, 2)) return rc;
   deflate_kernel<<<e.D, kFftThreads, sm, st>>>(pl, e, weight, U, V, W, scratch, spec);

@@ -637,6 +637,86 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
   }
 }
 
+// K9 over a cluster: deflation S_d -= weight F(cs_u) F(cs_v) F(cs_w) of
+// family d (deflate_kernel; cpd.cpp:79-87 in the frequency domain): w1 =
+// cs_u + i cs_v transformed once (both spectra by the Hermitian split), their
+// product kept per k in shared memory, then cs_w transformed; each CTA updates
+// the half-spectrum slots of its k (k <= M/2; slot f2p[0] holds X0, X_{M/2}).
+template <int RA, int RB, int kClThreads>
+__global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
+    deflate_cluster_kernel(FftPlan pl, EngArgs e, double weight, const double* __restrict__ U,
+                           const double* __restrict__ V, const double* __restrict__ W,
+                           double2* __restrict__ spec) {
+  using F = ClFft<RA, RB, kClThreads>;
+  constexpr int N2 = F::N2, M = F::M, P = F::P, Q = F::Q, ROWS = F::ROWS, COLS = F::COLS;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  cg::cluster_group cl = cg::this_cluster();
+  const F fx(smem_raw, static_cast<int>(cl.block_rank()));
+  double2* abbuf = fx.rowbuf + ROWS * kN1;  // A B per k of this CTA's rows
+  const int r = fx.r, t0 = fx.t0;
+  const int d = blockIdx.x / kClC;
+  cluster_arrive();
+  double2 twr[F::kTwPer];
+  fx.load_tw(pl, twr);
+  const uint32_t* tab = e.packed + static_cast<size_t>(d) * e.fam_stride;
+  // count sketch into this CTA's columns: first (real) and optional second (imag) vector
+  auto scatter = [&](const double* x0, int n0, const uint32_t* t0p, const double* x1, int n1,
+                     const uint32_t* t1p) {
+    for (int i = t0; i < COLS * N2; i += kClThreads) fx.colbuf[i] = make_double2(0.0, 0.0);
+    __syncthreads();
+    for (int i = t0; i < n0 + n1; i += kClThreads) {
+      const bool first = i < n0;
+      const double v = first ? x0[i] : x1[i - n0];
+      if (v == 0.0) continue;
+      const uint32_t t = __ldg(first ? t0p + i : t1p + (i - n0));
+      const uint32_t h = t & 0x7fffffffu;
+      const int n1c = static_cast<int>(h & 63u);
+      if (n1c / COLS != r) continue;
+      double2& sl = fx.colbuf[sw((n1c % COLS) * N2 + static_cast<int>(h >> 6))];
+      atomicAdd(first ? &sl.x : &sl.y, (t >> 31) ? -v : v);
+    }
+  };
+  scatter(U, e.dims[0], tab + e.tab_off[0], V, e.dims[1], tab + e.tab_off[1]);
+  fx.store_tw(twr);
+  __syncthreads();
+  fx.f1a();
+  __syncthreads();
+  cluster_wait();
+  fx.f1b_f3(cl);
+  for (int u = t0; u < ROWS * kN1; u += kClThreads) {
+    const int row = u >> 6, kk = u & 63;
+    const int k2 = row_k2<N2, Q>(r, row);
+    double2 a2, b2;
+    fx.spectra(row, k2, kk, a2, b2);
+    abbuf[row * kN1 + kk] = cmul(a2, b2);
+  }
+  __syncthreads();
+  cluster_arrive();  // every CTA has read its rows before the second transform writes them
+  scatter(W, e.dims[2], tab + e.tab_off[2], nullptr, 0, nullptr);
+  __syncthreads();
+  fx.f1a();
+  __syncthreads();
+  cluster_wait();
+  fx.f1b_f3(cl);
+  double2* S = spec + static_cast<size_t>(d) * P;
+  for (int u = t0; u < ROWS * kN1; u += kClThreads) {
+    const int row = u >> 6, kk = u & 63;
+    const int k2 = row_k2<N2, Q>(r, row);
+    const int k = k2 + N2 * kk;
+    if (k > P) continue;
+    const double2 c = fx.rowbuf[sw(row * kN1 + (kk >> 3) + 8 * (kk & 7))];
+    const double2 g = cmul(abbuf[row * kN1 + kk], c);
+    if (k == 0) {
+      S[__ldg(pl.f2p)].x -= weight * g.x;
+    } else if (k == P) {
+      S[__ldg(pl.f2p)].y -= weight * g.x;
+    } else {
+      double2& sv = S[__ldg(pl.f2p + k)];
+      sv = make_double2(sv.x - weight * g.x, sv.y - weight * g.y);
+    }
+  }
+}
+
 template <int RA, int RB, typename K>
 int cluster_prep(K k, int* max_clusters_out) {
   using Gm = ClGeom<RA, RB>;
@@ -703,7 +783,42 @@ int launch_inv_cl(const FftPlan& pl, const double2* acc, int D, double* out, int
   return ST_OK;
 }
 
+template <int RA, int RB>
+int launch_defl_cl(const FftPlan& pl, const EngArgs& e, double weight, const double* U,
+                   const double* V, const double* W, double2* spec, cudaStream_t st) {
+  auto k = deflate_cluster_kernel<RA, RB, 128>;
+  const size_t smem = ClGeom<RA, RB>::smem_bytes() +
+                      static_cast<size_t>(ClGeom<RA, RB>::ROWS) * kN1 * sizeof(double2);
+  static bool attr[64];
+  int dev = 0;
+  FCS_CUDA_TRY(cudaGetDevice(&dev));
+  if (!attr[dev & 63]) {
+    FCS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+    attr[dev & 63] = true;
+  }
+  k<<<static_cast<unsigned>(e.D) * kClC, 128, smem, st>>>(pl, e, weight, U, V, W, spec);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
 }  // namespace
+
+int launch_deflate_cluster(const FftPlan& pl, const EngArgs& e, double weight, const double* U,
+                           const double* V, const double* W, double2* spec, cudaStream_t st) {
+  static const bool off = std::getenv("ST_IUV_CLUSTER_OFF") != nullptr;  // A/B probe
+  if (off || pl.large_p1 || e.D <= 0 || e.D > 32) return 1;
+  switch (pl.M) {
+    case 12288: return launch_defl_cl<16, 12>(pl, e, weight, U, V, W, spec, st);
+    case 9216: return launch_defl_cl<16, 9>(pl, e, weight, U, V, W, spec, st);
+    case 8192: return launch_defl_cl<16, 8>(pl, e, weight, U, V, W, spec, st);
+    case 6144: return launch_defl_cl<16, 6>(pl, e, weight, U, V, W, spec, st);
+    case 4096: return launch_defl_cl<16, 4>(pl, e, weight, U, V, W, spec, st);
+    case 3072: return launch_defl_cl<16, 3>(pl, e, weight, U, V, W, spec, st);
+    case 2048: return launch_defl_cl<16, 2>(pl, e, weight, U, V, W, spec, st);
+    default: return 1;
+  }
+}
 
 int launch_spec_inverse_cluster(const FftPlan& pl, const double2* acc, int D, double* out, int jt,
                                 int accumulate, cudaStream_t st) {
