@@ -521,6 +521,41 @@ int st_engine_uvw(st_engine* e, size_t batch, const double* u, const double* v, 
   if (median) {  // small batches: <w, T(u, v, I)> per family on the cluster estimator, median fused
     const int rc = iuv_fused_ab(e, batch, u, v, 2, 4, out, nullptr, nullptr, st, w);
     if (rc != 1) return rc;
+    // beyond one CTA per SM (config 3's 15 restarts x 10 families): the first
+    // nb1 vectors on the one-CTA kernel + median, the rest as clusters on the
+    // side stream (median fused), as launch_iuv splits its batch
+    DeviceInfo di;
+    if (int rc2 = device_info(&di)) return rc2;
+    const size_t nb1 = static_cast<size_t>(di.sm_count) / e->D;
+    if (!e->plan.large_p1 && nb1 > 0 && batch > nb1) {
+      const size_t nb2 = batch - nb1;
+      if (int rc2 = e->scratch.ensure(nb1 * e->D * e->plan.P * sizeof(double2), st)) return rc2;
+      if (int rc2 = e->est.ensure((nb1 + nb2) * e->D * sizeof(double), st)) return rc2;
+      const size_t had = e->cnt.bytes;
+      if (int rc2 = e->cnt.ensure(std::max<size_t>(nb2, 64) * sizeof(int), st)) return rc2;
+      if (e->cnt.bytes != had) FCS_CUDA_TRY(cudaMemsetAsync(e->cnt.p, 0, e->cnt.bytes, st));
+      double* est = static_cast<double*>(e->est.p);
+      IuvTail t;
+      t.mode = 4;
+      t.cnt = static_cast<int*>(e->cnt.p);
+      t.out = out + nb1;
+      t.wvec = w + nb1 * e->dims[2];
+      cudaStream_t st2 = nullptr;
+      FCS_CUDA_TRY(fork_side(st, &st2));
+      const EngArgs args = e->args();
+      int rcc = launch_iuv_cluster(e->plan, args, static_cast<int>(nb2), u + nb1 * e->dims[0],
+                                   v + nb1 * e->dims[1], 0, 1, 2, est + nb1 * e->D, t, st2);
+      int rco = ST_OK;
+      if (rcc == 0) {
+        rco = launch_uvw(e->plan, args, static_cast<int>(nb1), u, v, w,
+                         static_cast<double2*>(e->scratch.p), est, st);
+        if (!rco)
+          rco = launch_median(est, static_cast<int>(nb1), static_cast<int>(e->D), 1, out, st);
+      }
+      FCS_CUDA_TRY(join_side(st));
+      if (rcc == 0) return rco;
+      if (rcc != 1) return rcc;
+    }
   }
   if (int rc = e->scratch.ensure(batch * e->D * e->plan.P * sizeof(double2), st)) return rc;
   double* est = out;
