@@ -349,7 +349,8 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
     for (int h = 0; h < 2; ++h) {
       const int k = k2 + N2 * (k1 + 32 * h);
       const int kh = k <= P ? k : M - k;  // half-spectrum frequency
-      sslot[g][h] = (u < ROWS * 32 && kh != 0 && kh != P) ? __ldg(pl.f2p + kh) : 0;
+      // the real bins (kh = 0, P) sit in slot f2p[0]
+      sslot[g][h] = u < ROWS * 32 ? __ldg(pl.f2p + (kh == P ? 0 : kh)) : 0;
     }
   }
   __syncthreads();
@@ -383,25 +384,13 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
   __syncthreads();
   fx.f1a();
   // spectrum values for the product phase, in flight through the forward passes
+  // (raw slot values: the real-bin / conjugate selection happens at the use,
+  // so no instruction waits on these loads before the forward passes)
   double2 sv[kGU][2];
 #pragma unroll
   for (int g = 0; g < kGU; ++g) {
-    const int u = t0 + g * kClThreads;
-    const int row = u >> 5, k1 = u & 31;
-    const int k2 = row_k2<N2, Q>(r, row < ROWS ? row : 0);
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int k = k2 + N2 * (k1 + 32 * h);
-      const int kh = k <= P ? k : M - k;
-      double2 x = make_double2(0.0, 0.0);
-      if (u < ROWS * 32) {
-        if (kh == 0) x = make_double2(__ldg(&sp[__ldg(pl.f2p)].x), 0.0);
-        else if (kh == P) x = make_double2(__ldg(&sp[__ldg(pl.f2p)].y), 0.0);
-        else x = __ldg(sp + sslot[g][h]);
-        if (k > P) x = cconj(x);
-      }
-      sv[g][h] = x;
-    }
+    for (int h = 0; h < 2; ++h) sv[g][h] = __ldg(sp + sslot[g][h]);
   }
   __syncthreads();
   cluster_wait();
@@ -418,7 +407,13 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
     for (int h = 0; h < 2; ++h) {
       double2 a2, b2;
       fx.spectra(row, k2, k1 + 32 * h, a2, b2);
-      gg[h] = cmul(sv[g][h], cconj(cmul(a2, b2)));
+      const int k = k2 + N2 * (k1 + 32 * h);
+      const int kh = k <= P ? k : M - k;
+      double2 sx = sv[g][h];
+      if (kh == 0) sx = make_double2(sx.x, 0.0);
+      else if (kh == P) sx = make_double2(sx.y, 0.0);
+      else if (k > P) sx = cconj(sx);
+      gg[h] = cmul(sx, cconj(cmul(a2, b2)));
     }
     fx.put_u(row, k2, k1, gg[0], gg[1]);
   }
