@@ -546,13 +546,14 @@ int st_engine_uvw(st_engine* e, size_t batch, const double* u, const double* v, 
       int rcc = launch_iuv_cluster(e->plan, args, static_cast<int>(nb2), u + nb1 * e->dims[0],
                                    v + nb1 * e->dims[1], 0, 1, 2, est + nb1 * e->D, t, st2);
       int rco = ST_OK;
-      if (rcc == 0) {
-        rco = launch_uvw(e->plan, args, static_cast<int>(nb1), u, v, w,
-                         static_cast<double2*>(e->scratch.p), est, st);
-        if (!rco)
-          rco = launch_median(est, static_cast<int>(nb1), static_cast<int>(e->D), 1, out, st);
-      }
+      if (rcc == 0)
+        rco = launch_uvw_dot(e->plan, args, static_cast<int>(nb1), u, v, w,
+                             static_cast<double2*>(e->scratch.p), est, st);
+      // join before the median: a join directly followed by the next call's
+      // fork measured a serialising stall (tools/experiments/iuv_split_probe.py)
       FCS_CUDA_TRY(join_side(st));
+      if (rcc == 0 && !rco)
+        rco = launch_median(est, static_cast<int>(nb1), static_cast<int>(e->D), 1, out, st);
       if (rcc == 0) return rco;
       if (rcc != 1) return rcc;
     }

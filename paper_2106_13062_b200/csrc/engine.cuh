@@ -26,6 +26,8 @@ int launch_uvw(const FftPlan&, const EngArgs&, int, const double*, const double*
 int launch_deflate(const FftPlan&, const EngArgs&, double, const double*, const double*,
                    const double*, double2*, double2*, cudaStream_t);
 int launch_median(const double*, int, int, int, double*, cudaStream_t);
+int launch_uvw_dot(const FftPlan&, const EngArgs&, int, const double*, const double*, const double*,
+                   double2*, double*, cudaStream_t);
 int launch_cs_columns(const double*, int, int, const uint32_t*, int, double*, cudaStream_t);
 int launch_normalize_rows(double*, int, int, cudaStream_t);
 int launch_median_normalize(const double*, int, int, int, double*, cudaStream_t);

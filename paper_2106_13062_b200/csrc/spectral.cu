@@ -332,9 +332,13 @@ __global__ void __launch_bounds__(kFftThreads) iuv_kernel(FftPlan pl, EngArgs e,
 // second shared buffer, halving shared memory so two CTAs fit per SM. Used when
 // the batch is slightly above one wave of the two-buffer kernel (config 3:
 // 15 x 10 = 150 items on 148 SMs), where it removes the nearly empty second wave.
+// wdot != nullptr: T(u, v, w) by linearity — est[item] = <w_b, T_d(u, v, I)>
+// instead of the free-mode vector (the uvw estimate, one transform fewer than
+// uvw_kernel's three forward ones).
 __global__ void __launch_bounds__(kFftThreads, 2) iuv1_kernel(FftPlan pl, EngArgs e, const double* A,
                                                            const double* B, int c1, int c2, int f,
-                                                           double2* scratch, double* est) {
+                                                           double2* scratch, double* est,
+                                                           const double* wdot = nullptr) {
   const Smem sm = carve(pl, 1);
   load_twiddles_async(sm.tw, pl);
   const int b = blockIdx.x, d = blockIdx.y;
@@ -376,6 +380,18 @@ __global__ void __launch_bounds__(kFftThreads, 2) iuv1_kernel(FftPlan pl, EngArg
   const double inv = 1.0 / pl.P;
   const int nf = e.dims[f];
   const uint32_t* tf = tab + e.tab_off[f];
+  if (wdot != nullptr) {
+    const double* wv = wdot + static_cast<size_t>(b) * nf;
+    double acc = 0.0;
+    for (int i = tid(); i < nf; i += blockDim.x) {
+      const uint32_t t = __ldg(tf + i);
+      const double z = packed_real(sm.buf, t & 0x7fffffffu) * inv;
+      acc += wv[i] * ((t >> 31) ? -z : z);
+    }
+    const double tot = block_sum(acc, sm.red);
+    if (tid() == 0) est[item] = tot;
+    return;
+  }
   double* o = est + item * nf;
   for (int i = tid(); i < nf; i += blockDim.x) {
     const uint32_t t = __ldg(tf + i);
@@ -657,6 +673,19 @@ int launch_iuv(const FftPlan& pl, const EngArgs& e, int batch, const double* A, 
     iuv1_kernel<<<dim3(batch, e.D), kFftThreads, sm1, st>>>(pl, e, A, B, c1, c2, f, scratch, est);
   else
     iuv_kernel<<<dim3(batch, e.D), kFftThreads, sm2, st>>>(pl, e, A, B, c1, c2, f, scratch, est);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+// T(u, v, w) through the one-buffer estimator with the dot product (one CTA
+// per item, the one-CTA part of a split batch): est[b D + d].
+int launch_uvw_dot(const FftPlan& pl, const EngArgs& e, int batch, const double* U,
+                   const double* V, const double* W, double2* scratch, double* est,
+                   cudaStream_t st) {
+  if (pl.large_p1) return 1;
+  size_t sm1;
+  if (int rc = prep(iuv1_kernel, pl, &sm1, 1)) return rc;
+  iuv1_kernel<<<dim3(batch, e.D), kFftThreads, sm1, st>>>(pl, e, U, V, 0, 1, 2, scratch, est, W);
   FCS_CUDA_TRY(cudaGetLastError());
   return ST_OK;
 }
