@@ -566,7 +566,6 @@ __global__ void __launch_bounds__(THREADS, 1) fcs_dense_fx_kernel(DenseArgs a,
 
   const uint64_t f_begin = chunk * a.fibers_per_chunk;
   const uint64_t f_end = min(a.fibers, f_begin + a.fibers_per_chunk);
-  int ovf = 0;
   float4 cur[NV], nxt[NV];
   auto load = [&](uint64_t fib, float4* dst) {
     const float4* src = reinterpret_cast<const float4*>(t + fib * i0n);
@@ -730,8 +729,7 @@ __device__ void fx_float_redo(const DenseArgs& a, const float* __restrict__ t,
 // 128-bit integers in the reduction, then scaled by 2^-S once.
 // Lane-owned mode-0 indices i_0 = lane + 32 k (k < NV) with their table
 // entries in registers; each lane keeps NV loads in flight per fiber.
-constexpr double kMagic64 = 6755399441055744.0;  // 1.5 * 2^52
-constexpr uint64_t kMagic64Bits = 0x4338000000000000ull;
+constexpr double kMagic64 = 6755399441055744.0;  // 1.5 * 2^52 (bits 0x4338000000000000)
 
 __device__ __forceinline__ double ld_stream64(const double* p) {
   double v;

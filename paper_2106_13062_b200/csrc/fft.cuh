@@ -480,7 +480,6 @@ template <int R, bool kForward>
 __device__ __forceinline__ void pair_group_pass(double2* buf, const FftPlan& pl,
                                                 const double2* tw) {
   const uint2* un = smem_units(tw, pl);
-  const uint32_t G = static_cast<uint32_t>(pl.P / R);
   const int hi_off = 1 << kTwLoBits;
   for (int u = threadIdx.x; u < pl.nunits; u += blockDim.x) {
     const uint2 d = un[u];

@@ -643,7 +643,7 @@ __global__ void __cluster_dims__(kClC, 1, 1) __launch_bounds__(kClThreads, 3)
                            const double* __restrict__ V, const double* __restrict__ W,
                            double2* __restrict__ spec) {
   using F = ClFft<RA, RB, kClThreads>;
-  constexpr int N2 = F::N2, M = F::M, P = F::P, Q = F::Q, ROWS = F::ROWS, COLS = F::COLS;
+  constexpr int N2 = F::N2, P = F::P, Q = F::Q, ROWS = F::ROWS, COLS = F::COLS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   cg::cluster_group cl = cg::this_cluster();
   const F fx(smem_raw, static_cast<int>(cl.block_rank()));
