@@ -1150,3 +1150,31 @@ def test_cluster_estimator_repeatable(cuda):
     for o in outs:
         for g, f in zip(o, first):
             rel_close(g, f, 1e-12)
+
+
+def test_dense_fuzz_paths_vs_oracle(cuda):
+    """Seeded random shapes through every K1 path (shared-memory atomics,
+    fp32 float4 / scalar-load fixed point, fp64 fixed point, fiber segments,
+    bucket ranges, global atomics): integer data must match the reference's
+    serial sum bit for bit, whatever path the planner picks."""
+    rng = np.random.default_rng(2024)
+    cases = []
+    for _ in range(6):   # small calls: shared-memory atomic kernels
+        cases.append((tuple(int(v) for v in rng.integers(3, 40, size=3)), int(rng.integers(20, 400)),
+                      int(rng.integers(1, 5)), rng.choice([np.float32, np.float64])))
+    cases += [((1024, 96, 88), 700, 1, np.float32),     # float4 fixed point
+              ((1021, 97, 86), 900, 2, np.float32),     # scalar-load fixed point (I0 % 4 != 0)
+              ((2500, 60, 56), 1100, 1, np.float32),    # fiber segments (fp32)
+              ((700, 120, 100), 1300, 1, np.float64),   # fp64 fixed point
+              ((1500, 80, 70), 2000, 1, np.float64),    # fp64 fiber segments
+              ((300, 160, 180), 11000, 1, np.float64),  # fp64 bucket ranges
+              ((300, 160, 180), 21000, 1, np.float32),  # fp32 bucket ranges
+              ((40, 50, 60), 30000, 1, np.float64)]     # beyond shared memory, small: global
+    for shape, J, D, dt in cases:
+        x = rng.integers(-6, 7, size=shape).astype(dt)
+        fams = st.families_for(list(shape), st.EstimatorConfig(J, D, int(rng.integers(1, 1 << 30))))
+        got = st.fcs_dense_batched(st.DenseTensor.from_array(x), fams).cpu().numpy()
+        for d, f in enumerate(fams):
+            b, s_, j = oracle_family(f)
+            want = O.fcs_dense(x.astype(np.float64), b, s_, j)
+            assert np.array_equal(got[d], want), (shape, J, D, dt, d)
