@@ -7,6 +7,9 @@
 // prologue), and products / sums over rank happen in the frequency domain
 // (K4) so each output needs a single inverse transform (K5).
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cstdlib>
 
 #include <math_constants.h>
@@ -543,12 +546,50 @@ __global__ void refine_update_kernel(double* __restrict__ best, const double* __
 // ------------------------------------------------------------ launchers
 namespace {
 
+// Per-(kernel, device) cache of the dynamic shared-memory opt-in (raised only
+// when a larger plan needs it) and of the occupancy per shared-memory size:
+// the per-call host work of a small step stays a map lookup.
+struct KernelCache {
+  std::mutex mu;
+  std::map<std::pair<const void*, int>, size_t> smem_set;
+  std::map<std::tuple<const void*, int, size_t>, int> occ;
+};
+KernelCache& kcache() {
+  static KernelCache c;
+  return c;
+}
+
 template <typename K>
 int prep(K kernel, const FftPlan& pl, size_t* smem, int nbuf = 1) {
   *smem = fft_smem_bytes(pl, false) + static_cast<size_t>(nbuf - 1) * pl.P * sizeof(double2) +
           32 * sizeof(double);
-  FCS_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(*smem)));
+  int dev = 0;
+  FCS_CUDA_TRY(cudaGetDevice(&dev));
+  KernelCache& c = kcache();
+  std::lock_guard<std::mutex> lock(c.mu);
+  size_t& cur = c.smem_set[{reinterpret_cast<const void*>(kernel), dev}];
+  if (*smem > cur) {
+    FCS_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(*smem)));
+    cur = *smem;
+  }
+  return ST_OK;
+}
+
+template <typename K>
+int occupancy(K kernel, int threads, size_t smem, int* out) {
+  int dev = 0;
+  FCS_CUDA_TRY(cudaGetDevice(&dev));
+  KernelCache& c = kcache();
+  std::lock_guard<std::mutex> lock(c.mu);
+  auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), dev, smem);
+  auto it = c.occ.find(key);
+  if (it == c.occ.end()) {
+    int n = 0;
+    FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem));
+    it = c.occ.emplace(key, n).first;
+  }
+  *out = it->second;
   return ST_OK;
 }
 
@@ -583,9 +624,8 @@ int launch_cp(const FftPlan& pl, const CpArgs& a, int D, const uint32_t* packed,
   if (a.r_count > 0) {
     // the one-buffer form when it needs fewer waves (as launch_iuv)
     int occ2 = 0, occ1 = 0;
-    FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, cp_rank_kernel, kFftThreads, sm));
-    FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, cp_rank1_kernel, kFftThreads,
-                                                               sm1));
+    if (int rc = occupancy(cp_rank_kernel, kFftThreads, sm, &occ2)) return rc;
+    if (int rc = occupancy(cp_rank1_kernel, kFftThreads, sm1, &occ1)) return rc;
     DeviceInfo di;
     if (int rc = device_info(&di)) return rc;
     const long items = static_cast<long>(a.r_count) * D;
@@ -641,8 +681,8 @@ int launch_iuv(const FftPlan& pl, const EngArgs& e, int batch, const double* A, 
   // waves of each form; the one-buffer kernel (scratch: batch x D x P slots)
   // wins when it fits the batch in fewer waves
   int occ2 = 0, occ1 = 0;
-  FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, iuv_kernel, kFftThreads, sm2));
-  FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, iuv1_kernel, kFftThreads, sm1));
+  if (int rc = occupancy(iuv_kernel, kFftThreads, sm2, &occ2)) return rc;
+  if (int rc = occupancy(iuv1_kernel, kFftThreads, sm1, &occ1)) return rc;
   DeviceInfo di;
   if (int rc = device_info(&di)) return rc;
   // One CTA per SM for the first nb1 vectors; the vectors beyond go to the
