@@ -357,6 +357,19 @@ int st_engine_iuv(st_engine* engine, size_t batch, const double* a, const double
 int st_engine_uvw(st_engine* engine, size_t batch, const double* u, const double* v,
                   const double* w, double* out, int median, void* stream);
 
+/* Estimator path of the FCS / TS engines (iuv and uvw; the other backends
+ * ignore it). ST_PATH_SPECTRAL: the reference's formulation, FFT correlation
+ * against the cached spectra (shared-memory or cluster transforms).
+ * ST_PATH_DIRECT: the same correlation in the time domain —
+ * est[i] = s_f(i) sum_{i1} a'(i1) Q[h_f(i) + h_c1(i1)],
+ * Q[k] = sum_{i2} b'(i2) sk[k + h_c2(i2)] (k < 2J - 1: no wrap at n = 3J - 2),
+ * exact up to fp64 rounding, cost (2J - 1) I_c2 + I_f I_c1 multiply-adds per
+ * item; hash lengths up to where Q fits one CTA's shared memory.
+ * ST_PATH_AUTO (default): the direct path when its cost is below the
+ * transforms' (engine.cu use_direct). Returns ST_EINVAL for an unknown path. */
+enum { ST_PATH_AUTO = 0, ST_PATH_SPECTRAL = 1, ST_PATH_DIRECT = 2 };
+int st_engine_set_path(st_engine* engine, int path);
+
 /* T <- T - weight * u o v o w in sketch space (device vectors).
  * Replaces FcsEngine::deflate, cpd.cpp:79-87. */
 int st_engine_deflate(st_engine* engine, double weight, const double* u, const double* v,

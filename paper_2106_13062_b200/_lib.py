@@ -65,6 +65,7 @@ SIGNATURES = {
     "st_engine_iuv": (i32, [p, sz, p, p, sz, p, i32, p]),
     "st_engine_uvw": (i32, [p, sz, p, p, p, p, i32, p]),
     "st_engine_deflate": (i32, [p, dbl, p, p, p, p]),
+    "st_engine_set_path": (i32, [p, i32]),
     "st_rtpm": (i32, [i32, p, sz, sz, sz, sz, sz, sz, u64, p, p, p]),
     "st_rtpm_backend": (i32, [i32, i32, p, sz, sz, sz, sz, sz, sz, u64, p, p, p]),
     "st_rtpm_asym": (i32, [i32, i32, p, p, sz, sz, sz, sz, sz, u64, p, p, p]),

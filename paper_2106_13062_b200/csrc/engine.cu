@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <limits>
 #include <string>
 #include <vector>
@@ -43,6 +44,7 @@ static int iuv_fused_ab(st_engine* e, size_t batch, const double* a, const doubl
                  int mode, double* out, double* best, int* stopped, cudaStream_t st,
                  const double* wvec = nullptr) {
   if (is_exact(e) || e->plan.large_p1 || batch == 0) return 1;
+  if (use_direct(e, batch, free_mode)) return 1;  // the caller's separate kernels run it
   int c1, c2;
   contracted(free_mode, &c1, &c2);
   const size_t nf = e->dims[free_mode];
@@ -59,6 +61,49 @@ static int iuv_fused_ab(st_engine* e, size_t batch, const double* a, const doubl
   t.wvec = wvec;
   return launch_iuv_cluster(e->plan, e->args(), static_cast<int>(batch), a, b, c1, c2,
                             static_cast<int>(free_mode), static_cast<double*>(e->est.p), t, st);
+}
+
+// ST_ENGINE_PATH=spectral|direct sets the initial path of new engines (A/B
+// runs of drivers that build their engine internally, e.g. st_rtpm).
+int default_path() {
+  const char* v = std::getenv("ST_ENGINE_PATH");
+  if (!v) return ST_PATH_AUTO;
+  const std::string s(v);
+  return s == "spectral" ? ST_PATH_SPECTRAL : s == "direct" ? ST_PATH_DIRECT : ST_PATH_AUTO;
+}
+
+// Cost rule of the direct path, fitted to the measured A/B of both paths on
+// one B200 (profiles/corr_sweep_r02.txt: I^3 tensors, I = 50-400, J =
+// 300-4000, D = 10, batch 1 and 15; times in us, F = (2J - 1) I_c2 + I_f I_c1
+// multiply-adds per item, P the transform length). The spectral path costs
+// about one transform latency per wave of items (~one item per SM), the
+// direct path a launch floor plus F at a fraction of the DFMA rate; the
+// direct path wins where I is small against J (e.g. I = 50, J >= 1000).
+bool use_direct(st_engine* e, size_t batch, size_t free_mode) {
+  if (is_exact(e) || batch == 0 || e->tsk == nullptr) return false;
+  if (e->path == ST_PATH_SPECTRAL) return false;
+  if (!corr_feasible(e, free_mode)) return false;
+  if (e->path == ST_PATH_DIRECT) return true;
+  if (e->plan.large_p1) return false;  // two-level transforms: not in the fitted range
+  int c1, c2;
+  contracted(free_mode, &c1, &c2);
+  const double J = static_cast<double>(e->hash_len);
+  const double F = (2 * J - 1) * static_cast<double>(e->dims[c2]) +
+                   static_cast<double>(e->dims[free_mode]) * static_cast<double>(e->dims[c1]);
+  const double P = static_cast<double>(e->plan.P);
+  const double items = static_cast<double>(batch) * static_cast<double>(e->D);
+  if (batch == 1) return 14.0 + 6.5e-6 * F * std::max(1.0, items / 10.0) < 10.4 + 6.5e-4 * P;
+  const double waves = std::max(1.0, std::ceil(items / 148.0));
+  return 20.0 + 3.3e-5 * F * items / 150.0 < (17.0 + 2.5e-3 * P) * waves;
+}
+
+int corr_sync(st_engine* e, cudaStream_t st) {
+  if (!e->tsk_stale) return ST_OK;
+  if (int rc = launch_real_from_spec(e->plan, e->spec, static_cast<int>(e->D), e->tsk, e->jt,
+                                     static_cast<int>(e->jt), 0, st))
+    return rc;
+  e->tsk_stale = false;
+  return ST_OK;
 }
 
 int engine_iuv_fused(st_engine* e, size_t batch, const double* a, size_t free_mode, int mode,
@@ -223,6 +268,7 @@ int st_engine_create_backend(st_engine** engine, int backend, int dtype, const v
   auto* e = new st_engine();
   FCS_CUDA_TRY(cudaGetDevice(&e->device));
   e->backend = backend;
+  e->path = default_path();
   for (int n = 0; n < 3; ++n) e->dims[n] = dims[n];
   e->hash_len = hash_len;
   e->D = sketch_count;
@@ -303,7 +349,13 @@ int st_engine_create_backend(st_engine** engine, int backend, int dtype, const v
   if (!rc)
     rc = launch_spec_from_real(e->plan, src, e->jt, static_cast<int>(e->jt),
                                static_cast<int>(sketch_count), e->spec, st);
-  cudaFreeAsync(vals, st);
+  if (backend == ST_BACKEND_FCS) {  // the direct estimator's time-domain sketches
+    e->tsk = vals;
+    e->tsk_own = true;
+  } else {
+    cudaFreeAsync(vals, st);
+    e->tsk = e->ext;
+  }
   cudaFreeAsync(ws, st);
   if (rc) {
     st_engine_destroy(e);
@@ -363,6 +415,7 @@ int st_engine_from_sketches(st_engine** engine, int backend, const double* sketc
   auto* e = new st_engine();
   FCS_CUDA_TRY(cudaGetDevice(&e->device));
   e->backend = backend;
+  e->path = default_path();
   for (int n = 0; n < 3; ++n) e->dims[n] = dims[n];
   e->hash_len = hash_len;
   e->D = sketch_count;
@@ -395,6 +448,19 @@ int st_engine_from_sketches(st_engine** engine, int backend, const double* sketc
     return fail(ST_ECUDA, "st_engine_from_sketches: table copy failed");
   }
   const double* src = sketches;
+  if (backend == ST_BACKEND_FCS) {
+    if (cudaMalloc(reinterpret_cast<void**>(&e->tsk), vbytes) != cudaSuccess) {
+      st_engine_destroy(e);
+      return fail(ST_ENOMEM, "st_engine_create: device allocation failed");
+    }
+    e->tsk_own = true;
+    if (cudaMemcpyAsync(e->tsk, sketches, vbytes, cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
+      st_engine_destroy(e);
+      return fail(ST_ECUDA, "st_engine_from_sketches: sketch copy failed");
+    }
+  } else {
+    e->tsk = e->ext;
+  }
   if (backend == ST_BACKEND_TS) {
     const size_t n = sketch_count * e->jt;
     ts_periodic_kernel<<<ceil_div(n, 256), 256, 0, st>>>(
@@ -427,6 +493,8 @@ int st_engine_destroy(st_engine* e) {
   if (e->one) cudaFree(e->one);
   if (e->dense) cudaFree(e->dense);
   if (e->seeds) cudaFree(e->seeds);
+  if (e->tsk && e->tsk_own) cudaFree(e->tsk);
+  e->corr.release(nullptr);
   e->scratch.release(nullptr);
   e->est.release(nullptr);
   e->vec.release(nullptr);
@@ -482,6 +550,18 @@ int st_engine_iuv(st_engine* e, size_t batch, const double* a, const double* b, 
                                static_cast<int>(nf), out, st)
                : ST_OK;
   }
+  if (use_direct(e, batch, free_mode)) {  // time-domain correlation (correlate.cu)
+    if (int rc = corr_sync(e, st)) return rc;
+    double* est = out;
+    if (median) {
+      if (int rc = e->est.ensure(batch * e->D * nf * sizeof(double), st)) return rc;
+      est = static_cast<double*>(e->est.p);
+    }
+    if (int rc = corr_estimate(e, batch, a, b, free_mode, nullptr, est, st)) return rc;
+    return median ? launch_median(est, static_cast<int>(batch), static_cast<int>(e->D),
+                                  static_cast<int>(nf), out, st)
+                  : ST_OK;
+  }
   if (median) {  // small batches: cluster estimator with the median fused in
     const int rc = iuv_fused_ab(e, batch, a, b, free_mode, 1, out, nullptr, nullptr, st);
     if (rc != 1) return rc;
@@ -517,6 +597,17 @@ int st_engine_uvw(st_engine* e, size_t batch, const double* u, const double* v, 
     if (int rc = exact_uvw(e, batch, u, v, w, est, st)) return rc;
     return med ? launch_median(est, static_cast<int>(batch), static_cast<int>(e->D), 1, out, st)
                : ST_OK;
+  }
+  if (use_direct(e, batch, 2)) {  // <w, T(u, v, I)> in the time domain (correlate.cu)
+    if (int rc = corr_sync(e, st)) return rc;
+    double* est = out;
+    if (median) {
+      if (int rc = e->est.ensure(batch * e->D * sizeof(double), st)) return rc;
+      est = static_cast<double*>(e->est.p);
+    }
+    if (int rc = corr_estimate(e, batch, u, v, 2, w, est, st)) return rc;
+    return median ? launch_median(est, static_cast<int>(batch), static_cast<int>(e->D), 1, out, st)
+                  : ST_OK;
   }
   if (median) {  // small batches: <w, T(u, v, I)> per family on the cluster estimator, median fused
     const int rc = iuv_fused_ab(e, batch, u, v, 2, 4, out, nullptr, nullptr, st, w);
@@ -608,8 +699,17 @@ int st_engine_deflate(st_engine* e, double weight, const double* u, const double
                                  static_cast<int>(e->D), e->spec, st);
   }
   if (int rc = e->scratch.ensure(e->D * e->plan.P * sizeof(double2), st)) return rc;
+  e->tsk_stale = true;  // rebuilt from the deflated spectra on the next direct estimate
   return launch_deflate(e->plan, e->args(), weight, u, v, w, static_cast<double2*>(e->scratch.p),
                         e->spec, st);
+}
+
+int st_engine_set_path(st_engine* e, int path) {
+  FCS_CHECK_ARG(e != nullptr, "st_engine_set_path: null engine");
+  FCS_CHECK_ARG(path == ST_PATH_AUTO || path == ST_PATH_SPECTRAL || path == ST_PATH_DIRECT,
+                "st_engine_set_path: unknown path");
+  e->path = path;
+  return ST_OK;
 }
 
 }  // extern "C"

@@ -160,6 +160,13 @@ struct st_engine {
   fcs::Scratch scratch, est, vec, vec2;
   fcs::Scratch cnt;  // per-vector arrival counters of the fused cluster tail (kept zero)
   fcs::Scratch est2;  // per-family estimates of the rtpm restart step
+  // time-domain sketches for the direct estimator (correlate.cu): FCS owns a
+  // D x jt copy (rebuilt from spec after a deflation), TS aliases ext
+  double* tsk = nullptr;
+  bool tsk_own = false;
+  bool tsk_stale = false;
+  int path = 0;        // ST_PATH_AUTO / ST_PATH_SPECTRAL / ST_PATH_DIRECT
+  fcs::Scratch corr;   // direct path: Q (batch x D x (2J - 1))
   fcs::EngArgs args() const {
     fcs::EngArgs e{};
     size_t off = 0;
@@ -183,6 +190,16 @@ namespace fcs {
 // apply (the caller runs the separate kernels).
 int engine_iuv_fused(st_engine* e, size_t batch, const double* a, size_t free_mode, int mode,
                      double* out, double* best, int* stopped, cudaStream_t st);
+// Direct (time-domain) estimator, correlate.cu.
+bool corr_feasible(const st_engine* e, size_t free_mode);
+int corr_estimate(st_engine* e, size_t batch, const double* a, const double* b, size_t free_mode,
+                  const double* w, double* est, cudaStream_t st);
+// Whether iuv / uvw over `batch` vectors with this free mode takes the direct
+// path (engine.cu: path override, feasibility, cost rule); rebuilds e->tsk
+// from the spectra when a deflation left it stale.
+bool use_direct(st_engine* e, size_t batch, size_t free_mode);
+int default_path();
+int corr_sync(st_engine* e, cudaStream_t st);
 inline bool is_exact(const st_engine* e) {
   return e->backend == ST_BACKEND_PLAIN || e->backend == ST_BACKEND_HCS ||
          e->backend == ST_BACKEND_CS;

@@ -113,6 +113,17 @@ class _DeviceEngine(ContractionEngine):
     def shape(self) -> List[int]:
         return list(self._shape)
 
+    _PATHS = {"auto": 0, "spectral": 1, "direct": 2}
+
+    def set_path(self, path: str) -> None:
+        """Estimator path of the FCS / TS backends (st_engine_set_path):
+        "spectral" (FFT correlation against the cached spectra), "direct"
+        (the same correlation in the time domain, correlate.cu) or "auto"
+        (the cheaper by the engine's cost rule)."""
+        if path not in self._PATHS:
+            raise ValueError("set_path: unknown path")
+        _check(L.lib().st_engine_set_path(self._h, self._PATHS[path]))
+
     def composed_len(self) -> int:
         """Sketch length: J~ = 3J - 2 (FCS) or J (TS)."""
         return int(L.lib().st_engine_composed_len(self._h))

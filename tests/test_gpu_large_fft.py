@@ -17,6 +17,13 @@ pytestmark = pytest.mark.gpu
 RTOL = 1e-10
 
 
+@pytest.fixture(autouse=True)
+def spectral_path(monkeypatch):
+    """Engines here take the spectral path (the two-level transforms under
+    test); the direct time-domain path has its own tests (test_gpu_correlate)."""
+    monkeypatch.setenv("ST_ENGINE_PATH", "spectral")
+
+
 def rel_close(got, want, rtol=RTOL):
     got = got.detach().cpu().numpy() if torch.is_tensor(got) else np.asarray(got)
     want = np.asarray(want)

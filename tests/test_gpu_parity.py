@@ -31,6 +31,14 @@ def rel_close(got, want, rtol):
     return True
 
 
+@pytest.fixture
+def spectral_path(monkeypatch):
+    """Engines built under this fixture take the spectral (FFT correlation)
+    estimator path: tests of the transform kernels must not be served by the
+    direct time-domain path the cost rule would pick at their sizes."""
+    monkeypatch.setenv("ST_ENGINE_PATH", "spectral")
+
+
 def oracle_family(fam: st.HashFamily):
     return ([fam.pair(n).bucket_map() for n in range(fam.modes())],
             [fam.pair(n).sign_map() for n in range(fam.modes())], fam.hash_lens())
@@ -1042,7 +1050,7 @@ def test_dense_f32_odd_fiber_fixed_point(cuda, shape, J, D):
                                            ((17, 23, 21), 4000, 3, 10),  # M = 12288 (radix 12)
                                            ((25, 20, 16), 1000, 4, 11),  # M = 3072
                                            ((16, 18, 20), 650, 3, 12)])  # M = 2048
-def test_cluster_estimator_vs_oracle(cuda, dims, J, D, seed):
+def test_cluster_estimator_vs_oracle(cuda, spectral_path, dims, J, D, seed):
     """The cluster estimator (spectral_cluster.cu) on both of its transform
     lengths, every free mode (non-cubic, so the contracted-mode tables differ),
     with the median fused in (batch 1 and 3: one wave of clusters) and without
@@ -1074,7 +1082,7 @@ def test_cluster_estimator_vs_oracle(cuda, dims, J, D, seed):
             assert abs(got[b] - want) <= RTOL64 * 2 * abs(want) + 1e-300, (got[b], want)
 
 
-def test_rtpm_cluster_tail_vs_oracle(cuda):
+def test_rtpm_cluster_tail_vs_oracle(cuda, spectral_path):
     """rtpm where both phases take the fused cluster tail (J = 2500 -> M = 8192;
     5 restarts x 5 families and the batch-1 refinement fit one wave): the
     median + row normalisation (restarts) and the refinement update with its
@@ -1097,7 +1105,7 @@ def test_rtpm_cluster_tail_vs_oracle(cuda):
     np.testing.assert_array_equal(cpz._factors_cm[0].t().cpu().numpy(), fz)
 
 
-def test_cluster_estimator_edges_vs_oracle(cuda):
+def test_cluster_estimator_edges_vs_oracle(cuda, spectral_path):
     """Cluster estimator edges: a free mode longer than the early-gather
     registers (nf = 300 > 256), D = 17 (the fused median's general branch),
     the TS engine (the FCS kernels on the J-periodic extension, J = 2500 ->
@@ -1129,7 +1137,7 @@ def test_cluster_estimator_edges_vs_oracle(cuda):
         rel_close(ts.iuv(a, b, f), ots.iuv(a, b, f), 1e-9)
 
 
-def test_cluster_estimator_repeatable(cuda):
+def test_cluster_estimator_repeatable(cuda, spectral_path):
     """Race check for the DSMEM exchanges, cluster barriers and the fused tail:
     100 rounds of back-to-back calls (T(I,u,v) at batch 1 and 4 with the fused
     median, and T(u,v,w)) must all agree with the first result to fp64
