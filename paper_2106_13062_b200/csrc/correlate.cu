@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 
@@ -134,22 +135,36 @@ corr_q_kernel(const double* __restrict__ sk, int jt, const uint32_t* __restrict_
     asm volatile("cp.async.commit_group;\n" ::);
     asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
+    for (int i = threadIdx.x; i < cn * VB; i += TH)  // B' = s_c2(i2) b
+      if (sC[i / VB] < 0) sB[i] = -sB[i];
+    __syncthreads();
+    // software-pipelined rows: the next row's sketch values and B' are loaded
+    // while the current row's KR x VB multiply-adds issue
     const double* sp = sS + threadIdx.x;
-    int h = sH[0];
+    double sv[KR], bv[VB];
+    {
+      const int h0 = sH[0];
+#pragma unroll
+      for (int r = 0; r < KR; ++r) sv[r] = sp[h0 + r * TH];
+#pragma unroll
+      for (int v = 0; v < VB; ++v) bv[v] = sB[v];
+    }
     for (int c = 0; c < cn; ++c) {
-      // the row's sign s_c2(i2) rides on the sketch values (B' = s b)
-      const double sg = sC[c] < 0 ? -1.0 : 1.0;
-      double sv[KR];
+      const int cn1 = min(c + 1, cn - 1);
+      const int h1 = sH[cn1];
+      double sn[KR], bn[VB];
 #pragma unroll
-      for (int r = 0; r < KR; ++r) sv[r] = sg * sp[h + r * TH];
-      h = sH[min(c + 1, cn - 1)];  // next row's bucket in flight during the FMAs
-      const double* bp = sB + c * VB;
+      for (int r = 0; r < KR; ++r) sn[r] = sp[h1 + r * TH];
 #pragma unroll
-      for (int v = 0; v < VB; ++v) {
-        const double bv = bp[v];
+      for (int v = 0; v < VB; ++v) bn[v] = sB[cn1 * VB + v];
 #pragma unroll
-        for (int r = 0; r < KR; ++r) acc[r][v] = fma(sv[r], bv, acc[r][v]);
-      }
+      for (int v = 0; v < VB; ++v)
+#pragma unroll
+        for (int r = 0; r < KR; ++r) acc[r][v] = fma(sv[r], bv[v], acc[r][v]);
+#pragma unroll
+      for (int r = 0; r < KR; ++r) sv[r] = sn[r];
+#pragma unroll
+      for (int v = 0; v < VB; ++v) bv[v] = bn[v];
     }
   }
   double* out = Qp + static_cast<size_t>(ks) * batch * D * K;
@@ -160,6 +175,136 @@ corr_q_kernel(const double* __restrict__ sk, int jt, const uint32_t* __restrict_
 #pragma unroll
     for (int v = 0; v < VB; ++v)
       if (v0 + v < batch) out[(static_cast<size_t>(v0 + v) * D + d) * K + k] = acc[r][v];
+  }
+}
+
+// The same Q partial on the fp64 tensor cores (DMMA, mma.sync m8n8k4.f64):
+// per warp MT x NT tiles of 8 k x 8 vectors, the k dimension of the MMA
+// running over 4 staged rows: A(m, kk) = sk[k + m + h(row kk)] (a Hankel
+// tile gathered from the sketch window), B(kk, n) = B'(row kk, v0 + n).
+// One m8n8k4 is 256 multiply-adds for two fragment loads per lane, so the
+// shared-memory pipe is far from binding and the tensor pipe reaches its
+// rate from 8 warps per SM (tools/microbench/dmma_peak.cu: 36.6 TFLOP/s at
+// 8 warps, while DFMA needs 2 issuing warps per SMSP for 32.5).
+template <int NT, int MT>
+__global__ void __launch_bounds__(128)
+corr_q_mma_kernel(const double* __restrict__ sk, int jt, const uint32_t* __restrict__ packed,
+                  int fam_stride, int tab_c2, int n2, const double* __restrict__ b, int batch,
+                  int D, int K, int ktiles, int ksplit, int J, double* __restrict__ Qp) {
+  constexpr int TH = 128, VB = 8 * NT, KT = 4 * 8 * MT;
+  extern __shared__ __align__(16) unsigned char smem[];
+  int blk = blockIdx.x;
+  const int kt = blk % ktiles;
+  blk /= ktiles;
+  const int d = blk % D;
+  blk /= D;
+  const int ks = blk % ksplit;
+  const int v0 = (blk / ksplit) * VB;
+  const int hlo = static_cast<int>(static_cast<long>(ks) * J / ksplit);
+  const int hhi = static_cast<int>(static_cast<long>(ks + 1) * J / ksplit);
+  const int win = KT + (hhi - hlo) - 1;
+  double* sS = reinterpret_cast<double*>(smem);
+  double* sB = sS + ((win + 1) & ~1);
+  int* sH = reinterpret_cast<int*>(sB + kQChunk * VB);
+  int* sC = sH + kQChunk;
+  __shared__ int s_cnt, s_scan;
+  const int k0 = kt * KT;
+  const double* S = sk + static_cast<size_t>(d) * jt + hlo;
+  for (int i = threadIdx.x; i < win; i += TH) {
+    const int g = k0 + i;
+    if (g + hlo < jt) {
+      const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(sS + i));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(S + g));
+    } else {
+      sS[i] = 0.0;
+    }
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+  const uint32_t* tab = packed + static_cast<size_t>(d) * fam_stride + tab_c2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gm = lane >> 2, tg = lane & 3;  // fragment row / column group
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+  int scan = 0;
+  while (scan < n2) {
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      int cnt = 0;
+      for (; scan < n2 && cnt + 32 <= kQChunk; scan += 32) {
+        const int c = scan + lane;
+        const uint32_t e = c < n2 ? __ldg(tab + c) : 0u;
+        const int h = static_cast<int>(e & 0x7fffffffu);
+        const bool in = c < n2 && h >= hlo && h < hhi;
+        const unsigned m = __ballot_sync(0xffffffffu, in);
+        if (in) {
+          const int pos = cnt + __popc(m & ((1u << lane) - 1));
+          sC[pos] = (e & 0x80000000u) ? -(c + 1) : (c + 1);
+          sH[pos] = h - hlo;
+        }
+        cnt += __popc(m);
+      }
+      if (lane == 0) {
+        s_cnt = cnt;
+        s_scan = scan;
+      }
+    }
+    __syncthreads();
+    scan = s_scan;
+    const int cn = s_cnt;
+    if (cn == 0) continue;
+    const int cn4 = (cn + 3) & ~3;  // rows padded to the MMA depth with B' = 0
+    for (int i = threadIdx.x; i < cn4 * VB; i += TH) {
+      const int r = i / VB, v = i - r * VB;
+      if (r < cn && v0 + v < batch) {
+        const int cs = sC[r];
+        const int c = (cs < 0 ? -cs : cs) - 1;
+        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(sB + i));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
+                     "l"(b + static_cast<size_t>(v0 + v) * n2 + c));
+      } else {
+        sB[i] = 0.0;
+        if (v == 0 && r >= cn) sH[r] = 0;
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncthreads();
+    for (int i = threadIdx.x; i < cn * VB; i += TH)  // B' = s_c2(i2) b
+      if (sC[i / VB] < 0) sB[i] = -sB[i];
+    __syncthreads();
+    const double* sa = sS + warp * 8 * MT + gm;
+    for (int r4 = 0; r4 < cn4; r4 += 4) {
+      const int h = sH[r4 + tg];
+      double bf[NT];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) bf[n] = sB[(r4 + tg) * VB + n * 8 + gm];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        const double af = sa[m * 8 + h];
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+          asm volatile(
+              "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+              : "+d"(acc[m][n][0]), "+d"(acc[m][n][1])
+              : "d"(af), "d"(bf[n]));
+      }
+    }
+  }
+  double* out = Qp + static_cast<size_t>(ks) * batch * D * K;
+#pragma unroll
+  for (int m = 0; m < MT; ++m) {
+    const int k = k0 + warp * 8 * MT + m * 8 + gm;
+    if (k >= K) continue;
+#pragma unroll
+    for (int n = 0; n < NT; ++n)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int v = v0 + n * 8 + 2 * tg + j;
+        if (v < batch) out[(static_cast<size_t>(v) * D + d) * K + k] = acc[m][n][j];
+      }
   }
 }
 
@@ -308,6 +453,27 @@ int launch_q_vb(const double* sk, int jt, const uint32_t* packed, int fam_stride
   return ST_OK;
 }
 
+constexpr int kMmaMt = 8;
+
+template <int NT>
+int launch_q_mma(const double* sk, int jt, const uint32_t* packed, int fam_stride, int tab_c2,
+                 int n2, const double* b, int batch, int D, int K, int J, int ks, double* Qp,
+                 cudaStream_t st) {
+  constexpr int KT = 4 * 8 * kMmaMt;
+  const int ktiles = (K + KT - 1) / KT;
+  const int vblocks = (batch + 8 * NT - 1) / (8 * NT);
+  const int win = KT + (J + ks - 1) / ks;
+  const size_t sm = static_cast<size_t>((win + 1) & ~1) * sizeof(double) +
+                    static_cast<size_t>(kQChunk) * 8 * NT * sizeof(double) +
+                    2 * kQChunk * sizeof(int);
+  auto kern = corr_q_mma_kernel<NT, kMmaMt>;
+  if (int rc = ensure_smem(kern, sm)) return rc;
+  kern<<<static_cast<unsigned>(ktiles) * D * vblocks * ks, 128, sm, st>>>(
+      sk, jt, packed, fam_stride, tab_c2, n2, b, batch, D, K, ktiles, ks, J, Qp);
+  FCS_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
 // Bucket-range splits: enough CTAs for ~12 resident warps per SM, each range
 // at least 32 buckets wide, at most kMaxSplit ranges (the Z kernel reads
 // every split's partial row).
@@ -352,21 +518,30 @@ int corr_estimate(st_engine* e, size_t batch, const double* a, const double* b, 
   const int n2 = g.dims[c2];
   // vector-block width and CTA size: wide blocks (FMA-bound) use 64 threads
   // so the launch still has warps on every SM
-  const int VB = nb >= 12 ? 16 : nb >= 6 ? 8 : nb >= 3 ? 4 : nb == 2 ? 2 : 1;
-  const int TH = VB >= 8 ? 64 : kQMaxThreads;
-  const int ctas = ((K + TH * kQKr - 1) / (TH * kQKr)) * D * ((nb + VB - 1) / VB);
+  // batches of 2+: the tensor-core kernel (vector blocks of 8 or 16); a single
+  // vector: the DFMA kernel (a matrix-vector product, shared-memory bound)
+  const bool mma = nb >= 2 && !std::getenv("ST_CORR_DFMA");
+  const int VB = mma ? (nb > 8 ? 16 : 8) : (nb >= 12 ? 16 : nb >= 6 ? 8 : nb >= 3 ? 4 : nb == 2 ? 2 : 1);
+  const int TH = mma ? 128 : VB >= 8 ? 64 : kQMaxThreads;
+  const int KT = mma ? 4 * 8 * kMmaMt : TH * kQKr;
+  const int ctas = ((K + KT - 1) / KT) * D * ((nb + VB - 1) / VB);
   const int ks = q_split(ctas, TH / 32, J, di.sm_count);
   const size_t qstride = batch * e->D * K;
   if (int rc = e->corr.ensure(ks * qstride * sizeof(double), st)) return rc;
   auto* Qp = static_cast<double*>(e->corr.p);
   const int tab = g.tab_off[c2];
   int rc;
-  switch (VB) {
-    case 16: rc = launch_q_vb<64, 16>(sk, jt, g.packed, g.fam_stride, tab, n2, b, nb, D, K, J, ks, Qp, st); break;
-    case 8: rc = launch_q_vb<64, 8>(sk, jt, g.packed, g.fam_stride, tab, n2, b, nb, D, K, J, ks, Qp, st); break;
-    case 4: rc = launch_q_vb<kQMaxThreads, 4>(sk, jt, g.packed, g.fam_stride, tab, n2, b, nb, D, K, J, ks, Qp, st); break;
-    case 2: rc = launch_q_vb<kQMaxThreads, 2>(sk, jt, g.packed, g.fam_stride, tab, n2, b, nb, D, K, J, ks, Qp, st); break;
-    default: rc = launch_q_vb<kQMaxThreads, 1>(sk, jt, g.packed, g.fam_stride, tab, n2, b, nb, D, K, J, ks, Qp, st); break;
+  if (mma) {
+    rc = VB == 16 ? launch_q_mma<2>(sk, jt, g.packed, g.fam_stride, tab, n2, b, nb, D, K, J, ks, Qp, st)
+                  : launch_q_mma<1>(sk, jt, g.packed, g.fam_stride, tab, n2, b, nb, D, K, J, ks, Qp, st);
+  } else {
+    switch (VB) {
+      case 16: rc = launch_q_vb<64, 16>(sk, jt, g.packed, g.fam_stride, tab, n2, b, nb, D, K, J, ks, Qp, st); break;
+      case 8: rc = launch_q_vb<64, 8>(sk, jt, g.packed, g.fam_stride, tab, n2, b, nb, D, K, J, ks, Qp, st); break;
+      case 4: rc = launch_q_vb<kQMaxThreads, 4>(sk, jt, g.packed, g.fam_stride, tab, n2, b, nb, D, K, J, ks, Qp, st); break;
+      case 2: rc = launch_q_vb<kQMaxThreads, 2>(sk, jt, g.packed, g.fam_stride, tab, n2, b, nb, D, K, J, ks, Qp, st); break;
+      default: rc = launch_q_vb<kQMaxThreads, 1>(sk, jt, g.packed, g.fam_stride, tab, n2, b, nb, D, K, J, ks, Qp, st); break;
+    }
   }
   if (rc) return rc;
   const int n1 = g.dims[c1], nf = g.dims[free_mode];

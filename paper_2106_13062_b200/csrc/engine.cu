@@ -74,11 +74,12 @@ int default_path() {
 
 // Cost rule of the direct path, fitted to the measured A/B of both paths on
 // one B200 (profiles/corr_sweep_r02.txt: I^3 tensors, I = 50-400, J =
-// 300-4000, D = 10, batch 1 and 15; times in us, F = (2J - 1) I_c2 + I_f I_c1
-// multiply-adds per item, P the transform length). The spectral path costs
-// about one transform latency per wave of items (~one item per SM), the
-// direct path a launch floor plus F at a fraction of the DFMA rate; the
-// direct path wins where I is small against J (e.g. I = 50, J >= 1000).
+// 300-4000, D = 10, batches 1 and 15; model times in us). Fq = (2J - 1) I_c2
+// multiply-adds of the Hankel product (tensor cores for batches of 2+,
+// shared-memory bound for one vector), Fz = I_f I_c1 gathered multiply-adds
+// of the readout, per (vector, family) item. The spectral path costs about
+// one transform latency per wave of items (~one item per SM). The direct
+// path wins where I is small against J (batch 15: I <= 100 with J >= 1000).
 bool use_direct(st_engine* e, size_t batch, size_t free_mode) {
   if (is_exact(e) || batch == 0 || e->tsk == nullptr) return false;
   if (e->path == ST_PATH_SPECTRAL) return false;
@@ -88,13 +89,17 @@ bool use_direct(st_engine* e, size_t batch, size_t free_mode) {
   int c1, c2;
   contracted(free_mode, &c1, &c2);
   const double J = static_cast<double>(e->hash_len);
-  const double F = (2 * J - 1) * static_cast<double>(e->dims[c2]) +
-                   static_cast<double>(e->dims[free_mode]) * static_cast<double>(e->dims[c1]);
+  const double Fq = (2 * J - 1) * static_cast<double>(e->dims[c2]);
+  const double Fz = static_cast<double>(e->dims[free_mode]) * static_cast<double>(e->dims[c1]);
   const double P = static_cast<double>(e->plan.P);
   const double items = static_cast<double>(batch) * static_cast<double>(e->D);
-  if (batch == 1) return 14.0 + 6.5e-6 * F * std::max(1.0, items / 10.0) < 10.4 + 6.5e-4 * P;
+  if (batch == 1) {
+    const double direct = 13.0 + (2.7e-6 * Fq + 6e-5 * Fz) * std::max(1.0, items / 10.0) + 1.5e-3 * J;
+    const double spectral = P < 2048 ? 18.5 : 10.4 + 6.5e-4 * P;
+    return direct < spectral;
+  }
   const double waves = std::max(1.0, std::ceil(items / 148.0));
-  return 20.0 + 3.3e-5 * F * items / 150.0 < (17.0 + 2.5e-3 * P) * waves;
+  return 17.0 + (1.7e-5 * Fq + 2.9e-4 * Fz) * items / 150.0 < (17.0 + 2.5e-3 * P) * waves;
 }
 
 int corr_sync(st_engine* e, cudaStream_t st) {

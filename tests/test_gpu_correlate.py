@@ -162,3 +162,20 @@ def test_rtpm_paths_vs_oracle(cuda, monkeypatch, path):
     rel_close(cp.weights, w, 1e-8)
     rel_close(cp._factors_cm[0].t(), f, 1e-8)
     assert np.allclose(np.sort(w)[::-1], [3.0, 2.0, 1.5], atol=0.15)
+
+
+@pytest.mark.parametrize("kernel", ["mma", "dfma"])
+def test_direct_q_kernels_agree(cuda, monkeypatch, kernel):
+    """Batches of 2+ build Q on the fp64 tensor cores (DMMA); ST_CORR_DFMA
+    selects the DFMA kernel (vector blocks 2, 4, 8, 16) — both match the oracle."""
+    if kernel == "dfma":
+        monkeypatch.setenv("ST_CORR_DFMA", "1")
+    rng = np.random.default_rng(41)
+    dims = (27, 33, 45)
+    t = rng.standard_normal(dims)
+    eng, oeng = _engines(t, 1200, 4, 17)
+    for n in (2, 3, 7, 9, 16, 33):
+        A, B = rng.standard_normal((n, 33)), rng.standard_normal((n, 45))
+        got = eng.iuv_batch(A, B, 0).cpu().numpy()
+        for b in sorted({0, n - 1}):
+            rel_close(got[b], oeng.iuv(A[b], B[b], 0), RTOL64)
