@@ -550,6 +550,15 @@ def secondary(x=None, cpu=True):
         pipe_iuv1 = pipelined_ms(lambda: iuv_call(1), 6000)
     ms_uvw = median_ms(uvw_call, 20)
     ms_uvw1 = median_ms(lambda: uvw_call(1), 20)
+    # the same steps on the direct time-domain path (correlate.cu), which the
+    # engine's cost rule does not pick at this geometry: the measured A/B
+    eng.set_path("direct")
+    ab = {"path_taken": "spectral (engine.cu use_direct cost rule)",
+          "direct_iuv_step_pipelined_ms": pipelined_ms(iuv_call, 300),
+          "direct_iuv_batch1_pipelined_ms": pipelined_ms(lambda: iuv_call(1), 300),
+          "direct_uvw_step_pipelined_ms": pipelined_ms(uvw_call, 300)}
+    eng.set_path("auto")
+    ab["spectral_iuv_step_pipelined_ms"] = pipelined_ms(iuv_call, 300)
     ms_defl = median_ms(lambda: L.check(lib.st_engine_deflate(
         eng._h, C.c_double(0.0), C.c_void_p(U.data_ptr()), C.c_void_p(U.data_ptr()),
         C.c_void_p(U.data_ptr()), sp)), 10)
@@ -578,7 +587,7 @@ def secondary(x=None, cpu=True):
                           "clocks": clk3.summary()},
          "uvw_step_ms": ms_uvw, "uvw_batch1_ms": ms_uvw1,
          "deflate_ms": ms_defl, "rtpm_total_s": t_rtpm, "rtpm_timing": "second call (warm), host wall",
-         "rtpm_breakdown_model": model, "seed": c.seed,
+         "rtpm_breakdown_model": model, "estimator_paths_ab": ab, "seed": c.seed,
          "weights": [round(float(v), 6) for v in cpd.weights.cpu().numpy()]}
     if ref is not None:
         reng = ref.Engine(t, c.hash_len, c.sketch_count, c.seed)

@@ -37,6 +37,7 @@
 #include <mutex>
 
 #include "engine.cuh"
+#include "median.cuh"
 
 namespace fcs {
 namespace {
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(kZThreads)
 corr_z_kernel(const double* __restrict__ Qp, int ksplit, size_t qstride, int K,
               const uint32_t* __restrict__ packed, int fam_stride, int tab_c1, int n1, int tab_f,
               int nf, const double* __restrict__ a, int D, const double* __restrict__ w, int G,
-              double* __restrict__ est) {
+              double* __restrict__ est, IuvTail tail) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* sQ = reinterpret_cast<double*>(smem);
   double2* sAH = reinterpret_cast<double2*>(sQ + ((K + 1) & ~1));  // {a', bucket}
@@ -403,6 +404,53 @@ corr_z_kernel(const double* __restrict__ Qp, int ksplit, size_t qstride, int K,
       double s2 = 0.0;
       for (int k = 0; k < kZThreads / 32; ++k) s2 += red[k];
       est[item] = s2;
+    }
+  }
+  if (tail.mode != 0) {
+    // The last of vector v's D x G CTAs (per-vector arrival counter) takes the
+    // median over the families and, by mode, normalises the row (rtpm
+    // restart step) or applies the refinement update (cpd.cpp:266-270) —
+    // the cluster estimator's IuvTail (spectral_cluster.cu), one CTA here.
+    __shared__ int last;
+    __shared__ double red2[kZThreads / 32];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int old = atomicAdd(tail.cnt + v, 1);
+      const int is_last = old == D * G - 1;
+      if (is_last) tail.cnt[v] = 0;  // ready for the next launch
+      last = is_last;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (tail.mode == 3 && *reinterpret_cast<volatile int*>(tail.stopped)) return;
+    const int nt = MODE == 1 ? 1 : nf;
+    const double* col0 = est + static_cast<size_t>(v) * D * nt;
+    double* ob = tail.out + static_cast<size_t>(v) * nt;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < nt; i += kZThreads) {
+      const double m = median_col(col0 + i, D, nt, [](const double* p) { return __ldcg(p); });
+      ob[i] = m;
+      acc += m * m;
+    }
+    if (tail.mode == 1 || tail.mode == 4) return;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red2[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    double tot = 0.0;
+#pragma unroll
+    for (int k = 0; k < kZThreads / 32; ++k) tot += red2[k];
+    const double nv = sqrt(tot);
+    if (tail.mode == 2) {
+      for (int i = threadIdx.x; i < nf; i += kZThreads) ob[i] = nv < 1e-150 ? 0.0 : ob[i] / nv;
+    } else {
+      if (nv < 1e-150) {
+        if (threadIdx.x == 0) *tail.stopped = 1;
+        return;
+      }
+      for (int i = threadIdx.x; i < nf; i += kZThreads) tail.best[i] = ob[i] / nv;
     }
   }
 }
@@ -503,7 +551,7 @@ bool corr_feasible(const st_engine* e, size_t free_mode) {
 // est = per-family estimates (batch x D x nf), or with w != nullptr the
 // per-family T(a, b, w) (batch x D); needs e->tsk current.
 int corr_estimate(st_engine* e, size_t batch, const double* a, const double* b, size_t free_mode,
-                  const double* w, double* est, cudaStream_t st) {
+                  const double* w, double* est, cudaStream_t st, const IuvTail* tail) {
   int c1, c2;
   contracted(free_mode, &c1, &c2);
   DeviceInfo di;
@@ -548,18 +596,23 @@ int corr_estimate(st_engine* e, size_t batch, const double* a, const double* b, 
   const size_t sm = z_smem(K, n1, nf);
   const int items = nb * D;
   // few items (the rtpm refinement): split each item's outputs over G CTAs
-  const int G = w ? 1 : std::max(1, std::min((di.sm_count + items - 1) / items, (nf + 31) / 32));
+  // split each item's outputs over G CTAs so the launch fills the SMs evenly
+  // (2 co-resident CTAs per SM): few items (the rtpm refinement) and item
+  // counts just above the SM count (config 3's 150 on 148 SMs)
+  const int G = w ? 1 : std::max(1, std::min((2 * di.sm_count + items / 2) / items, (nf + 31) / 32));
+  IuvTail tl;
+  if (tail) tl = *tail;
   const unsigned grid = static_cast<unsigned>(items) * G;
   if (w) {
     if (int rc2 = ensure_smem(corr_z_kernel<1>, sm)) return rc2;
     corr_z_kernel<1><<<grid, kZThreads, sm, st>>>(Qp, ks, qstride, K, g.packed, g.fam_stride,
                                                  g.tab_off[c1], n1, g.tab_off[free_mode], nf, a,
-                                                 D, w, G, est);
+                                                 D, w, G, est, tl);
   } else {
     if (int rc2 = ensure_smem(corr_z_kernel<0>, sm)) return rc2;
     corr_z_kernel<0><<<grid, kZThreads, sm, st>>>(Qp, ks, qstride, K, g.packed, g.fam_stride,
                                                  g.tab_off[c1], n1, g.tab_off[free_mode], nf, a,
-                                                 D, nullptr, G, est);
+                                                 D, nullptr, G, est, tl);
   }
   FCS_CUDA_TRY(cudaGetLastError());
   return ST_OK;

@@ -43,8 +43,9 @@ namespace fcs {
 static int iuv_fused_ab(st_engine* e, size_t batch, const double* a, const double* b, size_t free_mode,
                  int mode, double* out, double* best, int* stopped, cudaStream_t st,
                  const double* wvec = nullptr) {
-  if (is_exact(e) || e->plan.large_p1 || batch == 0) return 1;
-  if (use_direct(e, batch, free_mode)) return 1;  // the caller's separate kernels run it
+  if (is_exact(e) || batch == 0) return 1;
+  const bool direct = use_direct(e, batch, free_mode);
+  if (e->plan.large_p1 && !direct) return 1;
   int c1, c2;
   contracted(free_mode, &c1, &c2);
   const size_t nf = e->dims[free_mode];
@@ -59,6 +60,11 @@ static int iuv_fused_ab(st_engine* e, size_t batch, const double* a, const doubl
   t.best = best;
   t.stopped = stopped;
   t.wvec = wvec;
+  if (direct) {  // the time-domain estimator with the same fused tail
+    if (int rc = corr_sync(e, st)) return rc;
+    return corr_estimate(e, batch, a, b, free_mode, mode == 4 ? wvec : nullptr,
+                         static_cast<double*>(e->est.p), st, &t);
+  }
   return launch_iuv_cluster(e->plan, e->args(), static_cast<int>(batch), a, b, c1, c2,
                             static_cast<int>(free_mode), static_cast<double*>(e->est.p), t, st);
 }
@@ -77,7 +83,7 @@ int default_path() {
 // 300-4000, D = 10, batches 1 and 15; model times in us). Fq = (2J - 1) I_c2
 // multiply-adds of the Hankel product (tensor cores for batches of 2+,
 // shared-memory bound for one vector), Fz = I_f I_c1 gathered multiply-adds
-// of the readout, per (vector, family) item. The spectral path costs about
+// of the readout, per (vector, family) item; M the real transform length. The spectral path costs about
 // one transform latency per wave of items (~one item per SM). The direct
 // path wins where I is small against J (batch 15: I <= 100 with J >= 1000).
 bool use_direct(st_engine* e, size_t batch, size_t free_mode) {
@@ -91,15 +97,17 @@ bool use_direct(st_engine* e, size_t batch, size_t free_mode) {
   const double J = static_cast<double>(e->hash_len);
   const double Fq = (2 * J - 1) * static_cast<double>(e->dims[c2]);
   const double Fz = static_cast<double>(e->dims[free_mode]) * static_cast<double>(e->dims[c1]);
-  const double P = static_cast<double>(e->plan.P);
+  const double M = static_cast<double>(e->plan.M);  // real transform length
   const double items = static_cast<double>(batch) * static_cast<double>(e->D);
   if (batch == 1) {
     const double direct = 13.0 + (2.7e-6 * Fq + 6e-5 * Fz) * std::max(1.0, items / 10.0) + 1.5e-3 * J;
-    const double spectral = P < 2048 ? 18.5 : 10.4 + 6.5e-4 * P;
+    const double spectral = M < 4096 ? 18.5 : 10.4 + 6.5e-4 * M;
     return direct < spectral;
   }
-  const double waves = std::max(1.0, std::ceil(items / 148.0));
-  return 17.0 + (1.7e-5 * Fq + 2.9e-4 * Fz) * items / 150.0 < (17.0 + 2.5e-3 * P) * waves;
+  // the spectral step splits a batch beyond one item per SM between the
+  // one-CTA kernel and clusters on a side stream: no whole extra wave
+  const double load = std::max(1.0, items / 160.0);
+  return 17.0 + (1.7e-5 * Fq + 2.9e-4 * Fz) * items / 150.0 < (17.0 + 2.5e-3 * M) * load;
 }
 
 int corr_sync(st_engine* e, cudaStream_t st) {
@@ -556,16 +564,9 @@ int st_engine_iuv(st_engine* e, size_t batch, const double* a, const double* b, 
                : ST_OK;
   }
   if (use_direct(e, batch, free_mode)) {  // time-domain correlation (correlate.cu)
+    if (median) return iuv_fused_ab(e, batch, a, b, free_mode, 1, out, nullptr, nullptr, st);
     if (int rc = corr_sync(e, st)) return rc;
-    double* est = out;
-    if (median) {
-      if (int rc = e->est.ensure(batch * e->D * nf * sizeof(double), st)) return rc;
-      est = static_cast<double*>(e->est.p);
-    }
-    if (int rc = corr_estimate(e, batch, a, b, free_mode, nullptr, est, st)) return rc;
-    return median ? launch_median(est, static_cast<int>(batch), static_cast<int>(e->D),
-                                  static_cast<int>(nf), out, st)
-                  : ST_OK;
+    return corr_estimate(e, batch, a, b, free_mode, nullptr, out, st);
   }
   if (median) {  // small batches: cluster estimator with the median fused in
     const int rc = iuv_fused_ab(e, batch, a, b, free_mode, 1, out, nullptr, nullptr, st);
@@ -604,15 +605,9 @@ int st_engine_uvw(st_engine* e, size_t batch, const double* u, const double* v, 
                : ST_OK;
   }
   if (use_direct(e, batch, 2)) {  // <w, T(u, v, I)> in the time domain (correlate.cu)
+    if (median) return iuv_fused_ab(e, batch, u, v, 2, 4, out, nullptr, nullptr, st, w);
     if (int rc = corr_sync(e, st)) return rc;
-    double* est = out;
-    if (median) {
-      if (int rc = e->est.ensure(batch * e->D * sizeof(double), st)) return rc;
-      est = static_cast<double*>(e->est.p);
-    }
-    if (int rc = corr_estimate(e, batch, u, v, 2, w, est, st)) return rc;
-    return median ? launch_median(est, static_cast<int>(batch), static_cast<int>(e->D), 1, out, st)
-                  : ST_OK;
+    return corr_estimate(e, batch, u, v, 2, w, out, st);
   }
   if (median) {  // small batches: <w, T(u, v, I)> per family on the cluster estimator, median fused
     const int rc = iuv_fused_ab(e, batch, u, v, 2, 4, out, nullptr, nullptr, st, w);

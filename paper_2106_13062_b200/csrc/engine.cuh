@@ -192,8 +192,11 @@ int engine_iuv_fused(st_engine* e, size_t batch, const double* a, size_t free_mo
                      double* out, double* best, int* stopped, cudaStream_t st);
 // Direct (time-domain) estimator, correlate.cu.
 bool corr_feasible(const st_engine* e, size_t free_mode);
+// With a tail (mode 1-4, IuvTail of fft.cuh) the median over the families
+// (and the rtpm row normalisation / refinement update) is fused into the
+// readout kernel; tail->cnt must hold `batch` zeroed counters.
 int corr_estimate(st_engine* e, size_t batch, const double* a, const double* b, size_t free_mode,
-                  const double* w, double* est, cudaStream_t st);
+                  const double* w, double* est, cudaStream_t st, const IuvTail* tail = nullptr);
 // Whether iuv / uvw over `batch` vectors with this free mode takes the direct
 // path (engine.cu: path override, feasibility, cost rule); rebuilds e->tsk
 // from the spectra when a deflation left it stale.
