@@ -179,3 +179,16 @@ def test_direct_q_kernels_agree(cuda, monkeypatch, kernel):
         got = eng.iuv_batch(A, B, 0).cpu().numpy()
         for b in sorted({0, n - 1}):
             rel_close(got[b], oeng.iuv(A[b], B[b], 0), RTOL64)
+
+
+def test_direct_fused_tail_underflow(cuda, monkeypatch):
+    """The direct path's fused tail on a zero tensor: every restart row
+    underflows to 0 (normalisation branch) and the refinement stops at once
+    (sticky flag) — weights and factors equal the oracle rtpm bit for bit."""
+    monkeypatch.setenv("ST_ENGINE_PATH", "direct")
+    z = np.zeros((12, 12, 12))
+    cpz = st.rtpm(st.DenseTensor.from_array(z), st.RtpmConfig(2, 3, 4, st.SketchBackend.FCS,
+                                                             st.EstimatorConfig(300, 3, 5)))
+    wz, fz = O.rtpm(O.FcsEngine(z, 300, 3, 5), 12, 2, 3, 4, 5)
+    np.testing.assert_array_equal(cpz.weights.cpu().numpy(), wz)
+    np.testing.assert_array_equal(cpz._factors_cm[0].t().cpu().numpy(), fz)
