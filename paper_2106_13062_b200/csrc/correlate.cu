@@ -37,7 +37,7 @@
 #include <mutex>
 
 #include "engine.cuh"
-#include "median.cuh"
+#include "tail.cuh"
 
 namespace fcs {
 namespace {
@@ -323,7 +323,7 @@ corr_z_kernel(const double* __restrict__ Qp, int ksplit, size_t qstride, int K,
   double* sQ = reinterpret_cast<double*>(smem);
   double2* sAH = reinterpret_cast<double2*>(sQ + ((K + 1) & ~1));  // {a', bucket}
   double* sPart = reinterpret_cast<double*>(sAH + n1);               // [P][W]
-  __shared__ double red[kZThreads / 32];
+  __shared__ double red[kZThreads / 32 + 1];
   const int item = blockIdx.x / G, g = blockIdx.x - item * G;  // G CTAs split the outputs
   const int v = item / D, d = item - v * D;
   const int nfg = (nf + G - 1) / G;
@@ -406,53 +406,8 @@ corr_z_kernel(const double* __restrict__ Qp, int ksplit, size_t qstride, int K,
       est[item] = s2;
     }
   }
-  if (tail.mode != 0) {
-    // The last of vector v's D x G CTAs (per-vector arrival counter) takes the
-    // median over the families and, by mode, normalises the row (rtpm
-    // restart step) or applies the refinement update (cpd.cpp:266-270) —
-    // the cluster estimator's IuvTail (spectral_cluster.cu), one CTA here.
-    __shared__ int last;
-    __shared__ double red2[kZThreads / 32];
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const int old = atomicAdd(tail.cnt + v, 1);
-      const int is_last = old == D * G - 1;
-      if (is_last) tail.cnt[v] = 0;  // ready for the next launch
-      last = is_last;
-    }
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    if (tail.mode == 3 && *reinterpret_cast<volatile int*>(tail.stopped)) return;
-    const int nt = MODE == 1 ? 1 : nf;
-    const double* col0 = est + static_cast<size_t>(v) * D * nt;
-    double* ob = tail.out + static_cast<size_t>(v) * nt;
-    double acc = 0.0;
-    for (int i = threadIdx.x; i < nt; i += kZThreads) {
-      const double m = median_col(col0 + i, D, nt, [](const double* p) { return __ldcg(p); });
-      ob[i] = m;
-      acc += m * m;
-    }
-    if (tail.mode == 1 || tail.mode == 4) return;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) red2[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    double tot = 0.0;
-#pragma unroll
-    for (int k = 0; k < kZThreads / 32; ++k) tot += red2[k];
-    const double nv = sqrt(tot);
-    if (tail.mode == 2) {
-      for (int i = threadIdx.x; i < nf; i += kZThreads) ob[i] = nv < 1e-150 ? 0.0 : ob[i] / nv;
-    } else {
-      if (nv < 1e-150) {
-        if (threadIdx.x == 0) *tail.stopped = 1;
-        return;
-      }
-      for (int i = threadIdx.x; i < nf; i += kZThreads) tail.best[i] = ob[i] / nv;
-    }
-  }
+  if (tail.mode != 0)  // the last of vector v's D x G CTAs: median (+ normalise / refine)
+    estimator_tail<kZThreads>(tail, est, v, D, MODE == 1 ? 1 : nf, D * G, red);
 }
 
 std::mutex g_mu;

@@ -61,10 +61,15 @@ static int iuv_fused_ab(st_engine* e, size_t batch, const double* a, const doubl
   t.stopped = stopped;
   t.wvec = wvec;
   if (direct) {  // the time-domain estimator with the same fused tail
+    if (e->D > 16) return 1;  // the tail's register median: callers run the separate kernels
     if (int rc = corr_sync(e, st)) return rc;
     return corr_estimate(e, batch, a, b, free_mode, mode == 4 ? wvec : nullptr,
                          static_cast<double*>(e->est.p), st, &t);
   }
+  // beyond one wave of clusters the caller's separate kernels run (a tail
+  // fused into the split one-CTA + cluster step measured slower: the join
+  // directly followed by the next call's fork serialises the two parts,
+  // tools/experiments/iuv_fused_median.patch)
   return launch_iuv_cluster(e->plan, e->args(), static_cast<int>(batch), a, b, c1, c2,
                             static_cast<int>(free_mode), static_cast<double*>(e->est.p), t, st);
 }
@@ -564,9 +569,15 @@ int st_engine_iuv(st_engine* e, size_t batch, const double* a, const double* b, 
                : ST_OK;
   }
   if (use_direct(e, batch, free_mode)) {  // time-domain correlation (correlate.cu)
-    if (median) return iuv_fused_ab(e, batch, a, b, free_mode, 1, out, nullptr, nullptr, st);
+    if (median && e->D <= 16)
+      return iuv_fused_ab(e, batch, a, b, free_mode, 1, out, nullptr, nullptr, st);
     if (int rc = corr_sync(e, st)) return rc;
-    return corr_estimate(e, batch, a, b, free_mode, nullptr, out, st);
+    if (!median) return corr_estimate(e, batch, a, b, free_mode, nullptr, out, st);
+    if (int rc = e->est.ensure(batch * e->D * nf * sizeof(double), st)) return rc;
+    double* est = static_cast<double*>(e->est.p);
+    if (int rc = corr_estimate(e, batch, a, b, free_mode, nullptr, est, st)) return rc;
+    return launch_median(est, static_cast<int>(batch), static_cast<int>(e->D),
+                         static_cast<int>(nf), out, st);
   }
   if (median) {  // small batches: cluster estimator with the median fused in
     const int rc = iuv_fused_ab(e, batch, a, b, free_mode, 1, out, nullptr, nullptr, st);
@@ -605,9 +616,13 @@ int st_engine_uvw(st_engine* e, size_t batch, const double* u, const double* v, 
                : ST_OK;
   }
   if (use_direct(e, batch, 2)) {  // <w, T(u, v, I)> in the time domain (correlate.cu)
-    if (median) return iuv_fused_ab(e, batch, u, v, 2, 4, out, nullptr, nullptr, st, w);
+    if (median && e->D <= 16) return iuv_fused_ab(e, batch, u, v, 2, 4, out, nullptr, nullptr, st, w);
     if (int rc = corr_sync(e, st)) return rc;
-    return corr_estimate(e, batch, u, v, 2, w, out, st);
+    if (!median) return corr_estimate(e, batch, u, v, 2, w, out, st);
+    if (int rc = e->est.ensure(batch * e->D * sizeof(double), st)) return rc;
+    double* est = static_cast<double*>(e->est.p);
+    if (int rc = corr_estimate(e, batch, u, v, 2, w, est, st)) return rc;
+    return launch_median(est, static_cast<int>(batch), static_cast<int>(e->D), 1, out, st);
   }
   if (median) {  // small batches: <w, T(u, v, I)> per family on the cluster estimator, median fused
     const int rc = iuv_fused_ab(e, batch, u, v, 2, 4, out, nullptr, nullptr, st, w);

@@ -89,4 +89,37 @@ __device__ __forceinline__ double median_col(const double* col, int D, int len, 
   return (D & 1) ? v[D / 2] : 0.5 * (v[D / 2 - 1] + v[D / 2]);
 }
 
+// median_col for D <= 16 with at most a 16-entry local array (the
+// non-finite fallback): for kernels whose stack frame must stay small
+// (the fused tails of the one-CTA estimators share SMs with the cluster
+// kernel; median_col's 64-entry sort array doubled the one-CTA kernel's
+// stack and broke that co-residency — measured).
+template <typename Ld>
+__device__ __forceinline__ double median_col16(const double* col, int D, int len, Ld ld) {
+  double r;
+  bool ok = false;
+  switch (D) {
+#define FCS_MEDIAN_CASE(n) \
+  case n: ok = median_regs<n>(col, D, len, &r, ld); break;
+    FCS_MEDIAN_CASE(1) FCS_MEDIAN_CASE(2) FCS_MEDIAN_CASE(3) FCS_MEDIAN_CASE(4)
+    FCS_MEDIAN_CASE(5) FCS_MEDIAN_CASE(6) FCS_MEDIAN_CASE(7) FCS_MEDIAN_CASE(8)
+    FCS_MEDIAN_CASE(9) FCS_MEDIAN_CASE(10) FCS_MEDIAN_CASE(11) FCS_MEDIAN_CASE(12)
+    FCS_MEDIAN_CASE(13) FCS_MEDIAN_CASE(14) FCS_MEDIAN_CASE(15) FCS_MEDIAN_CASE(16)
+#undef FCS_MEDIAN_CASE
+    default: break;
+  }
+  if (ok) return r;
+  double v[16];  // the same insertion sort as median_col's fallback
+  for (int d = 0; d < D; ++d) {
+    const double x = ld(col + static_cast<size_t>(d) * len);
+    int k = d;
+    while (k > 0 && v[k - 1] > x) {
+      v[k] = v[k - 1];
+      --k;
+    }
+    v[k] = x;
+  }
+  return (D & 1) ? v[D / 2] : 0.5 * (v[D / 2 - 1] + v[D / 2]);
+}
+
 }  // namespace fcs

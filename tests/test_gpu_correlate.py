@@ -31,7 +31,8 @@ def _engines(t, J, D, seed, backend="fcs"):
                                            ((20, 26, 31), 3000, 4, 8),
                                            ((300, 270, 40), 700, 3, 9),    # chunks of 256 rows
                                            ((17, 23, 21), 1, 3, 10),       # J = 1: K = 1
-                                           ((5, 3, 4), 2, 2, 11)])
+                                           ((5, 3, 4), 2, 2, 11),
+                                           ((14, 12, 10), 500, 17, 12)])  # D > 16: separate median
 def test_direct_vs_oracle_every_mode_and_batch(cuda, dims, J, D, seed):
     """Every free mode (non-cubic, so the three tables differ), batch sizes that
     take each vector-block width (1, 2, 4, 8, 16) and several vector blocks,
