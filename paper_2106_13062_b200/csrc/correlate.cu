@@ -550,11 +550,32 @@ int corr_estimate(st_engine* e, size_t batch, const double* a, const double* b, 
   const int n1 = g.dims[c1], nf = g.dims[free_mode];
   const size_t sm = z_smem(K, n1, nf);
   const int items = nb * D;
-  // few items (the rtpm refinement): split each item's outputs over G CTAs
-  // split each item's outputs over G CTAs so the launch fills the SMs evenly
-  // (2 co-resident CTAs per SM): few items (the rtpm refinement) and item
-  // counts just above the SM count (config 3's 150 on 148 SMs)
-  const int G = w ? 1 : std::max(1, std::min((2 * di.sm_count + items / 2) / items, (nf + 31) / 32));
+  // few items (the rtpm refinement): split each item's outputs over G CTAs,
+  // as many as keep the launch within ONE wave of resident CTAs (a launch a
+  // few CTAs past a wave doubles its span: config 3's 150 items x 2 groups =
+  // 300 CTAs on 296 slots measured 19 us, one group 150 CTAs ...)
+  int occ = 1;
+  {
+    static std::mutex mu;
+    static std::map<std::pair<int, size_t>, int> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto key = std::make_pair(di.device * 2 + (w ? 1 : 0), sm);
+    auto it = cache.find(key);
+    if (it == cache.end()) {
+      int n = 0;
+      if (w) {
+        if (int rc2 = ensure_smem(corr_z_kernel<1>, sm)) return rc2;
+        FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, corr_z_kernel<1>, kZThreads, sm));
+      } else {
+        if (int rc2 = ensure_smem(corr_z_kernel<0>, sm)) return rc2;
+        FCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, corr_z_kernel<0>, kZThreads, sm));
+      }
+      it = cache.emplace(key, std::max(n, 1)).first;
+    }
+    occ = it->second;
+  }
+  const int slots = occ * di.sm_count;
+  const int G = w ? 1 : std::max(1, std::min(slots / std::max(items, 1), (nf + 31) / 32));
   IuvTail tl;
   if (tail) tl = *tail;
   const unsigned grid = static_cast<unsigned>(items) * G;
