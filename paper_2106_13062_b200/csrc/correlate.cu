@@ -357,6 +357,33 @@ corr_z_kernel(const double* __restrict__ Qp, int ksplit, size_t qstride, int K,
     sAH[c] = make_double2((e & 0x80000000u) ? -x : x,
                           __hiloint2double(0, static_cast<int>(e & 0x7fffffffu)));
   }
+  // Lane order of the outputs: the gather of output i at row c reads
+  // sQ[h_f(i) + h_c1(c)], whose 8-byte bank is (h_f(i) + h_c1(c)) mod 16 — the
+  // row shifts every lane's bank alike, so outputs dealt round-robin over the
+  // 16 classes h_f(i) mod 16 keep each warp's 32 gathers at ~2 lanes per bank
+  // (random outputs: ~4.5 wavefronts per gather). Any order gives the same
+  // sums (each output is summed by one thread in row order).
+  __shared__ int cls_cnt[16];
+  const int ne = ie - ib;
+  int* sRank = reinterpret_cast<int*>(sPart + kZThreads);  // (class << 16 | rank) per output
+  int* sOrd = sRank + ne;                                   // position -> output
+  if (threadIdx.x < 16) cls_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  for (int k = threadIdx.x; k < ne; k += kZThreads) {
+    const int cls = static_cast<int>(__ldg(tabf + ib + k) & 15u);
+    sRank[k] = (cls << 16) | atomicAdd(&cls_cnt[cls], 1);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < ne; k += kZThreads) {
+    const int cls = sRank[k] >> 16, j = sRank[k] & 0xffff;
+    int pos = 0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int n = cls_cnt[q];
+      pos += min(j, n) + (q < cls && n > j ? 1 : 0);
+    }
+    sOrd[pos] = ib + k;
+  }
   __syncthreads();
   const int W = max(1, min(ie - ib, kZThreads));
   const int P = kZThreads / W;
@@ -365,7 +392,7 @@ corr_z_kernel(const double* __restrict__ Qp, int ksplit, size_t qstride, int K,
   const int cb = min(n1, p * per), ce = min(n1, cb + per);
   double part_w = 0.0;
   for (int i0 = ib; i0 < ie; i0 += W) {
-    const int i = i0 + iw;
+    const int i = i0 + iw < ie ? sOrd[i0 + iw - ib] : ie;
     if (p < P && i < ie) {
       double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
       const double* q = sQ + (__ldg(tabf + i) & 0x7fffffffu);
@@ -435,9 +462,10 @@ size_t q_smem(int J, int VB, int TH, int ks = 1) {
   return static_cast<size_t>((win + 1) & ~1) * sizeof(double) +
          static_cast<size_t>(kQChunk) * VB * sizeof(double) + 2 * kQChunk * sizeof(int);
 }
-size_t z_smem(int K, int n1, int /*nf*/) {
+size_t z_smem(int K, int n1, int nf) {
   return static_cast<size_t>((K + 1) & ~1) * sizeof(double) + n1 * sizeof(double2) +
-         kZThreads * sizeof(double);  // sPart: P x W <= kZThreads
+         kZThreads * sizeof(double) +  // sPart: P x W <= kZThreads
+         2 * static_cast<size_t>(nf) * sizeof(int);  // output ranks and lane order
 }
 
 template <int TH, int VB>
