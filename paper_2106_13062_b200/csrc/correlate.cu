@@ -14,21 +14,30 @@
 // sketch.cpp:105-116, kept as nonzero lists: a collision is two terms of the
 // same sum). T(u,v,w) is <w, T(u,v,I)> (spectral_dot, estimators.cpp:38-64,
 // by linearity). Same estimate, no transform: the inputs are sparse (at most
-// I_n nonzeros of J per mode) and only I_f outputs are read, so for the CPD
-// geometries (config 3: I = 200, J = 3000) the (2J - 1) x I_c2 product per
-// item is cheaper than three length-n transforms run latency-bound at one
-// item per SM; engine.cu picks the path by a cost rule (st_engine_set_path
-// overrides it).
+// I_n nonzeros of J per mode) and only I_f outputs are read, so where I is
+// small against J the (2J - 1) x I_c2 product per item is cheaper than the
+// length-n transforms, which run latency-bound at one item per SM. engine.cu
+// picks the path per call by a cost rule fitted to measured A/B runs
+// (profiles/corr_sweep_r02.txt; config 3 stays on the transforms);
+// st_engine_set_path overrides it.
 //
-// corr_q_kernel: for one family, Q(k, v) = sum_{i2} sk[k + h(i2)] B'(i2, v) is
-//   a product of a Hankel matrix of the sketch with the batch's B' — each
-//   thread keeps KR k's x VB vectors of Q in registers; the sketch window and
-//   a chunk of B' (with its buckets) sit in shared memory (sketch reads
-//   conflict-free, B' reads warp-uniform broadcasts), so DFMA, not the LSU
-//   pipe, bounds it once VB >= 4.
-// corr_z_kernel: one CTA per (vector, family): Q_{v,d} in shared memory,
-//   est[i] = s_f(i) sum_{i1} a'(i1) Q[h_f(i) + h_c1(i1)] (fixed order), or for
-//   T(u,v,w) the block sum sum_i w[i] est[i] (fixed-order tree).
+// Q, per family, is a product of a Hankel matrix of the sketch with the
+// batch's B' (rows = the contracted mode's indices, split into bucket ranges
+// so each CTA's sketch window is KT + J / ranks):
+// corr_q_mma_kernel (batches of 2+): the fp64 tensor cores, mma.sync
+//   m8n8k4.f64 (DMMA) — A(m, kk) = sk[k + m + h(row kk)] gathered from the
+//   shared-memory window, B(kk, n) = B'(row kk, v); 8 or 16 vectors per CTA.
+// corr_q_kernel (one vector, or ST_CORR_DFMA): DFMA, each thread KR k's x VB
+//   vectors in registers, rows software-pipelined; for one vector a
+//   matrix-vector product bound by shared-memory loads.
+// corr_z_kernel: the readout, one item (vector, family) per CTA or its outputs
+//   split over G CTAs within one wave: the range partials of Q_{v,d} summed
+//   in a fixed order into shared memory, est[i] = s_f(i) sum_{i1} a'(i1)
+//   Q[h_f(i) + h_c1(i1)] (row order), outputs dealt to lanes round-robin over
+//   their bucket class mod 16 (fewer bank conflicts in the gathers); for
+//   T(u,v,w) the block sum sum_i w[i] est[i]; the median over the families
+//   (and the rtpm normalisation / refinement update) fused by the vector's
+//   last CTA (tail.cuh).
 #include <cuda_runtime.h>
 
 #include <algorithm>
