@@ -649,12 +649,12 @@ int st_engine_uvw(st_engine* e, size_t batch, const double* u, const double* v, 
       cudaStream_t st2 = nullptr;
       FCS_CUDA_TRY(fork_side(st, &st2));
       const EngArgs args = e->args();
+      // one-CTA part first (the submission order that keeps the two parts
+      // concurrent on any caller stream, as launch_iuv's split)
+      int rco = launch_uvw_dot(e->plan, args, static_cast<int>(nb1), u, v, w,
+                               static_cast<double2*>(e->scratch.p), est, st);
       int rcc = launch_iuv_cluster(e->plan, args, static_cast<int>(nb2), u + nb1 * e->dims[0],
                                    v + nb1 * e->dims[1], 0, 1, 2, est + nb1 * e->D, t, st2);
-      int rco = ST_OK;
-      if (rcc == 0)
-        rco = launch_uvw_dot(e->plan, args, static_cast<int>(nb1), u, v, w,
-                             static_cast<double2*>(e->scratch.p), est, st);
       // join before the median: a join directly followed by the next call's
       // fork measured a serialising stall (tools/experiments/iuv_split_probe.py)
       FCS_CUDA_TRY(join_side(st));

@@ -696,10 +696,13 @@ int launch_iuv(const FftPlan& pl, const EngArgs& e, int batch, const double* A, 
     cudaStream_t st2 = nullptr;
     FCS_CUDA_TRY(fork_side(st, &st2));
     const size_t na = e.dims[c1], nbv = e.dims[c2], nf = e.dims[f];
+    // the one-CTA part is submitted first: submitted after the clusters, the
+    // two parts ran serialised on a caller stream other than the legacy
+    // default stream (61 vs 41 us per step, tools/stream_probe.py); if the
+    // cluster form does not apply, the general path below redoes the batch
+    iuv1_kernel<<<dim3(nb1, e.D), kFftThreads, sm1, st>>>(pl, e, A, B, c1, c2, f, scratch, est);
     const int rc = launch_iuv_cluster(pl, e, batch - nb1, A + nb1 * na, B + nb1 * nbv, c1, c2, f,
                                       est + static_cast<size_t>(nb1) * e.D * nf, IuvTail{}, st2);
-    if (rc == 0)
-      iuv1_kernel<<<dim3(nb1, e.D), kFftThreads, sm1, st>>>(pl, e, A, B, c1, c2, f, scratch, est);
     const cudaError_t le = cudaGetLastError();
     FCS_CUDA_TRY(join_side(st));
     FCS_CUDA_TRY(le);
